@@ -1,0 +1,349 @@
+"""Golden-vector generator: runs the UNMODIFIED reference `fuseopt` package
+(pure Python, importable in the build container from /root/reference/pkg/src)
+and writes the fixtures the oracle and the CUDA path are pinned against.
+
+This script is test infrastructure.  It is the only file in the repo that
+imports the reference, and it only ever runs in the build container
+(/root/reference does not exist on the GPU box); its outputs are committed.
+
+Usage:  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [section ...]
+Sections: workloads rng cases search   (default: all)
+
+Inputs follow SURVEY.md section 8(d) / BASELINE.md section 3:
+  * graphs   gen_workload(WorkloadSpec(family, V, A, seed=0))      (workloads.py:131)
+  * profile  make_profile(g, HardwareParams())                       (workloads.py:307)
+  * MP model train(gen_training_samples(g, 256, (1, min(50, V)), hw, seed=0),
+                   TrainConfig(epochs=0, seed=0), MESSAGE_PASSING)   (estimator.py:623)
+  * candidate i: rng = random.Random(i); accumulating random_apply for
+    (nondup, dup, ar), each with n = rng.randint(0, 10)              (rewrite.py:222)
+"""
+
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import random
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+from fuseopt import (  # noqa: E402
+    EstimatorVariant,
+    HardwareParams,
+    OptimizationMethod,
+    SearchConfig,
+    TrainConfig,
+    WorkloadSpec,
+    backtracking_search,
+    build_graph,
+    canonical_hash,
+    cost,
+    featurize,
+    gen_training_samples,
+    gen_workload,
+    make_cost_providers,
+    make_profile,
+    oracle_providers,
+    predict_fused,
+    random_apply,
+    simulate,
+    train,
+)
+from fuseopt.comm import CommModelParams, save_params  # noqa: E402
+from fuseopt.estimator import analytic_model, save_model, save_profile  # noqa: E402
+from fuseopt.graph import DataEdge, OpNode, graph_to_doc  # noqa: E402
+
+OUT = HERE
+WL = os.path.join(OUT, "workloads")
+
+# name -> (family, V, A, comm C, comm D, model source)
+CONFIGS = {
+    # VGG-16 proxy, 8 workers: C = 2(N-1)/(N*B), N=8, B=12,500 B/us
+    "vgg16": ("chain", 144, 32, 2 * 7 / (8 * 12500.0), 100.0, None),
+    "resnet50": ("residual", 672, 161, None, None, None),
+    "bert": ("attention", 760, 199, None, None, None),
+    "gpt2m": ("attention", 5000, 292, None, None, "bert"),
+    "synth50k": ("residual", 50000, 1000, None, None, "resnet50"),
+}
+SMALL = {
+    "chain24": ("chain", 24, 4, None, None, None),
+    "residual40": ("residual", 40, 6, None, None, None),
+    "attention36": ("attention", 36, 5, None, None, None),
+    "recurrent30": ("recurrent", 30, 5, None, None, None),
+}
+
+METHODS = (
+    OptimizationMethod.NON_DUPLICATE_FUSION,
+    OptimizationMethod.DUPLICATE_FUSION,
+    OptimizationMethod.ALLREDUCE_FUSION,
+)
+
+
+def _dump_gz(path, doc):
+    with gzip.open(path, "wt", encoding="utf-8") as fh:
+        json.dump(doc, fh, sort_keys=True, separators=(",", ":"))
+
+
+def _dump(path, doc):
+    with open(path, "w", encoding="utf-8") as fh:
+        json.dump(doc, fh, sort_keys=True, separators=(",", ":"))
+        fh.write("\n")
+
+
+def make_candidate(g, i, beta=10):
+    """Candidate i of a random batch."""
+    rng = random.Random(i)
+    cur = g
+    for m in METHODS:
+        n = rng.randint(0, beta)
+        cur = random_apply(cur, m, n, rng).graph
+    return cur
+
+
+def state_doc(g):
+    """Sparse fusion state: only non-trivial groups/buckets."""
+    groups = []
+    for gr in g.groups:
+        trivial = len(gr.member_ops) == 1 and gr.id in gr.member_ops and not gr.duplicated_ops
+        if not trivial:
+            groups.append([gr.id, sorted(gr.member_ops), sorted(gr.duplicated_ops)])
+    buckets = []
+    for b in g.buckets:
+        if not (len(b.members) == 1 and b.id in b.members):
+            buckets.append([b.id, sorted(b.members)])
+    return {"groups": groups, "buckets": buckets}
+
+
+def _write_workload(name, family, V, A, C, D, model_src, hw):
+    t0 = time.time()
+    g = gen_workload(WorkloadSpec(family, V, A, seed=0), hw)
+    profile, _ = make_profile(g, hw)
+    comm = CommModelParams(C=C, D=D) if C is not None else hw.comm_params
+    base = os.path.join(WL, name)
+    _dump_gz(base + ".graph.json.gz", graph_to_doc(g))
+    tmp = base + ".tmp"
+    save_profile(tmp, profile)
+    with open(tmp) as fh:
+        _dump_gz(base + ".profile.json.gz", json.load(fh))
+    save_params(base + ".comm.json", comm)
+    if model_src is None:
+        samples = gen_training_samples(g, 256, (1, min(50, V)), hw, seed=0)
+        mp = train(samples, TrainConfig(epochs=0, seed=0), EstimatorVariant.MESSAGE_PASSING)
+        save_model(tmp, mp)
+        with open(tmp) as fh:
+            _dump_gz(base + ".mp.model.json.gz", json.load(fh))
+        lin = train(samples, TrainConfig(epochs=0, seed=0), EstimatorVariant.LINEAR_FEATURES)
+        save_model(base + ".lin.model.json", lin)
+    else:
+        meta = {"model_from": model_src}
+        _dump(base + ".model_from.json", meta)
+    os.remove(tmp)
+    print(f"workload {name}: V={len(g.ops)} E={len(g.edges)} A={len(g.allreduces)} "
+          f"in {time.time() - t0:.1f}s", flush=True)
+
+
+def section_workloads(names=None):
+    os.makedirs(WL, exist_ok=True)
+    hw = HardwareParams()
+    table = dict(CONFIGS)
+    table.update(SMALL)
+    for name, (family, V, A, C, D, src) in table.items():
+        if names and name not in names:
+            continue
+        _write_workload(name, family, V, A, C, D, src, hw)
+
+
+# ---------------------------------------------------------------------------
+# loading back (shared with the case/search sections)
+
+
+def load_workload(name):
+    from fuseopt.comm import load_params
+    from fuseopt.estimator import load_model, load_profile
+    from fuseopt.graph import graph_from_doc
+
+    base = os.path.join(WL, name)
+    with gzip.open(base + ".graph.json.gz", "rt") as fh:
+        g = graph_from_doc(json.load(fh))
+    tmp = f"/tmp/_golden_{os.getpid()}.json"
+    with gzip.open(base + ".profile.json.gz", "rt") as fh:
+        doc = json.load(fh)
+    with open(tmp, "w") as fh:
+        json.dump(doc, fh)
+    profile = load_profile(tmp)
+    comm = load_params(base + ".comm.json")
+    src = name
+    if os.path.exists(base + ".model_from.json"):
+        with open(base + ".model_from.json") as fh:
+            src = json.load(fh)["model_from"]
+    sbase = os.path.join(WL, src)
+    with gzip.open(sbase + ".mp.model.json.gz", "rt") as fh:
+        doc = json.load(fh)
+    with open(tmp, "w") as fh:
+        json.dump(doc, fh)
+    mp = load_model(tmp)
+    lin = load_model(sbase + ".lin.model.json")
+    os.remove(tmp)
+    return g, profile, comm, mp, lin
+
+
+def providers(profile, comm, mp, lin):
+    hw = HardwareParams()
+    return {
+        "mp": make_cost_providers(profile, comm, mp),
+        "lin": make_cost_providers(profile, comm, lin),
+        "analytic": make_cost_providers(profile, comm, analytic_model(5.0, 1.0 / 1024.0)),
+        "oracle": oracle_providers(hw),
+    }
+
+
+# ---------------------------------------------------------------------------
+# RNG golden sequences (CPython random.Random; search.py:88,119; rewrite.py:250)
+
+
+def section_rng():
+    out = {"randint_0_10": {}, "randrange": {}, "getrandbits32": {}}
+    for seed in [0, 1, 2, 7, 42, 1234, 2**32 + 5, 10**12 + 3]:
+        r = random.Random(seed)
+        out["randint_0_10"][str(seed)] = [r.randint(0, 10) for _ in range(64)]
+        r = random.Random(seed)
+        out["getrandbits32"][str(seed)] = [r.getrandbits(32) for _ in range(16)]
+        r = random.Random(seed)
+        seq = []
+        for k in [1, 2, 3, 5, 7, 8, 17, 100, 1000, 65537, 2**31 - 1]:
+            seq.append([k, r.randrange(k)])
+        for k in range(1, 200):
+            seq.append([k, r.randrange(k)])
+        out["randrange"][str(seed)] = seq
+    _dump(os.path.join(OUT, "rng.json"), out)
+    print("rng done", flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Scoring cases: candidates + reference costs + per-fused-group predictions
+
+
+def _case(name, g, profile, comm, mp, lin, n_cand, n_timeline):
+    cps = providers(profile, comm, mp, lin)
+    cands = []
+    t0 = time.time()
+    for i in range(n_cand):
+        c = make_candidate(g, i)
+        fresh = build_graph(
+            c.ops, c.edges,
+            [(ar.id, ar.producer_op, ar.tensor_bytes) for ar in c.allreduces],
+            groups=c.groups,
+            buckets=[(b.id, b.members) for b in c.buckets],
+            meta=c.meta,
+        )
+        rec = {"i": i, "state": state_doc(c), "hash_of_parent_equal": canonical_hash(c) == canonical_hash(g)}
+        rec["cost"] = {k: cost(fresh, cp) for k, cp in cps.items()}
+        fused = []
+        for gr in c.groups:
+            if len(gr.member_ops) > 1:
+                f = featurize(c, gr, profile)
+                fused.append({
+                    "id": gr.id,
+                    "members": sorted(gr.member_ops),
+                    "mp": predict_fused(mp, f),
+                    "lin": predict_fused(lin, f),
+                    "analytic": predict_fused(analytic_model(5.0, 1.0 / 1024.0), f),
+                    "oracle": cps["oracle"].op_cost(c, gr),
+                    "io": [f.internal_bytes, f.external_in_bytes, f.external_out_bytes],
+                    "longest": f.longest_path_len,
+                })
+        rec["fused"] = fused
+        if i < n_timeline:
+            tl = simulate(fresh, cps["mp"])
+            rec["timeline"] = {
+                "compute": [list(e) for e in tl.compute_events],
+                "comm": [list(e) for e in tl.comm_events],
+                "makespan": tl.makespan_us,
+            }
+        cands.append(rec)
+    base_cost = {k: cost(g, cp) for k, cp in cps.items()}
+    doc = {"workload": name, "base_cost": base_cost, "candidates": cands}
+    _dump_gz(os.path.join(OUT, "cases", f"{name}.cases.json.gz"), doc)
+    print(f"cases {name}: {n_cand} candidates in {time.time() - t0:.1f}s", flush=True)
+
+
+CASE_COUNTS = {
+    "chain24": (64, 8), "residual40": (64, 8), "attention36": (64, 8), "recurrent30": (64, 8),
+    "vgg16": (64, 4), "resnet50": (48, 4), "bert": (48, 4), "gpt2m": (6, 1), "synth50k": (1, 0),
+}
+
+
+def section_cases(names=None):
+    os.makedirs(os.path.join(OUT, "cases"), exist_ok=True)
+    for name, (n, nt) in CASE_COUNTS.items():
+        if names and name not in names:
+            continue
+        g, profile, comm, mp, lin = load_workload(name)
+        _case(name, g, profile, comm, mp, lin, n, nt)
+
+
+# ---------------------------------------------------------------------------
+# Search traces (search.py:84-155)
+
+
+SEARCHES = [
+    # (workload, provider, cfg kwargs)
+    ("chain24", "mp", dict(alpha=1.05, beta=4, seed=0, max_unchanged=60)),
+    ("chain24", "oracle", dict(alpha=1.05, beta=4, seed=1, max_unchanged=60)),
+    ("residual40", "mp", dict(alpha=1.05, beta=10, seed=2, max_unchanged=80)),
+    ("residual40", "analytic", dict(alpha=1.1, beta=5, seed=3, max_unchanged=80)),
+    ("attention36", "mp", dict(alpha=1.05, beta=10, seed=4, max_unchanged=80)),
+    ("attention36", "lin", dict(alpha=1.05, beta=6, seed=5, max_unchanged=80)),
+    ("recurrent30", "oracle", dict(alpha=1.02, beta=3, seed=6, max_unchanged=80)),
+    ("recurrent30", "mp", dict(alpha=1.2, beta=10, seed=7, max_unchanged=80)),
+    ("vgg16", "mp", dict()),  # reference defaults (BASELINE config 0)
+    ("bert", "mp", dict(seed=0, max_unchanged=60)),
+]
+
+
+def section_search(only=None):
+    os.makedirs(os.path.join(OUT, "search"), exist_ok=True)
+    for wl, prov, kw in SEARCHES:
+        tag = f"{wl}.{prov}.s{kw.get('seed', 0)}"
+        if only and tag not in only and wl not in only:
+            continue
+        g, profile, comm, mp, lin = load_workload(wl)
+        cp = providers(profile, comm, mp, lin)[prov]
+        cfg = SearchConfig(**kw)
+        t0 = time.time()
+        res = backtracking_search(g, cfg, cp)
+        wall = time.time() - t0
+        doc = {
+            "workload": wl, "provider": prov,
+            "cfg": {"alpha": cfg.alpha, "beta": cfg.beta, "max_unchanged": cfg.max_unchanged, "seed": cfg.seed},
+            "best_cost_us": res.best_cost_us, "steps": res.steps,
+            "candidates_evaluated": res.candidates_evaluated,
+            "candidates_enqueued": res.candidates_enqueued,
+            "best_state": state_doc(res.best_graph),
+            "trace": [[r.step, r.action, r.cost_us, r.best_cost_us, r.queue_len, r.enqueued] for r in res.trace],
+            "wall_s": wall,
+        }
+        _dump_gz(os.path.join(OUT, "search", f"{tag}.search.json.gz"), doc)
+        print(f"search {tag}: steps={res.steps} evals={res.candidates_evaluated} "
+              f"best={res.best_cost_us:.3f} in {wall:.1f}s", flush=True)
+
+
+def main(argv):
+    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search")]
+    names = [a for a in argv if a not in sections]
+    if not sections:
+        sections = ["workloads", "rng", "cases", "search"]
+    for s in sections:
+        {"workloads": section_workloads, "rng": section_rng,
+         "cases": section_cases, "search": section_search}[s](names or None) if s != "rng" else section_rng()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
