@@ -1,0 +1,195 @@
+/*
+ * disco_b200.h -- C-ABI of the B200-native DisCo candidate-scoring path.
+ *
+ * The reference (`fuseopt`, pure Python) exposes this path as Python
+ * callbacks and functions; each entry point below names the reference
+ * interface it replaces (paths relative to the reference's pkg/src/fuseopt/).
+ * Plain pointers and sizes only; no torch types.  Every function returns an
+ * fo_status; fo_last_error() gives a thread-local message for the last
+ * failure on the calling thread.
+ *
+ * Index conventions (identical to build_graph's sort order, graph.py:314-316):
+ *   ops        0..V-1 in ascending op id order
+ *   edges      0..E-1 sorted by (src, dst)
+ *   allreduces 0..A-1 in ascending AllReduce id order
+ * A candidate fusion state is three int32 arrays:
+ *   normal_gid[V]   group id of each op's normal membership
+ *   replica_gid[V]  group id of its replica membership, or -1
+ *   bucket_of[A]    bucket id of each AllReduce
+ * Group ids lie in [0, gid_bound) and bucket ids in [0, A); only their ORDER
+ * is observable (simulator tie-breaks, graph.py:269-273), so callers map the
+ * reference's ids to these ranges with any monotone relabelling.
+ */
+#ifndef DISCO_B200_H
+#define DISCO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes <-> fuseopt.errors classes (errors.py:4-53). */
+typedef enum {
+    FO_OK = 0,
+    FO_CYCLE = 1,             /* CycleError: schedule deadlock (simulator.py:133) */
+    FO_MISSING_COST = 2,      /* MissingCost (simulator.py:45-46, estimator.py:815-818) */
+    FO_NEGATIVE_DURATION = 3, /* ValueError (simulator.py:48-49) */
+    FO_DIM_MISMATCH = 4,      /* DimensionMismatch (estimator.py:358-360) */
+    FO_INVALID_ARG = 5,       /* malformed input (ids out of range, bad sizes) */
+    FO_CUDA_ERROR = 6,        /* CUDA runtime failure */
+    FO_UNSUPPORTED = 7        /* configuration outside the device path */
+} fo_status;
+
+/* Cost providers (simulator.py:28-35). */
+enum {
+    FO_PROVIDER_PROFILE = 0,  /* make_cost_providers(profile, comm, model), estimator.py:801-824 */
+    FO_PROVIDER_HW_ORACLE = 1 /* oracle_providers(hw), noise == 0, workloads.py:294-304 */
+};
+/* Fused-op estimator variants (estimator.py:254-257). */
+enum {
+    FO_EST_INVALID = -2, /* model whose shapes disagree: fused groups raise DimensionMismatch */
+    FO_EST_NONE = -1,    /* model=None: fused groups raise MissingCost (estimator.py:815) */
+    FO_EST_ANALYTIC = 0,
+    FO_EST_LINEAR = 1,
+    FO_EST_MESSAGE_PASSING = 2
+};
+/* Estimator arithmetic on the device. */
+enum {
+    FO_PREC_FP32 = 0, /* FP32 FFMA message passing: throughput mode, <= 1e-4 rel */
+    FO_PREC_FP64 = 1  /* FP64 message passing: decision-exact mode for the search */
+};
+
+/* Static graph (replaces HloGraph's ops/edges/allreduces, graph.py:277-299,
+ * plus the per-op profile lookup of estimator.py:63-69 resolved once). */
+typedef struct {
+    int32_t n_ops, n_edges, n_allreduces;
+    const int32_t *op_kind;       /* [V] 0 compute, 1 parameter, 2 control (graph.py:29-32) */
+    const int64_t *op_out_bytes;  /* [V] OpNode.out_bytes */
+    const double *op_profile_us;  /* [V] lookup(profile, op); NaN when the profile has no entry */
+    const double *op_compute_us;  /* [V] OpNode.compute_us; NaN for None */
+    const int32_t *edge_src;      /* [E] op indices */
+    const int32_t *edge_dst;      /* [E] */
+    const int64_t *edge_bytes;    /* [E] */
+    const int32_t *ar_producer;   /* [A] producer op index */
+    const int64_t *ar_bytes;      /* [A] tensor bytes */
+} fo_graph_desc;
+
+/* Cost model: what make_cost_providers / oracle_providers close over. */
+typedef struct {
+    int32_t provider;            /* FO_PROVIDER_* */
+    int32_t variant;             /* FO_EST_* (ignored by the hardware oracle) */
+    double comm_C, comm_D;       /* CommModelParams (comm.py:20-49) */
+    double launch_us;            /* analytic launch_overhead_us / HardwareParams.launch_overhead_us */
+    double mem_us_per_byte;      /* analytic mem_us_per_byte / HardwareParams.mem_us_per_byte */
+    int32_t layers, hidden, feat_dim; /* message passing hyper-parameters (estimator.py:264-278) */
+    const int32_t *op_vocab_slot;     /* [V] one-hot slot of each op's op_code (estimator.py:326-337) */
+    /* MESSAGE_PASSING: W_emb[h*F], W_1..W_L[L*h*h], W_r[h*h], A1[h*h], c1[h],
+     *                  A2[h*h], c2[h], a3[h], c3[1]   (row-major, estimator.py:554-576)
+     * LINEAR:          w[12], b[1]                    (estimator.py:557-561) */
+    const double *params;
+    int64_t n_params;
+    const double *norm_mean; /* node_norm (MP, F entries) or agg_norm (LINEAR, 12); NULL = none */
+    const double *norm_std;
+    double out_scale;
+} fo_cost_model;
+
+typedef struct fo_graph fo_graph;
+
+/* ---- graph handle ------------------------------------------------------ */
+int fo_graph_create(const fo_graph_desc *desc, int32_t device, fo_graph **out);
+int fo_graph_destroy(fo_graph *g);
+/* Replaces make_cost_providers(...) / oracle_providers(...) (estimator.py:801, workloads.py:294). */
+int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *model);
+
+/* ---- scoring ----------------------------------------------------------- */
+/* cost() for K candidates (simulator.py:143-145 over K fresh graphs).
+ * Device pointers; asynchronous on `stream` (cudaStream_t, NULL = legacy).
+ * ngid/rgid: [K*V], bkt: [K*A], cost_out: [K] fp64, status_out: [K] fo_status. */
+int fo_score(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
+             int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out, void *stream);
+/* Same through host buffers (pinned or pageable): H2D, kernel, D2H, synchronous. */
+int fo_score_host(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
+                  int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out);
+
+/* simulate() of one candidate with its Timeline (simulator.py:53-140).
+ * durations: NULL -> device cost model; else host fp64 durations in schedule
+ * node order [groups by id | buckets by id] (custom CostProviders; negative
+ * values -> FO_NEGATIVE_DURATION).  Event buffers are host arrays of
+ * capacity 2V (compute) and A (comm); ids written are the caller's ids.
+ * bad_node_out: first failing schedule node index (or -1). */
+int fo_simulate(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t gid_bound,
+                int32_t precision, const double *durations, int32_t *c_id, double *c_start, double *c_end,
+                int32_t *n_compute, int32_t *b_id, double *b_start, double *b_end, int32_t *n_comm,
+                double *makespan, int32_t *bad_node_out);
+
+/* Per-node durations of one candidate as the device computes them
+ * (_duration for every schedule node, simulator.py:62): dur_out [G+B] in node
+ * order, n_groups_out = G.  Used for predict_fused parity (estimator.py:462). */
+int fo_node_durations(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt,
+                      int32_t gid_bound, int32_t precision, double *dur_out, int32_t *n_groups_out,
+                      int32_t *bad_node_out);
+
+/* ---- native batch-expand (rewrite.py:222-263, search.py:88-119) -------- */
+/* Candidate k: random.Random(seeds[k]) then, for each enabled method in
+ * (nondup, dup, ar), n = randint(0, beta) accumulating random_apply steps,
+ * starting from the base state (NULL = unfused default).  Output states use
+ * compact group ids < gid_bound_out (returned).  Host threads: n_threads. */
+int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *base_rgid, const int32_t *base_bkt,
+                       const uint64_t *seeds, int32_t K, int32_t beta, int32_t methods_mask, int32_t n_threads,
+                       int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *gid_bound_out);
+
+/* random_apply (rewrite.py:222-263) on one state in place, driven by a
+ * CPython random.Random state: mt_state = getstate()[1] (624 words + index). */
+int fo_random_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int32_t method, int32_t n,
+                    uint32_t *mt_state, int32_t *applied_out);
+/* Every accepted single rewrite of a state in exhaustive_search's enumeration
+ * order (search.py:185-206): nondup / dup per fusible pair, then AllReduce
+ * fusion per bucket pair.  Outputs up to cap states; n_out = count. */
+int fo_expand_all(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t cap,
+                  int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *n_out);
+
+/* Canonical fusion-state hash (equality semantics of canonical_hash, graph.py:559-580). */
+int fo_state_hash(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
+                  uint64_t *hash_out);
+
+/* ---- backtracking search, lock-stepped seeds (search.py:84-155) -------- */
+typedef struct {
+    double alpha;
+    int32_t beta, max_unchanged, methods_mask; /* bit 0 nondup, bit 1 dup, bit 2 ar */
+    int32_t precision;                          /* FO_PREC_* for the estimator */
+    int32_t n_threads;                          /* host threads for the batch-expand */
+} fo_search_cfg;
+
+typedef struct {
+    int32_t step;
+    int32_t method; /* 0 nondup, 1 dup, 2 ar */
+    double cost_us, best_cost_us;
+    int32_t queue_len;
+    int32_t enqueued;
+} fo_trace_rec;
+
+typedef struct fo_search fo_search;
+/* R independent searches (seeds[r]) from the same start state (NULL = default). */
+int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seeds, int32_t R,
+                     const int32_t *ngid0, const int32_t *rgid0, const int32_t *bkt0, fo_search **out);
+/* One round: every active search does one step of Alg. 1; all their
+ * candidates are scored in ONE device batch.  active_out = searches still
+ * running; best_out[R] / best_cost_out: per-search best costs after the round. */
+int fo_search_round(fo_search *s, int32_t *active_out, double *best_cost_out);
+/* Counters: steps, candidates_evaluated, candidates_enqueued, trace length. */
+int fo_search_result(fo_search *s, int32_t r, double *best_cost, int64_t *counters4, int32_t *best_ngid,
+                     int32_t *best_rgid, int32_t *best_bkt, fo_trace_rec *trace, int64_t trace_cap);
+/* Per-round device time (ms) of the scoring kernels and host expand time (ms). */
+int fo_search_timing(fo_search *s, double *device_ms, double *expand_ms, int64_t *scored);
+int fo_search_destroy(fo_search *s);
+
+/* ---- misc -------------------------------------------------------------- */
+const char *fo_last_error(void);
+/* Device kernel launches issued by this process (for the bench's gpu_launches). */
+int64_t fo_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DISCO_B200_H */

@@ -1,0 +1,63 @@
+"""B200-native DisCo candidate scoring: the fused-op estimator and the
+iteration simulator on sm_100a, behind the reference ``fuseopt`` package's
+estimator / simulator / search entry points.
+
+The CUDA library (paper_2209_12769_b200/_build/libdiscob200.so) is required:
+every device entry point raises if it is missing; there is no CPU fallback.
+"""
+
+from .comm import CommModelParams, load_params, predict, save_params
+from .errors import (
+    CycleError,
+    DeviceError,
+    DimensionMismatch,
+    FuseoptError,
+    GraphFormatError,
+    InvalidConfig,
+    LimitExceeded,
+    MissingCost,
+    NotNeighbors,
+    UnknownOp,
+)
+from .estimator import (
+    DeviceCostProviders,
+    EstimatorModel,
+    EstimatorVariant,
+    Profile,
+    analytic_model,
+    load_model,
+    load_profile,
+    lookup,
+    make_cost_providers,
+    predict_fused_groups,
+)
+from .graph import (
+    AllReduceInstr,
+    DataEdge,
+    FusionGroup,
+    GraphMeta,
+    HloGraph,
+    OpNode,
+    TensorBucket,
+    build_graph,
+    canonical_hash,
+    graph_from_doc,
+    graph_to_doc,
+    load_graph,
+    save_graph,
+    with_fusion_state,
+)
+from .rewrite import OptimizationMethod, RewriteOutcome, make_candidates, random_apply
+from .search import (
+    LockstepSearch,
+    SearchConfig,
+    SearchResult,
+    TraceRecord,
+    backtracking_search,
+    exhaustive_search,
+    lockstep_search,
+)
+from .simulator import CostProviders, Timeline, cost, cost_batch, fo_bound, format_timeline, simulate
+from .workloads import HardwareParams, load_workload, oracle_providers
+
+__version__ = "0.1.0"

@@ -1,0 +1,456 @@
+// capi.cu -- C-ABI entry points (include/disco_b200.h): graph handle, cost
+// model upload, batched scoring, single-candidate simulate/timeline.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fo_internal.h"
+
+namespace fo {
+
+static thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int status, const std::string &msg) {
+    g_last_error = msg;
+    return status;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return fail(FO_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L) {
+    *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max);
+    size_t need = (size_t)L->total * (size_t)slots;
+    if (need > g->ws_bytes) {
+        if (g->d_ws) cudaFree(g->d_ws);
+        g->d_ws = nullptr;
+        g->ws_bytes = 0;
+        CUDA_TRY(cudaMalloc(&g->d_ws, need));
+        g->ws_bytes = need;
+    }
+    return FO_OK;
+}
+
+static int grid_for(fo_graph *g, int K, int precision) {
+    int w = score_warps_per_block();
+    int max_blocks = g->num_sms * score_blocks_per_sm(precision);
+    int want = (K + w - 1) / w;
+    return want < max_blocks ? (want > 0 ? want : 1) : max_blocks;
+}
+
+static int launch(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K, int VB,
+                  int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
+                  double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream, int grid) {
+    WsLayout L;
+    int slots = grid * score_warps_per_block();
+    int st = ensure_workspace(g, VB, slots, &L);
+    if (st) return st;
+    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, K, VB, precision, g->d_ws, L, slots, grid,
+                                 score_warps_per_block(), cost, status, ext_dur, tl, dur_out, bad_out, ngroups_out,
+                                 stream);
+    g_launches++;
+    if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score kernel launch: ") + cudaGetErrorString(e));
+    return FO_OK;
+}
+
+int score_device(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K, int VB,
+                 int precision, double *cost, int32_t *status, cudaStream_t stream) {
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set (fo_graph_set_cost_model)");
+    if (K <= 0) return FO_OK;
+    if (VB <= 0) return fail(FO_INVALID_ARG, "gid_bound must be > 0");
+    CUDA_TRY(cudaSetDevice(g->device));
+    TimelineOut tl{};
+    return launch(g, ngid, rgid, bkt, K, VB, precision, cost, status, nullptr, tl, nullptr, nullptr, nullptr, stream,
+                  grid_for(g, K, precision));
+}
+
+}  // namespace fo
+
+using namespace fo;
+
+extern "C" {
+
+const char *fo_last_error(void) { return fo::g_last_error.c_str(); }
+int64_t fo_kernel_launches(void) { return fo::g_launches.load(); }
+
+int fo_graph_create(const fo_graph_desc *d, int32_t device, fo_graph **out) {
+    if (!d || !out) return fail(FO_INVALID_ARG, "null argument");
+    const int V = d->n_ops, E = d->n_edges, A = d->n_allreduces;
+    if (V < 0 || E < 0 || A < 0) return fail(FO_INVALID_ARG, "negative sizes");
+    for (int e = 0; e < E; e++)
+        if (d->edge_src[e] < 0 || d->edge_src[e] >= V || d->edge_dst[e] < 0 || d->edge_dst[e] >= V)
+            return fail(FO_INVALID_ARG, "edge endpoint out of range");
+    for (int a = 0; a < A; a++)
+        if (d->ar_producer[a] < 0 || d->ar_producer[a] >= V) return fail(FO_INVALID_ARG, "AllReduce producer out of range");
+    fo_graph *g = new fo_graph();
+    g->device = device;
+    g->V = V; g->E = E; g->A = A;
+    g->op_kind.assign(d->op_kind, d->op_kind + V);
+    g->op_out.assign(d->op_out_bytes, d->op_out_bytes + V);
+    g->op_prof.assign(d->op_profile_us, d->op_profile_us + V);
+    g->op_compute.assign(d->op_compute_us, d->op_compute_us + V);
+    g->e_src.assign(d->edge_src, d->edge_src + E);
+    g->e_dst.assign(d->edge_dst, d->edge_dst + E);
+    g->e_bytes.assign(d->edge_bytes, d->edge_bytes + E);
+    g->ar_prod.assign(d->ar_producer, d->ar_producer + A);
+    g->ar_bytes.assign(d->ar_bytes, d->ar_bytes + A);
+    // CSRs (graph.py:128-154): stable, so per-op edge lists keep (src, dst) order
+    auto csr = [](int n, const std::vector<int32_t> &key, std::vector<int32_t> &ptr, std::vector<int32_t> &idx) {
+        ptr.assign(n + 1, 0);
+        idx.assign(key.size(), 0);
+        for (int32_t k : key) ptr[k + 1]++;
+        for (int i = 0; i < n; i++) ptr[i + 1] += ptr[i];
+        std::vector<int32_t> cur(ptr.begin(), ptr.end() - 1);
+        for (size_t i = 0; i < key.size(); i++) idx[cur[key[i]]++] = (int32_t)i;
+    };
+    csr(V, g->e_dst, g->in_ptr, g->in_e);
+    csr(V, g->e_src, g->out_ptr, g->out_e);
+    csr(V, g->ar_prod, g->arp_ptr, g->arp);
+    g->agg.assign(E, 0);
+    g->op_in.assign(V, 0);
+    int64_t pairs = A;
+    for (int e = 0; e < E; e++) {
+        int s = g->e_src[e], t = g->e_dst[e];
+        int nar = g->arp_ptr[s + 1] - g->arp_ptr[s];
+        // _consumes_aggregate (graph.py:231-235)
+        g->agg[e] = nar > 0 && g->out_ptr[t + 1] == g->out_ptr[t] && g->arp_ptr[t + 1] == g->arp_ptr[t];
+        g->op_in[t] += g->e_bytes[e];
+        pairs += g->agg[e] ? 2 * nar : 2;
+    }
+    if (pairs > INT32_MAX / 2) { delete g; return fail(FO_INVALID_ARG, "graph too large"); }
+    g->pairs_max = (int32_t)pairs;
+
+    if (device < 0) {  // host-only handle: the native batch-expand engine without a device
+        *out = g;
+        return FO_OK;
+    }
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce == cudaSuccess) ce = cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    // one allocation for the static arrays
+    struct Seg { const void *src; size_t bytes; size_t off; };
+    std::vector<uint8_t> kind8(V);
+    for (int v = 0; v < V; v++) kind8[v] = (uint8_t)g->op_kind[v];
+    Seg segs[] = {
+        {g->e_src.data(), 4u * E, 0}, {g->e_dst.data(), 4u * E, 0}, {g->e_bytes.data(), 8u * E, 0},
+        {g->agg.data(), (size_t)E, 0}, {g->in_ptr.data(), 4u * (V + 1), 0}, {g->in_e.data(), 4u * E, 0},
+        {g->out_ptr.data(), 4u * (V + 1), 0}, {g->out_e.data(), 4u * E, 0}, {g->arp_ptr.data(), 4u * (V + 1), 0},
+        {g->arp.data(), 4u * A, 0}, {g->ar_prod.data(), 4u * A, 0}, {g->ar_bytes.data(), 8u * A, 0},
+        {kind8.data(), (size_t)V, 0}, {g->op_prof.data(), 8u * V, 0}, {g->op_compute.data(), 8u * V, 0},
+        {g->op_out.data(), 8u * V, 0}, {g->op_in.data(), 8u * V, 0},
+    };
+    size_t total = 0;
+    for (auto &s : segs) { s.off = total; total += al256(s.bytes + 1); }
+    if (ce == cudaSuccess) ce = cudaMalloc(&g->d_static, total);
+    for (auto &s : segs)
+        if (ce == cudaSuccess && s.bytes) ce = cudaMemcpy((char *)g->d_static + s.off, s.src, s.bytes, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+        std::string m = std::string("fo_graph_create: ") + cudaGetErrorString(ce);
+        fo_graph_destroy(g);
+        return fail(FO_CUDA_ERROR, m);
+    }
+    char *b = (char *)g->d_static;
+    DGraph &dg = g->dg;
+    dg.V = V; dg.E = E; dg.A = A;
+    dg.e_src = (const int32_t *)(b + segs[0].off);
+    dg.e_dst = (const int32_t *)(b + segs[1].off);
+    dg.e_bytes = (const int64_t *)(b + segs[2].off);
+    dg.e_agg = (const uint8_t *)(b + segs[3].off);
+    dg.in_ptr = (const int32_t *)(b + segs[4].off);
+    dg.in_e = (const int32_t *)(b + segs[5].off);
+    dg.out_ptr = (const int32_t *)(b + segs[6].off);
+    dg.out_e = (const int32_t *)(b + segs[7].off);
+    dg.arp_ptr = (const int32_t *)(b + segs[8].off);
+    dg.arp = (const int32_t *)(b + segs[9].off);
+    dg.ar_prod = (const int32_t *)(b + segs[10].off);
+    dg.ar_bytes = (const int64_t *)(b + segs[11].off);
+    dg.op_kind = (const uint8_t *)(b + segs[12].off);
+    dg.op_prof = (const double *)(b + segs[13].off);
+    dg.op_compute = (const double *)(b + segs[14].off);
+    dg.op_out = (const int64_t *)(b + segs[15].off);
+    dg.op_in = (const int64_t *)(b + segs[16].off);
+    dg.pairs_max = g->pairs_max;
+    *out = g;
+    return FO_OK;
+}
+
+int fo_graph_destroy(fo_graph *g) {
+    if (!g) return FO_OK;
+    if (g->device < 0) { delete g; return FO_OK; }
+    cudaSetDevice(g->device);
+    if (g->stream) cudaStreamSynchronize(g->stream);
+    if (g->d_static) cudaFree(g->d_static);
+    if (g->d_model) cudaFree(g->d_model);
+    if (g->d_ws) cudaFree(g->d_ws);
+    if (g->d_io) cudaFree(g->d_io);
+    if (g->h_pinned) cudaFreeHost(g->h_pinned);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+    return FO_OK;
+}
+
+int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
+    if (!g || !m) return fail(FO_INVALID_ARG, "null argument");
+    std::lock_guard<std::mutex> lk(g->mu);
+    DGraph &dg = g->dg;
+    dg.provider = m->provider;
+    dg.variant = m->variant;
+    dg.C = m->comm_C;
+    dg.D = m->comm_D;
+    dg.launch = m->launch_us;
+    dg.mem = m->mem_us_per_byte;
+    dg.out_scale = m->out_scale;
+    dg.layers = 0;
+    dg.lin_norm = 0;
+    if (m->provider != FO_PROVIDER_PROFILE && m->provider != FO_PROVIDER_HW_ORACLE)
+        return fail(FO_INVALID_ARG, "unknown provider");
+    if (!(m->comm_C >= 0) || !(m->comm_D >= 0)) return fail(FO_INVALID_ARG, "C and D must be non-negative");
+    const int V = g->V;
+    if (m->provider == FO_PROVIDER_PROFILE && m->variant == FO_EST_LINEAR) {
+        if (!m->params || m->n_params != 13) return fail(FO_DIM_MISMATCH, "linear model needs w[12] and b");
+        for (int i = 0; i < 12; i++) dg.lin_w[i] = m->params[i];
+        dg.lin_b = m->params[12];
+        if (m->norm_mean && m->norm_std) {
+            dg.lin_norm = 1;
+            for (int i = 0; i < 12; i++) { dg.agg_mean[i] = m->norm_mean[i]; dg.agg_std[i] = m->norm_std[i]; }
+        }
+    }
+    if (m->provider == FO_PROVIDER_PROFILE && m->variant == FO_EST_MESSAGE_PASSING) {
+        const int h = m->hidden, F = m->feat_dim, L = m->layers;
+        if (h < 1 || h > kHidden) return fail(FO_UNSUPPORTED, "hidden size must be in [1, 32] on the device");
+        if (F < 6 || L < 0) return fail(FO_DIM_MISMATCH, "bad feature dimension / layers");
+        int64_t need = (int64_t)h * F + (int64_t)(L + 3) * h * h + 3 * h + 1;
+        if (!m->params || m->n_params != need) return fail(FO_DIM_MISMATCH, "message-passing parameter count mismatch");
+        if (!m->op_vocab_slot) return fail(FO_INVALID_ARG, "op_vocab_slot required");
+        for (int v = 0; v < V; v++)
+            if (m->op_vocab_slot[v] < 0 || 6 + m->op_vocab_slot[v] >= F)
+                return fail(FO_DIM_MISMATCH, "vocab slot outside W_emb");
+        const double *p = m->params;
+        const double *Wemb = p;
+        const double *Wl = Wemb + (int64_t)h * F;
+        const double *Wr = Wl + (int64_t)L * h * h;
+        const double *A1 = Wr + h * h;
+        const double *c1 = A1 + h * h;
+        const double *A2 = c1 + h;
+        const double *c2 = A2 + h * h;
+        const double *a3 = c2 + h;
+        const double c3 = a3[h];
+        // per-op embedded features H0 = standardize(X) @ W_emb^T (estimator.py:321-338, :369)
+        std::vector<double> H0((size_t)V * kHidden, 0.0), x(F);
+        for (int v = 0; v < V; v++) {
+            double c = g->op_prof[v], in = (double)g->op_in[v], o = (double)g->op_out[v];
+            std::fill(x.begin(), x.end(), 0.0);
+            x[0] = std::log1p(c); x[1] = c; x[2] = std::log1p(in); x[3] = in; x[4] = std::log1p(o); x[5] = o;
+            x[6 + m->op_vocab_slot[v]] = 1.0;
+            if (m->norm_mean && m->norm_std)
+                for (int k = 0; k < F; k++) x[k] = (x[k] - m->norm_mean[k]) / m->norm_std[k];
+            for (int ch = 0; ch < h; ch++) {
+                double acc = 0.0;
+                for (int k = 0; k < F; k++) acc += x[k] * Wemb[ch * F + k];
+                H0[(size_t)v * kHidden + ch] = acc;
+            }
+        }
+        MpLayout ml = mp_layout(L);
+        std::vector<double> W(ml.total, 0.0);
+        auto put_t = [&](int64_t off, const double *M) {  // W^T, zero padded to 32x32
+            for (int r = 0; r < h; r++)
+                for (int k = 0; k < h; k++) W[off + k * 32 + r] = M[r * h + k];
+        };
+        for (int l = 0; l < L; l++) put_t(ml.wl + (int64_t)l * 1024, Wl + (int64_t)l * h * h);
+        put_t(ml.wr, Wr);
+        put_t(ml.a1, A1);
+        put_t(ml.a2, A2);
+        for (int r = 0; r < h; r++) { W[ml.c1 + r] = c1[r]; W[ml.c2 + r] = c2[r]; W[ml.a3 + r] = a3[r]; }
+        W[ml.c3] = c3;
+        std::vector<float> H0f(H0.begin(), H0.end()), Wf(W.begin(), W.end());
+        size_t oH0d = 0, oH0f = al256(H0.size() * 8), oWd = oH0f + al256(H0f.size() * 4 + 4),
+               oWf = oWd + al256(W.size() * 8), tot = oWf + al256(Wf.size() * 4);
+        if (g->device < 0) { g->model_set = true; return FO_OK; }
+        CUDA_TRY(cudaSetDevice(g->device));
+        if (g->d_model) { cudaFree(g->d_model); g->d_model = nullptr; }
+        CUDA_TRY(cudaMalloc(&g->d_model, tot));
+        char *b = (char *)g->d_model;
+        if (!H0.empty()) {
+            CUDA_TRY(cudaMemcpy(b + oH0d, H0.data(), H0.size() * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(b + oH0f, H0f.data(), H0f.size() * 4, cudaMemcpyHostToDevice));
+        }
+        CUDA_TRY(cudaMemcpy(b + oWd, W.data(), W.size() * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(b + oWf, Wf.data(), Wf.size() * 4, cudaMemcpyHostToDevice));
+        dg.H0d = (const double *)(b + oH0d);
+        dg.H0f = (const float *)(b + oH0f);
+        dg.Wd = (const double *)(b + oWd);
+        dg.Wf = (const float *)(b + oWf);
+        dg.layers = L;
+    }
+    g->model_set = true;
+    return FO_OK;
+}
+
+int fo_score(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K, int32_t gid_bound,
+             int32_t precision, double *cost_out, int32_t *status_out, void *stream) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    std::lock_guard<std::mutex> lk(g->mu);
+    return score_device(g, ngid, rgid, bkt, K, gid_bound, precision, cost_out, status_out, (cudaStream_t)stream);
+}
+
+static int ensure_io(fo_graph *g, size_t bytes) {
+    if (bytes > g->io_bytes) {
+        if (g->d_io) cudaFree(g->d_io);
+        g->d_io = nullptr;
+        g->io_bytes = 0;
+        CUDA_TRY(cudaMalloc(&g->d_io, bytes));
+        g->io_bytes = bytes;
+    }
+    return FO_OK;
+}
+
+int fo_score_host(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
+                  int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (K <= 0) return FO_OK;
+    CUDA_TRY(cudaSetDevice(g->device));
+    size_t nv = (size_t)K * g->V * 4, na = (size_t)K * g->A * 4;
+    size_t o_r = al256(nv), o_b = o_r + al256(nv), o_c = o_b + al256(na + 4), o_s = o_c + al256((size_t)K * 8);
+    int st = ensure_io(g, o_s + al256((size_t)K * 4));
+    if (st) return st;
+    char *b = (char *)g->d_io;
+    cudaStream_t s = g->stream;
+    if (nv) {
+        CUDA_TRY(cudaMemcpyAsync(b, ngid, nv, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(b + o_r, rgid, nv, cudaMemcpyHostToDevice, s));
+    }
+    if (na) CUDA_TRY(cudaMemcpyAsync(b + o_b, bkt, na, cudaMemcpyHostToDevice, s));
+    st = score_device(g, (int32_t *)b, (int32_t *)(b + o_r), (int32_t *)(b + o_b), K, gid_bound, precision,
+                      (double *)(b + o_c), (int32_t *)(b + o_s), s);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpyAsync(cost_out, b + o_c, (size_t)K * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status_out, b + o_s, (size_t)K * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return FO_OK;
+}
+
+// single candidate through device temporaries (simulate / timeline / durations)
+static int single(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int VB, int precision,
+                  const double *durations, bool want_tl, bool want_dur, std::vector<char> &hout, size_t *offs) {
+    const int V = g->V, A = g->A;
+    size_t GMx = 2 * (size_t)V + 1, NMx = GMx + A + 1;
+    size_t o[16];
+    size_t t = 0;
+    auto take = [&](int i, size_t bytes) { o[i] = t; t += al256(bytes + 8); };
+    take(0, 4u * V); take(1, 4u * V); take(2, 4u * A);      // state
+    take(3, 8); take(4, 4);                                  // cost, status
+    take(5, 8 * NMx);                                        // ext durations
+    take(6, 4 * GMx); take(7, 8 * GMx); take(8, 8 * GMx);    // compute events
+    take(9, 4u * (A + 1)); take(10, 8u * (A + 1)); take(11, 8u * (A + 1));  // comm events
+    take(12, 4); take(13, 4);                                // counts
+    take(14, 8 * NMx);                                       // dur out
+    take(15, 16);                                            // bad, ngroups
+    int st = ensure_io(g, t);
+    if (st) return st;
+    char *b = (char *)g->d_io;
+    cudaStream_t s = g->stream;
+    CUDA_TRY(cudaMemsetAsync(b, 0, t, s));
+    if (V) {
+        CUDA_TRY(cudaMemcpyAsync(b + o[0], ngid, 4u * V, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(b + o[1], rgid, 4u * V, cudaMemcpyHostToDevice, s));
+    }
+    if (A) CUDA_TRY(cudaMemcpyAsync(b + o[2], bkt, 4u * A, cudaMemcpyHostToDevice, s));
+    const double *ext = nullptr;
+    if (durations) {
+        // caller passes G + B entries; the count is only known on the device, so
+        // copy the maximum the caller may have supplied (sized by the shim)
+        CUDA_TRY(cudaMemcpyAsync(b + o[5], durations, 8 * NMx, cudaMemcpyHostToDevice, s));
+        ext = (const double *)(b + o[5]);
+    }
+    TimelineOut tl{};
+    if (want_tl) {
+        tl.c_id = (int32_t *)(b + o[6]); tl.c_start = (double *)(b + o[7]); tl.c_end = (double *)(b + o[8]);
+        tl.b_id = (int32_t *)(b + o[9]); tl.b_start = (double *)(b + o[10]); tl.b_end = (double *)(b + o[11]);
+        tl.n_c = (int32_t *)(b + o[12]); tl.n_b = (int32_t *)(b + o[13]);
+    }
+    int32_t *bad = (int32_t *)(b + o[15]);
+    st = launch(g, (int32_t *)(b + o[0]), (int32_t *)(b + o[1]), (int32_t *)(b + o[2]), 1, VB, precision,
+                (double *)(b + o[3]), (int32_t *)(b + o[4]), ext, tl, want_dur ? (double *)(b + o[14]) : nullptr, bad,
+                bad + 1, s, 1);
+    if (st) return st;
+    hout.resize(t);
+    CUDA_TRY(cudaMemcpyAsync(hout.data(), b, t, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 0; i < 16; i++) offs[i] = o[i];
+    return FO_OK;
+}
+
+int fo_simulate(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t gid_bound,
+                int32_t precision, const double *durations, int32_t *c_id, double *c_start, double *c_end,
+                int32_t *n_compute, int32_t *b_id, double *b_start, double *b_end, int32_t *n_comm, double *makespan,
+                int32_t *bad_node_out) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (!g->model_set && !durations) return fail(FO_INVALID_ARG, "no cost model set");
+    CUDA_TRY(cudaSetDevice(g->device));
+    std::vector<char> h;
+    size_t o[16];
+    int st = single(g, ngid, rgid, bkt, gid_bound, precision, durations, true, false, h, o);
+    if (st) return st;
+    int status = *(int32_t *)(h.data() + o[4]);
+    *makespan = *(double *)(h.data() + o[3]);
+    int nc = *(int32_t *)(h.data() + o[12]), nb = *(int32_t *)(h.data() + o[13]);
+    if (n_compute) *n_compute = nc;
+    if (n_comm) *n_comm = nb;
+    if (c_id) {
+        memcpy(c_id, h.data() + o[6], 4u * nc);
+        memcpy(c_start, h.data() + o[7], 8u * nc);
+        memcpy(c_end, h.data() + o[8], 8u * nc);
+    }
+    if (b_id) {
+        memcpy(b_id, h.data() + o[9], 4u * nb);
+        memcpy(b_start, h.data() + o[10], 8u * nb);
+        memcpy(b_end, h.data() + o[11], 8u * nb);
+    }
+    if (bad_node_out) *bad_node_out = *(int32_t *)(h.data() + o[15]);
+    if (status == 100) return fail(FO_UNSUPPORTED, "fused group larger than the device estimator scratch");
+    return status;
+}
+
+int fo_node_durations(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t gid_bound,
+                      int32_t precision, double *dur_out, int32_t *n_groups_out, int32_t *bad_node_out) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set");
+    CUDA_TRY(cudaSetDevice(g->device));
+    std::vector<char> h;
+    size_t o[16];
+    int st = single(g, ngid, rgid, bkt, gid_bound, precision, nullptr, false, true, h, o);
+    if (st) return st;
+    int G = *(int32_t *)(h.data() + o[15] + 4);
+    *n_groups_out = G;
+    // the number of buckets is the number of distinct bucket ids
+    std::vector<char> seen(g->A + 1, 0);
+    int B = 0;
+    for (int a = 0; a < g->A; a++)
+        if (bkt[a] >= 0 && bkt[a] < g->A && !seen[bkt[a]]) { seen[bkt[a]] = 1; B++; }
+    memcpy(dur_out, h.data() + o[14], 8u * (G + B));
+    if (bad_node_out) *bad_node_out = *(int32_t *)(h.data() + o[15]);
+    int status = *(int32_t *)(h.data() + o[4]);
+    if (status == 100) return fail(FO_UNSUPPORTED, "fused group larger than the device estimator scratch");
+    return status;
+}
+
+}  // extern "C"

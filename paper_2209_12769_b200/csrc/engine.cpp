@@ -1,0 +1,875 @@
+// engine.cpp -- native batch-expand and the lock-stepped backtracking search.
+//
+// * CPython random.Random restated (MT19937 + init_by_array + _randbelow),
+//   because every draw of the reference's search and rewrites goes through it
+//   (search.py:88, :119; rewrite.py:250).
+// * The three rewrites with the reference's choice enumeration order, id
+//   assignment and validity rule (rewrite.py:49-263, graph.py:505-512).
+// * Alg. 1 (search.py:84-155) for R independent seeds advanced in lock step:
+//   each round expands every active seed on host threads and scores all of
+//   their candidates in ONE device batch (score.cu), then replays the
+//   reference's accept/prune bookkeeping in method order.
+#include <cuda_runtime.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <queue>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "fo_internal.h"
+
+namespace fo {
+
+// ---------------------------------------------------------------------------
+// CPython random.Random
+
+struct PyRng {
+    uint32_t mt[624];
+    int mti = 625;
+
+    void init_genrand(uint32_t s) {
+        mt[0] = s;
+        for (int i = 1; i < 624; i++) mt[i] = 1812433253u * (mt[i - 1] ^ (mt[i - 1] >> 30)) + (uint32_t)i;
+        mti = 624;
+    }
+    // random_seed(int) -> init_by_array over the 32-bit words of |seed|
+    explicit PyRng(uint64_t seed) {
+        uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+        int klen = (seed >> 32) ? 2 : 1;
+        init_genrand(19650218u);
+        int i = 1, j = 0;
+        for (int k = std::max(624, klen); k; k--) {
+            mt[i] = (mt[i] ^ ((mt[i - 1] ^ (mt[i - 1] >> 30)) * 1664525u)) + key[j] + (uint32_t)j;
+            if (++i >= 624) { mt[0] = mt[623]; i = 1; }
+            if (++j >= klen) j = 0;
+        }
+        for (int k = 623; k; k--) {
+            mt[i] = (mt[i] ^ ((mt[i - 1] ^ (mt[i - 1] >> 30)) * 1566083941u)) - (uint32_t)i;
+            if (++i >= 624) { mt[0] = mt[623]; i = 1; }
+        }
+        mt[0] = 0x80000000u;
+    }
+    uint32_t next() {
+        if (mti >= 624) {
+            static const uint32_t mag[2] = {0u, 0x9908b0dfu};
+            int k = 0;
+            uint32_t y;
+            for (; k < 624 - 397; k++) {
+                y = (mt[k] & 0x80000000u) | (mt[k + 1] & 0x7fffffffu);
+                mt[k] = mt[k + 397] ^ (y >> 1) ^ mag[y & 1u];
+            }
+            for (; k < 623; k++) {
+                y = (mt[k] & 0x80000000u) | (mt[k + 1] & 0x7fffffffu);
+                mt[k] = mt[k - 227] ^ (y >> 1) ^ mag[y & 1u];
+            }
+            y = (mt[623] & 0x80000000u) | (mt[0] & 0x7fffffffu);
+            mt[623] = mt[396] ^ (y >> 1) ^ mag[y & 1u];
+            mti = 0;
+        }
+        uint32_t y = mt[mti++];
+        y ^= y >> 11;
+        y ^= (y << 7) & 0x9d2c5680u;
+        y ^= (y << 15) & 0xefc60000u;
+        y ^= y >> 18;
+        return y;
+    }
+    // _randbelow_with_getrandbits(n), n >= 1
+    uint32_t below(uint32_t n) {
+        int k = 32 - __builtin_clz(n);
+        uint32_t r = next() >> (32 - k);
+        while (r >= n) r = next() >> (32 - k);
+        return r;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// fusion state + derived index (graph.py:117-274)
+
+struct State {
+    std::vector<int32_t> ng, rg, bk;
+};
+
+enum { M_NONDUP = 0, M_DUP = 1, M_AR = 2 };
+
+struct Engine;
+
+struct Index {
+    int G = 0, B = 0;
+    std::vector<int32_t> gid, bid;      // sorted ids of groups / buckets
+    std::vector<int32_t> nn, rr, bki;   // per op / per AR: node index
+    std::vector<int32_t> mptr, mem;     // members per group (ascending op), all memberships
+    std::vector<uint8_t> mdup, compute_ok, has_dup, feeds_ar, has_rep;
+    std::vector<int32_t> sptr, succ, pptr, pred;  // contracted adjacency, sorted unique
+    std::vector<int32_t> bptr, bex;               // per bucket: export groups of members (sorted unique)
+};
+
+struct Engine {
+    const fo_graph *g;
+    int V, E, A, VB;  // VB: gid bound used for every state this engine emits
+    explicit Engine(const fo_graph *gr) : g(gr), V(gr->V), E(gr->E), A(gr->A), VB(2 * gr->V + 2) {}
+
+    State default_state() const {
+        State s;
+        s.ng.resize(V);
+        s.rg.assign(V, -1);
+        s.bk.resize(A);
+        for (int v = 0; v < V; v++) s.ng[v] = v;
+        for (int a = 0; a < A; a++) s.bk[a] = a;
+        return s;
+    }
+
+    // group ids -> dense node order; returns G.  gnode sized VB.
+    int number_groups(const State &s, std::vector<int32_t> &gnode, std::vector<int32_t> *gid) const {
+        gnode.assign(VB, 0);
+        for (int v = 0; v < V; v++) {
+            gnode[s.ng[v]] = 1;
+            if (s.rg[v] >= 0) gnode[s.rg[v]] = 1;
+        }
+        int G = 0;
+        if (gid) gid->clear();
+        for (int i = 0; i < VB; i++) {
+            if (gnode[i]) {
+                if (gid) gid->push_back(i);
+                gnode[i] = G++;
+            } else gnode[i] = -1;
+        }
+        return G;
+    }
+
+    void build(const State &s, Index &ix) const {
+        std::vector<int32_t> gnode;
+        ix.G = number_groups(s, gnode, &ix.gid);
+        const int G = ix.G;
+        ix.nn.resize(V);
+        ix.rr.resize(V);
+        for (int v = 0; v < V; v++) {
+            ix.nn[v] = gnode[s.ng[v]];
+            ix.rr[v] = s.rg[v] >= 0 ? gnode[s.rg[v]] : -1;
+        }
+        // members, ascending op index
+        ix.mptr.assign(G + 1, 0);
+        for (int v = 0; v < V; v++) {
+            ix.mptr[ix.nn[v] + 1]++;
+            if (ix.rr[v] >= 0) ix.mptr[ix.rr[v] + 1]++;
+        }
+        for (int i = 0; i < G; i++) ix.mptr[i + 1] += ix.mptr[i];
+        ix.mem.resize(ix.mptr[G]);
+        ix.mdup.resize(ix.mptr[G]);
+        std::vector<int32_t> cur(ix.mptr.begin(), ix.mptr.end() - 1);
+        for (int v = 0; v < V; v++) {
+            int x = ix.nn[v];
+            ix.mdup[cur[x]] = 0;
+            ix.mem[cur[x]++] = v;
+            if (ix.rr[v] >= 0) {
+                x = ix.rr[v];
+                ix.mdup[cur[x]] = 1;
+                ix.mem[cur[x]++] = v;
+            }
+        }
+        ix.compute_ok.assign(G, 1);
+        ix.has_dup.assign(G, 0);
+        ix.feeds_ar.assign(G, 0);
+        ix.has_rep.assign(G, 0);
+        for (int x = 0; x < G; x++)
+            for (int k = ix.mptr[x]; k < ix.mptr[x + 1]; k++) {
+                int v = ix.mem[k];
+                if (g->op_kind[v] != 0) ix.compute_ok[x] = 0;
+                if (ix.mdup[k]) ix.has_dup[x] = 1;
+                if (g->arp_ptr[v + 1] > g->arp_ptr[v]) ix.feeds_ar[x] = 1;
+                if (ix.rr[v] >= 0) ix.has_rep[x] = 1;  // some member has a replica (rewrite.py:116)
+            }
+        // contracted succs/preds over ALL edges (graph.py:161-179)
+        std::vector<int32_t> ps, pt;
+        ps.reserve(2 * E);
+        pt.reserve(2 * E);
+        for (int e = 0; e < E; e++) {
+            int sv = g->e_src[e], dv = g->e_dst[e];
+            int ex = ix.rr[sv] >= 0 ? ix.rr[sv] : ix.nn[sv];
+            int c0 = ix.nn[dv], c1 = ix.rr[dv];
+            if (c0 != ix.nn[sv] && c0 != ix.rr[sv]) { ps.push_back(ex); pt.push_back(c0); }
+            if (c1 >= 0 && c1 != ix.nn[sv] && c1 != ix.rr[sv]) { ps.push_back(ex); pt.push_back(c1); }
+        }
+        csr_unique(G, ps, pt, ix.sptr, ix.succ);
+        csr_unique(G, pt, ps, ix.pptr, ix.pred);
+        // buckets
+        std::vector<int32_t> bnode(A, -1);
+        ix.bid.clear();
+        {
+            std::vector<uint8_t> f(A, 0);
+            for (int a = 0; a < A; a++) f[s.bk[a]] = 1;
+            int B = 0;
+            for (int i = 0; i < A; i++)
+                if (f[i]) { bnode[i] = B++; ix.bid.push_back(i); }
+            ix.B = B;
+        }
+        ix.bki.resize(A);
+        std::vector<int32_t> bs, bt;
+        for (int a = 0; a < A; a++) {
+            ix.bki[a] = bnode[s.bk[a]];
+            int pv = g->ar_prod[a];
+            bs.push_back(ix.bki[a]);
+            bt.push_back(ix.rr[pv] >= 0 ? ix.rr[pv] : ix.nn[pv]);
+        }
+        csr_unique(ix.B, bs, bt, ix.bptr, ix.bex);
+    }
+
+    static void csr_unique(int n, const std::vector<int32_t> &src, const std::vector<int32_t> &dst,
+                           std::vector<int32_t> &ptr, std::vector<int32_t> &out) {
+        ptr.assign(n + 1, 0);
+        for (int32_t x : src) ptr[x + 1]++;
+        for (int i = 0; i < n; i++) ptr[i + 1] += ptr[i];
+        out.resize(src.size());
+        std::vector<int32_t> cur(ptr.begin(), ptr.end() - 1);
+        for (size_t i = 0; i < src.size(); i++) out[cur[src[i]]++] = dst[i];
+        int w = 0;
+        for (int i = 0; i < n; i++) {
+            int b = ptr[i], e = ptr[i + 1];
+            std::sort(out.begin() + b, out.begin() + e);
+            ptr[i] = w;
+            int last = -1;
+            for (int k = b; k < e; k++)
+                if (k == b || out[k] != last) { last = out[k]; out[w++] = last; }
+        }
+        ptr[n] = w;
+        out.resize(w);
+    }
+
+    // rewrite_candidate_ok (graph.py:505-512): Kahn over the joint schedule
+    // dependency multigraph (multiplicity does not change acyclicity).
+    bool valid(const State &s, std::vector<int32_t> &scratch_gnode) const {
+        int G = number_groups(s, scratch_gnode, nullptr);
+        std::vector<uint8_t> f(A, 0);
+        for (int a = 0; a < A; a++) f[s.bk[a]] = 1;
+        std::vector<int32_t> bnode(A, -1);
+        int B = 0;
+        for (int i = 0; i < A; i++)
+            if (f[i]) bnode[i] = B++;
+        const int N = G + B;
+        auto nn = [&](int v) { return scratch_gnode[s.ng[v]]; };
+        auto rr = [&](int v) { return s.rg[v] >= 0 ? scratch_gnode[s.rg[v]] : -1; };
+        std::vector<int32_t> from, to;
+        from.reserve(2 * E + A);
+        to.reserve(2 * E + A);
+        for (int e = 0; e < E; e++) {
+            int sv = g->e_src[e], dv = g->e_dst[e];
+            int c0 = nn(dv), c1 = rr(dv);
+            if (!g->agg[e]) {
+                int ns = nn(sv), rs = rr(sv), ex = rs >= 0 ? rs : ns;
+                if (c0 != ns && c0 != rs) { from.push_back(ex); to.push_back(c0); }
+                if (c1 >= 0 && c1 != ns && c1 != rs) { from.push_back(ex); to.push_back(c1); }
+            } else {
+                for (int q = g->arp_ptr[sv]; q < g->arp_ptr[sv + 1]; q++) {
+                    int bn = G + bnode[s.bk[g->arp[q]]];
+                    from.push_back(bn); to.push_back(c0);
+                    if (c1 >= 0) { from.push_back(bn); to.push_back(c1); }
+                }
+            }
+        }
+        for (int a = 0; a < A; a++) {
+            int pv = g->ar_prod[a];
+            int ex = rr(pv) >= 0 ? rr(pv) : nn(pv);
+            from.push_back(ex);
+            to.push_back(G + bnode[s.bk[a]]);
+        }
+        std::vector<int32_t> ptr(N + 1, 0), adj(from.size()), indeg(N, 0);
+        for (size_t i = 0; i < from.size(); i++) { ptr[from[i] + 1]++; indeg[to[i]]++; }
+        for (int i = 0; i < N; i++) ptr[i + 1] += ptr[i];
+        std::vector<int32_t> cur(ptr.begin(), ptr.end() - 1);
+        for (size_t i = 0; i < from.size(); i++) adj[cur[from[i]]++] = to[i];
+        std::vector<int32_t> stack;
+        stack.reserve(N);
+        for (int i = 0; i < N; i++)
+            if (!indeg[i]) stack.push_back(i);
+        int seen = 0;
+        while (!stack.empty()) {
+            int u = stack.back();
+            stack.pop_back();
+            seen++;
+            for (int k = ptr[u]; k < ptr[u + 1]; k++)
+                if (--indeg[adj[k]] == 0) stack.push_back(adj[k]);
+        }
+        return seen == N;
+    }
+
+    // fusible_pairs (rewrite.py:49-61) + DUP filter (rewrite.py:242-247)
+    int fusible_pairs(const Index &ix, bool dup, int want, int *og, int *pg) const {
+        int cnt = 0;
+        for (int x = 0; x < ix.G; x++) {
+            if (!ix.compute_ok[x]) continue;
+            for (int k = ix.pptr[x]; k < ix.pptr[x + 1]; k++) {
+                int p = ix.pred[k];
+                if (!ix.compute_ok[p] || (dup && ix.has_dup[p])) continue;
+                if (cnt == want) { *og = x; *pg = p; }
+                cnt++;
+            }
+        }
+        return cnt;
+    }
+
+    // bucket_pairs (rewrite.py:212-219) via neighbors_allreduce (rewrite.py:156-178)
+    int bucket_pairs(const Index &ix, int want, int *bo, int *bn) const {
+        std::vector<int32_t> stamp(ix.G, -1);
+        int cnt = 0;
+        for (int b = 0; b < ix.B; b++) {
+            for (int k = ix.bptr[b]; k < ix.bptr[b + 1]; k++) {
+                int x = ix.bex[k];
+                stamp[x] = b;
+                for (int q = ix.sptr[x]; q < ix.sptr[x + 1]; q++) stamp[ix.succ[q]] = b;
+                for (int q = ix.pptr[x]; q < ix.pptr[x + 1]; q++) stamp[ix.pred[q]] = b;
+            }
+            for (int o = 0; o < ix.B; o++) {
+                if (o == b) continue;
+                bool hit = false;
+                for (int k = ix.bptr[o]; k < ix.bptr[o + 1] && !hit; k++) hit = stamp[ix.bex[k]] == b;
+                if (!hit) continue;
+                if (cnt == want) { *bo = b; *bn = o; }
+                cnt++;
+            }
+        }
+        return cnt;
+    }
+
+    void compact(State &s) const {  // monotone relabel of group ids to 0..G-1
+        std::vector<int32_t> gnode;
+        number_groups(s, gnode, nullptr);
+        for (int v = 0; v < V; v++) {
+            s.ng[v] = gnode[s.ng[v]];
+            if (s.rg[v] >= 0) s.rg[v] = gnode[s.rg[v]];
+        }
+    }
+
+    // fuse_nondup (rewrite.py:64-96) / fuse_dup (rewrite.py:99-153)
+    bool fuse_ops(const State &s, const Index &ix, int og, int pg, bool dup, State &out,
+                  std::vector<int32_t> &scratch) const {
+        if (og == pg) return false;
+        for (int k = ix.mptr[pg]; k < ix.mptr[pg + 1]; k++) {  // groups share a member (rewrite.py:76-79)
+            int v = ix.mem[k];
+            if (ix.nn[v] == og || ix.rr[v] == og) return false;
+        }
+        if (!ix.compute_ok[og] || !ix.compute_ok[pg]) return false;
+        int32_t gidx = ix.gid[og], gidp = ix.gid[pg];
+        int32_t merged = std::min(gidx, gidp);
+        out = s;
+        if (dup) {
+            if (ix.has_rep[pg]) return false;  // rewrite.py:116-118
+            bool other = false;
+            for (int k = ix.sptr[pg]; k < ix.sptr[pg + 1]; k++) other |= ix.succ[k] != og;
+            if (other || ix.feeds_ar[pg]) {
+                int32_t replica = ix.gid[ix.G - 1] + 1;  // rewrite.py:138
+                if (replica >= VB) {
+                    compact(out);
+                    // ids changed monotonically: recompute merged / replica in the new labelling
+                    std::vector<int32_t> gnode;
+                    number_groups(s, gnode, nullptr);
+                    merged = std::min(gnode[gidx], gnode[gidp]);
+                    replica = ix.G;
+                }
+                for (int k = ix.mptr[og]; k < ix.mptr[og + 1]; k++) {
+                    int v = ix.mem[k];
+                    if (ix.mdup[k]) out.rg[v] = merged; else out.ng[v] = merged;
+                }
+                for (int k = ix.mptr[pg]; k < ix.mptr[pg + 1]; k++) {
+                    int v = ix.mem[k];
+                    out.ng[v] = merged;
+                    out.rg[v] = replica;
+                }
+                return valid(out, scratch);
+            }
+        }
+        for (int x : {og, pg})
+            for (int k = ix.mptr[x]; k < ix.mptr[x + 1]; k++) {
+                int v = ix.mem[k];
+                if (ix.mdup[k]) out.rg[v] = merged; else out.ng[v] = merged;
+            }
+        return valid(out, scratch);
+    }
+
+    // fuse_allreduce (rewrite.py:181-209)
+    bool fuse_ar(const State &s, const Index &ix, int bo, int bn, State &out, std::vector<int32_t> &scratch) const {
+        int32_t merged = std::min(ix.bid[bo], ix.bid[bn]);
+        out = s;
+        for (int a = 0; a < A; a++)
+            if (ix.bki[a] == bo || ix.bki[a] == bn) out.bk[a] = merged;
+        return valid(out, scratch);
+    }
+
+    // random_apply (rewrite.py:222-263); state updated in place
+    bool random_apply(State &s, int method, int n, PyRng &rng) const {
+        bool applied = false;
+        Index ix;
+        State cand;
+        std::vector<int32_t> scratch;
+        for (int it = 0; it < n; it++) {
+            build(s, ix);
+            int x = -1, y = -1;
+            int cnt = method == M_AR ? bucket_pairs(ix, -1, &x, &y) : fusible_pairs(ix, method == M_DUP, -1, &x, &y);
+            if (cnt == 0) break;
+            int idx = (int)rng.below((uint32_t)cnt);
+            if (method == M_AR) bucket_pairs(ix, idx, &x, &y);
+            else fusible_pairs(ix, method == M_DUP, idx, &x, &y);
+            bool ok = method == M_AR ? fuse_ar(s, ix, x, y, cand, scratch)
+                                     : fuse_ops(s, ix, x, y, method == M_DUP, cand, scratch);
+            if (ok) {
+                std::swap(s, cand);
+                applied = true;
+            }
+        }
+        return applied;
+    }
+
+    // canonical state hash: the state is a set of (members, duplicated) group
+    // tuples plus a set of bucket member tuples (graph.py:559-580)
+    static uint64_t mix(uint64_t x) {
+        x += 0x9e3779b97f4a7c15ull;
+        x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+        x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+        return x ^ (x >> 31);
+    }
+    uint64_t hash(const State &s) const {
+        // group content hashes accumulated per group id (ops visited ascending)
+        std::vector<uint64_t> acc(VB, 0);
+        std::vector<uint8_t> used(VB, 0);
+        for (int v = 0; v < V; v++) {
+            int x = s.ng[v];
+            acc[x] = mix(acc[x] ^ (uint64_t)(2 * v + 2));
+            used[x] = 1;
+            if (s.rg[v] >= 0) {
+                x = s.rg[v];
+                acc[x] = mix(acc[x] ^ (uint64_t)(2 * v + 3));
+                used[x] = 1;
+            }
+        }
+        uint64_t h = 0x6a09e667f3bcc909ull;
+        for (int i = 0; i < VB; i++)
+            if (used[i]) h += mix(acc[i] + 0x3c6ef372fe94f82bull);
+        std::vector<uint64_t> bacc(A, 0);
+        std::vector<uint8_t> bused(A, 0);
+        for (int a = 0; a < A; a++) {
+            int b = s.bk[a];
+            bacc[b] = mix(bacc[b] ^ (uint64_t)(a + 1));
+            bused[b] = 1;
+        }
+        for (int b = 0; b < A; b++)
+            if (bused[b]) h += mix(bacc[b] + 0xa54ff53a5f1d36f1ull);
+        return h;
+    }
+
+    bool load_state(const int32_t *ng, const int32_t *rg, const int32_t *bk, State &s) const {
+        s = default_state();
+        if (!ng) return true;
+        std::vector<int32_t> ids;
+        for (int v = 0; v < V; v++) {
+            if (ng[v] < 0 || rg[v] < -1) return false;
+            ids.push_back(ng[v]);
+            if (rg[v] >= 0) ids.push_back(rg[v]);
+        }
+        std::sort(ids.begin(), ids.end());
+        ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+        auto rank = [&](int32_t x) { return (int32_t)(std::lower_bound(ids.begin(), ids.end(), x) - ids.begin()); };
+        for (int v = 0; v < V; v++) {
+            s.ng[v] = rank(ng[v]);
+            s.rg[v] = rg[v] >= 0 ? rank(rg[v]) : -1;
+        }
+        for (int a = 0; a < A; a++) {
+            if (bk[a] < 0 || bk[a] >= A) return false;
+            s.bk[a] = bk[a];
+        }
+        return true;
+    }
+};
+
+}  // namespace fo
+
+using namespace fo;
+
+extern "C" {
+
+int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *base_rgid, const int32_t *base_bkt,
+                       const uint64_t *seeds, int32_t K, int32_t beta, int32_t methods_mask, int32_t n_threads,
+                       int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *gid_bound_out) {
+    if (!g || !seeds || K < 0 || beta < 0) return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State base;
+    if (!eng.load_state(base_ngid, base_rgid, base_bkt, base)) return fail(FO_INVALID_ARG, "bad base state");
+    if (n_threads <= 0) n_threads = omp_get_max_threads();
+    const int V = g->V, A = g->A;
+#pragma omp parallel for num_threads(n_threads) schedule(dynamic, 1)
+    for (int k = 0; k < K; k++) {
+        PyRng rng(seeds[k]);
+        State s = base;
+        for (int m = 0; m < 3; m++) {
+            if (!(methods_mask & (1 << m))) continue;
+            int n = (int)rng.below((uint32_t)beta + 1);
+            eng.random_apply(s, m, n, rng);
+        }
+        std::copy(s.ng.begin(), s.ng.end(), ngid_out + (int64_t)k * V);
+        std::copy(s.rg.begin(), s.rg.end(), rgid_out + (int64_t)k * V);
+        std::copy(s.bk.begin(), s.bk.end(), bkt_out + (int64_t)k * A);
+    }
+    if (gid_bound_out) *gid_bound_out = eng.VB;
+    return FO_OK;
+}
+
+int fo_random_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int32_t method, int32_t n,
+                    uint32_t *mt_state, int32_t *applied_out) {
+    if (!g || !ngid || !rgid || !bkt || !mt_state || method < 0 || method > 2 || n < 0)
+        return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State s;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    PyRng rng(0);
+    std::copy(mt_state, mt_state + 624, rng.mt);
+    rng.mti = (int)mt_state[624];
+    bool applied = eng.random_apply(s, method, n, rng);
+    std::copy(rng.mt, rng.mt + 624, mt_state);
+    mt_state[624] = (uint32_t)rng.mti;
+    std::copy(s.ng.begin(), s.ng.end(), ngid);
+    std::copy(s.rg.begin(), s.rg.end(), rgid);
+    std::copy(s.bk.begin(), s.bk.end(), bkt);
+    if (applied_out) *applied_out = applied ? 1 : 0;
+    return FO_OK;
+}
+
+int fo_expand_all(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t cap,
+                  int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *n_out) {
+    if (!g || !n_out) return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State s;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    Index ix;
+    eng.build(s, ix);
+    std::vector<State> out;
+    State cand;
+    std::vector<int32_t> scratch;
+    // exhaustive_search's per-graph enumeration (search.py:185-206)
+    int x = -1, y = -1;
+    int np_ = eng.fusible_pairs(ix, false, -1, &x, &y);
+    for (int i = 0; i < np_; i++) {
+        eng.fusible_pairs(ix, false, i, &x, &y);
+        if (eng.fuse_ops(s, ix, x, y, false, cand, scratch)) out.push_back(cand);
+        bool other = ix.feeds_ar[y];
+        for (int k = ix.sptr[y]; k < ix.sptr[y + 1]; k++) other |= ix.succ[k] != x;
+        if (other && !ix.has_rep[y] && eng.fuse_ops(s, ix, x, y, true, cand, scratch)) out.push_back(cand);
+    }
+    int nb = eng.bucket_pairs(ix, -1, &x, &y);
+    for (int i = 0; i < nb; i++) {
+        eng.bucket_pairs(ix, i, &x, &y);
+        if (eng.fuse_ar(s, ix, x, y, cand, scratch)) out.push_back(cand);
+    }
+    *n_out = (int32_t)out.size();
+    if ((int)out.size() > cap) return fail(FO_INVALID_ARG, "output capacity too small");
+    const int V = g->V, A = g->A;
+    for (size_t k = 0; k < out.size(); k++) {
+        std::copy(out[k].ng.begin(), out[k].ng.end(), ngid_out + k * V);
+        std::copy(out[k].rg.begin(), out[k].rg.end(), rgid_out + k * V);
+        std::copy(out[k].bk.begin(), out[k].bk.end(), bkt_out + k * A);
+    }
+    return FO_OK;
+}
+
+int fo_state_hash(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
+                  uint64_t *hash_out) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    Engine eng(g);
+    for (int k = 0; k < K; k++) {
+        State s;
+        if (!eng.load_state(ngid + (int64_t)k * g->V, rgid + (int64_t)k * g->V, bkt + (int64_t)k * g->A, s))
+            return fail(FO_INVALID_ARG, "bad state");
+        hash_out[k] = eng.hash(s);
+    }
+    return FO_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// lock-stepped backtracking search (search.py:84-155)
+
+struct fo_search {
+    fo_graph *g = nullptr;
+    fo_search_cfg cfg{};
+    Engine *eng = nullptr;
+    struct QE {
+        double c;
+        int64_t seq;
+        uint64_t h;
+        int32_t slot;
+        bool operator>(const QE &o) const { return c != o.c ? c > o.c : seq > o.seq; }
+    };
+    struct Seed {
+        PyRng rng{0};
+        std::vector<State> pool;
+        std::priority_queue<QE, std::vector<QE>, std::greater<QE>> queue;
+        std::unordered_set<uint64_t> seen;
+        std::unordered_map<uint64_t, double> cache;
+        int64_t seq = 1, steps = 0, evaluated = 0, enqueued = 0;
+        int unchanged = 0;
+        double best = 0.0;
+        int32_t best_slot = 0;
+        bool active = true;
+        int status = FO_OK;
+        std::vector<fo_trace_rec> trace;
+        // per-round scratch
+        QE cur{};
+        int ncand = 0;
+        State cand[3];
+        int meth[3];
+        uint64_t h[3];
+        int64_t batch_pos[3];
+    };
+    std::vector<Seed> seeds;
+    // device batch buffers
+    int32_t *d_buf = nullptr;
+    size_t d_cap = 0;
+    int32_t *h_buf = nullptr;
+    size_t h_cap = 0;
+    double device_ms = 0, expand_ms = 0;
+    int64_t scored = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool started = false;
+};
+
+static int search_score(fo_search *S, int n, std::vector<double> &cost, std::vector<int32_t> &status) {
+    fo_graph *g = S->g;
+    const int V = g->V, A = g->A;
+    size_t W = 2 * (size_t)V + A;
+    size_t need_i = W * n;
+    size_t cost_off = (need_i * 4 + 255) & ~size_t(255);
+    size_t need = cost_off + 16 * (size_t)n + 256;
+    if (need > S->d_cap) {
+        if (S->d_buf) cudaFree(S->d_buf);
+        S->d_buf = nullptr;
+        if (cudaMalloc(&S->d_buf, need) != cudaSuccess) return fail(FO_CUDA_ERROR, "search batch alloc");
+        S->d_cap = need;
+    }
+    char *db = (char *)S->d_buf;
+    int32_t *dn = (int32_t *)db, *dr = dn + (size_t)V * n, *dk = dr + (size_t)V * n;
+    double *dc = (double *)(db + cost_off);
+    int32_t *ds = (int32_t *)(dc + n);
+    cudaStream_t st = g->stream;
+    if (cudaMemcpyAsync(db, S->h_buf, need_i * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return fail(FO_CUDA_ERROR, "search batch H2D");
+    cudaEventRecord(S->ev0, st);
+    int rc = score_device(g, dn, dr, dk, n, S->eng->VB, S->cfg.precision, dc, ds, st);
+    if (rc) return rc;
+    cudaEventRecord(S->ev1, st);
+    cost.resize(n);
+    status.resize(n);
+    cudaMemcpyAsync(cost.data(), dc, 8 * (size_t)n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(status.data(), ds, 4 * (size_t)n, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(FO_CUDA_ERROR, "search batch sync");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, S->ev0, S->ev1);
+    S->device_ms += ms;
+    S->scored += n;
+    return FO_OK;
+}
+
+static int32_t *stage(fo_search *S, size_t slots) {
+    size_t W = 2 * (size_t)S->g->V + S->g->A;
+    if (slots * W > S->h_cap) {
+        if (S->h_buf) cudaFreeHost(S->h_buf);
+        S->h_buf = nullptr;
+        size_t cap = std::max(slots * W, S->h_cap * 2);
+        if (cudaMallocHost(&S->h_buf, cap * 4) != cudaSuccess) return nullptr;
+        S->h_cap = cap;
+    }
+    return S->h_buf;
+}
+
+// write candidate j of the batch (SoA layout [ng * n | rg * n | bk * n])
+static void put(fo_search *S, int n, int j, const State &s) {
+    const int V = S->g->V, A = S->g->A;
+    std::copy(s.ng.begin(), s.ng.end(), S->h_buf + (size_t)j * V);
+    std::copy(s.rg.begin(), s.rg.end(), S->h_buf + (size_t)V * n + (size_t)j * V);
+    std::copy(s.bk.begin(), s.bk.end(), S->h_buf + (size_t)2 * V * n + (size_t)j * A);
+}
+
+extern "C" {
+
+int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seeds, int32_t R, const int32_t *ngid0,
+                     const int32_t *rgid0, const int32_t *bkt0, fo_search **out) {
+    if (!g || !cfg || !seeds || R <= 0 || !out) return fail(FO_INVALID_ARG, "bad arguments");
+    if (cfg->alpha < 1 || cfg->beta < 1 || cfg->max_unchanged < 1 || !(cfg->methods_mask & 7))
+        return fail(FO_INVALID_ARG, "invalid search config (search.py:53-61)");
+    if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set");
+    fo_search *S = new fo_search();
+    S->g = g;
+    S->cfg = *cfg;
+    S->eng = new Engine(g);
+    State s0;
+    if (!S->eng->load_state(ngid0, rgid0, bkt0, s0)) { delete S->eng; delete S; return fail(FO_INVALID_ARG, "bad start state"); }
+    S->seeds.resize(R);
+    uint64_t h0 = S->eng->hash(s0);
+    for (int r = 0; r < R; r++) {
+        auto &sd = S->seeds[r];
+        sd.rng = PyRng(seeds[r]);
+        sd.pool.push_back(s0);
+        sd.seen.insert(h0);
+        sd.cur.h = h0;
+    }
+    cudaSetDevice(g->device);
+    cudaEventCreate(&S->ev0);
+    cudaEventCreate(&S->ev1);
+    *out = S;
+    return FO_OK;
+}
+
+int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
+    if (!S) return fail(FO_INVALID_ARG, "null search");
+    fo_graph *g = S->g;
+    std::lock_guard<std::mutex> lk(g->mu);
+    cudaSetDevice(g->device);
+    const int R = (int)S->seeds.size();
+    std::vector<double> cost;
+    std::vector<int32_t> status;
+    if (!S->started) {  // eval_cost(g0) once per seed (search.py:101-102); same state -> one score
+        if (!stage(S, 1)) return fail(FO_CUDA_ERROR, "pinned alloc");
+        put(S, 1, 0, S->seeds[0].pool[0]);
+        int rc = search_score(S, 1, cost, status);
+        if (rc) return rc;
+        for (auto &sd : S->seeds) {
+            sd.status = status[0];
+            if (status[0]) { sd.active = false; continue; }
+            sd.best = cost[0];
+            sd.evaluated = 1;
+            sd.cache[sd.cur.h] = cost[0];
+            sd.queue.push({cost[0], 0, sd.cur.h, 0});
+        }
+        S->started = true;
+    }
+    // expand: every active seed pops and generates its step's candidates
+    auto t0 = std::chrono::steady_clock::now();
+    const Engine &eng = *S->eng;
+    int nthreads = S->cfg.n_threads > 0 ? S->cfg.n_threads : omp_get_max_threads();
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
+    for (int r = 0; r < R; r++) {
+        auto &sd = S->seeds[r];
+        sd.ncand = 0;
+        if (!sd.active) continue;
+        if (sd.queue.empty() || sd.unchanged >= S->cfg.max_unchanged) { sd.active = false; continue; }
+        sd.cur = sd.queue.top();
+        sd.queue.pop();
+        sd.steps++;
+        for (int m = 0; m < 3; m++) {
+            if (!(S->cfg.methods_mask & (1 << m))) continue;
+            int n = (int)sd.rng.below((uint32_t)S->cfg.beta + 1);
+            int j = sd.ncand++;
+            sd.cand[j] = sd.pool[sd.cur.slot];
+            bool applied = eng.random_apply(sd.cand[j], m, n, sd.rng);
+            sd.meth[j] = m;
+            sd.h[j] = applied ? eng.hash(sd.cand[j]) : sd.cur.h;
+        }
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    S->expand_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    // batch every candidate whose cost is not cached (dedupe within a step)
+    int n = 0;
+    for (auto &sd : S->seeds)
+        for (int j = 0; j < sd.ncand; j++) {
+            sd.batch_pos[j] = -1;
+            if (sd.cache.count(sd.h[j])) continue;
+            bool dup = false;
+            for (int q = 0; q < j; q++)
+                if (sd.h[q] == sd.h[j] && sd.batch_pos[q] >= 0) { sd.batch_pos[j] = sd.batch_pos[q]; dup = true; }
+            if (!dup) sd.batch_pos[j] = n++;
+        }
+    if (n > 0) {
+        if (!stage(S, n)) return fail(FO_CUDA_ERROR, "pinned alloc");
+        for (auto &sd : S->seeds)
+            for (int j = 0; j < sd.ncand; j++)
+                if (sd.batch_pos[j] >= 0) put(S, n, (int)sd.batch_pos[j], sd.cand[j]);
+        int rc = search_score(S, n, cost, status);
+        if (rc) return rc;
+    }
+    // replay the accept / prune bookkeeping in method order (search.py:120-146)
+    int active = 0;
+    for (int r = 0; r < R; r++) {
+        auto &sd = S->seeds[r];
+        bool requeued = false;
+        for (int j = 0; j < sd.ncand; j++) {
+            double c;
+            auto it = sd.cache.find(sd.h[j]);
+            if (it != sd.cache.end()) c = it->second;
+            else {
+                int p = (int)sd.batch_pos[j];
+                if (status[p]) { sd.status = status[p]; sd.active = false; break; }
+                c = cost[p];
+                sd.cache[sd.h[j]] = c;
+                sd.evaluated++;
+            }
+            int slot = -1;
+            if (c < sd.best) {
+                sd.best = c;
+                sd.pool.push_back(sd.cand[j]);
+                slot = (int)sd.pool.size() - 1;
+                sd.best_slot = slot;
+                sd.unchanged = 0;
+            } else sd.unchanged++;
+            int entered = 0;
+            if (c <= S->cfg.alpha * sd.best) {
+                bool push = false;
+                if (!sd.seen.count(sd.h[j])) { sd.seen.insert(sd.h[j]); push = true; sd.enqueued++; }
+                else if (sd.h[j] == sd.cur.h && !requeued) { push = true; requeued = true; }
+                if (push) {
+                    if (slot < 0) {
+                        if (sd.h[j] == sd.cur.h) slot = sd.cur.slot;
+                        else { sd.pool.push_back(sd.cand[j]); slot = (int)sd.pool.size() - 1; }
+                    }
+                    sd.queue.push({c, sd.seq++, sd.h[j], slot});
+                    entered = 1;
+                }
+            }
+            sd.trace.push_back({(int32_t)sd.steps, sd.meth[j], c, sd.best, (int32_t)sd.queue.size(), entered});
+        }
+        if (sd.active) active++;
+        if (best_cost_out) best_cost_out[r] = sd.best;
+    }
+    *active_out = active;
+    return FO_OK;
+}
+
+int fo_search_result(fo_search *S, int32_t r, double *best_cost, int64_t *counters4, int32_t *best_ngid,
+                     int32_t *best_rgid, int32_t *best_bkt, fo_trace_rec *trace, int64_t trace_cap) {
+    if (!S || r < 0 || r >= (int)S->seeds.size()) return fail(FO_INVALID_ARG, "bad search index");
+    auto &sd = S->seeds[r];
+    if (best_cost) *best_cost = sd.best;
+    if (counters4) {
+        counters4[0] = sd.steps;
+        counters4[1] = sd.evaluated;
+        counters4[2] = sd.enqueued;
+        counters4[3] = (int64_t)sd.trace.size();
+    }
+    const State &b = sd.pool[sd.best_slot];
+    if (best_ngid) std::copy(b.ng.begin(), b.ng.end(), best_ngid);
+    if (best_rgid) std::copy(b.rg.begin(), b.rg.end(), best_rgid);
+    if (best_bkt) std::copy(b.bk.begin(), b.bk.end(), best_bkt);
+    if (trace)
+        for (int64_t i = 0; i < (int64_t)sd.trace.size() && i < trace_cap; i++) trace[i] = sd.trace[i];
+    return sd.status;
+}
+
+int fo_search_timing(fo_search *S, double *device_ms, double *expand_ms, int64_t *scored) {
+    if (!S) return fail(FO_INVALID_ARG, "null search");
+    if (device_ms) *device_ms = S->device_ms;
+    if (expand_ms) *expand_ms = S->expand_ms;
+    if (scored) *scored = S->scored;
+    return FO_OK;
+}
+
+int fo_search_destroy(fo_search *S) {
+    if (!S) return FO_OK;
+    if (S->d_buf) cudaFree(S->d_buf);
+    if (S->h_buf) cudaFreeHost(S->h_buf);
+    if (S->ev0) cudaEventDestroy(S->ev0);
+    if (S->ev1) cudaEventDestroy(S->ev1);
+    delete S->eng;
+    delete S;
+    return FO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// Internal declarations shared by the CUDA scoring kernels (score.cu), the
+// C-ABI layer (capi.cu) and the native batch-expand / search engine
+// (engine.cpp).  Not part of the public ABI (include/disco_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/disco_b200.h"
+
+namespace fo {
+
+constexpr int kHidden = 32;  // lane = hidden channel in the message-passing kernel
+
+// Device-side view of one graph + cost model, passed by value to kernels.
+struct DGraph {
+    int32_t V, E, A;
+    // static graph (SoA, build_graph order)
+    const int32_t *e_src, *e_dst;
+    const int64_t *e_bytes;
+    const uint8_t *e_agg;       // _consumes_aggregate (graph.py:225-235)
+    const int32_t *in_ptr, *in_e;   // edge indices by destination op
+    const int32_t *out_ptr, *out_e; // edge indices by source op
+    const int32_t *arp_ptr, *arp;   // AllReduces by producer op
+    const int32_t *ar_prod;
+    const int64_t *ar_bytes;
+    const uint8_t *op_kind;
+    const double *op_prof;      // lookup(profile, op) or NaN
+    const double *op_compute;   // OpNode.compute_us or NaN
+    const int64_t *op_out, *op_in;
+    // message passing (lane = channel; hidden padded to 32 with zeros)
+    const float *H0f;           // [V][32]  X_std @ W_emb^T per op (estimator.py:369)
+    const double *H0d;
+    const float *Wf;            // packed transposed weights, see mp_layout()
+    const double *Wd;
+    int32_t layers;
+    // cost model
+    int32_t provider, variant;
+    double C, D, launch, mem, out_scale;
+    double lin_w[12], lin_b, agg_mean[12], agg_std[12];
+    int32_t lin_norm;
+    int32_t pairs_max;          // bound on contracted dependency pairs per candidate
+};
+
+// Packed message-passing weights (float or double), all transposed so lane c
+// reads element [k][c]:  W_l^T (L x 32 x 32) | W_r^T | A1^T | A2^T | c1 | c2 | a3 | c3
+struct MpLayout {
+    int64_t wl, wr, a1, a2, c1, c2, a3, c3, total;
+};
+__host__ __device__ inline MpLayout mp_layout(int layers) {
+    MpLayout m;
+    m.wl = 0;
+    m.wr = (int64_t)layers * 1024;
+    m.a1 = m.wr + 1024;
+    m.a2 = m.a1 + 1024;
+    m.c1 = m.a2 + 1024;
+    m.c2 = m.c1 + 32;
+    m.a3 = m.c2 + 32;
+    m.c3 = m.a3 + 32;
+    m.total = m.c3 + 32;
+    return m;
+}
+
+// Per-warp workspace (one candidate at a time), byte offsets.
+struct WsLayout {
+    int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, p2ng,
+        p2nb, heapg, heapb, dur, fused, gptr, gmem, msort, lidx, nbptr, nb, H, P, gint, gin, gout, vis, zl;
+    int64_t total;
+};
+WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max);
+
+struct TimelineOut {
+    int32_t *c_id;
+    double *c_start, *c_end;
+    int32_t *n_c;
+    int32_t *b_id;
+    double *b_start, *b_end;
+    int32_t *n_b;
+};
+
+// Kernel launch (score.cu).  ext_dur / tl / dur_out / bad_out are optional and
+// only used with K == 1.
+cudaError_t launch_score(const DGraph &g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K,
+                         int VB, int precision, char *ws, const WsLayout &L, int n_slots, int grid, int warps,
+                         double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
+                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream);
+int score_warps_per_block();
+int score_blocks_per_sm(int precision);
+
+}  // namespace fo
+
+// Host-side handle behind the opaque fo_graph.
+struct fo_graph {
+    int device = 0;
+    int V = 0, E = 0, A = 0;
+    // host copies
+    std::vector<int32_t> op_kind, e_src, e_dst, ar_prod;
+    std::vector<int64_t> op_out, op_in, e_bytes, ar_bytes;
+    std::vector<double> op_prof, op_compute;
+    std::vector<int32_t> in_ptr, in_e, out_ptr, out_e, arp_ptr, arp;
+    std::vector<uint8_t> agg;
+    int32_t pairs_max = 0;
+    // device buffers
+    void *d_static = nullptr;  // one allocation for the static graph
+    void *d_model = nullptr;   // H0 + weights
+    fo::DGraph dg{};
+    bool model_set = false;
+    // scoring workspace
+    char *d_ws = nullptr;
+    size_t ws_bytes = 0;
+    // host API staging
+    void *d_io = nullptr;
+    size_t io_bytes = 0;
+    void *h_pinned = nullptr;
+    size_t pinned_bytes = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 0;
+    std::mutex mu;
+};
+
+namespace fo {
+void set_error(const std::string &msg);
+int fail(int status, const std::string &msg);
+// Ensure the handle's workspace can hold `slots` warps for gid bound VB.
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L);
+// Score K device-resident candidates (used by fo_score and the search engine).
+int score_device(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K, int VB,
+                 int precision, double *cost, int32_t *status, cudaStream_t stream);
+}  // namespace fo

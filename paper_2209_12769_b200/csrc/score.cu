@@ -1,0 +1,854 @@
+// score.cu -- the fused candidate-scoring kernel for sm_100a.
+//
+// One warp scores one candidate fusion state end to end, persistently looping
+// over candidates (candidate k -> warp k mod nwarps):
+//
+//   K1 pack/contract   group numbering, per-group tie-break keys, bucket sizes
+//                      and the contracted schedule DAG as a successor CSR with
+//                      multiplicities (graph.py:117-274)                   [warp-parallel]
+//   K2 estimate        per fused group: message passing with lane = hidden
+//                      channel (estimator.py:321-389), or the analytic /
+//                      linear / hardware-oracle closed forms          [warp-parallel]
+//   K3 simulate        the two-lane discrete-event loop of simulator.py:53-140
+//                      with (rt, tiebreak, id) ready keys            [lane 0, fp64]
+//
+// fp64 schedule arithmetic (max and +) is bit-exact against the reference;
+// the file is compiled with -fmad=false so no multiply-add is contracted
+// except the explicit fma() in the message-passing transforms.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include "fo_internal.h"
+
+namespace fo {
+
+#define FULL 0xffffffffu
+constexpr int kWarps = 4;          // warps per block
+constexpr int kMpCap = 2048;       // max fused-group size held in the MP scratch
+constexpr int kRetryLarge = 100;   // internal status: group larger than kMpCap
+
+static inline int64_t align8(int64_t x) { return (x + 7) & ~int64_t(7); }
+
+WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max) {
+    WsLayout L{};
+    int64_t GM = (int64_t)(VB < 2 * V ? VB : 2 * V) + 1;
+    int64_t NM = GM + A + 1;
+    int64_t cap = V < kMpCap ? V : kMpCap;
+    int64_t o = 0;
+    auto take = [&](int64_t bytes) { int64_t r = o; o = align8(o + bytes); return r; };
+    L.gmap = take(4 * (int64_t)VB);
+    L.bmap = take(4 * (int64_t)A);
+    L.g2id = take(4 * GM);
+    L.b2id = take(4 * (int64_t)A);
+    L.nn = take(4 * (int64_t)V);
+    L.rr = take(4 * (int64_t)V);
+    L.bki = take(4 * (int64_t)A);
+    L.gmin = take(4 * GM);
+    L.gcnt = take(4 * GM);
+    L.bmin = take(4 * (int64_t)A);
+    L.btot = take(8 * (int64_t)A);
+    L.indeg = take(4 * NM);
+    L.scnt = take(4 * (NM + 1));
+    L.sptr = take(4 * (NM + 1));
+    L.succ = take(4 * (int64_t)(pairs_max + 1));
+    L.prank = take(4 * NM);
+    L.p2ng = take(4 * (2 * (int64_t)V + 1));
+    L.p2nb = take(4 * (int64_t)(A + 1));
+    L.heapg = take(8 * GM);
+    L.heapb = take(8 * (int64_t)(A + 1));
+    L.dur = take(8 * NM);
+    L.fused = take(4 * GM);
+    L.gptr = take(4 * (GM + 1));
+    L.gmem = take(4 * (2 * (int64_t)V + 1));
+    L.msort = take(4 * (cap + 1));
+    L.lidx = take(4 * (int64_t)V);
+    L.nbptr = take(4 * (cap + 1));
+    L.nb = take(4 * (2 * (int64_t)E + 1));
+    L.H = take(8 * cap * kHidden);
+    L.P = take(8 * cap * kHidden);
+    L.gint = take(8 * GM);
+    L.gin = take(8 * GM);
+    L.gout = take(8 * GM);
+    L.vis = take(4 * (int64_t)V);
+    L.zl = take(4 * NM);
+    L.total = align8(o) + 128;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Flags (0/1) in arr[0..n) -> ranks; inv[rank] = i.  Returns the count.
+__device__ int warp_rank_flags(int *arr, int *inv, int n, int lane) {
+    int carry = 0;
+    for (int base = 0; base < n; base += 32) {
+        int i = base + lane;
+        int f = (i < n) ? arr[i] : 0;
+        unsigned m = __ballot_sync(FULL, f != 0);
+        int r = carry + __popc(m & lanemask_lt());
+        if (f) { arr[i] = r; inv[r] = i; }
+        carry += __popc(m);
+    }
+    __syncwarp();
+    return carry;
+}
+
+// Exclusive scan of in[0..n) into out[0..n]; returns the total.
+__device__ int warp_exscan(const int *in, int *out, int n, int lane) {
+    int carry = 0;
+    for (int base = 0; base < n; base += 32) {
+        int i = base + lane;
+        int x = (i < n) ? in[i] : 0;
+        int v = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int y = __shfl_up_sync(FULL, v, d);
+            if (lane >= d) v += y;
+        }
+        if (i < n) out[i] = carry + v - x;
+        carry += __shfl_sync(FULL, v, 31);
+    }
+    if (lane == 0) out[n] = carry;
+    __syncwarp();
+    return carry;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    return v;
+}
+
+// numpy logaddexp(0, z) (estimator.py:297-298)
+__device__ __forceinline__ double softplus_d(double z) {
+    if (z == 0.0) return 0.6931471805599453;
+    if (z > 0.0) return __dadd_rn(z, log1p(exp(-z)));
+    return log1p(exp(z));
+}
+
+// ---------------------------------------------------------------------------
+// binary heaps of packed u64 keys (lane 0 only)
+
+__device__ __forceinline__ void heap_push(unsigned long long *h, int &n, unsigned long long k) {
+    int i = n++;
+    while (i > 0) {
+        int p = (i - 1) >> 1;
+        unsigned long long pk = h[p];
+        if (pk <= k) break;
+        h[i] = pk;
+        i = p;
+    }
+    h[i] = k;
+}
+__device__ __forceinline__ unsigned long long heap_pop(unsigned long long *h, int &n) {
+    unsigned long long top = h[0];
+    unsigned long long k = h[--n];
+    int i = 0;
+    for (;;) {
+        int l = 2 * i + 1;
+        if (l >= n) break;
+        unsigned long long lk = h[l];
+        int r = l + 1;
+        if (r < n) {
+            unsigned long long rk = h[r];
+            if (rk < lk) { lk = rk; l = r; }
+        }
+        if (k <= lk) break;
+        h[i] = lk;
+        i = l;
+    }
+    if (n > 0) h[i] = k;
+    return top;
+}
+
+// ---------------------------------------------------------------------------
+// message-passing forward for one fused group (estimator.py:363-389),
+// lane = hidden channel.  mem[0..n) sorted op indices of the members.
+
+template <typename T>
+struct MpW;
+template <>
+struct MpW<float> {
+    static __device__ __forceinline__ const float *W(const DGraph &g) { return g.Wf; }
+    static __device__ __forceinline__ const float *H0(const DGraph &g) { return g.H0f; }
+};
+template <>
+struct MpW<double> {
+    static __device__ __forceinline__ const double *W(const DGraph &g) { return g.Wd; }
+    static __device__ __forceinline__ const double *H0(const DGraph &g) { return g.H0d; }
+};
+
+template <typename T>
+__device__ __forceinline__ T fmaT(T a, T b, T c);
+template <>
+__device__ __forceinline__ float fmaT<float>(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+template <>
+__device__ __forceinline__ double fmaT<double>(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// dense 32x32 transform: out[c] = sum_k x[k] * Wt[k][c]  (x distributed over lanes)
+template <typename T>
+__device__ __forceinline__ T mat32(const T *__restrict__ Wt, T x, int lane) {
+    T acc = T(0);
+#pragma unroll 8
+    for (int k = 0; k < 32; k++) acc = fmaT<T>(__shfl_sync(FULL, x, k), __ldg(&Wt[k * 32 + lane]), acc);
+    return acc;
+}
+
+template <typename T>
+__device__ double mp_forward(const DGraph &g, const int *mem, int n, const int *nbptr, const int *nb, T *H, T *P,
+                             int lane) {
+    const MpLayout ml = mp_layout(g.layers);
+    const T *W = MpW<T>::W(g);
+    const T *H0 = MpW<T>::H0(g);
+    for (int i = 0; i < n; i++) H[i * 32 + lane] = __ldg(&H0[(int64_t)mem[i] * 32 + lane]);
+    __syncwarp();
+    for (int l = 0; l < g.layers; l++) {
+        const T *Wt = W + ml.wl + (int64_t)l * 1024;
+        T w[32];
+#pragma unroll
+        for (int k = 0; k < 32; k++) w[k] = __ldg(&Wt[k * 32 + lane]);
+        // mean aggregation over {i} U undirected internal neighbours (estimator.py:348-355, :374)
+        for (int i = 0; i < n; i++) {
+            int b = nbptr[i], e = nbptr[i + 1];
+            T acc = H[i * 32 + lane];
+            for (int q = b; q < e; q++) acc += H[nb[q] * 32 + lane];
+            P[i * 32 + lane] = acc / T(1 + e - b);
+        }
+        __syncwarp();
+        // H = relu(P @ W_l^T) (estimator.py:375-376)
+        for (int i = 0; i < n; i++) {
+            T p = P[i * 32 + lane];
+            T acc = T(0);
+#pragma unroll
+            for (int k = 0; k < 32; k++) acc = fmaT<T>(__shfl_sync(FULL, p, k), w[k], acc);
+            H[i * 32 + lane] = acc > T(0) ? acc : T(0);
+        }
+        __syncwarp();
+    }
+    // sum readout + dense head (estimator.py:380-389)
+    T s = T(0);
+    for (int i = 0; i < n; i++) s += H[i * 32 + lane];
+    T r = mat32<T>(W + ml.wr, s, lane);
+    r = r > T(0) ? r : T(0);
+    T d1 = mat32<T>(W + ml.a1, r, lane) + __ldg(&W[ml.c1 + lane]);
+    d1 = d1 > T(0) ? d1 : T(0);
+    T d2 = mat32<T>(W + ml.a2, d1, lane) + __ldg(&W[ml.c2 + lane]);
+    d2 = d2 > T(0) ? d2 : T(0);
+    T z = warp_sum<T>(__ldg(&W[ml.a3 + lane]) * d2) + __ldg(&W[ml.c3]);
+    double pred = __dmul_rn(softplus_d((double)z), g.out_scale);
+    return pred > 1e-9 ? pred : 1e-9;
+}
+
+// ---------------------------------------------------------------------------
+
+struct Ws {
+    int *gmap, *bmap, *g2id, *b2id, *nn, *rr, *bki, *gmin, *gcnt, *bmin;
+    long long *btot;
+    int *indeg, *scnt, *sptr, *succ, *prank, *p2ng, *p2nb;
+    unsigned long long *heapg, *heapb;
+    double *dur;
+    int *fused, *gptr, *gmem, *msort, *lidx, *nbptr, *nb;
+    char *H, *P;
+    long long *gint, *gin, *gout;
+    int *vis, *zl;
+};
+
+__device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) {
+    Ws w;
+    w.gmap = (int *)(base + L.gmap);
+    w.bmap = (int *)(base + L.bmap);
+    w.g2id = (int *)(base + L.g2id);
+    w.b2id = (int *)(base + L.b2id);
+    w.nn = (int *)(base + L.nn);
+    w.rr = (int *)(base + L.rr);
+    w.bki = (int *)(base + L.bki);
+    w.gmin = (int *)(base + L.gmin);
+    w.gcnt = (int *)(base + L.gcnt);
+    w.bmin = (int *)(base + L.bmin);
+    w.btot = (long long *)(base + L.btot);
+    w.indeg = (int *)(base + L.indeg);
+    w.scnt = (int *)(base + L.scnt);
+    w.sptr = (int *)(base + L.sptr);
+    w.succ = (int *)(base + L.succ);
+    w.prank = (int *)(base + L.prank);
+    w.p2ng = (int *)(base + L.p2ng);
+    w.p2nb = (int *)(base + L.p2nb);
+    w.heapg = (unsigned long long *)(base + L.heapg);
+    w.heapb = (unsigned long long *)(base + L.heapb);
+    w.dur = (double *)(base + L.dur);
+    w.fused = (int *)(base + L.fused);
+    w.gptr = (int *)(base + L.gptr);
+    w.gmem = (int *)(base + L.gmem);
+    w.msort = (int *)(base + L.msort);
+    w.lidx = (int *)(base + L.lidx);
+    w.nbptr = (int *)(base + L.nbptr);
+    w.nb = (int *)(base + L.nb);
+    w.H = base + L.H;
+    w.P = base + L.P;
+    w.gint = (long long *)(base + L.gint);
+    w.gin = (long long *)(base + L.gin);
+    w.gout = (long long *)(base + L.gout);
+    w.vis = (int *)(base + L.vis);
+    w.zl = (int *)(base + L.zl);
+    return w;
+}
+
+struct ScoreArgs {
+    DGraph g;
+    const int32_t *ngid, *rgid, *bkt;
+    int K, VB;
+    char *ws;
+    WsLayout L;
+    double *cost_out;
+    int32_t *status_out;
+    const double *ext_dur;
+    TimelineOut tl;
+    double *dur_out;
+    int32_t *bad_out;
+    int32_t *ngroups_out;
+};
+
+__device__ __forceinline__ bool in_grp(const Ws &w, int op, int gn) { return w.nn[op] == gn || w.rr[op] == gn; }
+__device__ __forceinline__ int export_of(const Ws &w, int op) { return w.rr[op] >= 0 ? w.rr[op] : w.nn[op]; }
+
+// status packed with the failing node so a warp min picks the first node in
+// schedule order (simulator.py:62 evaluates durations in node order)
+__device__ __forceinline__ long long pack_bad(int node, int code) { return ((long long)node << 8) | code; }
+
+template <typename T>
+__device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane) {
+    const DGraph &g = a.g;
+    const int V = g.V, E = g.E, A = g.A, VB = a.VB;
+    const int32_t *ng = a.ngid + (int64_t)k * V;
+    const int32_t *rg = a.rgid + (int64_t)k * V;
+    const int32_t *bk = a.bkt + (int64_t)k * A;
+
+    // ---- K1: group / bucket numbering (ids -> node order, graph.py:269-273)
+    for (int i = lane; i < VB; i += 32) w.gmap[i] = 0;
+    for (int i = lane; i < A; i += 32) w.bmap[i] = 0;
+    __syncwarp();
+    bool bad = false;
+    for (int v = lane; v < V; v += 32) {
+        int x = ng[v], y = rg[v];
+        if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
+        w.gmap[x] = 1;
+        if (y >= 0) w.gmap[y] = 1;
+        w.nn[v] = x;
+        w.rr[v] = y;
+    }
+    for (int i = lane; i < A; i += 32) {
+        int x = bk[i];
+        if (x < 0 || x >= A) { bad = true; continue; }
+        w.bmap[x] = 1;
+        w.bki[i] = x;
+    }
+    if (__any_sync(FULL, bad)) {
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_INVALID_ARG; }
+        return;
+    }
+    __syncwarp();
+    const int G = warp_rank_flags(w.gmap, w.g2id, VB, lane);
+    const int B = warp_rank_flags(w.bmap, w.b2id, A, lane);
+    const int N = G + B;
+    for (int v = lane; v < V; v += 32) {
+        w.nn[v] = w.gmap[w.nn[v]];
+        int y = w.rr[v];
+        w.rr[v] = y >= 0 ? w.gmap[y] : -1;
+    }
+    for (int i = lane; i < A; i += 32) w.bki[i] = w.bmap[w.bki[i]];
+    for (int i = lane; i < G; i += 32) { w.gmin[i] = INT_MAX; w.gcnt[i] = 0; }
+    for (int i = lane; i < B; i += 32) { w.bmin[i] = INT_MAX; w.btot[i] = 0; }
+    for (int i = lane; i < N; i += 32) { w.indeg[i] = 0; w.scnt[i] = 0; }
+    __syncwarp();
+
+    // per-group min member / size, per-bucket min AR / total bytes
+    for (int v = lane; v < V; v += 32) {
+        int x = w.nn[v], y = w.rr[v];
+        atomicMin(&w.gmin[x], v);
+        atomicAdd(&w.gcnt[x], 1);
+        if (y >= 0) { atomicMin(&w.gmin[y], v); atomicAdd(&w.gcnt[y], 1); }
+    }
+    for (int i = lane; i < A; i += 32) {
+        int b = w.bki[i];
+        atomicMin(&w.bmin[b], i);
+        atomicAdd((unsigned long long *)&w.btot[b], (unsigned long long)g.ar_bytes[i]);
+    }
+    __syncwarp();
+
+    // contracted schedule DAG with multiplicities (graph.py:237-274):
+    //   non-aggregate edge s->d: every copy C of d not holding s waits for export(s)
+    //   aggregate edge s->d:     every copy C of d waits for bucket(a), a in ARs(s)
+    //   bucket b:                waits for export(producer(a)), a in b
+    for (int pass = 0; pass < 2; pass++) {
+        for (int e = lane; e < E; e += 32) {
+            int s = g.e_src[e], d = g.e_dst[e];
+            int c0 = w.nn[d], c1 = w.rr[d];
+            if (!g.e_agg[e]) {
+                int ex = export_of(w, s);
+                int ns = w.nn[s], rs = w.rr[s];
+                if (c0 != ns && c0 != rs) {
+                    if (pass == 0) { atomicAdd(&w.scnt[ex], 1); atomicAdd(&w.indeg[c0], 1); }
+                    else w.succ[atomicAdd(&w.scnt[ex], 1)] = c0;
+                }
+                if (c1 >= 0 && c1 != ns && c1 != rs) {
+                    if (pass == 0) { atomicAdd(&w.scnt[ex], 1); atomicAdd(&w.indeg[c1], 1); }
+                    else w.succ[atomicAdd(&w.scnt[ex], 1)] = c1;
+                }
+            } else {
+                for (int q = g.arp_ptr[s]; q < g.arp_ptr[s + 1]; q++) {
+                    int bn = G + w.bki[g.arp[q]];
+                    if (pass == 0) {
+                        atomicAdd(&w.scnt[bn], c1 >= 0 ? 2 : 1);
+                        atomicAdd(&w.indeg[c0], 1);
+                        if (c1 >= 0) atomicAdd(&w.indeg[c1], 1);
+                    } else {
+                        w.succ[atomicAdd(&w.scnt[bn], 1)] = c0;
+                        if (c1 >= 0) w.succ[atomicAdd(&w.scnt[bn], 1)] = c1;
+                    }
+                }
+            }
+        }
+        for (int i = lane; i < A; i += 32) {
+            int bn = G + w.bki[i];
+            int ex = export_of(w, g.ar_prod[i]);
+            if (pass == 0) { atomicAdd(&w.scnt[ex], 1); atomicAdd(&w.indeg[bn], 1); }
+            else w.succ[atomicAdd(&w.scnt[ex], 1)] = bn;
+        }
+        __syncwarp();
+        if (pass == 0) {
+            warp_exscan(w.scnt, w.sptr, N, lane);
+            for (int i = lane; i < N; i += 32) w.scnt[i] = w.sptr[i];  // fill cursors
+            __syncwarp();
+        }
+    }
+
+    // tie-break ranks (simulator.py:63-64): group key (min member, id), bucket key min AR.
+    // prank = 2*min_member + (1 if the other group sharing that min member has a smaller id)
+    for (int gi = lane; gi < G; gi += 32) {
+        int t = w.gmin[gi];
+        int other = (w.nn[t] == gi) ? w.rr[t] : w.nn[t];
+        int sub = (other >= 0 && w.gmin[other] == t && other < gi) ? 1 : 0;
+        int pr = 2 * t + sub;
+        w.prank[gi] = pr;
+        w.p2ng[pr] = gi;
+    }
+    for (int b = lane; b < B; b += 32) {
+        int pr = w.bmin[b];
+        w.prank[G + b] = pr;
+        w.p2nb[pr] = G + b;
+    }
+
+    // ---- K2: durations of every node (simulator.py:62)
+    long long badk = LLONG_MAX;
+    for (int b = lane; b < B; b += 32) {  // comm.py:45-49
+        double d = __dadd_rn(__dmul_rn(g.C, (double)w.btot[b]), g.D);
+        w.dur[G + b] = d;
+        if (d < 0.0) badk = min(badk, pack_bad(G + b, FO_NEGATIVE_DURATION));
+    }
+    if (a.ext_dur) {
+        for (int i = lane; i < N; i += 32) {
+            double d = a.ext_dur[i];
+            w.dur[i] = d;
+            if (d < 0.0) badk = min(badk, pack_bad(i, FO_NEGATIVE_DURATION));
+        }
+    } else {
+        const bool hw = g.provider == FO_PROVIDER_HW_ORACLE;
+        const bool need_io = hw || g.variant == FO_EST_ANALYTIC || g.variant == FO_EST_LINEAR;
+        if (need_io) {  // group_io (graph.py:181-213)
+            for (int i = lane; i < G; i += 32) { w.gint[i] = 0; w.gin[i] = 0; w.gout[i] = 0; }
+            for (int v = lane; v < V; v += 32) w.vis[v] = 0;
+            __syncwarp();
+            for (int e = lane; e < E; e += 32) {
+                int s = g.e_src[e], d = g.e_dst[e];
+                unsigned long long by = (unsigned long long)g.e_bytes[e];
+                int cs[2] = {w.nn[d], w.rr[d]};
+                for (int c = 0; c < 2; c++) {
+                    int C = cs[c];
+                    if (C < 0) continue;
+                    if (in_grp(w, s, C)) atomicAdd((unsigned long long *)&w.gint[C], by);
+                    else { atomicAdd((unsigned long long *)&w.gin[C], by); w.vis[s] = 1; }
+                }
+            }
+            __syncwarp();
+            for (int v = lane; v < V; v += 32) {
+                if (w.vis[v] || g.out_ptr[v + 1] == g.out_ptr[v] || g.arp_ptr[v + 1] > g.arp_ptr[v])
+                    atomicAdd((unsigned long long *)&w.gout[export_of(w, v)], (unsigned long long)g.op_out[v]);
+            }
+            __syncwarp();
+        }
+        // singletons (estimator.py:810-814 / workloads.py:276-291) and the fused-group list
+        int nf = 0;
+        for (int base = 0; base < G; base += 32) {
+            int gi = base + lane;
+            bool fused = false;
+            if (gi < G) {
+                int n = w.gcnt[gi];
+                if (n == 1) {
+                    int v = w.gmin[gi];
+                    double d;
+                    if (hw) {
+                        double c = g.op_compute[v];
+                        d = g.op_kind[v] == 1 ? 0.0
+                                              : __dadd_rn(__dadd_rn(isnan(c) ? 0.0 : c, g.launch),
+                                                          __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
+                    } else if (g.op_kind[v] == 1) {
+                        d = 0.0;
+                    } else {
+                        d = g.op_prof[v];
+                        if (isnan(d)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); d = 0.0; }
+                    }
+                    w.dur[gi] = d;
+                } else {
+                    w.dur[gi] = 0.0;
+                    if (!hw && g.variant == FO_EST_NONE) badk = min(badk, pack_bad(gi, FO_MISSING_COST));
+                    else if (!hw && g.variant == FO_EST_INVALID) badk = min(badk, pack_bad(gi, FO_DIM_MISMATCH));
+                    else fused = true;
+                }
+            }
+            unsigned m = __ballot_sync(FULL, fused);
+            if (fused) w.fused[nf + __popc(m & lanemask_lt())] = gi;
+            nf += __popc(m);
+        }
+        __syncwarp();
+        if (nf > 0) {
+            // member lists of fused groups (order fixed below by sorting)
+            for (int f = lane; f < nf; f += 32) w.zl[f] = w.gcnt[w.fused[f]];
+            __syncwarp();
+            warp_exscan(w.zl, w.gptr, nf, lane);
+            // group -> fused position via prank scratch-free map: reuse gcnt as position+1 marker
+            for (int f = lane; f < nf; f += 32) w.gcnt[w.fused[f]] = -(f + 1);
+            __syncwarp();
+            for (int f = lane; f < nf; f += 32) w.zl[f] = w.gptr[f];
+            __syncwarp();
+            for (int v = lane; v < V; v += 32) {
+                int x = w.nn[v], y = w.rr[v];
+                int fx = w.gcnt[x];
+                if (fx < 0) w.gmem[atomicAdd(&w.zl[-fx - 1], 1)] = v;
+                if (y >= 0) {
+                    int fy = w.gcnt[y];
+                    if (fy < 0) w.gmem[atomicAdd(&w.zl[-fy - 1], 1)] = v;
+                }
+            }
+            __syncwarp();
+            for (int f = 0; f < nf; f++) {
+                const int gi = w.fused[f];
+                const int b0 = w.gptr[f], n = w.gptr[f + 1] - b0;
+                int *mem = w.gmem + b0;
+                if (n > kMpCap && !hw && (g.variant == FO_EST_MESSAGE_PASSING || g.variant == FO_EST_LINEAR)) {
+                    badk = min(badk, pack_bad(gi, kRetryLarge));
+                    continue;
+                }
+                // sort members ascending (estimator.py:160, node order = ascending op id)
+                if (n <= 32) {
+                    int x = lane < n ? mem[lane] : INT_MAX;
+                    for (int kk = 2; kk <= 32; kk <<= 1)
+                        for (int j = kk >> 1; j > 0; j >>= 1) {
+                            int y = __shfl_xor_sync(FULL, x, j);
+                            bool up = ((lane & kk) == 0);
+                            bool lower = (lane & j) == 0;
+                            int lo = min(x, y), hi = max(x, y);
+                            x = (lower == up) ? lo : hi;
+                        }
+                    if (lane < n) mem[lane] = x;
+                } else if (lane == 0) {  // insertion sort (rare: large groups)
+                    for (int i = 1; i < n; i++) {
+                        int x = mem[i], j = i - 1;
+                        while (j >= 0 && mem[j] > x) { mem[j + 1] = mem[j]; j--; }
+                        mem[j + 1] = x;
+                    }
+                }
+                __syncwarp();
+                double d = 0.0;
+                if (hw) {  // oracle_time (workloads.py:281-291): sum in ascending member order
+                    if (lane == 0) {
+                        bool all_param = true;
+                        double comp = 0.0;
+                        for (int i = 0; i < n; i++) {
+                            int v = mem[i];
+                            if (g.op_kind[v] != 1) all_param = false;
+                            double c = g.op_compute[v];
+                            comp = __dadd_rn(comp, isnan(c) ? 0.0 : c);
+                        }
+                        d = all_param ? 0.0
+                                      : __dadd_rn(__dadd_rn(comp, g.launch),
+                                                  __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
+                    }
+                    d = __shfl_sync(FULL, d, 0);
+                    if (lane == 0) w.dur[gi] = d;
+                    continue;
+                }
+                // featurize -> lookup for every member (estimator.py:170)
+                bool miss = false;
+                for (int i = lane; i < n; i += 32) miss |= isnan(g.op_prof[mem[i]]);
+                if (__any_sync(FULL, miss)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); continue; }
+                if (g.variant == FO_EST_ANALYTIC) {  // estimator.py:434-446
+                    if (lane == 0) {
+                        double sum = 0.0;
+                        for (int i = 0; i < n; i++) {
+                            int v = mem[i];
+                            double raw = __dsub_rn(__dsub_rn(g.op_prof[v], g.launch),
+                                                   __dmul_rn(g.mem, (double)(g.op_in[v] + g.op_out[v])));
+                            sum = __dadd_rn(sum, raw);
+                        }
+                        double pred = __dadd_rn(__dadd_rn(sum, g.launch), __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
+                        w.dur[gi] = pred > 1e-9 ? pred : 1e-9;
+                    }
+                    continue;
+                }
+                // member-local undirected neighbour lists (estimator.py:173-177, :348-355)
+                for (int i = lane; i < n; i += 32) w.lidx[mem[i]] = i;
+                __syncwarp();
+                for (int i = lane; i < n; i += 32) {
+                    int v = mem[i];
+                    w.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
+                }
+                __syncwarp();
+                warp_exscan(w.zl, w.nbptr, n, lane);
+                int dirE = 0;  // directed internal edges (linear variant's longest path)
+                for (int i = lane; i < n; i += 32) {
+                    int v = mem[i];
+                    int o = w.nbptr[i], c = 0;
+                    for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
+                        int s = g.e_src[g.in_e[q]];
+                        if (!in_grp(w, s, gi)) continue;
+                        dirE++;
+                        int j = w.lidx[s];
+                        bool dup = false;
+                        for (int t = 0; t < c; t++) dup |= (w.nb[o + t] == j);
+                        if (!dup) w.nb[o + c++] = j;
+                    }
+                    for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
+                        int d2 = g.e_dst[g.out_e[q]];
+                        if (!in_grp(w, d2, gi)) continue;
+                        int j = w.lidx[d2];
+                        bool dup = false;
+                        for (int t = 0; t < c; t++) dup |= (w.nb[o + t] == j);
+                        if (!dup) w.nb[o + c++] = j;
+                    }
+                    w.zl[i] = c;
+                }
+                __syncwarp();
+                // compact rows in place: nbptr -> [start, start + count)
+                // (store counts as end pointers in msort to keep nbptr monotone)
+                for (int i = lane; i < n; i += 32) w.msort[i] = w.zl[i];
+                __syncwarp();
+                if (g.variant == FO_EST_MESSAGE_PASSING) {
+                    // compact neighbour rows into a dense CSR (msort holds the counts)
+                    if (lane == 0) {
+                        int o = 0;
+                        for (int i = 0; i < n; i++) {
+                            int s0 = w.nbptr[i], c = w.msort[i];
+                            for (int t = 0; t < c; t++) w.nb[o + t] = w.nb[s0 + t];
+                            w.nbptr[i] = o;
+                            o += c;
+                        }
+                        w.nbptr[n] = o;
+                    }
+                    __syncwarp();
+                    double pred = mp_forward<T>(g, mem, n, w.nbptr, w.nb, (T *)w.H, (T *)w.P, lane);
+                    if (lane == 0) w.dur[gi] = pred;
+                } else {  // LINEAR (estimator.py:117-128, 341-345, 421-426)
+                    dirE = __reduce_add_sync(FULL, dirE);
+                    if (lane == 0) {
+                        // longest path in nodes over the directed internal edges (estimator.py:131-154)
+                        int *depth = w.msort;  // reuse: counts no longer needed
+                        for (int i = 0; i < n; i++) depth[i] = 1;
+                        for (int it = 0; it < n; it++) {
+                            bool ch = false;
+                            for (int i = 0; i < n; i++) {
+                                int v = mem[i];
+                                for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
+                                    int s = g.e_src[g.in_e[q]];
+                                    if (!in_grp(w, s, gi)) continue;
+                                    int j = w.lidx[s];
+                                    if (depth[j] + 1 > depth[i]) { depth[i] = depth[j] + 1; ch = true; }
+                                }
+                            }
+                            if (!ch) break;
+                        }
+                        int lp = 0;
+                        for (int i = 0; i < n; i++) lp = max(lp, depth[i]);
+                        double total = 0.0;
+                        for (int i = 0; i < n; i++) total = __dadd_rn(total, g.op_prof[mem[i]]);
+                        double agg[6] = {(double)n, total, (double)w.gint[gi], (double)w.gin[gi], (double)w.gout[gi],
+                                         (double)lp};
+                        double fs[12];
+                        for (int q = 0; q < 6; q++) { fs[q] = log1p(agg[q]); fs[6 + q] = agg[q]; }
+                        if (g.lin_norm)
+                            for (int q = 0; q < 12; q++) fs[q] = __ddiv_rn(__dsub_rn(fs[q], g.agg_mean[q]), g.agg_std[q]);
+                        double z = 0.0;
+                        for (int q = 0; q < 12; q++) z = __dadd_rn(z, __dmul_rn(g.lin_w[q], fs[q]));
+                        z = __dadd_rn(z, g.lin_b);
+                        double pred = __dmul_rn(softplus_d(z), g.out_scale);
+                        w.dur[gi] = pred > 1e-9 ? pred : 1e-9;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+    // first failing node in node order decides the error (simulator.py:62)
+#pragma unroll
+    for (int d = 16; d; d >>= 1) badk = min(badk, __shfl_xor_sync(FULL, badk, d));
+    __syncwarp();
+    if (a.dur_out) {
+        for (int i = lane; i < N; i += 32) a.dur_out[i] = w.dur[i];
+        if (lane == 0) *a.ngroups_out = G;
+    }
+    if (badk != LLONG_MAX) {
+        if (lane == 0) {
+            a.cost_out[k] = 0.0;
+            a.status_out[k] = (int)(badk & 0xff);
+            if (a.bad_out) *a.bad_out = (int)(badk >> 8);
+        }
+        return;
+    }
+
+    // ---- K3: two-lane discrete-event simulation (simulator.py:66-140)
+    // initial ready set: nodes with no deps, rt = 0.0 (level 0)
+    int nz = 0;
+    for (int base = 0; base < N; base += 32) {
+        int i = base + lane;
+        bool z = i < N && w.indeg[i] == 0;
+        unsigned m = __ballot_sync(FULL, z);
+        if (z) w.zl[nz + __popc(m & lanemask_lt())] = i;
+        nz += __popc(m);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int hg = 0, hb = 0;
+        for (int q = 0; q < nz; q++) {
+            int i = w.zl[q];
+            unsigned long long key = (unsigned long long)w.prank[i];  // level 0
+            if (i < G) heap_push(w.heapg, hg, key);
+            else heap_push(w.heapb, hb, key);
+        }
+        int run0 = -1, run1 = -1;
+        double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
+        unsigned long long level = 0;
+        int done = 0, st = FO_OK, nc = 0, nb = 0;
+        const bool want_tl = a.tl.c_id != nullptr;
+        while (done < N) {
+            // drain every completion with end <= now (simulator.py:122-125); at
+            // most one per lane, all with end == now, so their order is immaterial
+#pragma unroll
+            for (int lane_t = 0; lane_t < 2; lane_t++) {
+                int node = lane_t == 0 ? run0 : run1;
+                double en = lane_t == 0 ? end0 : end1;
+                if (node >= 0 && en <= now) {
+                    if (lane_t == 0) run0 = -1; else run1 = -1;
+                    done++;
+                    if (en > last) { last = en; level++; }
+                    // release successors (simulator.py:88-96); rt = en = max finish of deps
+                    for (int q = w.sptr[node]; q < w.sptr[node + 1]; q++) {
+                        int s = w.succ[q];
+                        int dg = w.indeg[s] - 1;
+                        w.indeg[s] = dg;
+                        if (dg == 0) {
+                            unsigned long long key = (level << 32) | (unsigned)w.prank[s];
+                            if (s < G) heap_push(w.heapg, hg, key);
+                            else heap_push(w.heapb, hb, key);
+                        }
+                    }
+                }
+            }
+            if (done >= N) break;
+            bool started = false;
+            // compute lane, then comm lane (simulator.py:101); start = max(now, rt) = now
+            if (run0 < 0 && hg > 0) {
+                unsigned long long key = heap_pop(w.heapg, hg);
+                int node = w.p2ng[(unsigned)(key & 0xffffffffu)];
+                end0 = __dadd_rn(now, w.dur[node]);
+                run0 = node;
+                if (end0 > mk) mk = end0;
+                if (want_tl) { a.tl.c_id[nc] = w.g2id[node]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; }
+                nc++;
+                started = true;
+            }
+            if (run1 < 0 && hb > 0) {
+                unsigned long long key = heap_pop(w.heapb, hb);
+                int node = w.p2nb[(unsigned)(key & 0xffffffffu)];
+                end1 = __dadd_rn(now, w.dur[node]);
+                run1 = node;
+                if (end1 > mk) mk = end1;
+                if (want_tl) { a.tl.b_id[nb] = w.b2id[node - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; }
+                nb++;
+                started = true;
+            }
+            if (started) continue;
+            if (run0 >= 0 || run1 >= 0) {  // advance to the next completion (simulator.py:130-132)
+                double t0 = run0 >= 0 ? end0 : DBL_MAX, t1 = run1 >= 0 ? end1 : DBL_MAX;
+                now = t0 < t1 ? t0 : t1;
+                continue;
+            }
+            st = FO_CYCLE;  // simulator.py:133
+            break;
+        }
+        a.cost_out[k] = st == FO_OK ? mk : 0.0;
+        a.status_out[k] = st;
+        if (want_tl) { *a.tl.n_c = nc; *a.tl.n_b = nb; }
+        if (a.bad_out) *a.bad_out = -1;
+    }
+    __syncwarp();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) score_kernel(ScoreArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int nw = gridDim.x * kWarps;
+    Ws w = ws_at(a.ws + (int64_t)wid * a.L.total, a.L);
+    for (int k = wid; k < a.K; k += nw) score_one<T>(a, k, w, lane);
+}
+
+int score_warps_per_block() { return kWarps; }
+
+int score_blocks_per_sm(int precision) {
+    int n = 0;
+    if (precision == FO_PREC_FP64)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel<double>, kWarps * 32, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel<float>, kWarps * 32, 0);
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_score(const DGraph &g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K,
+                         int VB, int precision, char *ws, const WsLayout &L, int n_slots, int grid, int warps,
+                         double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
+                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
+    (void)warps;
+    (void)n_slots;
+    ScoreArgs a;
+    a.g = g;
+    a.ngid = ngid;
+    a.rgid = rgid;
+    a.bkt = bkt;
+    a.K = K;
+    a.VB = VB;
+    a.ws = ws;
+    a.L = L;
+    a.cost_out = cost_out;
+    a.status_out = status_out;
+    a.ext_dur = ext_dur;
+    a.tl = tl;
+    a.dur_out = dur_out;
+    a.bad_out = bad_out;
+    a.ngroups_out = ngroups_out;
+    if (precision == FO_PREC_FP64)
+        score_kernel<double><<<grid, kWarps * 32, 0, stream>>>(a);
+    else
+        score_kernel<float><<<grid, kWarps * 32, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace fo

@@ -1,0 +1,176 @@
+"""Device handles: one ``fo_graph`` (include/disco_b200.h) per static graph and
+cost-provider configuration, plus the state encoding that crosses the C-ABI."""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+
+import numpy as np
+
+from . import _native as N
+from .errors import DeviceError, _raise
+from .graph import KIND_CODE, HloGraph, state_arrays
+
+
+def current_device() -> int:
+    """CUDA device of the calling rank, or -1 (host-only handle: the native
+    batch-expand engine works, every device entry point raises)."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:
+        pass
+    return -1
+
+
+class StaticArrays:
+    """A graph's static part in build_graph order (graph.py:314-316)."""
+
+    def __init__(self, g: HloGraph, op_time=None):
+        ops = sorted(g.ops, key=lambda o: o.id)
+        self.op_ids = [o.id for o in ops]
+        self.op_index = {o.id: i for i, o in enumerate(ops)}
+        ars = sorted(g.allreduces, key=lambda a: a.id)
+        self.ar_ids = [a.id for a in ars]
+        self.ar_index = {a.id: i for i, a in enumerate(ars)}
+        edges = sorted(g.edges, key=lambda e: (e.src, e.dst))
+        self.V, self.E, self.A = len(ops), len(edges), len(ars)
+        self.op_kind = np.array([KIND_CODE.get(o.kind, 0) for o in ops], np.int32)
+        self.op_out = np.array([o.out_bytes for o in ops], np.int64)
+        self.op_prof = np.array([math.nan if op_time is None else op_time(o) for o in ops], np.float64)
+        self.op_compute = np.array([math.nan if o.compute_us is None else float(o.compute_us) for o in ops],
+                                   np.float64)
+        self.e_src = np.array([self.op_index[e.src] for e in edges], np.int32)
+        self.e_dst = np.array([self.op_index[e.dst] for e in edges], np.int32)
+        self.e_bytes = np.array([e.bytes for e in edges], np.int64)
+        self.ar_prod = np.array([self.op_index[a.producer_op] for a in ars], np.int32)
+        self.ar_bytes = np.array([a.tensor_bytes for a in ars], np.int64)
+        self.op_codes = [o.op_code for o in ops]
+
+    def desc(self):
+        d = N.GraphDesc()
+        d.n_ops, d.n_edges, d.n_allreduces = self.V, self.E, self.A
+        d.op_kind = N.tptr(self.op_kind, C.c_int32)
+        d.op_out_bytes = N.tptr(self.op_out, C.c_int64)
+        d.op_profile_us = N.tptr(self.op_prof, C.c_double)
+        d.op_compute_us = N.tptr(self.op_compute, C.c_double)
+        d.edge_src = N.tptr(self.e_src, C.c_int32)
+        d.edge_dst = N.tptr(self.e_dst, C.c_int32)
+        d.edge_bytes = N.tptr(self.e_bytes, C.c_int64)
+        d.ar_producer = N.tptr(self.ar_prod, C.c_int32)
+        d.ar_bytes = N.tptr(self.ar_bytes, C.c_int64)
+        return d
+
+
+class DeviceGraph:
+    """An ``fo_graph`` handle with its cost model installed."""
+
+    def __init__(self, g: HloGraph, cost_model_fn, op_time=None, device=None):
+        self.static = StaticArrays(g, op_time)
+        self.V, self.E, self.A = self.static.V, self.static.E, self.static.A
+        self.device = current_device() if device is None else device
+        self._lock = threading.Lock()
+        L = N.lib()
+        h = C.c_void_p()
+        st = L.fo_graph_create(C.byref(self.static.desc()), self.device, C.byref(h))
+        _raise(st, "fo_graph_create", N.last_error())
+        self.h = h
+        self._keep = []
+        cm = cost_model_fn(self.static, self._keep)
+        st = L.fo_graph_set_cost_model(self.h, C.byref(cm))
+        _raise(st, "fo_graph_set_cost_model", N.last_error())
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                N.lib().fo_graph_destroy(h)
+            except Exception:
+                pass
+
+    # -- scoring -------------------------------------------------------------
+    def score_host(self, ng, rg, bk, gid_bound, precision=N.FO_PREC_FP32):
+        """cost() of K candidates held in host arrays [K, V] / [K, A]."""
+        ng = np.ascontiguousarray(ng, np.int32)
+        rg = np.ascontiguousarray(rg, np.int32)
+        bk = np.ascontiguousarray(bk, np.int32)
+        K = ng.shape[0] if ng.ndim == 2 else (bk.shape[0] if bk.ndim == 2 else 1)
+        cost = np.zeros(K, np.float64)
+        status = np.zeros(K, np.int32)
+        st = N.lib().fo_score_host(self.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), K, int(gid_bound), precision,
+                                   N.ptr(cost), N.ptr(status))
+        _raise(st, "fo_score_host", N.last_error())
+        return cost, status
+
+    def score_device(self, ng, rg, bk, gid_bound, cost, status, precision=N.FO_PREC_FP32, stream=None):
+        """Asynchronous scoring of device-resident candidates (torch tensors)."""
+        K = int(cost.shape[0])
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream().cuda_stream
+        st = N.lib().fo_score(self.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), K, int(gid_bound), precision, N.ptr(cost),
+                              N.ptr(status), C.c_void_p(stream))
+        _raise(st, "fo_score", N.last_error())
+
+    def simulate_arrays(self, ng, rg, bk, gid_bound, durations=None, precision=N.FO_PREC_FP32):
+        V, A = self.V, self.A
+        c_id = np.zeros(2 * V + 1, np.int32)
+        c_s = np.zeros(2 * V + 1)
+        c_e = np.zeros(2 * V + 1)
+        b_id = np.zeros(A + 1, np.int32)
+        b_s = np.zeros(A + 1)
+        b_e = np.zeros(A + 1)
+        nc, nb, bad = C.c_int32(), C.c_int32(), C.c_int32(-1)
+        mk = C.c_double()
+        dur = None
+        if durations is not None:
+            dur = np.zeros(2 * V + A + 2, np.float64)
+            dur[: len(durations)] = durations
+        st = N.lib().fo_simulate(self.h, N.ptr(np.ascontiguousarray(ng, np.int32)),
+                                 N.ptr(np.ascontiguousarray(rg, np.int32)),
+                                 N.ptr(np.ascontiguousarray(bk, np.int32)), int(gid_bound), precision, N.ptr(dur),
+                                 N.ptr(c_id), N.ptr(c_s), N.ptr(c_e), C.byref(nc), N.ptr(b_id), N.ptr(b_s),
+                                 N.ptr(b_e), C.byref(nb), C.byref(mk), C.byref(bad))
+        n1, n2 = nc.value, nb.value
+        return st, mk.value, (c_id[:n1], c_s[:n1], c_e[:n1]), (b_id[:n2], b_s[:n2], b_e[:n2]), bad.value
+
+    def node_durations_arrays(self, ng, rg, bk, gid_bound, precision=N.FO_PREC_FP32):
+        dur = np.zeros(2 * self.V + self.A + 2)
+        G, bad = C.c_int32(), C.c_int32(-1)
+        st = N.lib().fo_node_durations(self.h, N.ptr(np.ascontiguousarray(ng, np.int32)),
+                                       N.ptr(np.ascontiguousarray(rg, np.int32)),
+                                       N.ptr(np.ascontiguousarray(bk, np.int32)), int(gid_bound), precision,
+                                       N.ptr(dur), C.byref(G), C.byref(bad))
+        return st, dur, G.value, bad.value
+
+    # -- native batch-expand ----------------------------------------------------
+    def make_candidates(self, seeds, beta=10, methods_mask=7, base=None, n_threads=0):
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        K = len(seeds)
+        ng = np.zeros((K, self.V), np.int32)
+        rg = np.zeros((K, self.V), np.int32)
+        bk = np.zeros((K, self.A), np.int32)
+        vb = C.c_int32()
+        b0 = (None, None, None) if base is None else tuple(np.ascontiguousarray(x, np.int32) for x in base)
+        st = N.lib().fo_make_candidates(self.h, N.ptr(b0[0]), N.ptr(b0[1]), N.ptr(b0[2]), N.ptr(seeds), K, beta,
+                                        methods_mask, n_threads, N.ptr(ng), N.ptr(rg), N.ptr(bk), C.byref(vb))
+        _raise(st, "fo_make_candidates", N.last_error())
+        return ng, rg, bk, vb.value
+
+    def state_hash(self, ng, rg, bk):
+        ng = np.ascontiguousarray(np.atleast_2d(ng), np.int32)
+        rg = np.ascontiguousarray(np.atleast_2d(rg), np.int32)
+        bk = np.ascontiguousarray(bk, np.int32).reshape(ng.shape[0], -1)
+        out = np.zeros(ng.shape[0], np.uint64)
+        st = N.lib().fo_state_hash(self.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), ng.shape[0], N.ptr(out))
+        _raise(st, "fo_state_hash", N.last_error())
+        return out
+
+    # -- HloGraph conveniences ----------------------------------------------------
+    def encode(self, g: HloGraph):
+        return state_arrays(g)

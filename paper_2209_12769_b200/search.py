@@ -1,0 +1,201 @@
+"""Alg. 1 backtracking search and the exhaustive oracle with the reference's
+signatures (search.py:37-225), driven by the native engine and the device
+scorer.
+
+``backtracking_search`` reproduces the reference's trajectory for one seed.
+``lockstep_search`` runs R independent seeds in lock step: every round each
+active seed performs one step of Alg. 1 and all their candidates are scored
+in one device batch, so each seed's trajectory equals the single-seed one.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import heapq
+import time
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import InvalidConfig, LimitExceeded, _raise
+from .graph import HloGraph, canonical_hash, state_arrays, state_from_arrays
+from .rewrite import ALL_METHODS, METHOD_INDEX, OptimizationMethod, expand_all
+
+METHOD_NAMES = ("nondup", "dup", "ar")
+
+
+@dataclass(frozen=True)
+class SearchConfig:
+    alpha: float = 1.05
+    beta: int = 10
+    max_unchanged: int = 1000
+    seed: int = 0
+    methods: tuple = ALL_METHODS
+    time_budget_s: Optional[float] = None
+
+    def __post_init__(self) -> None:
+        if self.alpha < 1:
+            raise InvalidConfig("alpha must be >= 1")
+        if self.beta < 1:
+            raise InvalidConfig("beta must be >= 1")
+        if not self.methods:
+            raise InvalidConfig("method mask must be non-empty")
+        if self.max_unchanged < 1:
+            raise InvalidConfig("max_unchanged must be >= 1")
+
+
+@dataclass(frozen=True)
+class TraceRecord:
+    step: int
+    action: str
+    cost_us: float
+    best_cost_us: float
+    queue_len: int
+    enqueued: bool = False
+
+
+@dataclass
+class SearchResult:
+    best_graph: HloGraph
+    best_cost_us: float
+    steps: int
+    candidates_evaluated: int
+    candidates_enqueued: int
+    trace: list = field(default_factory=list)
+
+
+def _require_device(cp):
+    from .estimator import DeviceCostProviders
+
+    if not isinstance(cp, DeviceCostProviders):
+        raise TypeError("the native search needs device cost providers (make_cost_providers / oracle_providers)")
+
+
+class LockstepSearch:
+    """R lock-stepped Alg. 1 instances on one device (fo_search_*)."""
+
+    def __init__(self, g0: HloGraph, cfg: SearchConfig, cp, seeds: Sequence[int], precision=None, n_threads=0):
+        _require_device(cp)
+        self.g0, self.cfg, self.cp = g0, cfg, cp
+        self.dg = cp.device_graph(g0)
+        self.R = len(seeds)
+        c = N.SearchCfg()
+        c.alpha, c.beta, c.max_unchanged = cfg.alpha, cfg.beta, cfg.max_unchanged
+        c.methods_mask = sum(1 << METHOD_INDEX[m] for m in cfg.methods)
+        c.precision = N.FO_PREC_FP64 if precision is None else precision
+        c.n_threads = n_threads
+        ng, rg, bk, _, _, _ = state_arrays(g0)
+        self._seeds = np.ascontiguousarray(seeds, np.uint64)
+        h = C.c_void_p()
+        st = N.lib().fo_search_create(self.dg.h, C.byref(c), N.ptr(self._seeds), self.R, N.ptr(ng), N.ptr(rg),
+                                      N.ptr(bk), C.byref(h))
+        _raise(st, "fo_search_create", N.last_error())
+        self.h = h
+        self.best = np.full(self.R, np.inf)
+        self.active = self.R
+        self.rounds = 0
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                N.lib().fo_search_destroy(h)
+            except Exception:
+                pass
+
+    def round(self) -> int:
+        a = C.c_int32()
+        st = N.lib().fo_search_round(self.h, C.byref(a), N.ptr(self.best))
+        _raise(st, "fo_search_round", N.last_error())
+        self.active = a.value
+        self.rounds += 1
+        return self.active
+
+    def run(self, max_rounds: Optional[int] = None, started: Optional[float] = None):
+        t0 = time.monotonic() if started is None else started
+        while self.active > 0:
+            if max_rounds is not None and self.rounds >= max_rounds:
+                break
+            if self.cfg.time_budget_s is not None and time.monotonic() - t0 > self.cfg.time_budget_s:
+                break
+            self.round()
+        return [self.result(r) for r in range(self.R)]
+
+    def timing(self):
+        d, e, s = C.c_double(), C.c_double(), C.c_int64()
+        N.lib().fo_search_timing(self.h, C.byref(d), C.byref(e), C.byref(s))
+        return {"device_ms": d.value, "expand_ms": e.value, "scored": s.value}
+
+    def result(self, r: int, with_trace: bool = True) -> SearchResult:
+        V, A = self.dg.V, self.dg.A
+        best = C.c_double()
+        cnt = np.zeros(4, np.int64)
+        ng, rg, bk = np.zeros(V, np.int32), np.zeros(V, np.int32), np.zeros(A, np.int32)
+        st = N.lib().fo_search_result(self.h, r, C.byref(best), N.ptr(cnt), N.ptr(ng), N.ptr(rg), N.ptr(bk), None, 0)
+        trace = []
+        if with_trace and cnt[3] > 0:
+            buf = (N.TraceRec * int(cnt[3]))()
+            N.lib().fo_search_result(self.h, r, None, None, None, None, None, buf, int(cnt[3]))
+            trace = [TraceRecord(t.step, METHOD_NAMES[t.method], t.cost_us, t.best_cost_us, t.queue_len,
+                                 bool(t.enqueued)) for t in buf]
+        _raise(st, "search", N.last_error())
+        return SearchResult(state_from_arrays(self.g0, ng, rg, bk), best.value, int(cnt[0]), int(cnt[1]), int(cnt[2]),
+                            trace)
+
+
+def backtracking_search(g0: HloGraph, cfg: SearchConfig, cp, precision=None) -> SearchResult:
+    """Best fusion state found from g0; never worse than g0 (search.py:84-155)."""
+    return LockstepSearch(g0, cfg, cp, [cfg.seed], precision).run()[0]
+
+
+def lockstep_search(g0: HloGraph, cfg: SearchConfig, cp, seeds: Sequence[int], precision=None, n_threads=0):
+    """Independent searches for every seed, advanced in lock step."""
+    return LockstepSearch(g0, cfg, cp, seeds, precision, n_threads).run()
+
+
+def exhaustive_search(g0: HloGraph, cp, max_ops: int = 8, max_tensors: int = 4) -> SearchResult:
+    """BFS closure of the three rewrites with state dedupe (search.py:158-225);
+    each BFS level is scored as one device batch."""
+    _require_device(cp)
+    if len(g0.ops) > max_ops:
+        raise LimitExceeded(f"{len(g0.ops)} ops exceeds limit {max_ops}")
+    if len(g0.allreduces) > max_tensors:
+        raise LimitExceeded(f"{len(g0.allreduces)} tensors exceeds limit {max_tensors}")
+    dg = cp.device_graph(g0)
+    ng, rg, bk, vb, _, _ = state_arrays(g0)
+    h0 = int(dg.state_hash(ng, rg, bk)[0])
+    seen = {h0}
+    c0 = dg.score_host(ng[None], rg[None], bk[None], vb, N.FO_PREC_FP64)
+    _raise(int(c0[1][0]), "cost")
+    best = (ng, rg, bk)
+    best_cost = float(c0[0][0])
+    evaluated, steps = 1, 0
+    frontier = [(ng, rg, bk)]
+    gb = 2 * dg.V + 2
+    while frontier:
+        level = []
+        for s in frontier:
+            steps += 1
+            cn, cr, cb = expand_all(g0, *s)
+            if len(cn) == 0:
+                continue
+            hs = dg.state_hash(cn, cr, cb)
+            for i in range(len(cn)):
+                h = int(hs[i])
+                if h in seen:
+                    continue
+                seen.add(h)
+                level.append((cn[i], cr[i], cb[i]))
+        if not level:
+            break
+        cost, st = dg.score_host(np.stack([x[0] for x in level]), np.stack([x[1] for x in level]),
+                                 np.stack([x[2] for x in level]), gb, N.FO_PREC_FP64)
+        for i, x in enumerate(level):
+            _raise(int(st[i]), "cost")
+            evaluated += 1
+            if cost[i] < best_cost:  # strict: first in enumeration order wins (search.py:214-215)
+                best, best_cost = x, float(cost[i])
+        frontier = level
+    return SearchResult(state_from_arrays(g0, *best), best_cost, steps, evaluated, len(seen) - 1)
