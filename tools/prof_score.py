@@ -1,0 +1,21 @@
+"""Minimal driver for ncu: score one batch of candidates a few times."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2209_12769_b200 as P
+from paper_2209_12769_b200 import _native as N
+cfg = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+prec = N.FO_PREC_FP64 if (len(sys.argv) > 3 and sys.argv[3] == "fp64") else N.FO_PREC_FP32
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+torch.cuda.set_device(0)
+g, prof, comm, mp, lin = P.load_workload(cfg)
+cp = P.make_cost_providers(prof, comm, mp, precision=prec)
+dg = cp.device_graph(g)
+ng, rg, bk, gb = dg.make_candidates(np.arange(K, dtype=np.uint64))
+d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
+cost = torch.empty(K, dtype=torch.float64, device="cuda"); st = torch.empty(K, dtype=torch.int32, device="cuda")
+for _ in range(reps):
+    dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
+torch.cuda.synchronize()
+print("ok", float(cost.mean()), int(st.max()))
