@@ -68,8 +68,7 @@ __host__ __device__ inline MpLayout mp_layout(int layers) {
 
 // Per-warp workspace (one candidate at a time), byte offsets.
 struct WsLayout {
-    int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, p2ng,
-        p2nb, heapg, heapb, dur, fused, gptr, gmem, msort, lidx, nbptr, nb, H, P, gint, gin, gout, vis, zl;
+    int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, dur, fused, gptr, gmem, msort, lidx, nbptr, nb, H, P, gint, gin, gout, vis, zl, csim;
     int64_t total;
 };
 WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max);

@@ -55,10 +55,6 @@ WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max) {
     L.sptr = take(4 * (NM + 1));
     L.succ = take(4 * (int64_t)(pairs_max + 1));
     L.prank = take(4 * NM);
-    L.p2ng = take(4 * (2 * (int64_t)V + 1));
-    L.p2nb = take(4 * (int64_t)(A + 1));
-    L.heapg = take(8 * GM);
-    L.heapb = take(8 * (int64_t)(A + 1));
     L.dur = take(8 * NM);
     L.fused = take(4 * GM);
     L.gptr = take(4 * (GM + 1));
@@ -73,7 +69,8 @@ WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max) {
     L.gin = take(8 * GM);
     L.gout = take(8 * GM);
     L.vis = take(4 * (int64_t)V);
-    L.zl = take(4 * NM);
+    L.zl = take(4 * 2 * NM);
+    L.csim = take(4 * (NM + 2) * 2 + 8 * (int64_t)(pairs_max + 2) + 8 * (GM + A + 4) + 64);
     L.total = align8(o) + 128;
     return L;
 }
@@ -134,41 +131,6 @@ __device__ __forceinline__ double softplus_d(double z) {
     if (z == 0.0) return 0.6931471805599453;
     if (z > 0.0) return __dadd_rn(z, log1p(exp(-z)));
     return log1p(exp(z));
-}
-
-// ---------------------------------------------------------------------------
-// binary heaps of packed u64 keys (lane 0 only)
-
-__device__ __forceinline__ void heap_push(unsigned long long *h, int &n, unsigned long long k) {
-    int i = n++;
-    while (i > 0) {
-        int p = (i - 1) >> 1;
-        unsigned long long pk = h[p];
-        if (pk <= k) break;
-        h[i] = pk;
-        i = p;
-    }
-    h[i] = k;
-}
-__device__ __forceinline__ unsigned long long heap_pop(unsigned long long *h, int &n) {
-    unsigned long long top = h[0];
-    unsigned long long k = h[--n];
-    int i = 0;
-    for (;;) {
-        int l = 2 * i + 1;
-        if (l >= n) break;
-        unsigned long long lk = h[l];
-        int r = l + 1;
-        if (r < n) {
-            unsigned long long rk = h[r];
-            if (rk < lk) { lk = rk; l = r; }
-        }
-        if (k <= lk) break;
-        h[i] = lk;
-        i = l;
-    }
-    if (n > 0) h[i] = k;
-    return top;
 }
 
 // ---------------------------------------------------------------------------
@@ -254,13 +216,13 @@ __device__ double mp_forward(const DGraph &g, const int *mem, int n, const int *
 struct Ws {
     int *gmap, *bmap, *g2id, *b2id, *nn, *rr, *bki, *gmin, *gcnt, *bmin;
     long long *btot;
-    int *indeg, *scnt, *sptr, *succ, *prank, *p2ng, *p2nb;
-    unsigned long long *heapg, *heapb;
+    int *indeg, *scnt, *sptr, *succ, *prank;
     double *dur;
     int *fused, *gptr, *gmem, *msort, *lidx, *nbptr, *nb;
     char *H, *P;
     long long *gint, *gin, *gout;
     int *vis, *zl;
+    char *csim;
 };
 
 __device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) {
@@ -281,10 +243,6 @@ __device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) {
     w.sptr = (int *)(base + L.sptr);
     w.succ = (int *)(base + L.succ);
     w.prank = (int *)(base + L.prank);
-    w.p2ng = (int *)(base + L.p2ng);
-    w.p2nb = (int *)(base + L.p2nb);
-    w.heapg = (unsigned long long *)(base + L.heapg);
-    w.heapb = (unsigned long long *)(base + L.heapb);
     w.dur = (double *)(base + L.dur);
     w.fused = (int *)(base + L.fused);
     w.gptr = (int *)(base + L.gptr);
@@ -300,6 +258,7 @@ __device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) {
     w.gout = (long long *)(base + L.gout);
     w.vis = (int *)(base + L.vis);
     w.zl = (int *)(base + L.zl);
+    w.csim = base + L.csim;
     return w;
 }
 
@@ -324,6 +283,156 @@ __device__ __forceinline__ int export_of(const Ws &w, int op) { return w.rr[op] 
 // status packed with the failing node so a warp min picks the first node in
 // schedule order (simulator.py:62 evaluates durations in node order)
 __device__ __forceinline__ long long pack_bad(int node, int code) { return ((long long)node << 8) | code; }
+
+// Ready-set keys: (level, prank, node) packed in a u64 -- level counts the
+// distinct completion times so far, so (level, prank) orders exactly like the
+// reference's (rt, tiebreak, id) heap entries (simulator.py:63-77, :95-96).
+// Keys are pushed in non-decreasing level order, so each lane's ready set is
+// an insertion-sorted run [head, tail) of one array: O(1) pops, and a push
+// only moves past same-level entries.
+constexpr int kKeyNodeBits = 20;
+__device__ __forceinline__ unsigned long long make_key(unsigned long long level, unsigned prank, unsigned node) {
+    return (level << 40) | ((unsigned long long)prank << kKeyNodeBits) | node;
+}
+__device__ __forceinline__ void ready_push(unsigned long long *buf, int head, int &tail, unsigned long long key) {
+    int i = tail++;
+    while (i > head) {
+        unsigned long long p = buf[i - 1];
+        if (p <= key) break;
+        buf[i] = p;
+        i--;
+    }
+    buf[i] = key;
+}
+
+// successor entry -> (prank, node)
+template <typename SE>
+__device__ __forceinline__ unsigned se_node(SE e);
+template <>
+__device__ __forceinline__ unsigned se_node<uint32_t>(uint32_t e) { return e & 0xffffu; }
+template <>
+__device__ __forceinline__ unsigned se_node<unsigned long long>(unsigned long long e) { return (unsigned)(e & 0xfffffu); }
+template <typename SE>
+__device__ __forceinline__ unsigned se_prank(SE e);
+template <>
+__device__ __forceinline__ unsigned se_prank<uint32_t>(uint32_t e) { return e >> 16; }
+template <>
+__device__ __forceinline__ unsigned se_prank<unsigned long long>(unsigned long long e) { return (unsigned)(e >> 20); }
+template <typename SE>
+__device__ __forceinline__ SE se_make(unsigned prank, unsigned node);
+template <>
+__device__ __forceinline__ uint32_t se_make<uint32_t>(unsigned prank, unsigned node) { return (prank << 16) | node; }
+template <>
+__device__ __forceinline__ unsigned long long se_make<unsigned long long>(unsigned prank, unsigned node) {
+    return ((unsigned long long)prank << 20) | node;
+}
+
+template <bool TL, typename IT, typename SE>
+__device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const double *__restrict__ dur,
+                                           const IT *__restrict__ sptr, IT *__restrict__ indeg,
+                                           const SE *__restrict__ succ, unsigned long long *__restrict__ bufg,
+                                           unsigned long long *__restrict__ bufb, const Ws &w, int G, int N, int hg,
+                                           int hb) {
+    int headg = 0, tailg = hg, headb = 0, tailb = hb;
+    int run0 = -1, run1 = -1, done = 0, nc = 0, nb = 0, st = FO_OK;
+    double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
+    unsigned long long level = 0;
+    for (;;) {
+        // start_available (simulator.py:98-115): compute lane, then comm lane;
+        // start = max(now, rt) = now because rt is a drained completion time
+        if (run0 < 0 && headg < tailg) {
+            unsigned node = (unsigned)(bufg[headg++] & ((1u << kKeyNodeBits) - 1));
+            end0 = __dadd_rn(now, dur[node]);
+            run0 = (int)node;
+            mk = fmax(mk, end0);
+            if (TL) { a.tl.c_id[nc] = w.g2id[node]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
+        }
+        if (run1 < 0 && headb < tailb) {
+            unsigned node = (unsigned)(bufb[headb++] & ((1u << kKeyNodeBits) - 1));
+            end1 = __dadd_rn(now, dur[node]);
+            run1 = (int)node;
+            mk = fmax(mk, end1);
+            if (TL) { a.tl.b_id[nb] = w.b2id[node - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
+        }
+        if (run0 < 0 && run1 < 0) {
+            if (done != N) st = FO_CYCLE;  // simulator.py:133
+            break;
+        }
+        // advance to the next completion and drain every lane ending there
+        // (simulator.py:122-132); equal ends share one level
+        now = run0 < 0 ? end1 : (run1 < 0 ? end0 : fmin(end0, end1));
+        if (now > last) { last = now; level++; }
+#pragma unroll
+        for (int t = 0; t < 2; t++) {
+            int node = t == 0 ? run0 : run1;
+            if (node < 0 || (t == 0 ? end0 : end1) != now) continue;
+            if (t == 0) run0 = -1; else run1 = -1;
+            done++;
+            const int qe = sptr[node + 1];
+            for (int q = sptr[node]; q < qe; q++) {  // finish_node (simulator.py:88-96)
+                SE e = succ[q];
+                unsigned s = se_node<SE>(e);
+                IT d = indeg[s] - 1;
+                indeg[s] = d;
+                if (d == 0) {
+                    unsigned long long key = make_key(level, se_prank<SE>(e), s);
+                    if ((int)s < G) ready_push(bufg, headg, tailg, key);
+                    else ready_push(bufb, headb, tailb, key);
+                }
+            }
+        }
+    }
+    a.cost_out[k] = st == FO_OK ? mk : 0.0;
+    a.status_out[k] = st;
+    if (TL) { *a.tl.n_c = nc; *a.tl.n_b = nb; }
+    if (a.bad_out) *a.bad_out = -1;
+}
+
+template <typename IT, typename SE>
+__device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lane, int G, int N) {
+    // compact copies of the contracted DAG for the serial loop: narrow indices,
+    // successor entries carrying the successor's tie-break rank
+    IT *sptr = (IT *)w.csim;
+    IT *indeg = sptr + (N + 2);
+    SE *succ = (SE *)(((uintptr_t)(indeg + N + 2) + 15) & ~uintptr_t(15));
+    const int P = w.sptr[N];
+    unsigned long long *bufg = (unsigned long long *)(((uintptr_t)(succ + P + 1) + 15) & ~uintptr_t(15));
+    unsigned long long *bufb = bufg + G + 1;
+    for (int i = lane; i <= N; i += 32) sptr[i] = (IT)w.sptr[i];
+    for (int i = lane; i < N; i += 32) indeg[i] = (IT)w.indeg[i];
+    for (int q = lane; q < P; q += 32) {
+        int s = w.succ[q];
+        succ[q] = se_make<SE>((unsigned)w.prank[s], (unsigned)s);
+    }
+    // initial ready set: nodes with no deps at rt = 0.0 (level 0), keys sorted
+    int hg = 0, hb = 0;
+    for (int base = 0; base < N; base += 32) {
+        int i = base + lane;
+        bool z = i < N && w.indeg[i] == 0;
+        bool zg = z && i < G;
+        unsigned mg = __ballot_sync(FULL, zg), mb = __ballot_sync(FULL, z && !zg);
+        if (zg) w.zl[hg + __popc(mg & lanemask_lt())] = i;
+        if (z && !zg) w.zl[N + hb + __popc(mb & lanemask_lt())] = i;
+        hg += __popc(mg);
+        hb += __popc(mb);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int t = 0;
+        for (int q = 0; q < hg; q++) {
+            int i = w.zl[q];
+            ready_push(bufg, 0, t, make_key(0, (unsigned)w.prank[i], (unsigned)i));
+        }
+        t = 0;
+        for (int q = 0; q < hb; q++) {
+            int i = w.zl[N + q];
+            ready_push(bufb, 0, t, make_key(0, (unsigned)w.prank[i], (unsigned)i));
+        }
+        if (a.tl.c_id) event_loop<true, IT, SE>(a, k, w.dur, sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
+        else event_loop<false, IT, SE>(a, k, w.dur, sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
+    }
+    __syncwarp();
+}
 
 template <typename T>
 __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane) {
@@ -440,12 +549,10 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane) {
         int sub = (other >= 0 && w.gmin[other] == t && other < gi) ? 1 : 0;
         int pr = 2 * t + sub;
         w.prank[gi] = pr;
-        w.p2ng[pr] = gi;
     }
     for (int b = lane; b < B; b += 32) {
         int pr = w.bmin[b];
         w.prank[G + b] = pr;
-        w.p2nb[pr] = G + b;
     }
 
     // ---- K2: durations of every node (simulator.py:62)
@@ -715,95 +822,17 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane) {
     }
 
     // ---- K3: two-lane discrete-event simulation (simulator.py:66-140)
-    // initial ready set: nodes with no deps, rt = 0.0 (level 0)
-    int nz = 0;
-    for (int base = 0; base < N; base += 32) {
-        int i = base + lane;
-        bool z = i < N && w.indeg[i] == 0;
-        unsigned m = __ballot_sync(FULL, z);
-        if (z) w.zl[nz + __popc(m & lanemask_lt())] = i;
-        nz += __popc(m);
+    const bool small = N < 65536 && w.sptr[N] < 65536 && 2 * V < 65536;
+    if (!small && (N >= (1 << kKeyNodeBits) || 2 * V >= (1 << kKeyNodeBits))) {
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_UNSUPPORTED; }
+        return;
     }
-    __syncwarp();
-    if (lane == 0) {
-        int hg = 0, hb = 0;
-        for (int q = 0; q < nz; q++) {
-            int i = w.zl[q];
-            unsigned long long key = (unsigned long long)w.prank[i];  // level 0
-            if (i < G) heap_push(w.heapg, hg, key);
-            else heap_push(w.heapb, hb, key);
-        }
-        int run0 = -1, run1 = -1;
-        double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
-        unsigned long long level = 0;
-        int done = 0, st = FO_OK, nc = 0, nb = 0;
-        const bool want_tl = a.tl.c_id != nullptr;
-        while (done < N) {
-            // drain every completion with end <= now (simulator.py:122-125); at
-            // most one per lane, all with end == now, so their order is immaterial
-#pragma unroll
-            for (int lane_t = 0; lane_t < 2; lane_t++) {
-                int node = lane_t == 0 ? run0 : run1;
-                double en = lane_t == 0 ? end0 : end1;
-                if (node >= 0 && en <= now) {
-                    if (lane_t == 0) run0 = -1; else run1 = -1;
-                    done++;
-                    if (en > last) { last = en; level++; }
-                    // release successors (simulator.py:88-96); rt = en = max finish of deps
-                    for (int q = w.sptr[node]; q < w.sptr[node + 1]; q++) {
-                        int s = w.succ[q];
-                        int dg = w.indeg[s] - 1;
-                        w.indeg[s] = dg;
-                        if (dg == 0) {
-                            unsigned long long key = (level << 32) | (unsigned)w.prank[s];
-                            if (s < G) heap_push(w.heapg, hg, key);
-                            else heap_push(w.heapb, hb, key);
-                        }
-                    }
-                }
-            }
-            if (done >= N) break;
-            bool started = false;
-            // compute lane, then comm lane (simulator.py:101); start = max(now, rt) = now
-            if (run0 < 0 && hg > 0) {
-                unsigned long long key = heap_pop(w.heapg, hg);
-                int node = w.p2ng[(unsigned)(key & 0xffffffffu)];
-                end0 = __dadd_rn(now, w.dur[node]);
-                run0 = node;
-                if (end0 > mk) mk = end0;
-                if (want_tl) { a.tl.c_id[nc] = w.g2id[node]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; }
-                nc++;
-                started = true;
-            }
-            if (run1 < 0 && hb > 0) {
-                unsigned long long key = heap_pop(w.heapb, hb);
-                int node = w.p2nb[(unsigned)(key & 0xffffffffu)];
-                end1 = __dadd_rn(now, w.dur[node]);
-                run1 = node;
-                if (end1 > mk) mk = end1;
-                if (want_tl) { a.tl.b_id[nb] = w.b2id[node - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; }
-                nb++;
-                started = true;
-            }
-            if (started) continue;
-            if (run0 >= 0 || run1 >= 0) {  // advance to the next completion (simulator.py:130-132)
-                double t0 = run0 >= 0 ? end0 : DBL_MAX, t1 = run1 >= 0 ? end1 : DBL_MAX;
-                now = t0 < t1 ? t0 : t1;
-                continue;
-            }
-            st = FO_CYCLE;  // simulator.py:133
-            break;
-        }
-        a.cost_out[k] = st == FO_OK ? mk : 0.0;
-        a.status_out[k] = st;
-        if (want_tl) { *a.tl.n_c = nc; *a.tl.n_b = nb; }
-        if (a.bad_out) *a.bad_out = -1;
-    }
-    __syncwarp();
+    if (small) simulate_compact<uint16_t, uint32_t>(a, k, w, lane, G, N);
+    else simulate_compact<uint32_t, unsigned long long>(a, k, w, lane, G, N);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) score_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 4) score_kernel(ScoreArgs a) {
     const int lane = threadIdx.x & 31;
     const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int nw = gridDim.x * kWarps;
