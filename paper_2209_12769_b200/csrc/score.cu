@@ -70,7 +70,7 @@ WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max) {
     L.gout = take(8 * GM);
     L.vis = take(4 * (int64_t)V);
     L.zl = take(4 * 2 * NM);
-    L.csim = take(4 * (NM + 2) * 2 + 8 * (int64_t)(pairs_max + 2) + 8 * (GM + A + 4) + 64);
+    L.csim = take(4 * (NM + 2) * 2 + 8 * (int64_t)(pairs_max + 2) + 24 * (GM + A + 4) + 64);
     L.total = align8(o) + 128;
     return L;
 }
@@ -294,15 +294,22 @@ constexpr int kKeyNodeBits = 20;
 __device__ __forceinline__ unsigned long long make_key(unsigned long long level, unsigned prank, unsigned node) {
     return (level << 40) | ((unsigned long long)prank << kKeyNodeBits) | node;
 }
-__device__ __forceinline__ void ready_push(unsigned long long *buf, int head, int &tail, unsigned long long key) {
+// A ready entry carries everything the loop needs when the node starts and
+// completes, loaded when the node is released (off the pop critical path).
+struct ReadyEnt {
+    unsigned long long key;
+    double dur;
+    unsigned sb, se;  // successor range
+};
+__device__ __forceinline__ void ready_push(ReadyEnt *buf, int head, int &tail, const ReadyEnt &x) {
     int i = tail++;
     while (i > head) {
-        unsigned long long p = buf[i - 1];
-        if (p <= key) break;
+        ReadyEnt p = buf[i - 1];
+        if (p.key <= x.key) break;
         buf[i] = p;
         i--;
     }
-    buf[i] = key;
+    buf[i] = x;
 }
 
 // successor entry -> (prank, node)
@@ -330,29 +337,33 @@ __device__ __forceinline__ unsigned long long se_make<unsigned long long>(unsign
 template <bool TL, typename IT, typename SE>
 __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const double *__restrict__ dur,
                                            const IT *__restrict__ sptr, IT *__restrict__ indeg,
-                                           const SE *__restrict__ succ, unsigned long long *__restrict__ bufg,
-                                           unsigned long long *__restrict__ bufb, const Ws &w, int G, int N, int hg,
-                                           int hb) {
+                                           const SE *__restrict__ succ, ReadyEnt *__restrict__ bufg,
+                                           ReadyEnt *__restrict__ bufb, const Ws &w, int G, int N, int hg, int hb) {
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     int run0 = -1, run1 = -1, done = 0, nc = 0, nb = 0, st = FO_OK;
+    unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
     double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
     unsigned long long level = 0;
     for (;;) {
         // start_available (simulator.py:98-115): compute lane, then comm lane;
         // start = max(now, rt) = now because rt is a drained completion time
         if (run0 < 0 && headg < tailg) {
-            unsigned node = (unsigned)(bufg[headg++] & ((1u << kKeyNodeBits) - 1));
-            end0 = __dadd_rn(now, dur[node]);
-            run0 = (int)node;
-            mk = fmax(mk, end0);
-            if (TL) { a.tl.c_id[nc] = w.g2id[node]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
+            ReadyEnt x = bufg[headg++];
+            run0 = (int)(x.key & ((1u << kKeyNodeBits) - 1));
+            end0 = __dadd_rn(now, x.dur);
+            sb0 = x.sb;
+            se0 = x.se;
+            if (end0 > mk) mk = end0;
+            if (TL) { a.tl.c_id[nc] = w.g2id[run0]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
         }
         if (run1 < 0 && headb < tailb) {
-            unsigned node = (unsigned)(bufb[headb++] & ((1u << kKeyNodeBits) - 1));
-            end1 = __dadd_rn(now, dur[node]);
-            run1 = (int)node;
-            mk = fmax(mk, end1);
-            if (TL) { a.tl.b_id[nb] = w.b2id[node - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
+            ReadyEnt x = bufb[headb++];
+            run1 = (int)(x.key & ((1u << kKeyNodeBits) - 1));
+            end1 = __dadd_rn(now, x.dur);
+            sb1 = x.sb;
+            se1 = x.se;
+            if (end1 > mk) mk = end1;
+            if (TL) { a.tl.b_id[nb] = w.b2id[run1 - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
         }
         if (run0 < 0 && run1 < 0) {
             if (done != N) st = FO_CYCLE;  // simulator.py:133
@@ -360,24 +371,28 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
         }
         // advance to the next completion and drain every lane ending there
         // (simulator.py:122-132); equal ends share one level
-        now = run0 < 0 ? end1 : (run1 < 0 ? end0 : fmin(end0, end1));
+        now = run0 < 0 ? end1 : (run1 < 0 ? end0 : (end0 < end1 ? end0 : end1));
         if (now > last) { last = now; level++; }
 #pragma unroll
         for (int t = 0; t < 2; t++) {
-            int node = t == 0 ? run0 : run1;
-            if (node < 0 || (t == 0 ? end0 : end1) != now) continue;
+            if ((t == 0 ? run0 : run1) < 0 || (t == 0 ? end0 : end1) != now) continue;
+            const unsigned qb = t == 0 ? sb0 : sb1, qe = t == 0 ? se0 : se1;
             if (t == 0) run0 = -1; else run1 = -1;
             done++;
-            const int qe = sptr[node + 1];
-            for (int q = sptr[node]; q < qe; q++) {  // finish_node (simulator.py:88-96)
+            for (unsigned q = qb; q < qe; q++) {  // finish_node (simulator.py:88-96)
                 SE e = succ[q];
                 unsigned s = se_node<SE>(e);
+                // issue the release-time loads together with the indegree load
                 IT d = indeg[s] - 1;
+                ReadyEnt x;
+                x.dur = dur[s];
+                x.sb = sptr[s];
+                x.se = sptr[s + 1];
                 indeg[s] = d;
                 if (d == 0) {
-                    unsigned long long key = make_key(level, se_prank<SE>(e), s);
-                    if ((int)s < G) ready_push(bufg, headg, tailg, key);
-                    else ready_push(bufb, headb, tailb, key);
+                    x.key = make_key(level, se_prank<SE>(e), s);
+                    if ((int)s < G) ready_push(bufg, headg, tailg, x);
+                    else ready_push(bufb, headb, tailb, x);
                 }
             }
         }
@@ -396,8 +411,8 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lan
     IT *indeg = sptr + (N + 2);
     SE *succ = (SE *)(((uintptr_t)(indeg + N + 2) + 15) & ~uintptr_t(15));
     const int P = w.sptr[N];
-    unsigned long long *bufg = (unsigned long long *)(((uintptr_t)(succ + P + 1) + 15) & ~uintptr_t(15));
-    unsigned long long *bufb = bufg + G + 1;
+    ReadyEnt *bufg = (ReadyEnt *)(((uintptr_t)(succ + P + 1) + 15) & ~uintptr_t(15));
+    ReadyEnt *bufb = bufg + G + 1;
     for (int i = lane; i <= N; i += 32) sptr[i] = (IT)w.sptr[i];
     for (int i = lane; i < N; i += 32) indeg[i] = (IT)w.indeg[i];
     for (int q = lane; q < P; q += 32) {
@@ -419,14 +434,15 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lan
     __syncwarp();
     if (lane == 0) {
         int t = 0;
-        for (int q = 0; q < hg; q++) {
-            int i = w.zl[q];
-            ready_push(bufg, 0, t, make_key(0, (unsigned)w.prank[i], (unsigned)i));
-        }
-        t = 0;
-        for (int q = 0; q < hb; q++) {
-            int i = w.zl[N + q];
-            ready_push(bufb, 0, t, make_key(0, (unsigned)w.prank[i], (unsigned)i));
+        for (int q = 0; q < hg + hb; q++) {
+            int i = q < hg ? w.zl[q] : w.zl[N + q - hg];
+            ReadyEnt x;
+            x.key = make_key(0, (unsigned)w.prank[i], (unsigned)i);
+            x.dur = w.dur[i];
+            x.sb = (unsigned)w.sptr[i];
+            x.se = (unsigned)w.sptr[i + 1];
+            if (q == hg) t = 0;
+            ready_push(q < hg ? bufg : bufb, 0, t, x);
         }
         if (a.tl.c_id) event_loop<true, IT, SE>(a, k, w.dur, sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
         else event_loop<false, IT, SE>(a, k, w.dur, sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);

@@ -133,8 +133,15 @@ class DeviceCostProviders:
     def device_graph(self, g: HloGraph):
         from .device import DeviceGraph
 
-        key = (id(g.ops), id(g.edges), tuple((a.id, a.producer_op, a.tensor_bytes) for a in g.allreduces))
+        ar_key = tuple((a.id, a.producer_op, a.tensor_bytes) for a in g.allreduces)
+        key = (id(g.ops), id(g.edges), ar_key)
         ent = self._graphs.get(key)
+        if ent is None:  # same static content under new tuples (e.g. build_graph copies)
+            ckey = ("content", hash(g.ops), hash(g.edges), ar_key)
+            ent = self._graphs.get(ckey)
+            if ent is not None and ent[1] == g.ops and ent[2] == g.edges:
+                self._graphs[key] = (ent[0], g.ops, g.edges)
+                return ent[0]
         if ent is None:
             op_time = None
             if self.kind == "profile":
@@ -146,6 +153,7 @@ class DeviceCostProviders:
             dg = DeviceGraph(g, self._cost_model, op_time)
             ent = (dg, g.ops, g.edges)  # keep ops/edges alive so ids stay unique
             self._graphs[key] = ent
+            self._graphs[("content", hash(g.ops), hash(g.edges), ar_key)] = ent
         return ent[0]
 
     def _cost_model(self, static, keep):

@@ -335,14 +335,38 @@ def section_search(only=None):
               f"best={res.best_cost_us:.3f} in {wall:.1f}s", flush=True)
 
 
+def section_exhaustive(_=None):
+    """exhaustive_search (search.py:158-225) on small graphs, hardware-oracle
+    and analytic providers; mirrors test_exhaustive_dominates_backtracking."""
+    from fuseopt import exhaustive_search
+
+    out = []
+    rng = random.Random(5)
+    hw = HardwareParams()
+    for seed in range(8):
+        spec = WorkloadSpec(family=["chain", "residual", "attention", "recurrent"][seed % 4],
+                            op_count=rng.randrange(4, 9), tensor_count=rng.randrange(0, 3), seed=seed)
+        g = gen_workload(spec, hw)
+        profile, _ = make_profile(g, hw)
+        for prov_name, cp in (("oracle", oracle_providers(hw)),
+                              ("analytic", make_cost_providers(profile, hw.comm_params, analytic_model(5.0, 1 / 1024)))):
+            res = exhaustive_search(g, cp)
+            out.append({"graph": graph_to_doc(g), "profile": [[k[0], k[1], v] for k, v in sorted(profile.times.items())],
+                        "provider": prov_name, "best_cost_us": res.best_cost_us,
+                        "candidates_evaluated": res.candidates_evaluated, "steps": res.steps,
+                        "best_state": state_doc(res.best_graph)})
+    _dump_gz(os.path.join(OUT, "exhaustive.json.gz"), out)
+    print(f"exhaustive: {len(out)} cases", flush=True)
+
+
 def main(argv):
-    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search")]
+    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive")]
     names = [a for a in argv if a not in sections]
     if not sections:
-        sections = ["workloads", "rng", "cases", "search"]
+        sections = ["workloads", "rng", "cases", "search", "exhaustive"]
     for s in sections:
-        {"workloads": section_workloads, "rng": section_rng,
-         "cases": section_cases, "search": section_search}[s](names or None) if s != "rng" else section_rng()
+        {"workloads": section_workloads, "rng": lambda _: section_rng(), "exhaustive": section_exhaustive,
+         "cases": section_cases, "search": section_search}[s](names or None)
 
 
 if __name__ == "__main__":

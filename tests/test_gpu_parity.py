@@ -1,0 +1,275 @@
+"""Device parity: the CUDA scoring path (C-ABI library) against the reference's
+golden vectors and the CPU oracle on the same inputs.  Run on a B200 with
+``pytest -m gpu``.
+
+Tolerances: fp32 message-passing estimator <= 1e-4 relative (north star);
+fp64 estimator <= 1e-12 relative (different summation order than OpenBLAS);
+analytic / hardware-oracle / linear providers and every schedule are fp64
+max/+ arithmetic: bit-exact (rel 0) except linear (log1p, 1e-12).
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+import paper_2209_12769_b200 as P
+from paper_2209_12769_b200 import _native as N
+from paper_2209_12769_b200.graph import DataEdge, FusionGroup, OpNode, build_graph
+
+from _golden import canon_doc, canon_graph, cases, graph_with_state, read
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["chain24", "residual40", "attention36", "recurrent30", "vgg16", "resnet50", "bert"]
+TOL = {("mp", N.FO_PREC_FP32): 1e-4, ("mp", N.FO_PREC_FP64): 1e-12, ("lin", N.FO_PREC_FP32): 1e-12,
+       ("lin", N.FO_PREC_FP64): 1e-12, ("analytic", N.FO_PREC_FP32): 0.0, ("analytic", N.FO_PREC_FP64): 0.0,
+       ("oracle", N.FO_PREC_FP32): 0.0, ("oracle", N.FO_PREC_FP64): 0.0}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    import torch
+
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    torch.cuda.set_device(0)
+
+
+def providers(name, precision):
+    g, prof, comm, mp, lin = P.load_workload(name)
+    return g, {
+        "mp": P.make_cost_providers(prof, comm, mp, precision=precision),
+        "lin": P.make_cost_providers(prof, comm, lin, precision=precision),
+        "analytic": P.make_cost_providers(prof, comm, P.analytic_model(5.0, 1 / 1024), precision=precision),
+        "oracle": P.oracle_providers(P.HardwareParams(), precision=precision),
+    }
+
+
+@pytest.mark.parametrize("precision", [N.FO_PREC_FP32, N.FO_PREC_FP64])
+@pytest.mark.parametrize("name", SMALL + ["gpt2m", "synth50k"])
+def test_costs_match_reference(name, precision):
+    g, cps = providers(name, precision)
+    doc = cases(name)
+    graphs = [graph_with_state(g, c["state"]) for c in doc["candidates"]]
+    for pname, cp in cps.items():
+        got = P.cost_batch(graphs, cp)
+        ref = np.array([c["cost"][pname] for c in doc["candidates"]])
+        tol = TOL[(pname, precision)]
+        np.testing.assert_allclose(got, ref, rtol=tol, atol=0, err_msg=f"{name}/{pname}")
+        assert P.cost(g, cp) == pytest.approx(doc["base_cost"][pname], rel=tol, abs=0)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_fused_group_predictions_match_predict_fused(name):
+    for precision in (N.FO_PREC_FP32, N.FO_PREC_FP64):
+        g, cps = providers(name, precision)
+        for c in cases(name)["candidates"][:16]:
+            cand = graph_with_state(g, c["state"])
+            for pname in ("mp", "lin", "analytic", "oracle"):
+                pred = P.predict_fused_groups(cps[pname], cand)
+                for f in c["fused"]:
+                    assert pred[f["id"]] == pytest.approx(f[pname], rel=max(TOL[(pname, precision)], 1e-15))
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_timelines_match_reference(name):
+    g, cps = providers(name, N.FO_PREC_FP64)
+    for c in cases(name)["candidates"]:
+        if "timeline" not in c:
+            continue
+        tl = P.simulate(graph_with_state(g, c["state"]), cps["mp"])
+        ref = c["timeline"]
+        assert [e[0] for e in tl.compute_events] == [e[0] for e in ref["compute"]]
+        assert [e[0] for e in tl.comm_events] == [e[0] for e in ref["comm"]]
+        for a, b in zip(tl.compute_events + tl.comm_events, [tuple(x) for x in ref["compute"] + ref["comm"]]):
+            assert a[1] == pytest.approx(b[1], rel=1e-12, abs=1e-9) and a[2] == pytest.approx(b[2], rel=1e-12, abs=1e-9)
+        assert tl.makespan_us == pytest.approx(ref["makespan"], rel=1e-12)
+
+
+def test_full_batch_against_oracle_and_bounds():
+    """BASELINE configs[1] at full size: 4096 ResNet-50 candidates scored in one
+    batch; a 512-candidate sample checked against the C oracle, and every
+    candidate against the size-independent bounds fo <= cost <= sum (test_simulator.py:112-122)."""
+    from oracle.oracle import Oracle, load_workload
+
+    g, cps = providers("resnet50", N.FO_PREC_FP32)
+    cp = cps["mp"]
+    dg = cp.device_graph(g)
+    ng, rg, bk, gb = dg.make_candidates(np.arange(4096, dtype=np.uint64))
+    cost, st = dg.score_host(ng, rg, bk, gb, N.FO_PREC_FP32)
+    assert (st == 0).all()
+    o = Oracle(load_workload("resnet50"), "mp")
+    idx = np.arange(0, 4096, 8)
+    sts, ref = o.cost_batch(*(np.stack([o.make_candidate(int(i))[j] for i in idx]) for j in range(3)))
+    assert (sts == 0).all()
+    np.testing.assert_allclose(cost[idx], ref, rtol=1e-4)
+    # bounds through the durations the device used
+    for k in range(0, 4096, 64):
+        st2, dur, G, bad = dg.node_durations_arrays(ng[k], rg[k], bk[k], gb, N.FO_PREC_FP32)
+        B = len(set(bk[k].tolist()))
+        lo = max(dur[:G].sum(), dur[G:G + B].sum())
+        assert lo <= cost[k] * (1 + 1e-12) and cost[k] <= dur[:G + B].sum() * (1 + 1e-12)
+
+
+def test_device_and_host_entry_points_agree():
+    import torch
+
+    g, cps = providers("bert", N.FO_PREC_FP32)
+    dg = cps["mp"].device_graph(g)
+    ng, rg, bk, gb = dg.make_candidates(np.arange(300, dtype=np.uint64))
+    c1, s1 = dg.score_host(ng, rg, bk, gb)
+    d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
+    c2 = torch.empty(300, dtype=torch.float64, device="cuda")
+    s2 = torch.empty(300, dtype=torch.int32, device="cuda")
+    dg.score_device(d[0], d[1], d[2], gb, c2, s2)
+    torch.cuda.synchronize()
+    assert np.array_equal(c1, c2.cpu().numpy()) and np.array_equal(s1, s2.cpu().numpy())
+
+
+@pytest.mark.parametrize("path", [p for p in __import__("glob").glob(
+    __import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "search", "*.search.json.gz"))],
+    ids=lambda p: p.split("/")[-1].split(".search")[0])
+def test_search_trace_bit_exact(path):
+    d = read(path.split("golden/")[1])
+    g, cps = providers(d["workload"], N.FO_PREC_FP64)
+    cfg = P.SearchConfig(alpha=d["cfg"]["alpha"], beta=d["cfg"]["beta"], max_unchanged=d["cfg"]["max_unchanged"],
+                         seed=d["cfg"]["seed"])
+    r = P.backtracking_search(g, cfg, cps[d["provider"]])
+    assert (r.steps, r.candidates_evaluated, r.candidates_enqueued) == (
+        d["steps"], d["candidates_evaluated"], d["candidates_enqueued"])
+    assert len(r.trace) == len(d["trace"])
+    for a, b in zip(r.trace, d["trace"]):
+        assert (a.step, a.action, a.queue_len, a.enqueued) == (b[0], b[1], b[4], b[5])
+        assert a.cost_us == pytest.approx(b[2], rel=1e-12) and a.best_cost_us == pytest.approx(b[3], rel=1e-12)
+    assert canon_graph(r.best_graph) == canon_doc(g, d["best_state"])
+    assert r.best_cost_us == pytest.approx(d["best_cost_us"], rel=1e-12)
+
+
+@pytest.mark.parametrize("name,prov", [("chain24", "mp"), ("residual40", "analytic"), ("recurrent30", "oracle")])
+def test_lockstep_seeds_equal_single_seed_oracle(name, prov):
+    """R lock-stepped searches scored in shared batches: each seed's trajectory
+    equals the oracle's single-seed Alg. 1 run with that seed."""
+    from oracle.oracle import Oracle, load_workload
+
+    g, cps = providers(name, N.FO_PREC_FP64)
+    cfg = P.SearchConfig(alpha=1.05, beta=6, max_unchanged=50)
+    seeds = list(range(12))
+    res = P.lockstep_search(g, cfg, cps[prov], seeds)
+    o = Oracle(load_workload(name), prov)
+    for s, r in zip(seeds, res):
+        ref = o.search(alpha=1.05, beta=6, max_unchanged=50, seed=s)
+        assert (r.steps, r.candidates_evaluated, r.candidates_enqueued) == (
+            ref["steps"], ref["candidates_evaluated"], ref["candidates_enqueued"])
+        assert [(t.step, t.action, t.queue_len, t.enqueued) for t in r.trace] == [
+            (t[0], t[1], t[4], t[5]) for t in ref["trace"]]
+        np.testing.assert_allclose([t.cost_us for t in r.trace], [t[2] for t in ref["trace"]], rtol=1e-12)
+
+
+def test_exhaustive_search_matches_reference():
+    from paper_2209_12769_b200.graph import graph_from_doc
+
+    for case in read("exhaustive.json.gz"):
+        g = graph_from_doc(case["graph"])
+        if case["provider"] == "oracle":
+            cp = P.oracle_providers(P.HardwareParams())
+        else:
+            prof = P.Profile({(a, b): v for a, b, v in case["profile"]})
+            cp = P.make_cost_providers(prof, P.CommModelParams(0.001, 100.0), P.analytic_model(5.0, 1 / 1024))
+        r = P.exhaustive_search(g, cp)
+        assert r.candidates_evaluated == case["candidates_evaluated"]
+        assert r.steps == case["steps"]
+        assert r.best_cost_us == pytest.approx(case["best_cost_us"], rel=1e-12)
+        assert canon_graph(r.best_graph) == canon_doc(g, case["best_state"])
+
+
+# ---- the reference's own simulator tests (test_simulator.py) through the device
+
+def op(i, code="Mul", kind="compute", out=1024, us=10.0, key=None):
+    return OpNode(id=i, op_code=code, kind=kind, input_shape_key=key if key is not None else f"k{i}",
+                  out_bytes=out, compute_us=us)
+
+
+def chain(n, us=10.0, out=1024, allreduces=()):
+    return build_graph([op(i, us=us, out=out) for i in range(n)], [DataEdge(i, i + 1, out) for i in range(n - 1)],
+                       allreduces)
+
+
+def fixed_costs(op_us=None, comm_us=None):
+    def op_cost(g, group):
+        return sum((op_us[m] if op_us is not None else (g.op(m).compute_us or 0.0)) for m in group.member_ops)
+
+    def comm_cost(g, bucket):
+        return 1.0 if comm_us is None else comm_us[bucket.id]
+
+    return P.CostProviders(op_cost=op_cost, comm_cost=comm_cost)
+
+
+def test_serial_chain():
+    tl = P.simulate(chain(2), fixed_costs(op_us={0: 10.0, 1: 20.0}))
+    assert tl.compute_events == ((0, 0.0, 10.0), (1, 10.0, 30.0)) and tl.makespan_us == 30.0
+
+
+def test_full_overlap_and_update_waits_for_bucket():
+    g = build_graph([op(0, us=10.0), op(1, us=20.0)], [], [(0, 0, 1000)])
+    tl = P.simulate(g, fixed_costs(comm_us={0: 15.0}))
+    assert tl.compute_events == ((0, 0.0, 10.0), (1, 10.0, 30.0)) and tl.comm_events == ((0, 10.0, 25.0),)
+    g = build_graph([op(0, us=10.0), op(2, code="ApplyGrad", us=5.0)], [DataEdge(0, 2, 1000)], [(0, 0, 1000)])
+    tl = P.simulate(g, fixed_costs(comm_us={0: 15.0}))
+    assert tl.comm_events == ((0, 10.0, 25.0),)
+    assert next(e for e in tl.compute_events if e[0] == 2) == (2, 25.0, 30.0) and tl.makespan_us == 30.0
+
+
+def test_comm_fifo_by_ready_time_and_zero_durations():
+    g = build_graph([op(0, us=5.0), op(1, us=50.0)], [], [(0, 1, 100), (1, 0, 100)])
+    tl = P.simulate(g, fixed_costs(comm_us={0: 10.0, 1: 10.0}))
+    assert tl.comm_events[0] == (1, 5.0, 15.0) and tl.comm_events[1] == (0, 55.0, 65.0)
+    tl = P.simulate(chain(2), fixed_costs(op_us={0: 0.0, 1: 0.0}))
+    assert tl.makespan_us == 0.0 and tl.compute_events == ((0, 0.0, 0.0), (1, 0.0, 0.0))
+
+
+def test_empty_graph_and_format_timeline():
+    assert P.cost(build_graph([], [], []), fixed_costs()) == 0.0
+    text = P.format_timeline(P.simulate(build_graph([op(0, us=10.0)], [], [(0, 0, 100)]), fixed_costs(comm_us={0: 4.0})))
+    lines = text.strip().splitlines()
+    assert lines[0] == "kind id start_us end_us" and lines[1].startswith("compute 0 0.000000")
+    assert lines[-1] == "makespan_us 14.000000"
+
+
+def test_bounds_on_random_graphs():
+    rng = random.Random(77)
+    for _ in range(60):
+        n = rng.randrange(2, 14)
+        ops = [op(i, us=round(rng.uniform(1, 40), 1), out=rng.randrange(256, 65536)) for i in range(n)]
+        edges = [DataEdge(i, j, 64) for j in range(1, n) for i in range(j) if rng.random() < 0.35]
+        ars = [(t, p, 1000) for t, p in enumerate(rng.sample(range(n), min(rng.randrange(0, 4), n)))]
+        g = build_graph(ops, edges, ars)
+        comm = {b.id: rng.uniform(0.5, 60.0) for b in g.buckets}
+        cp = fixed_costs(comm_us=comm)
+        c = P.cost(g, cp)
+        assert P.fo_bound(g, cp) <= c + 1e-9
+        assert c <= sum(o.compute_us for o in ops) + sum(comm.values()) + 1e-9
+
+
+def test_error_mapping():
+    g = chain(1)
+    with pytest.raises(ValueError):
+        P.simulate(g, P.CostProviders(op_cost=lambda g, gr: -1.0, comm_cost=lambda g, b: 1.0))
+
+    def boom(g, gr):
+        raise KeyError("nope")
+
+    with pytest.raises(P.MissingCost):
+        P.simulate(g, P.CostProviders(op_cost=boom, comm_cost=lambda g, b: 1.0))
+    # fused group with no estimator -> MissingCost (estimator.py:815-818)
+    fused = build_graph(chain(2).ops, chain(2).edges, groups=[FusionGroup(0, frozenset({0, 1}))])
+    prof = P.Profile({("Mul", "k0"): 10.0, ("Mul", "k1"): 12.0})
+    with pytest.raises(P.MissingCost):
+        P.cost(fused, P.make_cost_providers(prof, P.CommModelParams(0.0, 1.0), None))
+    # missing profile entry -> MissingCost via UnknownOp (simulator.py:45-46)
+    with pytest.raises(P.MissingCost):
+        P.cost(chain(2), P.make_cost_providers(P.Profile({("Mul", "k0"): 10.0}), P.CommModelParams(0.0, 1.0)))
+    # an update op fused into its gradient producer deadlocks -> CycleError (test_rewrite.py:216-224)
+    ops = [op(0, us=10.0), op(1, code="ApplyGrad", us=1.0)]
+    cyc = build_graph(ops, [DataEdge(0, 1, 100)], [(0, 0, 1000)], groups=[FusionGroup(0, frozenset({0, 1}))])
+    with pytest.raises(P.CycleError):
+        P.simulate(cyc, P.oracle_providers(P.HardwareParams()))
