@@ -365,6 +365,25 @@ static void group_io(const orc_static *s, const orc_index *ix, int64_t *internal
 }
 
 /* ------------------------------------------------------------------------ */
+/* CPython 3.12 built-in sum() over floats: Neumaier-compensated
+ * (Objects/bltinmodule.c builtin_sum_impl).  The reference sums member
+ * times with sum() (estimator.py:186, :442; workloads.py:284).              */
+
+typedef struct { double f, c; int n; } pysum_t;
+static void pysum_add(pysum_t *s, double x) {
+    if (s->n++ == 0) { s->f = 0.0 + x; s->c = 0.0; return; }
+    double t = s->f + x;
+    if (fabs(s->f) >= fabs(x)) s->c += (s->f - t) + x;
+    else s->c += (x - t) + s->f;
+    s->f = t;
+}
+static double pysum_get(const pysum_t *s) {
+    double f = s->f;
+    if (s->c != 0.0 && isfinite(s->c)) f += s->c;
+    return s->n ? f : 0.0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* estimator (estimator.py:131-470)                                          */
 
 static double softplus(double z) { /* np.logaddexp(0, z) */
@@ -409,13 +428,13 @@ static int predict_group(const orc_static *s, const orc_model *m, const orc_inde
     for (int i = 0; i < n; i++)
         if (isnan(s->op_prof[mem[i]])) return ORC_MISSING_COST; /* lookup -> UnknownOp */
     if (m->variant == VAR_ANALYTIC) { /* estimator.py:434-446 */
-        double sum = 0.0;
+        pysum_t acc = {0.0, 0.0, 0};
         for (int i = 0; i < n; i++) {
             int v = mem[i];
             double raw = (s->op_prof[v] - m->launch) - m->mem * (double)(s->in_bytes[v] + s->op_out_bytes[v]);
-            sum = sum + raw;
+            pysum_add(&acc, raw);
         }
-        double pred = (sum + m->launch) + m->mem * (double)(io_in[g] + io_out[g]);
+        double pred = (pysum_get(&acc) + m->launch) + m->mem * (double)(io_in[g] + io_out[g]);
         *out = pred > 1e-9 ? pred : 1e-9;
         return ORC_OK;
     }
@@ -432,8 +451,9 @@ static int predict_group(const orc_static *s, const orc_model *m, const orc_inde
     }
     int st = ORC_OK;
     if (m->variant == VAR_LINEAR) { /* estimator.py:117-128, 341-345, 421-426 */
-        double total = 0.0;
-        for (int i = 0; i < n; i++) total = total + s->op_prof[mem[i]];
+        pysum_t acc = {0.0, 0.0, 0};
+        for (int i = 0; i < n; i++) pysum_add(&acc, s->op_prof[mem[i]]);
+        double total = pysum_get(&acc);
         double agg[6] = {(double)n, total, (double)io_int[g], (double)io_in[g], (double)io_out[g],
                          (double)longest_path(n, ne, ls, ld)};
         double fs[12];
@@ -541,13 +561,13 @@ static int node_durations(const orc_static *s, const orc_model *m, const orc_ind
         double d = 0.0;
         if (m->provider == PROV_HW_ORACLE) { /* oracle_time, noise 0 (workloads.py:276-291) */
             int all_param = 1;
-            double comp = 0.0;
+            pysum_t acc = {0.0, 0.0, 0};
             for (int i = 0; i < n; i++) {
                 if (s->op_kind[mem[i]] != KIND_PARAMETER) all_param = 0;
                 double c = s->op_compute[mem[i]];
-                comp = comp + (isnan(c) ? 0.0 : c);
+                pysum_add(&acc, isnan(c) ? 0.0 : c);
             }
-            d = all_param ? 0.0 : (comp + m->launch) + m->mem * (double)(io_in[g] + io_out[g]);
+            d = all_param ? 0.0 : (pysum_get(&acc) + m->launch) + m->mem * (double)(io_in[g] + io_out[g]);
         } else if (n == 1) { /* estimator.py:810-814 */
             int v = mem[0];
             if (s->op_kind[v] == KIND_PARAMETER) d = 0.0;

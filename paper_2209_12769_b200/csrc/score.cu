@@ -126,6 +126,22 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// CPython 3.12 sum() over floats is Neumaier-compensated (bltinmodule.c
+// builtin_sum_impl); the reference sums member times with it
+// (estimator.py:186, :442; workloads.py:284).
+struct PySum {
+    double f = 0.0, c = 0.0;
+    int n = 0;
+    __device__ __forceinline__ void add(double x) {
+        if (n++ == 0) { f = x; return; }
+        double t = __dadd_rn(f, x);
+        if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+        else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+        f = t;
+    }
+    __device__ __forceinline__ double get() const { return (c != 0.0 && isfinite(c)) ? __dadd_rn(f, c) : f; }
+};
+
 // numpy logaddexp(0, z) (estimator.py:297-298)
 __device__ __forceinline__ double softplus_d(double z) {
     if (z == 0.0) return 0.6931471805599453;
@@ -695,15 +711,15 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane) {
                 if (hw) {  // oracle_time (workloads.py:281-291): sum in ascending member order
                     if (lane == 0) {
                         bool all_param = true;
-                        double comp = 0.0;
+                        PySum comp;
                         for (int i = 0; i < n; i++) {
                             int v = mem[i];
                             if (g.op_kind[v] != 1) all_param = false;
                             double c = g.op_compute[v];
-                            comp = __dadd_rn(comp, isnan(c) ? 0.0 : c);
+                            comp.add(isnan(c) ? 0.0 : c);
                         }
                         d = all_param ? 0.0
-                                      : __dadd_rn(__dadd_rn(comp, g.launch),
+                                      : __dadd_rn(__dadd_rn(comp.get(), g.launch),
                                                   __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
                     }
                     d = __shfl_sync(FULL, d, 0);
@@ -716,14 +732,14 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane) {
                 if (__any_sync(FULL, miss)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); continue; }
                 if (g.variant == FO_EST_ANALYTIC) {  // estimator.py:434-446
                     if (lane == 0) {
-                        double sum = 0.0;
+                        PySum sum;
                         for (int i = 0; i < n; i++) {
                             int v = mem[i];
                             double raw = __dsub_rn(__dsub_rn(g.op_prof[v], g.launch),
                                                    __dmul_rn(g.mem, (double)(g.op_in[v] + g.op_out[v])));
-                            sum = __dadd_rn(sum, raw);
+                            sum.add(raw);
                         }
-                        double pred = __dadd_rn(__dadd_rn(sum, g.launch), __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
+                        double pred = __dadd_rn(__dadd_rn(sum.get(), g.launch), __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
                         w.dur[gi] = pred > 1e-9 ? pred : 1e-9;
                     }
                     continue;
@@ -801,8 +817,9 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane) {
                         }
                         int lp = 0;
                         for (int i = 0; i < n; i++) lp = max(lp, depth[i]);
-                        double total = 0.0;
-                        for (int i = 0; i < n; i++) total = __dadd_rn(total, g.op_prof[mem[i]]);
+                        PySum tot;
+                        for (int i = 0; i < n; i++) tot.add(g.op_prof[mem[i]]);
+                        const double total = tot.get();
                         double agg[6] = {(double)n, total, (double)w.gint[gi], (double)w.gin[gi], (double)w.gout[gi],
                                          (double)lp};
                         double fs[12];
