@@ -43,23 +43,16 @@ int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L) {
     return FO_OK;
 }
 
-static int grid_for(fo_graph *g, int K, int precision) {
-    int w = score_warps_per_block();
-    int max_blocks = g->num_sms * score_blocks_per_sm(precision);
-    int want = (K + w - 1) / w;
-    return want < max_blocks ? (want > 0 ? want : 1) : max_blocks;
-}
-
 static int launch(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K, int VB,
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
-                  double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream, int grid) {
+                  double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
+    ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
     WsLayout L;
-    int slots = grid * score_warps_per_block();
+    int slots = geo.grid * score_warps_per_block();
     int st = ensure_workspace(g, VB, slots, &L);
     if (st) return st;
-    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, K, VB, precision, g->d_ws, L, slots, grid,
-                                 score_warps_per_block(), cost, status, ext_dur, tl, dur_out, bad_out, ngroups_out,
-                                 stream);
+    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, K, VB, precision, g->d_ws, L, geo, cost, status, ext_dur, tl,
+                                 dur_out, bad_out, ngroups_out, stream);
     g_launches++;
     if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score kernel launch: ") + cudaGetErrorString(e));
     return FO_OK;
@@ -73,8 +66,7 @@ int score_device(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const in
     if (VB <= 0) return fail(FO_INVALID_ARG, "gid_bound must be > 0");
     CUDA_TRY(cudaSetDevice(g->device));
     TimelineOut tl{};
-    return launch(g, ngid, rgid, bkt, K, VB, precision, cost, status, nullptr, tl, nullptr, nullptr, nullptr, stream,
-                  grid_for(g, K, precision));
+    return launch(g, ngid, rgid, bkt, K, VB, precision, cost, status, nullptr, tl, nullptr, nullptr, nullptr, stream);
 }
 
 }  // namespace fo
@@ -386,7 +378,7 @@ static int single(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
     int32_t *bad = (int32_t *)(b + o[15]);
     st = launch(g, (int32_t *)(b + o[0]), (int32_t *)(b + o[1]), (int32_t *)(b + o[2]), 1, VB, precision,
                 (double *)(b + o[3]), (int32_t *)(b + o[4]), ext, tl, want_dur ? (double *)(b + o[14]) : nullptr, bad,
-                bad + 1, s, 1);
+                bad + 1, s);
     if (st) return st;
     hout.resize(t);
     CUDA_TRY(cudaMemcpyAsync(hout.data(), b, t, cudaMemcpyDeviceToHost, s));

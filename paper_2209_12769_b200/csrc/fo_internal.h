@@ -68,7 +68,7 @@ __host__ __device__ inline MpLayout mp_layout(int layers) {
 
 // Per-warp workspace (one candidate at a time), byte offsets.
 struct WsLayout {
-    int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, dur, fused, gptr, gmem, msort, lidx, nbptr, nb, H, P, gint, gin, gout, vis, zl, csim;
+    int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, dur, fused, gptr, gmem, msort, lidx, nbptr, nb, H, P, gint, gin, gout, vis, zl, csim, rank, tlid;
     int64_t total;
 };
 WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max);
@@ -82,14 +82,18 @@ struct TimelineOut {
     int32_t *n_b;
 };
 
+// Launch geometry: persistent grid and the per-warp shared-memory arena.
+struct ScoreGeo {
+    int grid, blocks_per_sm, sm_nodes, sm_pairs, sm_bytes;
+};
+ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision);
 // Kernel launch (score.cu).  ext_dur / tl / dur_out / bad_out are optional and
 // only used with K == 1.
 cudaError_t launch_score(const DGraph &g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K,
-                         int VB, int precision, char *ws, const WsLayout &L, int n_slots, int grid, int warps,
+                         int VB, int precision, char *ws, const WsLayout &L, const ScoreGeo &geo,
                          double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
                          double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream);
 int score_warps_per_block();
-int score_blocks_per_sm(int precision);
 
 }  // namespace fo
 
