@@ -54,7 +54,9 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    sh = ShardedSearch(g, cfg, cp, seeds, rank, ws, precision=prec, n_threads=args.threads)
+    local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    threads = args.threads or max(1, (os.cpu_count() or 1) // local_ws)  # no oversubscription across ranks
+    sh = ShardedSearch(g, cfg, cp, seeds, rank, ws, precision=prec, n_threads=threads)
     best_cost, best_seed = sh.run(dev)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
