@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libdiscob200.so")
+LIB_PATH = os.environ.get("FO_LIB_PATH") or os.path.join(HERE, "_build", "libdiscob200.so")
 
 FO_OK, FO_CYCLE, FO_MISSING_COST, FO_NEGATIVE_DURATION, FO_DIM_MISMATCH = 0, 1, 2, 3, 4
 FO_INVALID_ARG, FO_CUDA_ERROR, FO_UNSUPPORTED = 5, 6, 7

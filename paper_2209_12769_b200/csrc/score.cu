@@ -196,9 +196,6 @@ __device__ double mp_forward(const DGraph &g, const int *mem, int n, const int *
     __syncwarp();
     for (int l = 0; l < g.layers; l++) {
         const T *Wt = W + ml.wl + (int64_t)l * 1024;
-        T w[32];
-#pragma unroll
-        for (int k = 0; k < 32; k++) w[k] = __ldg(&Wt[k * 32 + lane]);
         // mean aggregation over {i} U undirected internal neighbours (estimator.py:348-355, :374)
         for (int i = 0; i < n; i++) {
             int b = nbptr[i], e = nbptr[i + 1];
@@ -207,13 +204,19 @@ __device__ double mp_forward(const DGraph &g, const int *mem, int n, const int *
             P[i * 32 + lane] = acc / T(1 + e - b);
         }
         __syncwarp();
-        // H = relu(P @ W_l^T) (estimator.py:375-376)
-        for (int i = 0; i < n; i++) {
-            T p = P[i * 32 + lane];
-            T acc = T(0);
-#pragma unroll
-            for (int k = 0; k < 32; k++) acc = fmaT<T>(__shfl_sync(FULL, p, k), w[k], acc);
-            H[i * 32 + lane] = acc > T(0) ? acc : T(0);
+        // H = relu(P @ W_l^T) (estimator.py:375-376); two nodes share each weight load
+        for (int i = 0; i < n; i += 2) {
+            const bool two = i + 1 < n;
+            T p0 = P[i * 32 + lane], p1 = two ? P[(i + 1) * 32 + lane] : T(0);
+            T a0 = T(0), a1 = T(0);
+#pragma unroll 8
+            for (int k = 0; k < 32; k++) {
+                T wk = __ldg(&Wt[k * 32 + lane]);
+                a0 = fmaT<T>(__shfl_sync(FULL, p0, k), wk, a0);
+                a1 = fmaT<T>(__shfl_sync(FULL, p1, k), wk, a1);
+            }
+            H[i * 32 + lane] = a0 > T(0) ? a0 : T(0);
+            if (two) H[(i + 1) * 32 + lane] = a1 > T(0) ? a1 : T(0);
         }
         __syncwarp();
     }
@@ -233,56 +236,48 @@ __device__ double mp_forward(const DGraph &g, const int *mem, int n, const int *
 
 // ---------------------------------------------------------------------------
 
+// Workspace arrays are base + offset, the offsets read from the __grid_constant__
+// launch parameters, so no pointer table occupies registers.
 struct Ws {
-    int *gmap, *bmap, *g2id, *b2id, *nn, *rr, *bki, *gmin, *gcnt, *bmin;
-    long long *btot;
-    int *indeg, *scnt, *sptr, *succ, *prank;
-    double *dur;
-    int *fused, *gptr, *gmem, *msort, *lidx, *nbptr, *nb;
-    char *H, *P;
-    long long *gint, *gin, *gout;
-    int *vis, *zl, *rank, *tlid;
-    char *csim;
+    char *b;
+    const WsLayout *L;
+    __device__ __forceinline__ int *gmap() const { return (int *)(b + L->gmap); }
+    __device__ __forceinline__ int *bmap() const { return (int *)(b + L->bmap); }
+    __device__ __forceinline__ int *g2id() const { return (int *)(b + L->g2id); }
+    __device__ __forceinline__ int *b2id() const { return (int *)(b + L->b2id); }
+    __device__ __forceinline__ int *nn() const { return (int *)(b + L->nn); }
+    __device__ __forceinline__ int *rr() const { return (int *)(b + L->rr); }
+    __device__ __forceinline__ int *bki() const { return (int *)(b + L->bki); }
+    __device__ __forceinline__ int *gmin() const { return (int *)(b + L->gmin); }
+    __device__ __forceinline__ int *gcnt() const { return (int *)(b + L->gcnt); }
+    __device__ __forceinline__ int *bmin() const { return (int *)(b + L->bmin); }
+    __device__ __forceinline__ long long *btot() const { return (long long *)(b + L->btot); }
+    __device__ __forceinline__ int *indeg() const { return (int *)(b + L->indeg); }
+    __device__ __forceinline__ int *scnt() const { return (int *)(b + L->scnt); }
+    __device__ __forceinline__ int *sptr() const { return (int *)(b + L->sptr); }
+    __device__ __forceinline__ int *succ() const { return (int *)(b + L->succ); }
+    __device__ __forceinline__ int *prank() const { return (int *)(b + L->prank); }
+    __device__ __forceinline__ double *dur() const { return (double *)(b + L->dur); }
+    __device__ __forceinline__ int *fused() const { return (int *)(b + L->fused); }
+    __device__ __forceinline__ int *gptr() const { return (int *)(b + L->gptr); }
+    __device__ __forceinline__ int *gmem() const { return (int *)(b + L->gmem); }
+    __device__ __forceinline__ int *msort() const { return (int *)(b + L->msort); }
+    __device__ __forceinline__ int *lidx() const { return (int *)(b + L->lidx); }
+    __device__ __forceinline__ int *nbptr() const { return (int *)(b + L->nbptr); }
+    __device__ __forceinline__ int *nb() const { return (int *)(b + L->nb); }
+    __device__ __forceinline__ char *H() const { return (char *)(b + L->H); }
+    __device__ __forceinline__ char *P() const { return (char *)(b + L->P); }
+    __device__ __forceinline__ long long *gint() const { return (long long *)(b + L->gint); }
+    __device__ __forceinline__ long long *gin() const { return (long long *)(b + L->gin); }
+    __device__ __forceinline__ long long *gout() const { return (long long *)(b + L->gout); }
+    __device__ __forceinline__ int *vis() const { return (int *)(b + L->vis); }
+    __device__ __forceinline__ int *zl() const { return (int *)(b + L->zl); }
+    __device__ __forceinline__ int *rank() const { return (int *)(b + L->rank); }
+    __device__ __forceinline__ int *tlid() const { return (int *)(b + L->tlid); }
+    __device__ __forceinline__ char *csim() const { return (char *)(b + L->csim); }
 };
 
-__device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) {
-    Ws w;
-    w.gmap = (int *)(base + L.gmap);
-    w.bmap = (int *)(base + L.bmap);
-    w.g2id = (int *)(base + L.g2id);
-    w.b2id = (int *)(base + L.b2id);
-    w.nn = (int *)(base + L.nn);
-    w.rr = (int *)(base + L.rr);
-    w.bki = (int *)(base + L.bki);
-    w.gmin = (int *)(base + L.gmin);
-    w.gcnt = (int *)(base + L.gcnt);
-    w.bmin = (int *)(base + L.bmin);
-    w.btot = (long long *)(base + L.btot);
-    w.indeg = (int *)(base + L.indeg);
-    w.scnt = (int *)(base + L.scnt);
-    w.sptr = (int *)(base + L.sptr);
-    w.succ = (int *)(base + L.succ);
-    w.prank = (int *)(base + L.prank);
-    w.dur = (double *)(base + L.dur);
-    w.fused = (int *)(base + L.fused);
-    w.gptr = (int *)(base + L.gptr);
-    w.gmem = (int *)(base + L.gmem);
-    w.msort = (int *)(base + L.msort);
-    w.lidx = (int *)(base + L.lidx);
-    w.nbptr = (int *)(base + L.nbptr);
-    w.nb = (int *)(base + L.nb);
-    w.H = base + L.H;
-    w.P = base + L.P;
-    w.gint = (long long *)(base + L.gint);
-    w.gin = (long long *)(base + L.gin);
-    w.gout = (long long *)(base + L.gout);
-    w.vis = (int *)(base + L.vis);
-    w.zl = (int *)(base + L.zl);
-    w.csim = base + L.csim;
-    w.rank = (int *)(base + L.rank);
-    w.tlid = (int *)(base + L.tlid);
-    return w;
-}
+__device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) { return Ws{base, &L}; }
 
 struct ScoreArgs {
     DGraph g;
@@ -300,8 +295,8 @@ struct ScoreArgs {
     int32_t *ngroups_out;
 };
 
-__device__ __forceinline__ bool in_grp(const Ws &w, int op, int gn) { return w.nn[op] == gn || w.rr[op] == gn; }
-__device__ __forceinline__ int export_of(const Ws &w, int op) { return w.rr[op] >= 0 ? w.rr[op] : w.nn[op]; }
+__device__ __forceinline__ bool in_grp(const Ws &w, int op, int gn) { return w.nn()[op] == gn || w.rr()[op] == gn; }
+__device__ __forceinline__ int export_of(const Ws &w, int op) { return w.rr()[op] >= 0 ? w.rr()[op] : w.nn()[op]; }
 
 // status packed with the failing node so a warp min picks the first node in
 // schedule order (simulator.py:62 evaluates durations in node order)
@@ -377,7 +372,7 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
             sb0 = x.sb;
             se0 = x.se;
             if (end0 > mk) mk = end0;
-            if (TL) { a.tl.c_id[nc] = w.g2id[run0]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
+            if (TL) { a.tl.c_id[nc] = w.g2id()[run0]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
         }
         if (run1 < 0 && headb < tailb) {
             ReadyEnt x = bufb[headb++];
@@ -386,7 +381,7 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
             sb1 = x.sb;
             se1 = x.se;
             if (end1 > mk) mk = end1;
-            if (TL) { a.tl.b_id[nb] = w.b2id[run1 - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
+            if (TL) { a.tl.b_id[nb] = w.b2id()[run1 - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
         }
         if (run0 < 0 && run1 < 0) {
             if (done != N) st = FO_CYCLE;  // simulator.py:133
@@ -430,27 +425,27 @@ template <typename IT, typename SE>
 __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lane, int G, int N) {
     // compact copies of the contracted DAG for the serial loop: narrow indices,
     // successor entries carrying the successor's tie-break rank
-    IT *sptr = (IT *)w.csim;
+    IT *sptr = (IT *)w.csim();
     IT *indeg = sptr + (N + 2);
     SE *succ = (SE *)(((uintptr_t)(indeg + N + 2) + 15) & ~uintptr_t(15));
-    const int P = w.sptr[N];
+    const int P = w.sptr()[N];
     ReadyEnt *bufg = (ReadyEnt *)(((uintptr_t)(succ + P + 1) + 15) & ~uintptr_t(15));
     ReadyEnt *bufb = bufg + G + 1;
-    for (int i = lane; i <= N; i += 32) sptr[i] = (IT)w.sptr[i];
-    for (int i = lane; i < N; i += 32) indeg[i] = (IT)w.indeg[i];
+    for (int i = lane; i <= N; i += 32) sptr[i] = (IT)w.sptr()[i];
+    for (int i = lane; i < N; i += 32) indeg[i] = (IT)w.indeg()[i];
     for (int q = lane; q < P; q += 32) {
-        int s = w.succ[q];
-        succ[q] = se_make<SE>((unsigned)w.prank[s], (unsigned)s);
+        int s = w.succ()[q];
+        succ[q] = se_make<SE>((unsigned)w.prank()[s], (unsigned)s);
     }
     // initial ready set: nodes with no deps at rt = 0.0 (level 0), keys sorted
     int hg = 0, hb = 0;
     for (int base = 0; base < N; base += 32) {
         int i = base + lane;
-        bool z = i < N && w.indeg[i] == 0;
+        bool z = i < N && w.indeg()[i] == 0;
         bool zg = z && i < G;
         unsigned mg = __ballot_sync(FULL, zg), mb = __ballot_sync(FULL, z && !zg);
-        if (zg) w.zl[hg + __popc(mg & lanemask_lt())] = i;
-        if (z && !zg) w.zl[N + hb + __popc(mb & lanemask_lt())] = i;
+        if (zg) w.zl()[hg + __popc(mg & lanemask_lt())] = i;
+        if (z && !zg) w.zl()[N + hb + __popc(mb & lanemask_lt())] = i;
         hg += __popc(mg);
         hb += __popc(mb);
     }
@@ -458,17 +453,17 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lan
     if (lane == 0) {
         int t = 0;
         for (int q = 0; q < hg + hb; q++) {
-            int i = q < hg ? w.zl[q] : w.zl[N + q - hg];
+            int i = q < hg ? w.zl()[q] : w.zl()[N + q - hg];
             ReadyEnt x;
-            x.key = make_key(0, (unsigned)w.prank[i], (unsigned)i);
-            x.dur = w.dur[i];
-            x.sb = (unsigned)w.sptr[i];
-            x.se = (unsigned)w.sptr[i + 1];
+            x.key = make_key(0, (unsigned)w.prank()[i], (unsigned)i);
+            x.dur = w.dur()[i];
+            x.sb = (unsigned)w.sptr()[i];
+            x.se = (unsigned)w.sptr()[i + 1];
             if (q == hg) t = 0;
             ready_push(q < hg ? bufg : bufb, 0, t, x);
         }
-        if (a.tl.c_id) event_loop<true, IT, SE>(a, k, w.dur, sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
-        else event_loop<false, IT, SE>(a, k, w.dur, sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
+        if (a.tl.c_id) event_loop<true, IT, SE>(a, k, w.dur(), sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
+        else event_loop<false, IT, SE>(a, k, w.dur(), sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
     }
     __syncwarp();
 }
@@ -544,7 +539,7 @@ __device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const doubl
 
 __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int lane, int G, int N, char *sm) {
     const int V = a.g.V, A = a.g.A, B = N - G;
-    const int P = w.sptr[N];
+    const int P = w.sptr()[N];
     const int cn = a.sm_nodes, cp = a.sm_pairs;
     if (sm == nullptr || N > cn || P > cp || N >= 65536 || 2 * V + A >= 65536) return false;
     double *dur = (double *)sm;
@@ -553,22 +548,22 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int lane, 
     uint16_t *succ = indeg + cn;
     uint32_t *ready = (uint32_t *)(((uintptr_t)(succ + cp) + 3) & ~uintptr_t(3));
     // sim order: rank of prank among groups / of min AR among buckets
-    int *rk = w.rank;  // [0, 2V) group pranks, [2V, 2V + A) bucket pranks
+    int *rk = w.rank();  // [0, 2V) group pranks, [2V, 2V + A) bucket pranks
     for (int i = lane; i < 2 * V + A; i += 32) rk[i] = 0;
     __syncwarp();
-    for (int i = lane; i < N; i += 32) rk[i < G ? w.prank[i] : 2 * V + w.prank[i]] = 1;
+    for (int i = lane; i < N; i += 32) rk[i < G ? w.prank()[i] : 2 * V + w.prank()[i]] = 1;
     __syncwarp();
-    warp_rank_flags(rk, w.zl, 2 * V, lane);
-    warp_rank_flags(rk + 2 * V, w.zl, A, lane);
-    int *sim = w.zl;       // [0, N): setup node -> sim node
-    int *cnt = w.zl + N;   // [N, 2N): successor counts in sim order
+    warp_rank_flags(rk, w.zl(), 2 * V, lane);
+    warp_rank_flags(rk + 2 * V, w.zl(), A, lane);
+    int *sim = w.zl();       // [0, N): setup node -> sim node
+    int *cnt = w.zl() + N;   // [N, 2N): successor counts in sim order
     for (int i = lane; i < N; i += 32) {
-        int j = i < G ? rk[w.prank[i]] : G + rk[2 * V + w.prank[i]];
+        int j = i < G ? rk[w.prank()[i]] : G + rk[2 * V + w.prank()[i]];
         sim[i] = j;
-        cnt[j] = w.sptr[i + 1] - w.sptr[i];
-        dur[j] = w.dur[i];
-        indeg[j] = (uint16_t)w.indeg[i];
-        if (a.tl.c_id) w.tlid[j] = i < G ? w.g2id[i] : w.b2id[i - G];
+        cnt[j] = w.sptr()[i + 1] - w.sptr()[i];
+        dur[j] = w.dur()[i];
+        indeg[j] = (uint16_t)w.indeg()[i];
+        if (a.tl.c_id) w.tlid()[j] = i < G ? w.g2id()[i] : w.b2id()[i - G];
     }
     __syncwarp();
     {  // exclusive scan of counts -> sptr (u16)
@@ -589,7 +584,7 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int lane, 
     __syncwarp();
     for (int i = lane; i < N; i += 32) {
         int o = sptr[sim[i]];
-        for (int q = w.sptr[i]; q < w.sptr[i + 1]; q++) succ[o++] = (uint16_t)sim[w.succ[q]];
+        for (int q = w.sptr()[i]; q < w.sptr()[i + 1]; q++) succ[o++] = (uint16_t)sim[w.succ()[q]];
     }
     // initial ready runs: indegree-0 nodes at level 0, already in key order
     uint32_t *rg = ready, *rb = ready + G;
@@ -607,8 +602,8 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int lane, 
     }
     __syncwarp();
     if (lane == 0) {
-        if (a.tl.c_id) smem_loop<true>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid, G, N, hg, hb);
-        else smem_loop<false>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid, G, N, hg, hb);
+        if (a.tl.c_id) smem_loop<true>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
+        else smem_loop<false>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
     }
     __syncwarp();
     (void)B;
@@ -624,54 +619,54 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     const int32_t *bk = a.bkt + (int64_t)k * A;
 
     // ---- K1: group / bucket numbering (ids -> node order, graph.py:269-273)
-    for (int i = lane; i < VB; i += 32) w.gmap[i] = 0;
-    for (int i = lane; i < A; i += 32) w.bmap[i] = 0;
+    for (int i = lane; i < VB; i += 32) w.gmap()[i] = 0;
+    for (int i = lane; i < A; i += 32) w.bmap()[i] = 0;
     __syncwarp();
     bool bad = false;
     for (int v = lane; v < V; v += 32) {
         int x = ng[v], y = rg[v];
         if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
-        w.gmap[x] = 1;
-        if (y >= 0) w.gmap[y] = 1;
-        w.nn[v] = x;
-        w.rr[v] = y;
+        w.gmap()[x] = 1;
+        if (y >= 0) w.gmap()[y] = 1;
+        w.nn()[v] = x;
+        w.rr()[v] = y;
     }
     for (int i = lane; i < A; i += 32) {
         int x = bk[i];
         if (x < 0 || x >= A) { bad = true; continue; }
-        w.bmap[x] = 1;
-        w.bki[i] = x;
+        w.bmap()[x] = 1;
+        w.bki()[i] = x;
     }
     if (__any_sync(FULL, bad)) {
         if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_INVALID_ARG; }
         return;
     }
     __syncwarp();
-    const int G = warp_rank_flags(w.gmap, w.g2id, VB, lane);
-    const int B = warp_rank_flags(w.bmap, w.b2id, A, lane);
+    const int G = warp_rank_flags(w.gmap(), w.g2id(), VB, lane);
+    const int B = warp_rank_flags(w.bmap(), w.b2id(), A, lane);
     const int N = G + B;
     for (int v = lane; v < V; v += 32) {
-        w.nn[v] = w.gmap[w.nn[v]];
-        int y = w.rr[v];
-        w.rr[v] = y >= 0 ? w.gmap[y] : -1;
+        w.nn()[v] = w.gmap()[w.nn()[v]];
+        int y = w.rr()[v];
+        w.rr()[v] = y >= 0 ? w.gmap()[y] : -1;
     }
-    for (int i = lane; i < A; i += 32) w.bki[i] = w.bmap[w.bki[i]];
-    for (int i = lane; i < G; i += 32) { w.gmin[i] = INT_MAX; w.gcnt[i] = 0; }
-    for (int i = lane; i < B; i += 32) { w.bmin[i] = INT_MAX; w.btot[i] = 0; }
-    for (int i = lane; i < N; i += 32) { w.indeg[i] = 0; w.scnt[i] = 0; }
+    for (int i = lane; i < A; i += 32) w.bki()[i] = w.bmap()[w.bki()[i]];
+    for (int i = lane; i < G; i += 32) { w.gmin()[i] = INT_MAX; w.gcnt()[i] = 0; }
+    for (int i = lane; i < B; i += 32) { w.bmin()[i] = INT_MAX; w.btot()[i] = 0; }
+    for (int i = lane; i < N; i += 32) { w.indeg()[i] = 0; w.scnt()[i] = 0; }
     __syncwarp();
 
     // per-group min member / size, per-bucket min AR / total bytes
     for (int v = lane; v < V; v += 32) {
-        int x = w.nn[v], y = w.rr[v];
-        atomicMin(&w.gmin[x], v);
-        atomicAdd(&w.gcnt[x], 1);
-        if (y >= 0) { atomicMin(&w.gmin[y], v); atomicAdd(&w.gcnt[y], 1); }
+        int x = w.nn()[v], y = w.rr()[v];
+        atomicMin(&w.gmin()[x], v);
+        atomicAdd(&w.gcnt()[x], 1);
+        if (y >= 0) { atomicMin(&w.gmin()[y], v); atomicAdd(&w.gcnt()[y], 1); }
     }
     for (int i = lane; i < A; i += 32) {
-        int b = w.bki[i];
-        atomicMin(&w.bmin[b], i);
-        atomicAdd((unsigned long long *)&w.btot[b], (unsigned long long)g.ar_bytes[i]);
+        int b = w.bki()[i];
+        atomicMin(&w.bmin()[b], i);
+        atomicAdd((unsigned long long *)&w.btot()[b], (unsigned long long)g.ar_bytes[i]);
     }
     __syncwarp();
 
@@ -682,42 +677,42 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     for (int pass = 0; pass < 2; pass++) {
         for (int e = lane; e < E; e += 32) {
             int s = g.e_src[e], d = g.e_dst[e];
-            int c0 = w.nn[d], c1 = w.rr[d];
+            int c0 = w.nn()[d], c1 = w.rr()[d];
             if (!g.e_agg[e]) {
                 int ex = export_of(w, s);
-                int ns = w.nn[s], rs = w.rr[s];
+                int ns = w.nn()[s], rs = w.rr()[s];
                 if (c0 != ns && c0 != rs) {
-                    if (pass == 0) { atomicAdd(&w.scnt[ex], 1); atomicAdd(&w.indeg[c0], 1); }
-                    else w.succ[atomicAdd(&w.scnt[ex], 1)] = c0;
+                    if (pass == 0) { atomicAdd(&w.scnt()[ex], 1); atomicAdd(&w.indeg()[c0], 1); }
+                    else w.succ()[atomicAdd(&w.scnt()[ex], 1)] = c0;
                 }
                 if (c1 >= 0 && c1 != ns && c1 != rs) {
-                    if (pass == 0) { atomicAdd(&w.scnt[ex], 1); atomicAdd(&w.indeg[c1], 1); }
-                    else w.succ[atomicAdd(&w.scnt[ex], 1)] = c1;
+                    if (pass == 0) { atomicAdd(&w.scnt()[ex], 1); atomicAdd(&w.indeg()[c1], 1); }
+                    else w.succ()[atomicAdd(&w.scnt()[ex], 1)] = c1;
                 }
             } else {
                 for (int q = g.arp_ptr[s]; q < g.arp_ptr[s + 1]; q++) {
-                    int bn = G + w.bki[g.arp[q]];
+                    int bn = G + w.bki()[g.arp[q]];
                     if (pass == 0) {
-                        atomicAdd(&w.scnt[bn], c1 >= 0 ? 2 : 1);
-                        atomicAdd(&w.indeg[c0], 1);
-                        if (c1 >= 0) atomicAdd(&w.indeg[c1], 1);
+                        atomicAdd(&w.scnt()[bn], c1 >= 0 ? 2 : 1);
+                        atomicAdd(&w.indeg()[c0], 1);
+                        if (c1 >= 0) atomicAdd(&w.indeg()[c1], 1);
                     } else {
-                        w.succ[atomicAdd(&w.scnt[bn], 1)] = c0;
-                        if (c1 >= 0) w.succ[atomicAdd(&w.scnt[bn], 1)] = c1;
+                        w.succ()[atomicAdd(&w.scnt()[bn], 1)] = c0;
+                        if (c1 >= 0) w.succ()[atomicAdd(&w.scnt()[bn], 1)] = c1;
                     }
                 }
             }
         }
         for (int i = lane; i < A; i += 32) {
-            int bn = G + w.bki[i];
+            int bn = G + w.bki()[i];
             int ex = export_of(w, g.ar_prod[i]);
-            if (pass == 0) { atomicAdd(&w.scnt[ex], 1); atomicAdd(&w.indeg[bn], 1); }
-            else w.succ[atomicAdd(&w.scnt[ex], 1)] = bn;
+            if (pass == 0) { atomicAdd(&w.scnt()[ex], 1); atomicAdd(&w.indeg()[bn], 1); }
+            else w.succ()[atomicAdd(&w.scnt()[ex], 1)] = bn;
         }
         __syncwarp();
         if (pass == 0) {
-            warp_exscan(w.scnt, w.sptr, N, lane);
-            for (int i = lane; i < N; i += 32) w.scnt[i] = w.sptr[i];  // fill cursors
+            warp_exscan(w.scnt(), w.sptr(), N, lane);
+            for (int i = lane; i < N; i += 32) w.scnt()[i] = w.sptr()[i];  // fill cursors
             __syncwarp();
         }
     }
@@ -725,52 +720,52 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     // tie-break ranks (simulator.py:63-64): group key (min member, id), bucket key min AR.
     // prank = 2*min_member + (1 if the other group sharing that min member has a smaller id)
     for (int gi = lane; gi < G; gi += 32) {
-        int t = w.gmin[gi];
-        int other = (w.nn[t] == gi) ? w.rr[t] : w.nn[t];
-        int sub = (other >= 0 && w.gmin[other] == t && other < gi) ? 1 : 0;
+        int t = w.gmin()[gi];
+        int other = (w.nn()[t] == gi) ? w.rr()[t] : w.nn()[t];
+        int sub = (other >= 0 && w.gmin()[other] == t && other < gi) ? 1 : 0;
         int pr = 2 * t + sub;
-        w.prank[gi] = pr;
+        w.prank()[gi] = pr;
     }
     for (int b = lane; b < B; b += 32) {
-        int pr = w.bmin[b];
-        w.prank[G + b] = pr;
+        int pr = w.bmin()[b];
+        w.prank()[G + b] = pr;
     }
 
     // ---- K2: durations of every node (simulator.py:62)
     long long badk = LLONG_MAX;
     for (int b = lane; b < B; b += 32) {  // comm.py:45-49
-        double d = __dadd_rn(__dmul_rn(g.C, (double)w.btot[b]), g.D);
-        w.dur[G + b] = d;
+        double d = __dadd_rn(__dmul_rn(g.C, (double)w.btot()[b]), g.D);
+        w.dur()[G + b] = d;
         if (d < 0.0) badk = min(badk, pack_bad(G + b, FO_NEGATIVE_DURATION));
     }
     if (a.ext_dur) {
         for (int i = lane; i < N; i += 32) {
             double d = a.ext_dur[i];
-            w.dur[i] = d;
+            w.dur()[i] = d;
             if (d < 0.0) badk = min(badk, pack_bad(i, FO_NEGATIVE_DURATION));
         }
     } else {
         const bool hw = g.provider == FO_PROVIDER_HW_ORACLE;
         const bool need_io = hw || g.variant == FO_EST_ANALYTIC || g.variant == FO_EST_LINEAR;
         if (need_io) {  // group_io (graph.py:181-213)
-            for (int i = lane; i < G; i += 32) { w.gint[i] = 0; w.gin[i] = 0; w.gout[i] = 0; }
-            for (int v = lane; v < V; v += 32) w.vis[v] = 0;
+            for (int i = lane; i < G; i += 32) { w.gint()[i] = 0; w.gin()[i] = 0; w.gout()[i] = 0; }
+            for (int v = lane; v < V; v += 32) w.vis()[v] = 0;
             __syncwarp();
             for (int e = lane; e < E; e += 32) {
                 int s = g.e_src[e], d = g.e_dst[e];
                 unsigned long long by = (unsigned long long)g.e_bytes[e];
-                int cs[2] = {w.nn[d], w.rr[d]};
+                int cs[2] = {w.nn()[d], w.rr()[d]};
                 for (int c = 0; c < 2; c++) {
                     int C = cs[c];
                     if (C < 0) continue;
-                    if (in_grp(w, s, C)) atomicAdd((unsigned long long *)&w.gint[C], by);
-                    else { atomicAdd((unsigned long long *)&w.gin[C], by); w.vis[s] = 1; }
+                    if (in_grp(w, s, C)) atomicAdd((unsigned long long *)&w.gint()[C], by);
+                    else { atomicAdd((unsigned long long *)&w.gin()[C], by); w.vis()[s] = 1; }
                 }
             }
             __syncwarp();
             for (int v = lane; v < V; v += 32) {
-                if (w.vis[v] || g.out_ptr[v + 1] == g.out_ptr[v] || g.arp_ptr[v + 1] > g.arp_ptr[v])
-                    atomicAdd((unsigned long long *)&w.gout[export_of(w, v)], (unsigned long long)g.op_out[v]);
+                if (w.vis()[v] || g.out_ptr[v + 1] == g.out_ptr[v] || g.arp_ptr[v + 1] > g.arp_ptr[v])
+                    atomicAdd((unsigned long long *)&w.gout()[export_of(w, v)], (unsigned long long)g.op_out[v]);
             }
             __syncwarp();
         }
@@ -780,58 +775,58 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
             int gi = base + lane;
             bool fused = false;
             if (gi < G) {
-                int n = w.gcnt[gi];
+                int n = w.gcnt()[gi];
                 if (n == 1) {
-                    int v = w.gmin[gi];
+                    int v = w.gmin()[gi];
                     double d;
                     if (hw) {
                         double c = g.op_compute[v];
                         d = g.op_kind[v] == 1 ? 0.0
                                               : __dadd_rn(__dadd_rn(isnan(c) ? 0.0 : c, g.launch),
-                                                          __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
+                                                          __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
                     } else if (g.op_kind[v] == 1) {
                         d = 0.0;
                     } else {
                         d = g.op_prof[v];
                         if (isnan(d)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); d = 0.0; }
                     }
-                    w.dur[gi] = d;
+                    w.dur()[gi] = d;
                 } else {
-                    w.dur[gi] = 0.0;
+                    w.dur()[gi] = 0.0;
                     if (!hw && g.variant == FO_EST_NONE) badk = min(badk, pack_bad(gi, FO_MISSING_COST));
                     else if (!hw && g.variant == FO_EST_INVALID) badk = min(badk, pack_bad(gi, FO_DIM_MISMATCH));
                     else fused = true;
                 }
             }
             unsigned m = __ballot_sync(FULL, fused);
-            if (fused) w.fused[nf + __popc(m & lanemask_lt())] = gi;
+            if (fused) w.fused()[nf + __popc(m & lanemask_lt())] = gi;
             nf += __popc(m);
         }
         __syncwarp();
         if (nf > 0) {
             // member lists of fused groups (order fixed below by sorting)
-            for (int f = lane; f < nf; f += 32) w.zl[f] = w.gcnt[w.fused[f]];
+            for (int f = lane; f < nf; f += 32) w.zl()[f] = w.gcnt()[w.fused()[f]];
             __syncwarp();
-            warp_exscan(w.zl, w.gptr, nf, lane);
+            warp_exscan(w.zl(), w.gptr(), nf, lane);
             // group -> fused position via prank scratch-free map: reuse gcnt as position+1 marker
-            for (int f = lane; f < nf; f += 32) w.gcnt[w.fused[f]] = -(f + 1);
+            for (int f = lane; f < nf; f += 32) w.gcnt()[w.fused()[f]] = -(f + 1);
             __syncwarp();
-            for (int f = lane; f < nf; f += 32) w.zl[f] = w.gptr[f];
+            for (int f = lane; f < nf; f += 32) w.zl()[f] = w.gptr()[f];
             __syncwarp();
             for (int v = lane; v < V; v += 32) {
-                int x = w.nn[v], y = w.rr[v];
-                int fx = w.gcnt[x];
-                if (fx < 0) w.gmem[atomicAdd(&w.zl[-fx - 1], 1)] = v;
+                int x = w.nn()[v], y = w.rr()[v];
+                int fx = w.gcnt()[x];
+                if (fx < 0) w.gmem()[atomicAdd(&w.zl()[-fx - 1], 1)] = v;
                 if (y >= 0) {
-                    int fy = w.gcnt[y];
-                    if (fy < 0) w.gmem[atomicAdd(&w.zl[-fy - 1], 1)] = v;
+                    int fy = w.gcnt()[y];
+                    if (fy < 0) w.gmem()[atomicAdd(&w.zl()[-fy - 1], 1)] = v;
                 }
             }
             __syncwarp();
             for (int f = 0; f < nf; f++) {
-                const int gi = w.fused[f];
-                const int b0 = w.gptr[f], n = w.gptr[f + 1] - b0;
-                int *mem = w.gmem + b0;
+                const int gi = w.fused()[f];
+                const int b0 = w.gptr()[f], n = w.gptr()[f + 1] - b0;
+                int *mem = w.gmem() + b0;
                 if (n > kMpCap && !hw && (g.variant == FO_EST_MESSAGE_PASSING || g.variant == FO_EST_LINEAR)) {
                     badk = min(badk, pack_bad(gi, kRetryLarge));
                     continue;
@@ -869,10 +864,10 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                         }
                         d = all_param ? 0.0
                                       : __dadd_rn(__dadd_rn(comp.get(), g.launch),
-                                                  __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
+                                                  __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
                     }
                     d = __shfl_sync(FULL, d, 0);
-                    if (lane == 0) w.dur[gi] = d;
+                    if (lane == 0) w.dur()[gi] = d;
                     continue;
                 }
                 // featurize -> lookup for every member (estimator.py:170)
@@ -888,68 +883,68 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                                                    __dmul_rn(g.mem, (double)(g.op_in[v] + g.op_out[v])));
                             sum.add(raw);
                         }
-                        double pred = __dadd_rn(__dadd_rn(sum.get(), g.launch), __dmul_rn(g.mem, (double)(w.gin[gi] + w.gout[gi])));
-                        w.dur[gi] = pred > 1e-9 ? pred : 1e-9;
+                        double pred = __dadd_rn(__dadd_rn(sum.get(), g.launch), __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
+                        w.dur()[gi] = pred > 1e-9 ? pred : 1e-9;
                     }
                     continue;
                 }
                 // member-local undirected neighbour lists (estimator.py:173-177, :348-355)
-                for (int i = lane; i < n; i += 32) w.lidx[mem[i]] = i;
+                for (int i = lane; i < n; i += 32) w.lidx()[mem[i]] = i;
                 __syncwarp();
                 for (int i = lane; i < n; i += 32) {
                     int v = mem[i];
-                    w.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
+                    w.zl()[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
                 }
                 __syncwarp();
-                warp_exscan(w.zl, w.nbptr, n, lane);
+                warp_exscan(w.zl(), w.nbptr(), n, lane);
                 int dirE = 0;  // directed internal edges (linear variant's longest path)
                 for (int i = lane; i < n; i += 32) {
                     int v = mem[i];
-                    int o = w.nbptr[i], c = 0;
+                    int o = w.nbptr()[i], c = 0;
                     for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
                         int s = g.e_src[g.in_e[q]];
                         if (!in_grp(w, s, gi)) continue;
                         dirE++;
-                        int j = w.lidx[s];
+                        int j = w.lidx()[s];
                         bool dup = false;
-                        for (int t = 0; t < c; t++) dup |= (w.nb[o + t] == j);
-                        if (!dup) w.nb[o + c++] = j;
+                        for (int t = 0; t < c; t++) dup |= (w.nb()[o + t] == j);
+                        if (!dup) w.nb()[o + c++] = j;
                     }
                     for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
                         int d2 = g.e_dst[g.out_e[q]];
                         if (!in_grp(w, d2, gi)) continue;
-                        int j = w.lidx[d2];
+                        int j = w.lidx()[d2];
                         bool dup = false;
-                        for (int t = 0; t < c; t++) dup |= (w.nb[o + t] == j);
-                        if (!dup) w.nb[o + c++] = j;
+                        for (int t = 0; t < c; t++) dup |= (w.nb()[o + t] == j);
+                        if (!dup) w.nb()[o + c++] = j;
                     }
-                    w.zl[i] = c;
+                    w.zl()[i] = c;
                 }
                 __syncwarp();
                 // compact rows in place: nbptr -> [start, start + count)
                 // (store counts as end pointers in msort to keep nbptr monotone)
-                for (int i = lane; i < n; i += 32) w.msort[i] = w.zl[i];
+                for (int i = lane; i < n; i += 32) w.msort()[i] = w.zl()[i];
                 __syncwarp();
                 if (g.variant == FO_EST_MESSAGE_PASSING) {
                     // compact neighbour rows into a dense CSR (msort holds the counts)
                     if (lane == 0) {
                         int o = 0;
                         for (int i = 0; i < n; i++) {
-                            int s0 = w.nbptr[i], c = w.msort[i];
-                            for (int t = 0; t < c; t++) w.nb[o + t] = w.nb[s0 + t];
-                            w.nbptr[i] = o;
+                            int s0 = w.nbptr()[i], c = w.msort()[i];
+                            for (int t = 0; t < c; t++) w.nb()[o + t] = w.nb()[s0 + t];
+                            w.nbptr()[i] = o;
                             o += c;
                         }
-                        w.nbptr[n] = o;
+                        w.nbptr()[n] = o;
                     }
                     __syncwarp();
-                    double pred = mp_forward<T>(g, mem, n, w.nbptr, w.nb, (T *)w.H, (T *)w.P, lane);
-                    if (lane == 0) w.dur[gi] = pred;
+                    double pred = mp_forward<T>(g, mem, n, w.nbptr(), w.nb(), (T *)w.H(), (T *)w.P(), lane);
+                    if (lane == 0) w.dur()[gi] = pred;
                 } else {  // LINEAR (estimator.py:117-128, 341-345, 421-426)
                     dirE = __reduce_add_sync(FULL, dirE);
                     if (lane == 0) {
                         // longest path in nodes over the directed internal edges (estimator.py:131-154)
-                        int *depth = w.msort;  // reuse: counts no longer needed
+                        int *depth = w.msort();  // reuse: counts no longer needed
                         for (int i = 0; i < n; i++) depth[i] = 1;
                         for (int it = 0; it < n; it++) {
                             bool ch = false;
@@ -958,7 +953,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                                 for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
                                     int s = g.e_src[g.in_e[q]];
                                     if (!in_grp(w, s, gi)) continue;
-                                    int j = w.lidx[s];
+                                    int j = w.lidx()[s];
                                     if (depth[j] + 1 > depth[i]) { depth[i] = depth[j] + 1; ch = true; }
                                 }
                             }
@@ -969,7 +964,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                         PySum tot;
                         for (int i = 0; i < n; i++) tot.add(g.op_prof[mem[i]]);
                         const double total = tot.get();
-                        double agg[6] = {(double)n, total, (double)w.gint[gi], (double)w.gin[gi], (double)w.gout[gi],
+                        double agg[6] = {(double)n, total, (double)w.gint()[gi], (double)w.gin()[gi], (double)w.gout()[gi],
                                          (double)lp};
                         double fs[12];
                         for (int q = 0; q < 6; q++) { fs[q] = log1p(agg[q]); fs[6 + q] = agg[q]; }
@@ -979,7 +974,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                         for (int q = 0; q < 12; q++) z = __dadd_rn(z, __dmul_rn(g.lin_w[q], fs[q]));
                         z = __dadd_rn(z, g.lin_b);
                         double pred = __dmul_rn(softplus_d(z), g.out_scale);
-                        w.dur[gi] = pred > 1e-9 ? pred : 1e-9;
+                        w.dur()[gi] = pred > 1e-9 ? pred : 1e-9;
                     }
                 }
                 __syncwarp();
@@ -991,7 +986,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     for (int d = 16; d; d >>= 1) badk = min(badk, __shfl_xor_sync(FULL, badk, d));
     __syncwarp();
     if (a.dur_out) {
-        for (int i = lane; i < N; i += 32) a.dur_out[i] = w.dur[i];
+        for (int i = lane; i < N; i += 32) a.dur_out[i] = w.dur()[i];
         if (lane == 0) *a.ngroups_out = G;
     }
     if (badk != LLONG_MAX) {
@@ -1004,7 +999,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     }
 
     // ---- K3: two-lane discrete-event simulation (simulator.py:66-140)
-    const bool small = N < 65536 && w.sptr[N] < 65536 && 2 * V < 65536;
+    const bool small = N < 65536 && w.sptr()[N] < 65536 && 2 * V < 65536;
     if (!small && (N >= (1 << kKeyNodeBits) || 2 * V >= (1 << kKeyNodeBits))) {
         if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_UNSUPPORTED; }
         return;
@@ -1015,7 +1010,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32, 4) score_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel(const __grid_constant__ ScoreArgs a) {
     const int lane = threadIdx.x & 31;
     const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int nw = gridDim.x * kWarps;
