@@ -74,7 +74,7 @@ WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max) {
     L.zl = take(4 * 2 * NM);
     L.rank = take(4 * (2 * (int64_t)V + A + 64));
     L.tlid = take(4 * NM);
-    L.csim = take(4 * (NM + 2) * 2 + 8 * (int64_t)(pairs_max + 2) + 24 * (GM + A + 4) + 64);
+    L.csim = take(4 * (NM + 2) * 2 + 8 * (int64_t)(pairs_max + 2) + std::max<int64_t>(24 * (GM + A + 4), 16 * 2 * 256) + 64);
     L.total = align8(o) + 128;
     return L;
 }
@@ -421,6 +421,86 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
     if (a.bad_out) *a.bad_out = -1;
 }
 
+// Small-graph loop with 16-byte ready entries in two ring buffers of
+// kRing slots: keys are (level << 16 | prank), so a ring only holds the
+// currently ready nodes and its working set stays in L1.  Returns false on
+// ring overflow (the caller reruns the linear-buffer loop).
+constexpr int kRing = 256;
+struct Ent16 {
+    uint32_t key;
+    uint16_t sb, se;
+    double dur;
+};
+__device__ __forceinline__ bool ring_push(Ent16 *buf, int head, int &tail, const Ent16 &x) {
+    if (tail - head >= kRing) return false;
+    int i = tail++;
+    while (i > head) {
+        Ent16 p = buf[(i - 1) & (kRing - 1)];
+        if (p.key <= x.key) break;
+        buf[i & (kRing - 1)] = p;
+        i--;
+    }
+    buf[i & (kRing - 1)] = x;
+    return true;
+}
+
+__device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const double *__restrict__ dur,
+                                          const uint16_t *__restrict__ sptr, uint16_t *__restrict__ indeg,
+                                          const uint32_t *__restrict__ succ, Ent16 *__restrict__ rg,
+                                          Ent16 *__restrict__ rb, int G, int N, int hg, int hb) {
+    int headg = 0, tailg = hg, headb = 0, tailb = hb;
+    int run0 = -1, run1 = -1, done = 0;
+    unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
+    double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
+    uint32_t level = 0;
+    for (;;) {
+        if (run0 < 0 && headg < tailg) {  // start_available (simulator.py:98-115)
+            Ent16 x = rg[(headg++) & (kRing - 1)];
+            run0 = 1;
+            end0 = __dadd_rn(now, x.dur);
+            sb0 = x.sb;
+            se0 = x.se;
+            if (end0 > mk) mk = end0;
+        }
+        if (run1 < 0 && headb < tailb) {
+            Ent16 x = rb[(headb++) & (kRing - 1)];
+            run1 = 1;
+            end1 = __dadd_rn(now, x.dur);
+            sb1 = x.sb;
+            se1 = x.se;
+            if (end1 > mk) mk = end1;
+        }
+        if (run0 < 0 && run1 < 0) break;
+        now = run0 < 0 ? end1 : (run1 < 0 ? end0 : (end0 < end1 ? end0 : end1));
+        if (now > last) { last = now; level += 0x10000u; }
+#pragma unroll
+        for (int t = 0; t < 2; t++) {
+            if ((t == 0 ? run0 : run1) < 0 || (t == 0 ? end0 : end1) != now) continue;
+            const unsigned qb = t == 0 ? sb0 : sb1, qe = t == 0 ? se0 : se1;
+            if (t == 0) run0 = -1; else run1 = -1;
+            done++;
+            for (unsigned q = qb; q < qe; q++) {  // finish_node (simulator.py:88-96)
+                const uint32_t e = succ[q];
+                const unsigned s = e & 0xffffu;
+                const int d = indeg[s] - 1;
+                Ent16 x;
+                x.dur = dur[s];
+                x.sb = sptr[s];
+                x.se = sptr[s + 1];
+                indeg[s] = (uint16_t)d;
+                if (d == 0) {
+                    x.key = level | (e >> 16);
+                    if (!((int)s < G ? ring_push(rg, headg, tailg, x) : ring_push(rb, headb, tailb, x))) return false;
+                }
+            }
+        }
+    }
+    a.cost_out[k] = done == N ? mk : 0.0;
+    a.status_out[k] = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
+    if (a.bad_out) *a.bad_out = -1;
+    return true;
+}
+
 template <typename IT, typename SE>
 __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lane, int G, int N) {
     // compact copies of the contracted DAG for the serial loop: narrow indices,
@@ -451,19 +531,40 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lan
     }
     __syncwarp();
     if (lane == 0) {
-        int t = 0;
-        for (int q = 0; q < hg + hb; q++) {
-            int i = q < hg ? w.zl()[q] : w.zl()[N + q - hg];
-            ReadyEnt x;
-            x.key = make_key(0, (unsigned)w.prank()[i], (unsigned)i);
-            x.dur = w.dur()[i];
-            x.sb = (unsigned)w.sptr()[i];
-            x.se = (unsigned)w.sptr()[i + 1];
-            if (q == hg) t = 0;
-            ready_push(q < hg ? bufg : bufb, 0, t, x);
+        bool done = false;
+        if (sizeof(IT) == 2 && !a.tl.c_id && hg <= kRing && hb <= kRing) {
+            Ent16 *rg = (Ent16 *)bufg, *rb = rg + kRing;
+            for (int q = 0; q < hg + hb; q++) {  // level-0 runs: node order == prank order per lane
+                int i = q < hg ? w.zl()[q] : w.zl()[N + q - hg];
+                Ent16 x;
+                x.key = (uint32_t)w.prank()[i];
+                x.dur = w.dur()[i];
+                x.sb = (uint16_t)w.sptr()[i];
+                x.se = (uint16_t)w.sptr()[i + 1];
+                int t = q < hg ? q : q - hg;
+                int dummy = t;
+                ring_push(q < hg ? rg : rb, 0, dummy, x);
+            }
+            done = ring_loop(a, k, w.dur(), (const uint16_t *)sptr, (uint16_t *)indeg, (const uint32_t *)succ, rg, rb,
+                             G, N, hg, hb);
+            if (!done)  // ring overflow: restore the indegrees and rerun with linear buffers
+                for (int i = 0; i < N; i++) indeg[i] = (IT)w.indeg()[i];
         }
-        if (a.tl.c_id) event_loop<true, IT, SE>(a, k, w.dur(), sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
-        else event_loop<false, IT, SE>(a, k, w.dur(), sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
+        if (!done) {
+            int t = 0;
+            for (int q = 0; q < hg + hb; q++) {
+                int i = q < hg ? w.zl()[q] : w.zl()[N + q - hg];
+                ReadyEnt x;
+                x.key = make_key(0, (unsigned)w.prank()[i], (unsigned)i);
+                x.dur = w.dur()[i];
+                x.sb = (unsigned)w.sptr()[i];
+                x.se = (unsigned)w.sptr()[i + 1];
+                if (q == hg) t = 0;
+                ready_push(q < hg ? bufg : bufb, 0, t, x);
+            }
+            if (a.tl.c_id) event_loop<true, IT, SE>(a, k, w.dur(), sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
+            else event_loop<false, IT, SE>(a, k, w.dur(), sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
+        }
     }
     __syncwarp();
 }
@@ -1043,7 +1144,10 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
     // The shared-memory arena takes the L1 capacity the global-workspace
     // setup phase lives on (measured: 2.65 ms vs 1.81 ms per 4096-candidate
     // ResNet-50 batch), so it is opt-in until setup moves on-chip as well.
-    static const bool arena_on = getenv("FO_SIM_SMEM") && getenv("FO_SIM_SMEM")[0] == '1';
+    // Small batches (search rounds: one block per SM at most) are latency-bound
+    // and have L1 to spare, so they always take the arena.
+    static const char *env = getenv("FO_SIM_SMEM");
+    const bool arena_on = env ? env[0] == '1' : K <= num_sms * kWarps;
     geo.sm_bytes = (arena_on && bytes * kWarps <= 200 * 1024 && n < 65536) ? (int)bytes : 0;
     int per_sm = precision == FO_PREC_FP64 ? blocks_per_sm<double>(geo.sm_bytes * kWarps)
                                            : blocks_per_sm<float>(geo.sm_bytes * kWarps);
