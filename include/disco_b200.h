@@ -108,9 +108,14 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *model);
  * ngid/rgid: [K*V], bkt: [K*A], cost_out: [K] fp64, status_out: [K] fo_status. */
 int fo_score(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
              int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out, void *stream);
+/* int16 encodings (gid_bound and A <= 32767): half the bytes in HBM and over PCIe. */
+int fo_score_i16(fo_graph *g, const int16_t *ngid, const int16_t *rgid, const int16_t *bkt, int32_t K,
+                 int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out, void *stream);
 /* Same through host buffers (pinned or pageable): H2D, kernel, D2H, synchronous. */
 int fo_score_host(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
                   int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out);
+int fo_score_host_i16(fo_graph *g, const int16_t *ngid, const int16_t *rgid, const int16_t *bkt, int32_t K,
+                      int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out);
 
 /* simulate() of one candidate with its Timeline (simulator.py:53-140).
  * durations: NULL -> device cost model; else host fp64 durations in schedule

@@ -55,6 +55,8 @@ SIGNATURES = [
     ("fo_graph_set_cost_model", C.c_int, [vp, P(CostModel)]),
     ("fo_score", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]),
     ("fo_score_host", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp]),
+    ("fo_score_i16", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]),
+    ("fo_score_host_i16", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp]),
     ("fo_simulate", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, P(C.c_int32), vp, vp, vp,
                               P(C.c_int32), P(C.c_double), P(C.c_int32)]),
     ("fo_node_durations", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, P(C.c_int32), P(C.c_int32)]),

@@ -43,7 +43,7 @@ int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L) {
     return FO_OK;
 }
 
-static int launch(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K, int VB,
+static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
                   double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
     ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
@@ -51,22 +51,24 @@ static int launch(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
     int slots = geo.grid * score_warps_per_block();
     int st = ensure_workspace(g, VB, slots, &L);
     if (st) return st;
-    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, K, VB, precision, g->d_ws, L, geo, cost, status, ext_dur, tl,
+    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws, L, geo, cost, status, ext_dur, tl,
                                  dur_out, bad_out, ngroups_out, stream);
     g_launches++;
     if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score kernel launch: ") + cudaGetErrorString(e));
     return FO_OK;
 }
 
-int score_device(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K, int VB,
+int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                  int precision, double *cost, int32_t *status, cudaStream_t stream) {
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
     if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set (fo_graph_set_cost_model)");
     if (K <= 0) return FO_OK;
     if (VB <= 0) return fail(FO_INVALID_ARG, "gid_bound must be > 0");
+    if (idx16 && (VB > 32767 || g->A > 32767)) return fail(FO_INVALID_ARG, "int16 encoding needs gid_bound and A <= 32767");
     CUDA_TRY(cudaSetDevice(g->device));
     TimelineOut tl{};
-    return launch(g, ngid, rgid, bkt, K, VB, precision, cost, status, nullptr, tl, nullptr, nullptr, nullptr, stream);
+    return launch(g, ngid, rgid, bkt, idx16, K, VB, precision, cost, status, nullptr, tl, nullptr, nullptr, nullptr,
+                  stream);
 }
 
 }  // namespace fo
@@ -295,7 +297,14 @@ int fo_score(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_
              int32_t precision, double *cost_out, int32_t *status_out, void *stream) {
     if (!g) return fail(FO_INVALID_ARG, "null graph");
     std::lock_guard<std::mutex> lk(g->mu);
-    return score_device(g, ngid, rgid, bkt, K, gid_bound, precision, cost_out, status_out, (cudaStream_t)stream);
+    return score_device(g, ngid, rgid, bkt, 0, K, gid_bound, precision, cost_out, status_out, (cudaStream_t)stream);
+}
+
+int fo_score_i16(fo_graph *g, const int16_t *ngid, const int16_t *rgid, const int16_t *bkt, int32_t K,
+                 int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out, void *stream) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    std::lock_guard<std::mutex> lk(g->mu);
+    return score_device(g, ngid, rgid, bkt, 1, K, gid_bound, precision, cost_out, status_out, (cudaStream_t)stream);
 }
 
 static int ensure_io(fo_graph *g, size_t bytes) {
@@ -309,14 +318,14 @@ static int ensure_io(fo_graph *g, size_t bytes) {
     return FO_OK;
 }
 
-int fo_score_host(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
-                  int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out) {
+static int score_host_impl(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int es, int32_t K,
+                           int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out) {
     if (!g) return fail(FO_INVALID_ARG, "null graph");
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
     std::lock_guard<std::mutex> lk(g->mu);
     if (K <= 0) return FO_OK;
     CUDA_TRY(cudaSetDevice(g->device));
-    size_t nv = (size_t)K * g->V * 4, na = (size_t)K * g->A * 4;
+    size_t nv = (size_t)K * g->V * es, na = (size_t)K * g->A * es;
     size_t o_r = al256(nv), o_b = o_r + al256(nv), o_c = o_b + al256(na + 4), o_s = o_c + al256((size_t)K * 8);
     int st = ensure_io(g, o_s + al256((size_t)K * 4));
     if (st) return st;
@@ -327,13 +336,23 @@ int fo_score_host(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
         CUDA_TRY(cudaMemcpyAsync(b + o_r, rgid, nv, cudaMemcpyHostToDevice, s));
     }
     if (na) CUDA_TRY(cudaMemcpyAsync(b + o_b, bkt, na, cudaMemcpyHostToDevice, s));
-    st = score_device(g, (int32_t *)b, (int32_t *)(b + o_r), (int32_t *)(b + o_b), K, gid_bound, precision,
-                      (double *)(b + o_c), (int32_t *)(b + o_s), s);
+    st = score_device(g, b, b + o_r, b + o_b, es == 2, K, gid_bound, precision, (double *)(b + o_c),
+                      (int32_t *)(b + o_s), s);
     if (st) return st;
     CUDA_TRY(cudaMemcpyAsync(cost_out, b + o_c, (size_t)K * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status_out, b + o_s, (size_t)K * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return FO_OK;
+}
+
+int fo_score_host(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
+                  int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out) {
+    return score_host_impl(g, ngid, rgid, bkt, 4, K, gid_bound, precision, cost_out, status_out);
+}
+
+int fo_score_host_i16(fo_graph *g, const int16_t *ngid, const int16_t *rgid, const int16_t *bkt, int32_t K,
+                      int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out) {
+    return score_host_impl(g, ngid, rgid, bkt, 2, K, gid_bound, precision, cost_out, status_out);
 }
 
 // single candidate through device temporaries (simulate / timeline / durations)
@@ -376,7 +395,7 @@ static int single(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
         tl.n_c = (int32_t *)(b + o[12]); tl.n_b = (int32_t *)(b + o[13]);
     }
     int32_t *bad = (int32_t *)(b + o[15]);
-    st = launch(g, (int32_t *)(b + o[0]), (int32_t *)(b + o[1]), (int32_t *)(b + o[2]), 1, VB, precision,
+    st = launch(g, b + o[0], b + o[1], b + o[2], 0, 1, VB, precision,
                 (double *)(b + o[3]), (int32_t *)(b + o[4]), ext, tl, want_dur ? (double *)(b + o[14]) : nullptr, bad,
                 bad + 1, s);
     if (st) return st;

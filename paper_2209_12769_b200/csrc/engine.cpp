@@ -654,7 +654,7 @@ static int search_score(fo_search *S, int n, std::vector<double> &cost, std::vec
     if (cudaMemcpyAsync(db, S->h_buf, need_i * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
         return fail(FO_CUDA_ERROR, "search batch H2D");
     cudaEventRecord(S->ev0, st);
-    int rc = score_device(g, dn, dr, dk, n, S->eng->VB, S->cfg.precision, dc, ds, st);
+    int rc = score_device(g, dn, dr, dk, 0, n, S->eng->VB, S->cfg.precision, dc, ds, st);
     if (rc) return rc;
     cudaEventRecord(S->ev1, st);
     cost.resize(n);

@@ -89,7 +89,7 @@ struct ScoreGeo {
 ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision);
 // Kernel launch (score.cu).  ext_dur / tl / dur_out / bad_out are optional and
 // only used with K == 1.
-cudaError_t launch_score(const DGraph &g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K,
+cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K,
                          int VB, int precision, char *ws, const WsLayout &L, const ScoreGeo &geo,
                          double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
                          double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream);
@@ -132,6 +132,6 @@ int fail(int status, const std::string &msg);
 // Ensure the handle's workspace can hold `slots` warps for gid bound VB.
 int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L);
 // Score K device-resident candidates (used by fo_score and the search engine).
-int score_device(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K, int VB,
+int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                  int precision, double *cost, int32_t *status, cudaStream_t stream);
 }  // namespace fo

@@ -281,7 +281,8 @@ __device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) { return Ws{b
 
 struct ScoreArgs {
     DGraph g;
-    const int32_t *ngid, *rgid, *bkt;
+    const void *ngid, *rgid, *bkt;  // int32, or int16 when idx16
+    int idx16;
     int K, VB;
     int sm_nodes, sm_pairs, sm_bytes;  // per-warp shared-memory simulation arena
     char *ws;
@@ -715,9 +716,11 @@ template <typename T>
 __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char *sm) {
     const DGraph &g = a.g;
     const int V = g.V, E = g.E, A = g.A, VB = a.VB;
-    const int32_t *ng = a.ngid + (int64_t)k * V;
-    const int32_t *rg = a.rgid + (int64_t)k * V;
-    const int32_t *bk = a.bkt + (int64_t)k * A;
+    // candidate encoding: int32 or int16 ids (the int16 form halves the bytes moved)
+    auto ldid = [&](const void *p, int64_t i) -> int {
+        return a.idx16 ? (int)((const int16_t *)p)[i] : ((const int32_t *)p)[i];
+    };
+    const int64_t ob = (int64_t)k * V, oa = (int64_t)k * A;
 
     // ---- K1: group / bucket numbering (ids -> node order, graph.py:269-273)
     for (int i = lane; i < VB; i += 32) w.gmap()[i] = 0;
@@ -725,7 +728,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     __syncwarp();
     bool bad = false;
     for (int v = lane; v < V; v += 32) {
-        int x = ng[v], y = rg[v];
+        int x = ldid(a.ngid, ob + v), y = ldid(a.rgid, ob + v);
         if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
         w.gmap()[x] = 1;
         if (y >= 0) w.gmap()[y] = 1;
@@ -733,7 +736,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
         w.rr()[v] = y;
     }
     for (int i = lane; i < A; i += 32) {
-        int x = bk[i];
+        int x = ldid(a.bkt, oa + i);
         if (x < 0 || x >= A) { bad = true; continue; }
         w.bmap()[x] = 1;
         w.bki()[i] = x;
@@ -1162,7 +1165,7 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
     return geo;
 }
 
-cudaError_t launch_score(const DGraph &g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int K,
+cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K,
                          int VB, int precision, char *ws, const WsLayout &L, const ScoreGeo &geo,
                          double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
                          double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
@@ -1171,6 +1174,7 @@ cudaError_t launch_score(const DGraph &g, const int32_t *ngid, const int32_t *rg
     a.ngid = ngid;
     a.rgid = rgid;
     a.bkt = bkt;
+    a.idx16 = idx16;
     a.K = K;
     a.VB = VB;
     a.sm_nodes = geo.sm_nodes;

@@ -94,15 +94,18 @@ class DeviceGraph:
 
     # -- scoring -------------------------------------------------------------
     def score_host(self, ng, rg, bk, gid_bound, precision=N.FO_PREC_FP32):
-        """cost() of K candidates held in host arrays [K, V] / [K, A]."""
-        ng = np.ascontiguousarray(ng, np.int32)
-        rg = np.ascontiguousarray(rg, np.int32)
-        bk = np.ascontiguousarray(bk, np.int32)
+        """cost() of K candidates held in host arrays [K, V] / [K, A]; int16
+        arrays take the half-width path (fo_score_host_i16)."""
+        i16 = np.asarray(ng).dtype == np.int16
+        dt = np.int16 if i16 else np.int32
+        ng = np.ascontiguousarray(ng, dt)
+        rg = np.ascontiguousarray(rg, dt)
+        bk = np.ascontiguousarray(bk, dt)
         K = ng.shape[0] if ng.ndim == 2 else (bk.shape[0] if bk.ndim == 2 else 1)
         cost = np.zeros(K, np.float64)
         status = np.zeros(K, np.int32)
-        st = N.lib().fo_score_host(self.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), K, int(gid_bound), precision,
-                                   N.ptr(cost), N.ptr(status))
+        fn = N.lib().fo_score_host_i16 if i16 else N.lib().fo_score_host
+        st = fn(self.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), K, int(gid_bound), precision, N.ptr(cost), N.ptr(status))
         _raise(st, "fo_score_host", N.last_error())
         return cost, status
 
@@ -113,8 +116,11 @@ class DeviceGraph:
             import torch
 
             stream = torch.cuda.current_stream().cuda_stream
-        st = N.lib().fo_score(self.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), K, int(gid_bound), precision, N.ptr(cost),
-                              N.ptr(status), C.c_void_p(stream))
+        import torch
+
+        fn = N.lib().fo_score_i16 if ng.dtype == torch.int16 else N.lib().fo_score
+        st = fn(self.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), K, int(gid_bound), precision, N.ptr(cost), N.ptr(status),
+                C.c_void_p(stream))
         _raise(st, "fo_score", N.last_error())
 
     def simulate_arrays(self, ng, rg, bk, gid_bound, durations=None, precision=N.FO_PREC_FP32):

@@ -273,3 +273,20 @@ def test_error_mapping():
     cyc = build_graph(ops, [DataEdge(0, 1, 100)], [(0, 0, 1000)], groups=[FusionGroup(0, frozenset({0, 1}))])
     with pytest.raises(P.CycleError):
         P.simulate(cyc, P.oracle_providers(P.HardwareParams()))
+
+
+def test_int16_encoding_matches_int32():
+    import torch
+
+    g, cps = providers("resnet50", N.FO_PREC_FP32)
+    dg = cps["mp"].device_graph(g)
+    ng, rg, bk, gb = dg.make_candidates(np.arange(512, dtype=np.uint64))
+    c32, s32 = dg.score_host(ng, rg, bk, gb)
+    c16, s16 = dg.score_host(ng.astype(np.int16), rg.astype(np.int16), bk.astype(np.int16), gb)
+    assert np.array_equal(c32, c16) and np.array_equal(s32, s16)
+    d = [torch.from_numpy(x.astype(np.int16)).cuda() for x in (ng, rg, bk)]
+    c = torch.empty(512, dtype=torch.float64, device="cuda")
+    s = torch.empty(512, dtype=torch.int32, device="cuda")
+    dg.score_device(d[0], d[1], d[2], gb, c, s)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy(), c32)
