@@ -105,7 +105,47 @@ struct Index {
     std::vector<uint8_t> mdup, compute_ok, has_dup, feeds_ar, has_rep;
     std::vector<int32_t> sptr, succ, pptr, pred;  // contracted adjacency, sorted unique
     std::vector<int32_t> bptr, bex;               // per bucket: export groups of members (sorted unique)
+    std::vector<int32_t> xbptr, xb;               // per group: buckets listing it in bex (inverse)
 };
+
+// Per-thread scratch: every buffer the rewrite loop needs, reused across
+// iterations (no allocation, no thread-local lookups in the hot loop).
+struct Scratch {
+    std::vector<int32_t> gnode, bnode, cur, from, to, ptr, adj, indeg, stack, stamp, bstamp, near, nbrs;
+    std::vector<int32_t> ps, pt;
+    std::vector<std::pair<int32_t, int32_t>> pairs;
+    Index ix;
+    State cand;
+};
+
+// sorted-unique CSR from (src, dst) pairs via counting sort + per-row insertion sort
+static void csr_unique(int n, const std::vector<int32_t> &src, const std::vector<int32_t> &dst,
+                       std::vector<int32_t> &ptr, std::vector<int32_t> &out, std::vector<int32_t> &cur) {
+    ptr.assign(n + 1, 0);
+    for (int32_t x : src) ptr[x + 1]++;
+    for (int i = 0; i < n; i++) ptr[i + 1] += ptr[i];
+    out.resize(src.size());
+    cur.assign(ptr.begin(), ptr.end() - 1);
+    for (size_t i = 0; i < src.size(); i++) out[cur[src[i]]++] = dst[i];
+    int w = 0;
+    int32_t *o = out.data();
+    for (int i = 0; i < n; i++) {
+        int b = ptr[i], e = ptr[i + 1];
+        ptr[i] = w;
+        if (e - b > 32) std::sort(o + b, o + e);
+        else
+            for (int k = b + 1; k < e; k++) {
+                int32_t x = o[k];
+                int j = k - 1;
+                while (j >= b && o[j] > x) { o[j + 1] = o[j]; j--; }
+                o[j + 1] = x;
+            }
+        for (int k = b; k < e; k++)
+            if (k == b || o[k] != o[w - 1]) o[w++] = o[k];
+    }
+    ptr[n] = w;
+    out.resize(w);
+}
 
 struct Engine {
     const fo_graph *g;
@@ -124,31 +164,44 @@ struct Engine {
 
     // group ids -> dense node order; returns G.  gnode sized VB.
     int number_groups(const State &s, std::vector<int32_t> &gnode, std::vector<int32_t> *gid) const {
-        gnode.assign(VB, 0);
+        gnode.assign(VB, -1);
+        int32_t *gn = gnode.data();
         for (int v = 0; v < V; v++) {
-            gnode[s.ng[v]] = 1;
-            if (s.rg[v] >= 0) gnode[s.rg[v]] = 1;
+            gn[s.ng[v]] = 0;
+            if (s.rg[v] >= 0) gn[s.rg[v]] = 0;
         }
         int G = 0;
         if (gid) gid->clear();
-        for (int i = 0; i < VB; i++) {
-            if (gnode[i]) {
+        for (int i = 0; i < VB; i++)
+            if (gn[i] == 0) {
                 if (gid) gid->push_back(i);
-                gnode[i] = G++;
-            } else gnode[i] = -1;
-        }
+                gn[i] = G++;
+            }
         return G;
     }
 
-    void build(const State &s, Index &ix) const {
-        std::vector<int32_t> gnode;
-        ix.G = number_groups(s, gnode, &ix.gid);
+    int number_buckets(const State &s, std::vector<int32_t> &bnode, std::vector<int32_t> *bid) const {
+        bnode.assign(A, -1);
+        for (int a = 0; a < A; a++) bnode[s.bk[a]] = 0;
+        int B = 0;
+        if (bid) bid->clear();
+        for (int i = 0; i < A; i++)
+            if (bnode[i] == 0) {
+                if (bid) bid->push_back(i);
+                bnode[i] = B++;
+            }
+        return B;
+    }
+
+    void build(const State &s, Index &ix, Scratch &sc) const {
+        ix.G = number_groups(s, sc.gnode, &ix.gid);
         const int G = ix.G;
+        const int32_t *gn = sc.gnode.data();
         ix.nn.resize(V);
         ix.rr.resize(V);
         for (int v = 0; v < V; v++) {
-            ix.nn[v] = gnode[s.ng[v]];
-            ix.rr[v] = s.rg[v] >= 0 ? gnode[s.rg[v]] : -1;
+            ix.nn[v] = gn[s.ng[v]];
+            ix.rr[v] = s.rg[v] >= 0 ? gn[s.rg[v]] : -1;
         }
         // members, ascending op index
         ix.mptr.assign(G + 1, 0);
@@ -159,129 +212,95 @@ struct Engine {
         for (int i = 0; i < G; i++) ix.mptr[i + 1] += ix.mptr[i];
         ix.mem.resize(ix.mptr[G]);
         ix.mdup.resize(ix.mptr[G]);
-        std::vector<int32_t> cur(ix.mptr.begin(), ix.mptr.end() - 1);
-        for (int v = 0; v < V; v++) {
-            int x = ix.nn[v];
-            ix.mdup[cur[x]] = 0;
-            ix.mem[cur[x]++] = v;
-            if (ix.rr[v] >= 0) {
-                x = ix.rr[v];
-                ix.mdup[cur[x]] = 1;
-                ix.mem[cur[x]++] = v;
-            }
-        }
+        sc.cur.assign(ix.mptr.begin(), ix.mptr.end() - 1);
         ix.compute_ok.assign(G, 1);
         ix.has_dup.assign(G, 0);
         ix.feeds_ar.assign(G, 0);
         ix.has_rep.assign(G, 0);
-        for (int x = 0; x < G; x++)
-            for (int k = ix.mptr[x]; k < ix.mptr[x + 1]; k++) {
-                int v = ix.mem[k];
-                if (g->op_kind[v] != 0) ix.compute_ok[x] = 0;
-                if (ix.mdup[k]) ix.has_dup[x] = 1;
-                if (g->arp_ptr[v + 1] > g->arp_ptr[v]) ix.feeds_ar[x] = 1;
-                if (ix.rr[v] >= 0) ix.has_rep[x] = 1;  // some member has a replica (rewrite.py:116)
+        for (int v = 0; v < V; v++) {
+            const bool notc = g->op_kind[v] != 0, far = g->arp_ptr[v + 1] > g->arp_ptr[v], rep = ix.rr[v] >= 0;
+            int x = ix.nn[v];
+            ix.mdup[sc.cur[x]] = 0;
+            ix.mem[sc.cur[x]++] = v;
+            if (notc) ix.compute_ok[x] = 0;
+            if (far) ix.feeds_ar[x] = 1;
+            if (rep) ix.has_rep[x] = 1;  // some member has a replica (rewrite.py:116)
+            if (rep) {
+                x = ix.rr[v];
+                ix.mdup[sc.cur[x]] = 1;
+                ix.mem[sc.cur[x]++] = v;
+                if (notc) ix.compute_ok[x] = 0;
+                if (far) ix.feeds_ar[x] = 1;
+                ix.has_dup[x] = 1;
+                ix.has_rep[x] = 1;
             }
+        }
         // contracted succs/preds over ALL edges (graph.py:161-179)
-        std::vector<int32_t> ps, pt;
-        ps.reserve(2 * E);
-        pt.reserve(2 * E);
+        sc.ps.clear();
+        sc.pt.clear();
         for (int e = 0; e < E; e++) {
             int sv = g->e_src[e], dv = g->e_dst[e];
-            int ex = ix.rr[sv] >= 0 ? ix.rr[sv] : ix.nn[sv];
+            int ns = ix.nn[sv], rs = ix.rr[sv], ex = rs >= 0 ? rs : ns;
             int c0 = ix.nn[dv], c1 = ix.rr[dv];
-            if (c0 != ix.nn[sv] && c0 != ix.rr[sv]) { ps.push_back(ex); pt.push_back(c0); }
-            if (c1 >= 0 && c1 != ix.nn[sv] && c1 != ix.rr[sv]) { ps.push_back(ex); pt.push_back(c1); }
+            if (c0 != ns && c0 != rs) { sc.ps.push_back(ex); sc.pt.push_back(c0); }
+            if (c1 >= 0 && c1 != ns && c1 != rs) { sc.ps.push_back(ex); sc.pt.push_back(c1); }
         }
-        csr_unique(G, ps, pt, ix.sptr, ix.succ);
-        csr_unique(G, pt, ps, ix.pptr, ix.pred);
-        // buckets
-        std::vector<int32_t> bnode(A, -1);
-        ix.bid.clear();
-        {
-            std::vector<uint8_t> f(A, 0);
-            for (int a = 0; a < A; a++) f[s.bk[a]] = 1;
-            int B = 0;
-            for (int i = 0; i < A; i++)
-                if (f[i]) { bnode[i] = B++; ix.bid.push_back(i); }
-            ix.B = B;
-        }
+        csr_unique(G, sc.ps, sc.pt, ix.sptr, ix.succ, sc.cur);
+        csr_unique(G, sc.pt, sc.ps, ix.pptr, ix.pred, sc.cur);
+        // buckets: export groups of their members, and the inverse
+        ix.B = number_buckets(s, sc.bnode, &ix.bid);
         ix.bki.resize(A);
-        std::vector<int32_t> bs, bt;
+        sc.ps.clear();
+        sc.pt.clear();
         for (int a = 0; a < A; a++) {
-            ix.bki[a] = bnode[s.bk[a]];
+            ix.bki[a] = sc.bnode[s.bk[a]];
             int pv = g->ar_prod[a];
-            bs.push_back(ix.bki[a]);
-            bt.push_back(ix.rr[pv] >= 0 ? ix.rr[pv] : ix.nn[pv]);
+            sc.ps.push_back(ix.bki[a]);
+            sc.pt.push_back(ix.rr[pv] >= 0 ? ix.rr[pv] : ix.nn[pv]);
         }
-        csr_unique(ix.B, bs, bt, ix.bptr, ix.bex);
-    }
-
-    static void csr_unique(int n, const std::vector<int32_t> &src, const std::vector<int32_t> &dst,
-                           std::vector<int32_t> &ptr, std::vector<int32_t> &out) {
-        ptr.assign(n + 1, 0);
-        for (int32_t x : src) ptr[x + 1]++;
-        for (int i = 0; i < n; i++) ptr[i + 1] += ptr[i];
-        out.resize(src.size());
-        std::vector<int32_t> cur(ptr.begin(), ptr.end() - 1);
-        for (size_t i = 0; i < src.size(); i++) out[cur[src[i]]++] = dst[i];
-        int w = 0;
-        for (int i = 0; i < n; i++) {
-            int b = ptr[i], e = ptr[i + 1];
-            std::sort(out.begin() + b, out.begin() + e);
-            ptr[i] = w;
-            int last = -1;
-            for (int k = b; k < e; k++)
-                if (k == b || out[k] != last) { last = out[k]; out[w++] = last; }
-        }
-        ptr[n] = w;
-        out.resize(w);
+        csr_unique(ix.B, sc.ps, sc.pt, ix.bptr, ix.bex, sc.cur);
+        csr_unique(G, sc.pt, sc.ps, ix.xbptr, ix.xb, sc.cur);
     }
 
     // rewrite_candidate_ok (graph.py:505-512): Kahn over the joint schedule
     // dependency multigraph (multiplicity does not change acyclicity).
-    bool valid(const State &s, std::vector<int32_t> &scratch_gnode) const {
-        int G = number_groups(s, scratch_gnode, nullptr);
-        std::vector<uint8_t> f(A, 0);
-        for (int a = 0; a < A; a++) f[s.bk[a]] = 1;
-        std::vector<int32_t> bnode(A, -1);
-        int B = 0;
-        for (int i = 0; i < A; i++)
-            if (f[i]) bnode[i] = B++;
+    bool valid(const State &s, Scratch &sc) const {
+        const int G = number_groups(s, sc.gnode, nullptr);
+        const int B = number_buckets(s, sc.bnode, nullptr);
         const int N = G + B;
-        auto nn = [&](int v) { return scratch_gnode[s.ng[v]]; };
-        auto rr = [&](int v) { return s.rg[v] >= 0 ? scratch_gnode[s.rg[v]] : -1; };
-        std::vector<int32_t> from, to;
-        from.reserve(2 * E + A);
-        to.reserve(2 * E + A);
+        const int32_t *gn = sc.gnode.data(), *bn = sc.bnode.data();
+        auto &from = sc.from, &to = sc.to;
+        from.clear();
+        to.clear();
         for (int e = 0; e < E; e++) {
             int sv = g->e_src[e], dv = g->e_dst[e];
-            int c0 = nn(dv), c1 = rr(dv);
+            int c0 = gn[s.ng[dv]], c1 = s.rg[dv] >= 0 ? gn[s.rg[dv]] : -1;
             if (!g->agg[e]) {
-                int ns = nn(sv), rs = rr(sv), ex = rs >= 0 ? rs : ns;
+                int ns = gn[s.ng[sv]], rs = s.rg[sv] >= 0 ? gn[s.rg[sv]] : -1, ex = rs >= 0 ? rs : ns;
                 if (c0 != ns && c0 != rs) { from.push_back(ex); to.push_back(c0); }
                 if (c1 >= 0 && c1 != ns && c1 != rs) { from.push_back(ex); to.push_back(c1); }
             } else {
                 for (int q = g->arp_ptr[sv]; q < g->arp_ptr[sv + 1]; q++) {
-                    int bn = G + bnode[s.bk[g->arp[q]]];
-                    from.push_back(bn); to.push_back(c0);
-                    if (c1 >= 0) { from.push_back(bn); to.push_back(c1); }
+                    int b = G + bn[s.bk[g->arp[q]]];
+                    from.push_back(b); to.push_back(c0);
+                    if (c1 >= 0) { from.push_back(b); to.push_back(c1); }
                 }
             }
         }
         for (int a = 0; a < A; a++) {
             int pv = g->ar_prod[a];
-            int ex = rr(pv) >= 0 ? rr(pv) : nn(pv);
-            from.push_back(ex);
-            to.push_back(G + bnode[s.bk[a]]);
+            from.push_back(s.rg[pv] >= 0 ? gn[s.rg[pv]] : gn[s.ng[pv]]);
+            to.push_back(G + bn[s.bk[a]]);
         }
-        std::vector<int32_t> ptr(N + 1, 0), adj(from.size()), indeg(N, 0);
+        auto &ptr = sc.ptr, &adj = sc.adj, &indeg = sc.indeg, &stack = sc.stack;
+        ptr.assign(N + 1, 0);
+        indeg.assign(N, 0);
+        adj.resize(from.size());
         for (size_t i = 0; i < from.size(); i++) { ptr[from[i] + 1]++; indeg[to[i]]++; }
         for (int i = 0; i < N; i++) ptr[i + 1] += ptr[i];
-        std::vector<int32_t> cur(ptr.begin(), ptr.end() - 1);
-        for (size_t i = 0; i < from.size(); i++) adj[cur[from[i]]++] = to[i];
-        std::vector<int32_t> stack;
-        stack.reserve(N);
+        sc.cur.assign(ptr.begin(), ptr.end() - 1);
+        for (size_t i = 0; i < from.size(); i++) adj[sc.cur[from[i]]++] = to[i];
+        stack.clear();
         for (int i = 0; i < N; i++)
             if (!indeg[i]) stack.push_back(i);
         int seen = 0;
@@ -295,56 +314,57 @@ struct Engine {
         return seen == N;
     }
 
-    // fusible_pairs (rewrite.py:49-61) + DUP filter (rewrite.py:242-247)
-    int fusible_pairs(const Index &ix, bool dup, int want, int *og, int *pg) const {
-        int cnt = 0;
+    // fusible_pairs (rewrite.py:49-61) + DUP filter (rewrite.py:242-247), in order
+    void fusible_pairs(const Index &ix, bool dup, std::vector<std::pair<int32_t, int32_t>> &out) const {
+        out.clear();
         for (int x = 0; x < ix.G; x++) {
             if (!ix.compute_ok[x]) continue;
             for (int k = ix.pptr[x]; k < ix.pptr[x + 1]; k++) {
                 int p = ix.pred[k];
                 if (!ix.compute_ok[p] || (dup && ix.has_dup[p])) continue;
-                if (cnt == want) { *og = x; *pg = p; }
-                cnt++;
+                out.emplace_back(x, p);
             }
         }
-        return cnt;
     }
 
-    // bucket_pairs (rewrite.py:212-219) via neighbors_allreduce (rewrite.py:156-178)
-    int bucket_pairs(const Index &ix, int want, int *bo, int *bn) const {
-        std::vector<int32_t> stamp(ix.G, -1);
-        int cnt = 0;
+    // bucket_pairs (rewrite.py:212-219) via neighbors_allreduce (rewrite.py:156-178):
+    // nearby = own | succs(own) | preds(own); neighbours = buckets exporting from nearby
+    void bucket_pairs(const Index &ix, Scratch &sc, std::vector<std::pair<int32_t, int32_t>> &out) const {
+        out.clear();
+        sc.stamp.assign(ix.G, -1);
+        sc.bstamp.assign(ix.B, -1);
         for (int b = 0; b < ix.B; b++) {
+            sc.near.clear();
+            auto mark = [&](int x) {
+                if (sc.stamp[x] != b) { sc.stamp[x] = b; sc.near.push_back(x); }
+            };
             for (int k = ix.bptr[b]; k < ix.bptr[b + 1]; k++) {
                 int x = ix.bex[k];
-                stamp[x] = b;
-                for (int q = ix.sptr[x]; q < ix.sptr[x + 1]; q++) stamp[ix.succ[q]] = b;
-                for (int q = ix.pptr[x]; q < ix.pptr[x + 1]; q++) stamp[ix.pred[q]] = b;
+                mark(x);
+                for (int q = ix.sptr[x]; q < ix.sptr[x + 1]; q++) mark(ix.succ[q]);
+                for (int q = ix.pptr[x]; q < ix.pptr[x + 1]; q++) mark(ix.pred[q]);
             }
-            for (int o = 0; o < ix.B; o++) {
-                if (o == b) continue;
-                bool hit = false;
-                for (int k = ix.bptr[o]; k < ix.bptr[o + 1] && !hit; k++) hit = stamp[ix.bex[k]] == b;
-                if (!hit) continue;
-                if (cnt == want) { *bo = b; *bn = o; }
-                cnt++;
-            }
+            sc.nbrs.clear();
+            for (int x : sc.near)
+                for (int q = ix.xbptr[x]; q < ix.xbptr[x + 1]; q++) {
+                    int o = ix.xb[q];
+                    if (o != b && sc.bstamp[o] != b) { sc.bstamp[o] = b; sc.nbrs.push_back(o); }
+                }
+            std::sort(sc.nbrs.begin(), sc.nbrs.end());
+            for (int o : sc.nbrs) out.emplace_back(b, o);
         }
-        return cnt;
     }
 
-    void compact(State &s) const {  // monotone relabel of group ids to 0..G-1
-        std::vector<int32_t> gnode;
-        number_groups(s, gnode, nullptr);
+    void compact(State &s, Scratch &sc) const {  // monotone relabel of group ids to 0..G-1
+        number_groups(s, sc.gnode, nullptr);
         for (int v = 0; v < V; v++) {
-            s.ng[v] = gnode[s.ng[v]];
-            if (s.rg[v] >= 0) s.rg[v] = gnode[s.rg[v]];
+            s.ng[v] = sc.gnode[s.ng[v]];
+            if (s.rg[v] >= 0) s.rg[v] = sc.gnode[s.rg[v]];
         }
     }
 
     // fuse_nondup (rewrite.py:64-96) / fuse_dup (rewrite.py:99-153)
-    bool fuse_ops(const State &s, const Index &ix, int og, int pg, bool dup, State &out,
-                  std::vector<int32_t> &scratch) const {
+    bool fuse_ops(const State &s, const Index &ix, int og, int pg, bool dup, State &out, Scratch &sc) const {
         if (og == pg) return false;
         for (int k = ix.mptr[pg]; k < ix.mptr[pg + 1]; k++) {  // groups share a member (rewrite.py:76-79)
             int v = ix.mem[k];
@@ -360,12 +380,9 @@ struct Engine {
             for (int k = ix.sptr[pg]; k < ix.sptr[pg + 1]; k++) other |= ix.succ[k] != og;
             if (other || ix.feeds_ar[pg]) {
                 int32_t replica = ix.gid[ix.G - 1] + 1;  // rewrite.py:138
-                if (replica >= VB) {
-                    compact(out);
-                    // ids changed monotonically: recompute merged / replica in the new labelling
-                    std::vector<int32_t> gnode;
-                    number_groups(s, gnode, nullptr);
-                    merged = std::min(gnode[gidx], gnode[gidp]);
+                if (replica >= VB) {  // ids only matter by order: compact, then recompute
+                    compact(out, sc);
+                    merged = std::min(og, pg);
                     replica = ix.G;
                 }
                 for (int k = ix.mptr[og]; k < ix.mptr[og + 1]; k++) {
@@ -377,7 +394,7 @@ struct Engine {
                     out.ng[v] = merged;
                     out.rg[v] = replica;
                 }
-                return valid(out, scratch);
+                return valid(out, sc);
             }
         }
         for (int x : {og, pg})
@@ -385,36 +402,31 @@ struct Engine {
                 int v = ix.mem[k];
                 if (ix.mdup[k]) out.rg[v] = merged; else out.ng[v] = merged;
             }
-        return valid(out, scratch);
+        return valid(out, sc);
     }
 
     // fuse_allreduce (rewrite.py:181-209)
-    bool fuse_ar(const State &s, const Index &ix, int bo, int bn, State &out, std::vector<int32_t> &scratch) const {
+    bool fuse_ar(const State &s, const Index &ix, int bo, int bn, State &out, Scratch &sc) const {
         int32_t merged = std::min(ix.bid[bo], ix.bid[bn]);
         out = s;
         for (int a = 0; a < A; a++)
             if (ix.bki[a] == bo || ix.bki[a] == bn) out.bk[a] = merged;
-        return valid(out, scratch);
+        return valid(out, sc);
     }
 
     // random_apply (rewrite.py:222-263); state updated in place
-    bool random_apply(State &s, int method, int n, PyRng &rng) const {
+    bool random_apply(State &s, int method, int n, PyRng &rng, Scratch &sc) const {
         bool applied = false;
-        Index ix;
-        State cand;
-        std::vector<int32_t> scratch;
         for (int it = 0; it < n; it++) {
-            build(s, ix);
-            int x = -1, y = -1;
-            int cnt = method == M_AR ? bucket_pairs(ix, -1, &x, &y) : fusible_pairs(ix, method == M_DUP, -1, &x, &y);
-            if (cnt == 0) break;
-            int idx = (int)rng.below((uint32_t)cnt);
-            if (method == M_AR) bucket_pairs(ix, idx, &x, &y);
-            else fusible_pairs(ix, method == M_DUP, idx, &x, &y);
-            bool ok = method == M_AR ? fuse_ar(s, ix, x, y, cand, scratch)
-                                     : fuse_ops(s, ix, x, y, method == M_DUP, cand, scratch);
+            build(s, sc.ix, sc);
+            if (method == M_AR) bucket_pairs(sc.ix, sc, sc.pairs);
+            else fusible_pairs(sc.ix, method == M_DUP, sc.pairs);
+            if (sc.pairs.empty()) break;
+            auto pr = sc.pairs[rng.below((uint32_t)sc.pairs.size())];
+            bool ok = method == M_AR ? fuse_ar(s, sc.ix, pr.first, pr.second, sc.cand, sc)
+                                     : fuse_ops(s, sc.ix, pr.first, pr.second, method == M_DUP, sc.cand, sc);
             if (ok) {
-                std::swap(s, cand);
+                std::swap(s, sc.cand);
                 applied = true;
             }
         }
@@ -499,12 +511,13 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
     const int V = g->V, A = g->A;
 #pragma omp parallel for num_threads(n_threads) schedule(dynamic, 1)
     for (int k = 0; k < K; k++) {
+        thread_local Scratch sc;
         PyRng rng(seeds[k]);
         State s = base;
         for (int m = 0; m < 3; m++) {
             if (!(methods_mask & (1 << m))) continue;
             int n = (int)rng.below((uint32_t)beta + 1);
-            eng.random_apply(s, m, n, rng);
+            eng.random_apply(s, m, n, rng, sc);
         }
         std::copy(s.ng.begin(), s.ng.end(), ngid_out + (int64_t)k * V);
         std::copy(s.rg.begin(), s.rg.end(), rgid_out + (int64_t)k * V);
@@ -524,7 +537,8 @@ int fo_random_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int
     PyRng rng(0);
     std::copy(mt_state, mt_state + 624, rng.mt);
     rng.mti = (int)mt_state[624];
-    bool applied = eng.random_apply(s, method, n, rng);
+    Scratch sc;
+    bool applied = eng.random_apply(s, method, n, rng, sc);
     std::copy(rng.mt, rng.mt + 624, mt_state);
     mt_state[624] = (uint32_t)rng.mti;
     std::copy(s.ng.begin(), s.ng.end(), ngid);
@@ -540,26 +554,24 @@ int fo_expand_all(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
     Engine eng(g);
     State s;
     if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    Scratch sc;
     Index ix;
-    eng.build(s, ix);
+    eng.build(s, ix, sc);
     std::vector<State> out;
     State cand;
-    std::vector<int32_t> scratch;
     // exhaustive_search's per-graph enumeration (search.py:185-206)
-    int x = -1, y = -1;
-    int np_ = eng.fusible_pairs(ix, false, -1, &x, &y);
-    for (int i = 0; i < np_; i++) {
-        eng.fusible_pairs(ix, false, i, &x, &y);
-        if (eng.fuse_ops(s, ix, x, y, false, cand, scratch)) out.push_back(cand);
+    std::vector<std::pair<int32_t, int32_t>> fp, bp;
+    eng.fusible_pairs(ix, false, fp);
+    for (auto pr : fp) {
+        int x = pr.first, y = pr.second;
+        if (eng.fuse_ops(s, ix, x, y, false, cand, sc)) out.push_back(cand);
         bool other = ix.feeds_ar[y];
         for (int k = ix.sptr[y]; k < ix.sptr[y + 1]; k++) other |= ix.succ[k] != x;
-        if (other && !ix.has_rep[y] && eng.fuse_ops(s, ix, x, y, true, cand, scratch)) out.push_back(cand);
+        if (other && !ix.has_rep[y] && eng.fuse_ops(s, ix, x, y, true, cand, sc)) out.push_back(cand);
     }
-    int nb = eng.bucket_pairs(ix, -1, &x, &y);
-    for (int i = 0; i < nb; i++) {
-        eng.bucket_pairs(ix, i, &x, &y);
-        if (eng.fuse_ar(s, ix, x, y, cand, scratch)) out.push_back(cand);
-    }
+    eng.bucket_pairs(ix, sc, bp);
+    for (auto pr : bp)
+        if (eng.fuse_ar(s, ix, pr.first, pr.second, cand, sc)) out.push_back(cand);
     *n_out = (int32_t)out.size();
     if ((int)out.size() > cap) return fail(FO_INVALID_ARG, "output capacity too small");
     const int V = g->V, A = g->A;
@@ -620,6 +632,7 @@ struct fo_search {
         int meth[3];
         uint64_t h[3];
         int64_t batch_pos[3];
+        Scratch sc;
     };
     std::vector<Seed> seeds;
     // device batch buffers
@@ -760,7 +773,7 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
             int n = (int)sd.rng.below((uint32_t)S->cfg.beta + 1);
             int j = sd.ncand++;
             sd.cand[j] = sd.pool[sd.cur.slot];
-            bool applied = eng.random_apply(sd.cand[j], m, n, sd.rng);
+            bool applied = eng.random_apply(sd.cand[j], m, n, sd.rng, sd.sc);
             sd.meth[j] = m;
             sd.h[j] = applied ? eng.hash(sd.cand[j]) : sd.cur.h;
         }
