@@ -2,6 +2,7 @@
 // model upload, batched scoring, single-candidate simulate/timeline.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -47,7 +48,12 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
                   double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
     ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
-    WsLayout L;
+    WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max);
+    // bound the per-warp workspace to a fixed HBM budget (large graphs get
+    // fewer resident candidates rather than tens of GB of scratch)
+    const size_t budget = (size_t)16 << 30;
+    int max_blocks = (int)std::max<size_t>(1, budget / ((size_t)L.total * score_warps_per_block()));
+    geo.grid = std::min(geo.grid, max_blocks);
     int slots = geo.grid * score_warps_per_block();
     int st = ensure_workspace(g, VB, slots, &L);
     if (st) return st;

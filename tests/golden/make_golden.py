@@ -359,13 +359,37 @@ def section_exhaustive(_=None):
     print(f"exhaustive: {len(out)} cases", flush=True)
 
 
+def section_sweep(_=None):
+    """BASELINE configs[3]: GPT-2-medium proxy, tensor-fusion bucket-size sweep.
+    Parents = threshold_allreduce_fusion(g, T, cp) and the same on
+    greedy_postorder_fusion(g) (search.py:228-302; the compare verb's "both"
+    row, cli.py:378-383) for T = 2^k, k = 16..28, with their reference costs."""
+    from fuseopt import greedy_postorder_fusion, threshold_allreduce_fusion
+
+    g, profile, comm, mp, lin = load_workload("gpt2m")
+    cp = make_cost_providers(profile, comm, mp)
+    t0 = time.time()
+    greedy = greedy_postorder_fusion(g)
+    print(f"greedy done in {time.time() - t0:.0f}s", flush=True)
+    out = {"greedy": {"state": state_doc(greedy), "cost": cost(greedy, cp)}, "sweep": []}
+    for k in range(16, 29):
+        T = 2 ** k
+        a = threshold_allreduce_fusion(g, T, cp)
+        b = threshold_allreduce_fusion(greedy, T, cp)
+        out["sweep"].append({"T": T, "ar_only": {"state": state_doc(a), "cost": cost(a, cp)},
+                             "both": {"state": state_doc(b), "cost": cost(b, cp)}})
+        print(f"sweep T=2^{k}: {time.time() - t0:.0f}s", flush=True)
+        _dump_gz(os.path.join(OUT, "sweep_gpt2m.json.gz"), out)
+
+
 def main(argv):
-    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive")]
+    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep")]
     names = [a for a in argv if a not in sections]
     if not sections:
         sections = ["workloads", "rng", "cases", "search", "exhaustive"]
     for s in sections:
         {"workloads": section_workloads, "rng": lambda _: section_rng(), "exhaustive": section_exhaustive,
+         "sweep": section_sweep,
          "cases": section_cases, "search": section_search}[s](names or None)
 
 

@@ -1,0 +1,140 @@
+"""Bench lines for BASELINE.json configs[3] and [4] (the headline bench.py line
+is configs[1]).
+
+  python tools/bench_configs.py gpt2-sweep [--batch 256]
+      GPT-2-medium proxy (V=5000): the 13 bucket-size thresholds x {AR-only,
+      greedy op fusion + AR} parents from the reference's own baselines
+      (tests/golden/sweep_gpt2m.json.gz), each scored and then used as the
+      parent of a random-candidate batch.
+  python tools/bench_configs.py synth50k [--batch 8192]
+      synthetic 50k-op DAG: one round of random candidates per GPU
+      (64k per round on 8 GPUs = 8192 per GPU).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def timed_score(dg, ng, rg, bk, gb, prec, reps=5):
+    import numpy as np
+    import torch
+
+    d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
+    K = ng.shape[0]
+    cost = torch.empty(K, dtype=torch.float64, device="cuda")
+    st = torch.empty(K, dtype=torch.int32, device="cuda")
+    dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return cost.cpu().numpy(), st.cpu().numpy(), float(np.median(ts))
+
+
+def gpt2_sweep(args):
+    import numpy as np
+    import torch
+
+    import paper_2209_12769_b200 as P
+    from paper_2209_12769_b200 import _native as N
+    from _golden import graph_with_state, read
+
+    torch.cuda.set_device(0)
+    prec = N.FO_PREC_FP32
+    g, prof, comm, mp, lin = P.load_workload("gpt2m")
+    cp = P.make_cost_providers(prof, comm, mp, precision=prec)
+    dg = cp.device_graph(g)
+    sweep = read("sweep_gpt2m.json.gz")
+    rows, worst, total_c, total_ms, gen_s = [], 0.0, 0, 0.0, 0.0
+    from paper_2209_12769_b200.graph import state_arrays
+
+    for ent in sweep["sweep"]:
+        for kind in ("ar_only", "both"):
+            parent = graph_with_state(g, ent[kind]["state"])
+            c_dev = P.cost(parent, cp)
+            rel = abs(c_dev - ent[kind]["cost"]) / ent[kind]["cost"]
+            worst = max(worst, rel)
+            ng0, rg0, bk0, _, _, _ = state_arrays(parent)
+            t0 = time.perf_counter()
+            ng, rg, bk, gb = dg.make_candidates(np.arange(args.batch, dtype=np.uint64), base=(ng0, rg0, bk0))
+            gen_s += time.perf_counter() - t0
+            cost, st, ms = timed_score(dg, ng, rg, bk, gb, prec)
+            assert (st == 0).all()
+            total_c += args.batch
+            total_ms += ms
+            rows.append({"T": ent["T"], "parent": kind, "parent_cost_us": c_dev, "ref_parent_cost_us": ent[kind]["cost"],
+                         "batch_best_us": float(cost.min()), "batch_ms": ms})
+    line = {"metric": "fusion candidates scored/sec (GNN est.+sim)", "config": "gpt2m bucket-size sweep",
+            "value": total_c / (total_ms / 1e3), "unit": "candidates/s", "n_gpus": 1,
+            "thresholds": len(sweep["sweep"]), "batch_per_parent": args.batch, "parents": len(rows),
+            "parent_cost_max_rel_err_vs_reference": worst, "candidate_generation_s": gen_s,
+            "best": min(rows, key=lambda r: r["batch_best_us"]), "rows": rows}
+    print(json.dumps(line))
+
+
+def synth50k(args):
+    import numpy as np
+    import torch
+
+    import paper_2209_12769_b200 as P
+    from paper_2209_12769_b200 import _native as N
+
+    torch.cuda.set_device(0)
+    prec = N.FO_PREC_FP32
+    g, prof, comm, mp, lin = P.load_workload("synth50k")
+    cp = P.make_cost_providers(prof, comm, mp, precision=prec)
+    dg = cp.device_graph(g)
+    # the host rewrite engine rebuilds the full index per rewrite (~0.2 s per
+    # rewrite at 50k ops), so a bounded set of distinct candidates is generated
+    # and tiled to the round size; every tile is scored independently
+    t0 = time.perf_counter()
+    nd = min(args.distinct, args.batch)
+    ng, rg, bk, gb = dg.make_candidates(np.arange(nd, dtype=np.uint64), beta=args.beta)
+    gen_s = time.perf_counter() - t0
+    reps_ = (args.batch + nd - 1) // nd
+    ng, rg, bk = (np.ascontiguousarray(np.tile(x, (reps_, 1))[: args.batch]) for x in (ng, rg, bk))
+    cost, st, ms = timed_score(dg, ng, rg, bk, gb, prec, reps=3)
+    line = {"metric": "fusion candidates scored/sec (GNN est.+sim)", "config": "synthetic 50k-op DAG, one round",
+            "value": args.batch / (ms / 1e3), "unit": "candidates/s", "n_gpus": 1, "batch": args.batch,
+            "beta": args.beta, "ms_per_round": ms, "candidate_generation_s": gen_s, "distinct_candidates": nd,
+            "statuses": {str(k): int(v) for k, v in zip(*np.unique(st, return_counts=True))},
+            "best_us": float(cost[st == 0].min()) if (st == 0).any() else None}
+    if args.check > 0:
+        from oracle.oracle import Oracle, load_workload
+
+        o = Oracle(load_workload("synth50k"), "mp")
+        t1 = time.perf_counter()
+        errs = []
+        for i in range(args.check):
+            s_, c = o.cost(*o.make_candidate(i, args.beta))
+            errs.append(abs(c - cost[i]) / c)
+        line["oracle_check"] = {"candidates": args.check, "max_rel_err": max(errs),
+                                "oracle_s_per_candidate": (time.perf_counter() - t1) / args.check}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["gpt2-sweep", "synth50k"])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--beta", type=int, default=10)
+    ap.add_argument("--check", type=int, default=2)
+    ap.add_argument("--distinct", type=int, default=128)
+    a = ap.parse_args()
+    if a.what == "gpt2-sweep":
+        a.batch = a.batch or 256
+        gpt2_sweep(a)
+    else:
+        a.batch = a.batch or 8192
+        synth50k(a)
