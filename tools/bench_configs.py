@@ -130,7 +130,7 @@ if __name__ == "__main__":
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--beta", type=int, default=10)
     ap.add_argument("--check", type=int, default=2)
-    ap.add_argument("--distinct", type=int, default=128)
+    ap.add_argument("--distinct", type=int, default=1024)
     a = ap.parse_args()
     if a.what == "gpt2-sweep":
         a.batch = a.batch or 256
