@@ -31,15 +31,17 @@ int fail(int status, const std::string &msg) {
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L) {
-    *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max);
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big) {
+    *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, big ? g->V : kMpCapDefault);
     size_t need = (size_t)L->total * (size_t)slots;
-    if (need > g->ws_bytes) {
-        if (g->d_ws) cudaFree(g->d_ws);
-        g->d_ws = nullptr;
-        g->ws_bytes = 0;
-        CUDA_TRY(cudaMalloc(&g->d_ws, need));
-        g->ws_bytes = need;
+    char *&buf = big ? g->d_ws_big : g->d_ws;
+    size_t &have = big ? g->ws_big_bytes : g->ws_bytes;
+    if (need > have) {
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        have = 0;
+        CUDA_TRY(cudaMalloc(&buf, need));
+        have = need;
     }
     return FO_OK;
 }
@@ -48,7 +50,7 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
                   double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
     ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
-    WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max);
+    WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, kMpCapDefault);
     // bound the per-warp workspace to a fixed HBM budget (large graphs get
     // fewer resident candidates rather than tens of GB of scratch)
     const size_t budget = (size_t)16 << 30;
@@ -61,6 +63,22 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
                                  dur_out, bad_out, ngroups_out, stream);
     g_launches++;
     if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score kernel launch: ") + cudaGetErrorString(e));
+    if (g->V > kMpCapDefault) {
+        // second pass, same stream: only candidates whose fused groups exceeded
+        // the first pass's estimator scratch, with scratch for whole-graph groups
+        WsLayout Lb;
+        ScoreGeo gb = geo;
+        gb.sm_bytes = 0;
+        gb.grid = std::min(std::max(1, (K + score_warps_per_block() - 1) / score_warps_per_block()), g->num_sms);
+        Lb = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, g->V);
+        gb.grid = std::min<int>(gb.grid, (int)std::max<size_t>(1, budget / ((size_t)Lb.total * score_warps_per_block())));
+        st = ensure_workspace(g, VB, gb.grid * score_warps_per_block(), &Lb, true);
+        if (st) return st;
+        e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws_big, Lb, gb, cost, status, ext_dur, tl,
+                         dur_out, bad_out, ngroups_out, stream, 1);
+        g_launches++;
+        if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score retry launch: ") + cudaGetErrorString(e));
+    }
     return FO_OK;
 }
 
@@ -195,6 +213,7 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_static) cudaFree(g->d_static);
     if (g->d_model) cudaFree(g->d_model);
     if (g->d_ws) cudaFree(g->d_ws);
+    if (g->d_ws_big) cudaFree(g->d_ws_big);
     if (g->d_io) cudaFree(g->d_io);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     if (g->stream) cudaStreamDestroy(g->stream);

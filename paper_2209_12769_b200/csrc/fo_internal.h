@@ -70,8 +70,10 @@ __host__ __device__ inline MpLayout mp_layout(int layers) {
 struct WsLayout {
     int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, dur, fused, gptr, gmem, msort, lidx, nbptr, nb, H, P, gint, gin, gout, vis, zl, csim, rank, tlid;
     int64_t total;
+    int32_t mpcap;
 };
-WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max);
+WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap);
+constexpr int kMpCapDefault = 2048;  // fused-group size the per-warp MP scratch holds
 
 struct TimelineOut {
     int32_t *c_id;
@@ -92,7 +94,8 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision);
 cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K,
                          int VB, int precision, char *ws, const WsLayout &L, const ScoreGeo &geo,
                          double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
-                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream);
+                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream,
+                         int retry_only = 0);
 int score_warps_per_block();
 
 }  // namespace fo
@@ -116,6 +119,8 @@ struct fo_graph {
     // scoring workspace
     char *d_ws = nullptr;
     size_t ws_bytes = 0;
+    char *d_ws_big = nullptr;  // second-pass workspace for fused groups beyond kMpCapDefault
+    size_t ws_big_bytes = 0;
     // host API staging
     void *d_io = nullptr;
     size_t io_bytes = 0;
@@ -130,7 +135,7 @@ namespace fo {
 void set_error(const std::string &msg);
 int fail(int status, const std::string &msg);
 // Ensure the handle's workspace can hold `slots` warps for gid bound VB.
-int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L);
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big = false);
 // Score K device-resident candidates (used by fo_score and the search engine).
 int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                  int precision, double *cost, int32_t *status, cudaStream_t stream);

@@ -29,16 +29,16 @@ namespace fo {
 
 #define FULL 0xffffffffu
 constexpr int kWarps = 4;          // warps per block
-constexpr int kMpCap = 2048;       // max fused-group size held in the MP scratch
-constexpr int kRetryLarge = 100;   // internal status: group larger than kMpCap
+constexpr int kRetryLarge = 100;   // internal status: fused group larger than the MP scratch (L.mpcap)
 
 static inline int64_t align8(int64_t x) { return (x + 7) & ~int64_t(7); }
 
-WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max) {
+WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap) {
     WsLayout L{};
+    L.mpcap = mpcap;
     int64_t GM = (int64_t)(VB < 2 * V ? VB : 2 * V) + 1;
     int64_t NM = GM + A + 1;
-    int64_t cap = V < kMpCap ? V : kMpCap;
+    int64_t cap = V < mpcap ? V : mpcap;
     int64_t o = 0;
     auto take = [&](int64_t bytes) { int64_t r = o; o = align8(o + bytes); return r; };
     L.gmap = take(4 * (int64_t)VB);
@@ -283,6 +283,7 @@ struct ScoreArgs {
     DGraph g;
     const void *ngid, *rgid, *bkt;  // int32, or int16 when idx16
     int idx16;
+    int retry_only;  // second pass: only candidates a first pass flagged kRetryLarge
     int K, VB;
     int sm_nodes, sm_pairs, sm_bytes;  // per-warp shared-memory simulation arena
     char *ws;
@@ -931,7 +932,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                 const int gi = w.fused()[f];
                 const int b0 = w.gptr()[f], n = w.gptr()[f + 1] - b0;
                 int *mem = w.gmem() + b0;
-                if (n > kMpCap && !hw && (g.variant == FO_EST_MESSAGE_PASSING || g.variant == FO_EST_LINEAR)) {
+                if (n > a.L.mpcap && !hw && (g.variant == FO_EST_MESSAGE_PASSING || g.variant == FO_EST_LINEAR)) {
                     badk = min(badk, pack_bad(gi, kRetryLarge));
                     continue;
                 }
@@ -1121,7 +1122,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel(const __grid_cons
     extern __shared__ __align__(16) char smem_arena[];
     Ws w = ws_at(a.ws + (int64_t)wid * a.L.total, a.L);
     char *sm = a.sm_bytes > 0 ? smem_arena + (threadIdx.x >> 5) * a.sm_bytes : nullptr;
-    for (int k = wid; k < a.K; k += nw) score_one<T>(a, k, w, lane, sm);
+    for (int k = wid; k < a.K; k += nw) {
+        if (a.retry_only && a.status_out[k] != kRetryLarge) continue;
+        score_one<T>(a, k, w, lane, sm);
+    }
 }
 
 int score_warps_per_block() { return kWarps; }
@@ -1168,8 +1172,9 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
 cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K,
                          int VB, int precision, char *ws, const WsLayout &L, const ScoreGeo &geo,
                          double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
-                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
+                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream, int retry_only) {
     ScoreArgs a;
+    a.retry_only = retry_only;
     a.g = g;
     a.ngid = ngid;
     a.rgid = rgid;

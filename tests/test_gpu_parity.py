@@ -290,3 +290,19 @@ def test_int16_encoding_matches_int32():
     dg.score_device(d[0], d[1], d[2], gb, c, s)
     torch.cuda.synchronize()
     assert np.array_equal(c.cpu().numpy(), c32)
+
+
+def test_gpt2_sweep_parents_match_reference():
+    """BASELINE configs[3]: the bucket-size sweep parents (threshold AR fusion on
+    the unfused and on the greedily op-fused GPT-2 graph).  The greedy parent
+    holds fused groups of thousands of ops (the large-group second pass)."""
+    doc = read("sweep_gpt2m.json.gz")
+    for precision in (N.FO_PREC_FP32, N.FO_PREC_FP64):
+        g, cps = providers("gpt2m", precision)
+        graphs, ref = [graph_with_state(g, doc["greedy"]["state"])], [doc["greedy"]["cost"]]
+        for ent in doc["sweep"]:
+            for kind in ("ar_only", "both"):
+                graphs.append(graph_with_state(g, ent[kind]["state"]))
+                ref.append(ent[kind]["cost"])
+        got = P.cost_batch(graphs, cps["mp"])
+        np.testing.assert_allclose(got, ref, rtol=1e-4 if precision == N.FO_PREC_FP32 else 1e-12)
