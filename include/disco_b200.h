@@ -102,6 +102,14 @@ int fo_graph_destroy(fo_graph *g);
 /* Replaces make_cost_providers(...) / oracle_providers(...) (estimator.py:801, workloads.py:294). */
 int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *model);
 
+/* ---- estimator memo ---------------------------------------------------- */
+/* Message-passing predictions are a pure function of the fused group's member
+ * set (estimator.py:157-191, :363-389); the device caches them per handle.
+ * fo_memo_clear empties the cache, ordered on `stream` (NULL: the handle's own
+ * stream, which fo_score_host / fo_simulate use); fo_memo_enable(0) turns it off. */
+int fo_memo_clear(fo_graph *g, void *stream);
+int fo_memo_enable(fo_graph *g, int32_t enable);
+
 /* ---- scoring ----------------------------------------------------------- */
 /* cost() for K candidates (simulator.py:143-145 over K fresh graphs).
  * Device pointers; asynchronous on `stream` (cudaStream_t, NULL = legacy).

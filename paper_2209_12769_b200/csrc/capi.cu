@@ -214,6 +214,7 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_model) cudaFree(g->d_model);
     if (g->d_ws) cudaFree(g->d_ws);
     if (g->d_ws_big) cudaFree(g->d_ws_big);
+    if (g->d_memo) cudaFree(g->d_memo);
     if (g->d_io) cudaFree(g->d_io);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     if (g->stream) cudaStreamDestroy(g->stream);
@@ -308,6 +309,13 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         }
         CUDA_TRY(cudaMemcpy(b + oWd, W.data(), W.size() * 8, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(b + oWf, Wf.data(), Wf.size() * 4, cudaMemcpyHostToDevice));
+        // estimator memo: 2 x 2^20 slots, cleared whenever the model changes
+        const size_t slots = (size_t)1 << 20;
+        if (!g->d_memo) CUDA_TRY(cudaMalloc(&g->d_memo, 2 * slots * sizeof(MemoEnt)));
+        CUDA_TRY(cudaMemset(g->d_memo, 0, 2 * slots * sizeof(MemoEnt)));
+        dg.memo[0] = (MemoEnt *)g->d_memo;
+        dg.memo[1] = (MemoEnt *)g->d_memo + slots;
+        dg.memo_mask = (uint32_t)(slots - 1);
         dg.H0d = (const double *)(b + oH0d);
         dg.H0f = (const float *)(b + oH0f);
         dg.Wd = (const double *)(b + oWd);
@@ -315,6 +323,27 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         dg.layers = L;
     }
     g->model_set = true;
+    return FO_OK;
+}
+
+int fo_memo_clear(fo_graph *g, void *stream) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (!g->d_memo) return FO_OK;
+    cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;  // NULL: the handle's own stream
+    CUDA_TRY(cudaMemsetAsync(g->d_memo, 0, 2 * ((size_t)g->dg.memo_mask + 1) * sizeof(MemoEnt), s));
+    return FO_OK;
+}
+
+int fo_memo_enable(fo_graph *g, int32_t enable) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    std::lock_guard<std::mutex> lk(g->mu);
+    const size_t slots = (size_t)g->dg.memo_mask + 1;
+    if (enable && g->d_memo) {
+        g->dg.memo[0] = (MemoEnt *)g->d_memo;
+        g->dg.memo[1] = (MemoEnt *)g->d_memo + slots;
+    } else {
+        g->dg.memo[0] = g->dg.memo[1] = nullptr;
+    }
     return FO_OK;
 }
 

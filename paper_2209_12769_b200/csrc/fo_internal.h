@@ -17,6 +17,12 @@ namespace fo {
 
 constexpr int kHidden = 32;  // lane = hidden channel in the message-passing kernel
 
+struct MemoEnt {  // estimator memo slot (score.cu)
+    unsigned long long k1, k2;
+    double v;
+    unsigned long long pad;
+};
+
 // Device-side view of one graph + cost model, passed by value to kernels.
 struct DGraph {
     int32_t V, E, A;
@@ -45,6 +51,8 @@ struct DGraph {
     double lin_w[12], lin_b, agg_mean[12], agg_std[12];
     int32_t lin_norm;
     int32_t pairs_max;          // bound on contracted dependency pairs per candidate
+    MemoEnt *memo[2];           // MP predictions by member set: [fp32, fp64]
+    uint32_t memo_mask;
 };
 
 // Packed message-passing weights (float or double), all transposed so lane c
@@ -114,6 +122,7 @@ struct fo_graph {
     // device buffers
     void *d_static = nullptr;  // one allocation for the static graph
     void *d_model = nullptr;   // H0 + weights
+    void *d_memo = nullptr;    // estimator memo tables
     fo::DGraph dg{};
     bool model_set = false;
     // scoring workspace

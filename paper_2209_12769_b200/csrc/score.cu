@@ -146,6 +146,65 @@ struct PySum {
     __device__ __forceinline__ double get() const { return (c != 0.0 && isfinite(c)) ? __dadd_rn(f, c) : f; }
 };
 
+// Group-level estimator memo: the message-passing prediction is
+// a pure function of the member set (per-op features, member-internal edges),
+// so predictions are cached per graph handle in an open-addressing table keyed
+// by two independent 64-bit set hashes.  k1 == 0 empty, 2 pending, odd ready.
+__device__ __forceinline__ unsigned long long smix(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+// commutative hashes of the member set, warp-wide (order independent)
+__device__ __forceinline__ void set_hash(const int *mem, int n, int lane, unsigned long long &h1,
+                                         unsigned long long &h2) {
+    unsigned long long a = 0, b = 0;
+    for (int i = lane; i < n; i += 32) {
+        a += smix((unsigned long long)mem[i] * 2 + 1);
+        b += smix(((unsigned long long)mem[i] << 32) ^ 0x5bd1e995ull);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        a += __shfl_xor_sync(FULL, a, d);
+        b += __shfl_xor_sync(FULL, b, d);
+    }
+    h1 = smix(a + (unsigned long long)n) | 1ull;
+    h2 = smix(b ^ ((unsigned long long)n * 0xff51afd7ed558ccdull));
+}
+constexpr int kMemoProbe = 16;
+__device__ __forceinline__ bool memo_get(const MemoEnt *t, unsigned mask, unsigned long long h1, unsigned long long h2,
+                                         double *v) {
+    for (int p = 0; p < kMemoProbe; p++) {
+        const MemoEnt *e = &t[(unsigned)(h1 + p) & mask];
+        unsigned long long k = *(volatile const unsigned long long *)&e->k1;
+        if (k == 0) return false;
+        if (k == h1) {
+            __threadfence();
+            if (*(volatile const unsigned long long *)&e->k2 == h2) {
+                *v = *(volatile const double *)&e->v;
+                return true;
+            }
+        }
+    }
+    return false;
+}
+__device__ __forceinline__ void memo_put(MemoEnt *t, unsigned mask, unsigned long long h1, unsigned long long h2,
+                                         double v) {
+    for (int p = 0; p < kMemoProbe; p++) {
+        MemoEnt *e = &t[(unsigned)(h1 + p) & mask];
+        unsigned long long k = atomicCAS(&e->k1, 0ull, 2ull);
+        if (k == 0) {
+            e->k2 = h2;
+            e->v = v;
+            __threadfence();
+            atomicExch(&e->k1, h1);
+            return;
+        }
+        if (k == h1) return;  // already present
+    }
+}
+
 // numpy logaddexp(0, z) (estimator.py:297-298)
 __device__ __forceinline__ double softplus_d(double z) {
     if (z == 0.0) return 0.6931471805599453;
@@ -932,6 +991,19 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                 const int gi = w.fused()[f];
                 const int b0 = w.gptr()[f], n = w.gptr()[f + 1] - b0;
                 int *mem = w.gmem() + b0;
+                unsigned long long mh1 = 0, mh2 = 0;
+                MemoEnt *memo = (!hw && g.variant == FO_EST_MESSAGE_PASSING) ? g.memo[sizeof(T) == 8] : nullptr;
+                if (memo) {
+                    set_hash(mem, n, lane, mh1, mh2);
+                    double mv = 0.0;
+                    bool hit = false;
+                    if (lane == 0) hit = memo_get(memo, g.memo_mask, mh1, mh2, &mv);
+                    hit = __shfl_sync(FULL, hit, 0);
+                    if (hit) {
+                        if (lane == 0) w.dur()[gi] = mv;
+                        continue;
+                    }
+                }
                 if (n > a.L.mpcap && !hw && (g.variant == FO_EST_MESSAGE_PASSING || g.variant == FO_EST_LINEAR)) {
                     badk = min(badk, pack_bad(gi, kRetryLarge));
                     continue;
@@ -948,11 +1020,19 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                             x = (lower == up) ? lo : hi;
                         }
                     if (lane < n) mem[lane] = x;
-                } else if (lane == 0) {  // insertion sort (rare: large groups)
-                    for (int i = 1; i < n; i++) {
-                        int x = mem[i], j = i - 1;
-                        while (j >= 0 && mem[j] > x) { mem[j + 1] = mem[j]; j--; }
-                        mem[j + 1] = x;
+                } else {  // large groups: mark members, then a ballot scan over ops yields them in order
+                    int *mark = w.vis();
+                    for (int v = lane; v < V; v += 32) mark[v] = 0;
+                    __syncwarp();
+                    for (int i = lane; i < n; i += 32) mark[mem[i]] = 1;
+                    __syncwarp();
+                    int o = 0;
+                    for (int base = 0; base < V; base += 32) {
+                        int v = base + lane;
+                        bool m = v < V && mark[v];
+                        unsigned bm = __ballot_sync(FULL, m);
+                        if (m) mem[o + __popc(bm & lanemask_lt())] = v;
+                        o += __popc(bm);
                     }
                 }
                 __syncwarp();
@@ -1044,7 +1124,10 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                     }
                     __syncwarp();
                     double pred = mp_forward<T>(g, mem, n, w.nbptr(), w.nb(), (T *)w.H(), (T *)w.P(), lane);
-                    if (lane == 0) w.dur()[gi] = pred;
+                    if (lane == 0) {
+                        w.dur()[gi] = pred;
+                        if (memo) memo_put(memo, g.memo_mask, mh1, mh2, pred);
+                    }
                 } else {  // LINEAR (estimator.py:117-128, 341-345, 421-426)
                     dirE = __reduce_add_sync(FULL, dirE);
                     if (lane == 0) {

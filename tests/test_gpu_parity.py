@@ -306,3 +306,17 @@ def test_gpt2_sweep_parents_match_reference():
                 ref.append(ent[kind]["cost"])
         got = P.cost_batch(graphs, cps["mp"])
         np.testing.assert_allclose(got, ref, rtol=1e-4 if precision == N.FO_PREC_FP32 else 1e-12)
+
+
+def test_estimator_memo_is_exact():
+    """Memo hits return the very prediction computed for the same member set."""
+    g, cps = providers("resnet50", N.FO_PREC_FP32)
+    dg = cps["mp"].device_graph(g)
+    ng, rg, bk, gb = dg.make_candidates(np.arange(1024, dtype=np.uint64))
+    N.lib().fo_memo_enable(dg.h, 0)
+    off, _ = dg.score_host(ng, rg, bk, gb)
+    N.lib().fo_memo_enable(dg.h, 1)
+    N.lib().fo_memo_clear(dg.h, None)
+    cold, _ = dg.score_host(ng, rg, bk, gb)
+    warm, _ = dg.score_host(ng, rg, bk, gb)
+    assert np.array_equal(off, cold) and np.array_equal(off, warm)
