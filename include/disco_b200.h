@@ -102,6 +102,16 @@ int fo_graph_destroy(fo_graph *g);
 /* Replaces make_cost_providers(...) / oracle_providers(...) (estimator.py:801, workloads.py:294). */
 int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *model);
 
+/* Per-round best of a scored batch (device pointers, async): out_pair[2] =
+ * {min cost, id_offset + argmin}, lowest id among equal costs (strict-<,
+ * search.py:124, :214); candidates with a non-OK status are skipped.  This is
+ * the 16-byte value the multi-GPU exchange all-gathers. */
+int fo_batch_best(const double *cost, const int32_t *status, int32_t K, int64_t id_offset, double *out_pair,
+                  void *stream);
+/* Lexicographic min over n (cost, id) pairs, e.g. the all-gathered exchange
+ * buffer of every rank's fo_batch_best. */
+int fo_pairs_best(const double *pairs, int32_t n, double *out_pair, void *stream);
+
 /* ---- estimator memo ---------------------------------------------------- */
 /* Message-passing predictions are a pure function of the fused group's member
  * set (estimator.py:157-191, :363-389); the device caches them per handle.

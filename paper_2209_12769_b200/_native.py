@@ -53,6 +53,8 @@ SIGNATURES = [
     ("fo_graph_create", C.c_int, [P(GraphDesc), C.c_int32, P(vp)]),
     ("fo_graph_destroy", C.c_int, [vp]),
     ("fo_graph_set_cost_model", C.c_int, [vp, P(CostModel)]),
+    ("fo_batch_best", C.c_int, [vp, vp, C.c_int32, C.c_int64, vp, vp]),
+    ("fo_pairs_best", C.c_int, [vp, C.c_int32, vp, vp]),
     ("fo_memo_clear", C.c_int, [vp, vp]),
     ("fo_memo_enable", C.c_int, [vp, C.c_int32]),
     ("fo_score", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]),

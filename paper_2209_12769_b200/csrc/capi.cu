@@ -326,6 +326,23 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
     return FO_OK;
 }
 
+int fo_batch_best(const double *cost, const int32_t *status, int32_t K, int64_t id_offset, double *out_pair,
+                  void *stream) {
+    if (!cost || !out_pair || K < 0) return fail(FO_INVALID_ARG, "bad arguments");
+    cudaError_t e = launch_batch_best(cost, status, K, id_offset, out_pair, (cudaStream_t)stream);
+    g_launches++;
+    if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("batch_best launch: ") + cudaGetErrorString(e));
+    return FO_OK;
+}
+
+int fo_pairs_best(const double *pairs, int32_t n, double *out_pair, void *stream) {
+    if (!pairs || !out_pair || n < 0) return fail(FO_INVALID_ARG, "bad arguments");
+    cudaError_t e = launch_batch_best(pairs, nullptr, n, 0, out_pair, (cudaStream_t)stream, 1);
+    g_launches++;
+    if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("pairs_best launch: ") + cudaGetErrorString(e));
+    return FO_OK;
+}
+
 int fo_memo_clear(fo_graph *g, void *stream) {
     if (!g) return fail(FO_INVALID_ARG, "null graph");
     if (!g->d_memo) return FO_OK;

@@ -105,6 +105,8 @@ cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, co
                          double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream,
                          int retry_only = 0);
 int score_warps_per_block();
+cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, int64_t id_offset, double *out,
+                              cudaStream_t stream, int pairs = 0);
 
 }  // namespace fo
 

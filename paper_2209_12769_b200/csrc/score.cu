@@ -205,6 +205,19 @@ __device__ __forceinline__ void memo_put(MemoEnt *t, unsigned mask, unsigned lon
     }
 }
 
+// Drop dead workspace lines from L2 without writing them back
+// (discard.global.L2): the per-warp scratch of ~4,000 resident candidates
+// exceeds the 126 MB L2, and write-backs of dead setup arrays were most of
+// the kernel's DRAM traffic.  Only whole 128-byte lines inside the range.
+__device__ __forceinline__ void l2_discard(const void *p, int64_t bytes, int lane) {
+    uintptr_t lo = ((uintptr_t)p + 127) & ~uintptr_t(127);
+    uintptr_t hi = ((uintptr_t)p + (uintptr_t)bytes) & ~uintptr_t(127);
+    for (uintptr_t a = lo + (uintptr_t)lane * 128; a < hi; a += 32 * 128) {
+        size_t ga = __cvta_generic_to_global((const void *)a);
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(ga) : "memory");
+    }
+}
+
 // numpy logaddexp(0, z) (estimator.py:297-298)
 __device__ __forceinline__ double softplus_d(double z) {
     if (z == 0.0) return 0.6931471805599453;
@@ -577,6 +590,19 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lan
     for (int q = lane; q < P; q += 32) {
         int s = w.succ()[q];
         succ[q] = se_make<SE>((unsigned)w.prank()[s], (unsigned)s);
+    }
+    // setup-only arrays are dead from here on: drop them from L2
+    {
+        const int V = a.g.V, A = a.g.A;
+        __syncwarp();
+        l2_discard(w.gmap(), 4ll * a.VB, lane);
+        l2_discard(w.nn(), 4ll * V, lane);
+        l2_discard(w.rr(), 4ll * V, lane);
+        l2_discard(w.gmin(), 4ll * G, lane);
+        l2_discard(w.gcnt(), 4ll * G, lane);
+        l2_discard(w.scnt(), 4ll * (N + 1), lane);
+        l2_discard(w.succ(), 4ll * P, lane);
+        l2_discard(w.bki(), 4ll * A, lane);
     }
     // initial ready set: nodes with no deps at rt = 0.0 (level 0), keys sorted
     int hg = 0, hb = 0;
@@ -1209,6 +1235,54 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel(const __grid_cons
         if (a.retry_only && a.status_out[k] != kRetryLarge) continue;
         score_one<T>(a, k, w, lane, sm);
     }
+}
+
+// Per-round best (cost, candidate id) of a scored batch: one block, strict-<
+// order (the lowest id wins among equal costs, search.py:124, :214).  Non-OK
+// candidates are skipped.  out = {cost, id}; (inf, -1) for an empty batch.
+// pairs != 0: cost holds (cost, id) pairs (an all-gathered exchange buffer)
+__global__ void batch_best_kernel(const double *__restrict__ cost, const int32_t *__restrict__ status, int K,
+                                  int64_t id_offset, double *out, int pairs) {
+    __shared__ double sc[32];
+    __shared__ long long si[32];
+    double bc = __longlong_as_double(0x7ff0000000000000ll);
+    long long bi = LLONG_MAX;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        if (status && status[k] != 0) continue;
+        double c = pairs ? cost[2 * k] : cost[k];
+        long long id = pairs ? (long long)cost[2 * k + 1] : k;
+        if (pairs && id < 0) continue;
+        if (c < bc || (c == bc && id < bi)) { bc = c; bi = id; }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        double oc = __shfl_xor_sync(FULL, bc, d);
+        long long oi = __shfl_xor_sync(FULL, bi, d);
+        if (oc < bc || (oc == bc && oi < bi)) { bc = oc; bi = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { sc[threadIdx.x >> 5] = bc; si[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int nw = blockDim.x >> 5;
+        bc = threadIdx.x < nw ? sc[threadIdx.x] : __longlong_as_double(0x7ff0000000000000ll);
+        bi = threadIdx.x < nw ? si[threadIdx.x] : LLONG_MAX;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            double oc = __shfl_xor_sync(FULL, bc, d);
+            long long oi = __shfl_xor_sync(FULL, bi, d);
+            if (oc < bc || (oc == bc && oi < bi)) { bc = oc; bi = oi; }
+        }
+        if (threadIdx.x == 0) {
+            out[0] = bc;
+            out[1] = bi == LLONG_MAX ? -1.0 : (double)(bi + (pairs ? 0 : id_offset));
+        }
+    }
+}
+
+cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, int64_t id_offset, double *out,
+                              cudaStream_t stream, int pairs) {
+    batch_best_kernel<<<1, 512, 0, stream>>>(cost, status, K, id_offset, out, pairs);
+    return cudaGetLastError();
 }
 
 int score_warps_per_block() { return kWarps; }

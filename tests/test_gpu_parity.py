@@ -320,3 +320,22 @@ def test_estimator_memo_is_exact():
     cold, _ = dg.score_host(ng, rg, bk, gb)
     warm, _ = dg.score_host(ng, rg, bk, gb)
     assert np.array_equal(off, cold) and np.array_equal(off, warm)
+
+
+def test_batch_best_and_pairs_best():
+    import torch
+
+    cost = torch.tensor([5.0, 2.0, 7.0, 2.0, 9.0], dtype=torch.float64, device="cuda")
+    st = torch.tensor([0, 0, 0, 0, 0], dtype=torch.int32, device="cuda")
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    N.lib().fo_batch_best(N.ptr(cost), N.ptr(st), 5, 100, N.ptr(out), None)
+    torch.cuda.synchronize()
+    assert out.tolist() == [2.0, 101.0]  # strict <: lowest id among equal costs
+    st[1] = 2  # a failed candidate is skipped
+    N.lib().fo_batch_best(N.ptr(cost), N.ptr(st), 5, 100, N.ptr(out), None)
+    torch.cuda.synchronize()
+    assert out.tolist() == [2.0, 103.0]
+    pairs = torch.tensor([3.0, 40.0, 1.0, 77.0, 1.0, 12.0, float("inf"), -1.0], dtype=torch.float64, device="cuda")
+    N.lib().fo_pairs_best(N.ptr(pairs), 4, N.ptr(out), None)
+    torch.cuda.synchronize()
+    assert out.tolist() == [1.0, 12.0]
