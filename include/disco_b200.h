@@ -200,6 +200,10 @@ int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seed
  * candidates are scored in ONE device batch.  active_out = searches still
  * running; best_out[R] / best_cost_out: per-search best costs after the round. */
 int fo_search_round(fo_search *s, int32_t *active_out, double *best_cost_out);
+/* Run every search to completion (max_rounds <= 0: unbounded) natively.  With
+ * R >= 2 the seeds run in two halves whose device batches overlap the other
+ * half's host-side expand; each seed's step sequence is unchanged. */
+int fo_search_run(fo_search *s, int64_t max_rounds, int32_t *active_out);
 /* Counters: steps, candidates_evaluated, candidates_enqueued, trace length. */
 int fo_search_result(fo_search *s, int32_t r, double *best_cost, int64_t *counters4, int32_t *best_ngid,
                      int32_t *best_rgid, int32_t *best_bkt, fo_trace_rec *trace, int64_t trace_cap);

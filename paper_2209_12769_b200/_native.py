@@ -71,6 +71,7 @@ SIGNATURES = [
     ("fo_state_hash", C.c_int, [vp, vp, vp, vp, C.c_int32, vp]),
     ("fo_search_create", C.c_int, [vp, P(SearchCfg), vp, C.c_int32, vp, vp, vp, P(vp)]),
     ("fo_search_round", C.c_int, [vp, P(C.c_int32), vp]),
+    ("fo_search_run", C.c_int, [vp, C.c_int64, P(C.c_int32)]),
     ("fo_search_result", C.c_int, [vp, C.c_int32, P(C.c_double), vp, vp, vp, vp, P(TraceRec), C.c_int64]),
     ("fo_search_timing", C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int64)]),
     ("fo_search_destroy", C.c_int, [vp]),

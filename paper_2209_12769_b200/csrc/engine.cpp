@@ -625,7 +625,7 @@ struct fo_search {
         bool active = true;
         int status = FO_OK;
         std::vector<fo_trace_rec> trace;
-        // per-round scratch
+        // per-step scratch
         QE cur{};
         int ncand = 0;
         State cand[3];
@@ -634,133 +634,127 @@ struct fo_search {
         int64_t batch_pos[3];
         Scratch sc;
     };
+    // one in-flight device batch: pinned staging, device buffers, results
+    struct Lane {
+        int32_t *h_buf = nullptr;
+        size_t h_cap = 0;
+        char *d_buf = nullptr;
+        size_t d_cap = 0;
+        double *h_cost = nullptr;
+        int32_t *h_status = nullptr;
+        size_t hc_cap = 0;
+        int n = 0;
+        cudaEvent_t done = nullptr, e0 = nullptr, e1 = nullptr;
+    };
     std::vector<Seed> seeds;
-    // device batch buffers
-    int32_t *d_buf = nullptr;
-    size_t d_cap = 0;
-    int32_t *h_buf = nullptr;
-    size_t h_cap = 0;
+    Lane lanes[2];
     double device_ms = 0, expand_ms = 0;
     int64_t scored = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool started = false;
 };
 
-static int search_score(fo_search *S, int n, std::vector<double> &cost, std::vector<int32_t> &status) {
+static int lane_reserve(fo_search *S, fo_search::Lane &L, int n) {
+    const size_t W = 2 * (size_t)S->g->V + S->g->A;
+    if ((size_t)n * W > L.h_cap) {
+        if (L.h_buf) cudaFreeHost(L.h_buf);
+        L.h_buf = nullptr;
+        size_t cap = std::max((size_t)n * W, L.h_cap * 2);
+        if (cudaMallocHost(&L.h_buf, cap * 4) != cudaSuccess) return fail(FO_CUDA_ERROR, "pinned alloc");
+        L.h_cap = cap;
+    }
+    if ((size_t)n > L.hc_cap) {
+        if (L.h_cost) cudaFreeHost(L.h_cost);
+        if (L.h_status) cudaFreeHost(L.h_status);
+        size_t cap = std::max((size_t)n, L.hc_cap * 2);
+        if (cudaMallocHost(&L.h_cost, cap * 8) != cudaSuccess || cudaMallocHost(&L.h_status, cap * 4) != cudaSuccess)
+            return fail(FO_CUDA_ERROR, "pinned alloc");
+        L.hc_cap = cap;
+    }
+    size_t need = ((W * n * 4 + 255) & ~size_t(255)) + 16 * (size_t)n + 256;
+    if (need > L.d_cap) {
+        if (L.d_buf) cudaFree(L.d_buf);
+        L.d_buf = nullptr;
+        if (cudaMalloc(&L.d_buf, need) != cudaSuccess) return fail(FO_CUDA_ERROR, "search batch alloc");
+        L.d_cap = need;
+    }
+    if (!L.done) {
+        cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming);
+        cudaEventCreate(&L.e0);
+        cudaEventCreate(&L.e1);
+    }
+    return FO_OK;
+}
+
+// write candidate j of an n-candidate batch (SoA [ng * n | rg * n | bk * n])
+static void lane_put(fo_search *S, fo_search::Lane &L, int n, int j, const State &s) {
+    const int V = S->g->V, A = S->g->A;
+    std::copy(s.ng.begin(), s.ng.end(), L.h_buf + (size_t)j * V);
+    std::copy(s.rg.begin(), s.rg.end(), L.h_buf + (size_t)V * n + (size_t)j * V);
+    std::copy(s.bk.begin(), s.bk.end(), L.h_buf + (size_t)2 * V * n + (size_t)j * A);
+}
+
+// H2D, score, D2H on the handle's stream; asynchronous until lane_wait
+static int lane_launch(fo_search *S, fo_search::Lane &L, int n) {
     fo_graph *g = S->g;
     const int V = g->V, A = g->A;
-    size_t W = 2 * (size_t)V + A;
-    size_t need_i = W * n;
-    size_t cost_off = (need_i * 4 + 255) & ~size_t(255);
-    size_t need = cost_off + 16 * (size_t)n + 256;
-    if (need > S->d_cap) {
-        if (S->d_buf) cudaFree(S->d_buf);
-        S->d_buf = nullptr;
-        if (cudaMalloc(&S->d_buf, need) != cudaSuccess) return fail(FO_CUDA_ERROR, "search batch alloc");
-        S->d_cap = need;
-    }
-    char *db = (char *)S->d_buf;
+    const size_t W = 2 * (size_t)V + A;
+    L.n = n;
+    if (n == 0) return FO_OK;
+    char *db = L.d_buf;
+    size_t cost_off = (W * n * 4 + 255) & ~size_t(255);
     int32_t *dn = (int32_t *)db, *dr = dn + (size_t)V * n, *dk = dr + (size_t)V * n;
     double *dc = (double *)(db + cost_off);
     int32_t *ds = (int32_t *)(dc + n);
     cudaStream_t st = g->stream;
-    if (cudaMemcpyAsync(db, S->h_buf, need_i * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    if (cudaMemcpyAsync(db, L.h_buf, W * n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
         return fail(FO_CUDA_ERROR, "search batch H2D");
-    cudaEventRecord(S->ev0, st);
+    cudaEventRecord(L.e0, st);
     int rc = score_device(g, dn, dr, dk, 0, n, S->eng->VB, S->cfg.precision, dc, ds, st);
     if (rc) return rc;
-    cudaEventRecord(S->ev1, st);
-    cost.resize(n);
-    status.resize(n);
-    cudaMemcpyAsync(cost.data(), dc, 8 * (size_t)n, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(status.data(), ds, 4 * (size_t)n, cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(FO_CUDA_ERROR, "search batch sync");
+    cudaEventRecord(L.e1, st);
+    cudaMemcpyAsync(L.h_cost, dc, 8 * (size_t)n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(L.h_status, ds, 4 * (size_t)n, cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(L.done, st);
+    return FO_OK;
+}
+
+static int lane_wait(fo_search *S, fo_search::Lane &L) {
+    if (L.n == 0) return FO_OK;
+    if (cudaEventSynchronize(L.done) != cudaSuccess) return fail(FO_CUDA_ERROR, "search batch sync");
     float ms = 0;
-    cudaEventElapsedTime(&ms, S->ev0, S->ev1);
+    cudaEventElapsedTime(&ms, L.e0, L.e1);
     S->device_ms += ms;
-    S->scored += n;
+    S->scored += L.n;
     return FO_OK;
 }
 
-static int32_t *stage(fo_search *S, size_t slots) {
-    size_t W = 2 * (size_t)S->g->V + S->g->A;
-    if (slots * W > S->h_cap) {
-        if (S->h_buf) cudaFreeHost(S->h_buf);
-        S->h_buf = nullptr;
-        size_t cap = std::max(slots * W, S->h_cap * 2);
-        if (cudaMallocHost(&S->h_buf, cap * 4) != cudaSuccess) return nullptr;
-        S->h_cap = cap;
+// eval_cost(g0) once per seed (search.py:101-102); the same state -> one score
+static int search_start(fo_search *S) {
+    if (S->started) return FO_OK;
+    auto &L = S->lanes[0];
+    int rc = lane_reserve(S, L, 1);
+    if (rc) return rc;
+    lane_put(S, L, 1, 0, S->seeds[0].pool[0]);
+    if ((rc = lane_launch(S, L, 1)) || (rc = lane_wait(S, L))) return rc;
+    for (auto &sd : S->seeds) {
+        sd.status = L.h_status[0];
+        if (L.h_status[0]) { sd.active = false; continue; }
+        sd.best = L.h_cost[0];
+        sd.evaluated = 1;
+        sd.cache[sd.cur.h] = L.h_cost[0];
+        sd.queue.push({L.h_cost[0], 0, sd.cur.h, 0});
     }
-    return S->h_buf;
-}
-
-// write candidate j of the batch (SoA layout [ng * n | rg * n | bk * n])
-static void put(fo_search *S, int n, int j, const State &s) {
-    const int V = S->g->V, A = S->g->A;
-    std::copy(s.ng.begin(), s.ng.end(), S->h_buf + (size_t)j * V);
-    std::copy(s.rg.begin(), s.rg.end(), S->h_buf + (size_t)V * n + (size_t)j * V);
-    std::copy(s.bk.begin(), s.bk.end(), S->h_buf + (size_t)2 * V * n + (size_t)j * A);
-}
-
-extern "C" {
-
-int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seeds, int32_t R, const int32_t *ngid0,
-                     const int32_t *rgid0, const int32_t *bkt0, fo_search **out) {
-    if (!g || !cfg || !seeds || R <= 0 || !out) return fail(FO_INVALID_ARG, "bad arguments");
-    if (cfg->alpha < 1 || cfg->beta < 1 || cfg->max_unchanged < 1 || !(cfg->methods_mask & 7))
-        return fail(FO_INVALID_ARG, "invalid search config (search.py:53-61)");
-    if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set");
-    fo_search *S = new fo_search();
-    S->g = g;
-    S->cfg = *cfg;
-    S->eng = new Engine(g);
-    State s0;
-    if (!S->eng->load_state(ngid0, rgid0, bkt0, s0)) { delete S->eng; delete S; return fail(FO_INVALID_ARG, "bad start state"); }
-    S->seeds.resize(R);
-    uint64_t h0 = S->eng->hash(s0);
-    for (int r = 0; r < R; r++) {
-        auto &sd = S->seeds[r];
-        sd.rng = PyRng(seeds[r]);
-        sd.pool.push_back(s0);
-        sd.seen.insert(h0);
-        sd.cur.h = h0;
-    }
-    cudaSetDevice(g->device);
-    cudaEventCreate(&S->ev0);
-    cudaEventCreate(&S->ev1);
-    *out = S;
+    S->started = true;
     return FO_OK;
 }
 
-int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
-    if (!S) return fail(FO_INVALID_ARG, "null search");
-    fo_graph *g = S->g;
-    std::lock_guard<std::mutex> lk(g->mu);
-    cudaSetDevice(g->device);
-    const int R = (int)S->seeds.size();
-    std::vector<double> cost;
-    std::vector<int32_t> status;
-    if (!S->started) {  // eval_cost(g0) once per seed (search.py:101-102); same state -> one score
-        if (!stage(S, 1)) return fail(FO_CUDA_ERROR, "pinned alloc");
-        put(S, 1, 0, S->seeds[0].pool[0]);
-        int rc = search_score(S, 1, cost, status);
-        if (rc) return rc;
-        for (auto &sd : S->seeds) {
-            sd.status = status[0];
-            if (status[0]) { sd.active = false; continue; }
-            sd.best = cost[0];
-            sd.evaluated = 1;
-            sd.cache[sd.cur.h] = cost[0];
-            sd.queue.push({cost[0], 0, sd.cur.h, 0});
-        }
-        S->started = true;
-    }
-    // expand: every active seed pops and generates its step's candidates
+// every active seed in [lo, hi) pops and generates its step's candidates
+static void search_expand(fo_search *S, int lo, int hi) {
     auto t0 = std::chrono::steady_clock::now();
     const Engine &eng = *S->eng;
     int nthreads = S->cfg.n_threads > 0 ? S->cfg.n_threads : omp_get_max_threads();
 #pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
-    for (int r = 0; r < R; r++) {
+    for (int r = lo; r < hi; r++) {
         auto &sd = S->seeds[r];
         sd.ncand = 0;
         if (!sd.active) continue;
@@ -778,11 +772,14 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
             sd.h[j] = applied ? eng.hash(sd.cand[j]) : sd.cur.h;
         }
     }
-    auto t1 = std::chrono::steady_clock::now();
-    S->expand_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
-    // batch every candidate whose cost is not cached (dedupe within a step)
+    S->expand_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// batch every uncached candidate of seeds [lo, hi) (dedupe within a step) and launch
+static int search_launch(fo_search *S, fo_search::Lane &L, int lo, int hi) {
     int n = 0;
-    for (auto &sd : S->seeds)
+    for (int r = lo; r < hi; r++) {
+        auto &sd = S->seeds[r];
         for (int j = 0; j < sd.ncand; j++) {
             sd.batch_pos[j] = -1;
             if (sd.cache.count(sd.h[j])) continue;
@@ -791,17 +788,22 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
                 if (sd.h[q] == sd.h[j] && sd.batch_pos[q] >= 0) { sd.batch_pos[j] = sd.batch_pos[q]; dup = true; }
             if (!dup) sd.batch_pos[j] = n++;
         }
-    if (n > 0) {
-        if (!stage(S, n)) return fail(FO_CUDA_ERROR, "pinned alloc");
-        for (auto &sd : S->seeds)
-            for (int j = 0; j < sd.ncand; j++)
-                if (sd.batch_pos[j] >= 0) put(S, n, (int)sd.batch_pos[j], sd.cand[j]);
-        int rc = search_score(S, n, cost, status);
-        if (rc) return rc;
     }
-    // replay the accept / prune bookkeeping in method order (search.py:120-146)
-    int active = 0;
-    for (int r = 0; r < R; r++) {
+    if (n > 0) {
+        int rc = lane_reserve(S, L, n);
+        if (rc) return rc;
+        for (int r = lo; r < hi; r++) {
+            auto &sd = S->seeds[r];
+            for (int j = 0; j < sd.ncand; j++)
+                if (sd.batch_pos[j] >= 0) lane_put(S, L, n, (int)sd.batch_pos[j], sd.cand[j]);
+        }
+    }
+    return lane_launch(S, L, n);
+}
+
+// replay the accept / prune bookkeeping in method order (search.py:120-146)
+static void search_replay(fo_search *S, fo_search::Lane &L, int lo, int hi) {
+    for (int r = lo; r < hi; r++) {
         auto &sd = S->seeds[r];
         bool requeued = false;
         for (int j = 0; j < sd.ncand; j++) {
@@ -810,8 +812,8 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
             if (it != sd.cache.end()) c = it->second;
             else {
                 int p = (int)sd.batch_pos[j];
-                if (status[p]) { sd.status = status[p]; sd.active = false; break; }
-                c = cost[p];
+                if (L.h_status[p]) { sd.status = L.h_status[p]; sd.active = false; break; }
+                c = L.h_cost[p];
                 sd.cache[sd.h[j]] = c;
                 sd.evaluated++;
             }
@@ -839,10 +841,124 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
             }
             sd.trace.push_back({(int32_t)sd.steps, sd.meth[j], c, sd.best, (int32_t)sd.queue.size(), entered});
         }
-        if (sd.active) active++;
-        if (best_cost_out) best_cost_out[r] = sd.best;
+        sd.ncand = 0;
     }
-    *active_out = active;
+}
+
+static int count_active(fo_search *S, double *best_cost_out) {
+    int active = 0;
+    for (size_t r = 0; r < S->seeds.size(); r++) {
+        if (S->seeds[r].active) active++;
+        if (best_cost_out) best_cost_out[r] = S->seeds[r].best;
+    }
+    return active;
+}
+
+extern "C" {
+
+int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seeds, int32_t R, const int32_t *ngid0,
+                     const int32_t *rgid0, const int32_t *bkt0, fo_search **out) {
+    if (!g || !cfg || !seeds || R <= 0 || !out) return fail(FO_INVALID_ARG, "bad arguments");
+    if (cfg->alpha < 1 || cfg->beta < 1 || cfg->max_unchanged < 1 || !(cfg->methods_mask & 7))
+        return fail(FO_INVALID_ARG, "invalid search config (search.py:53-61)");
+    if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set");
+    fo_search *S = new fo_search();
+    S->g = g;
+    S->cfg = *cfg;
+    S->eng = new Engine(g);
+    State s0;
+    if (!S->eng->load_state(ngid0, rgid0, bkt0, s0)) { delete S->eng; delete S; return fail(FO_INVALID_ARG, "bad start state"); }
+    S->seeds.resize(R);
+    uint64_t h0 = S->eng->hash(s0);
+    for (int r = 0; r < R; r++) {
+        auto &sd = S->seeds[r];
+        sd.rng = PyRng(seeds[r]);
+        sd.pool.push_back(s0);
+        sd.seen.insert(h0);
+        sd.cur.h = h0;
+    }
+    cudaSetDevice(g->device);
+    *out = S;
+    return FO_OK;
+}
+
+// One round: every active search does one step of Alg. 1; all of their
+// candidates are scored in ONE device batch.
+int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
+    if (!S) return fail(FO_INVALID_ARG, "null search");
+    fo_graph *g = S->g;
+    std::lock_guard<std::mutex> lk(g->mu);
+    cudaSetDevice(g->device);
+    int rc = search_start(S);
+    if (rc) return rc;
+    const int R = (int)S->seeds.size();
+    search_expand(S, 0, R);
+    if ((rc = search_launch(S, S->lanes[0], 0, R)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
+    search_replay(S, S->lanes[0], 0, R);
+    *active_out = count_active(S, best_cost_out);
+    return FO_OK;
+}
+
+// Run every search to completion (or max_rounds steps per seed) in native
+// code.  With R >= 2 the seeds are split in two halves whose device batches
+// alternate with the other half's host-side expand, so host and device
+// overlap; each seed's own step sequence is unchanged.
+int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
+    if (!S) return fail(FO_INVALID_ARG, "null search");
+    fo_graph *g = S->g;
+    std::lock_guard<std::mutex> lk(g->mu);
+    cudaSetDevice(g->device);
+    int rc = search_start(S);
+    if (rc) return rc;
+    const int R = (int)S->seeds.size();
+    auto any_active = [&](int lo, int hi) {
+        for (int r = lo; r < hi; r++)
+            if (S->seeds[r].active) return true;
+        return false;
+    };
+    if (R == 1) {
+        for (int64_t it = 0; (max_rounds <= 0 || it < max_rounds) && any_active(0, 1); it++) {
+            search_expand(S, 0, 1);
+            if ((rc = search_launch(S, S->lanes[0], 0, 1)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
+            search_replay(S, S->lanes[0], 0, 1);
+        }
+    } else {
+        const int mid = R / 2;
+        auto &LA = S->lanes[0], &LB = S->lanes[1];
+        bool b_inflight = false;
+        search_expand(S, 0, mid);
+        if ((rc = search_launch(S, LA, 0, mid))) return rc;
+        for (int64_t it = 0; max_rounds <= 0 || it < max_rounds; it++) {
+            if (b_inflight) {
+                if ((rc = lane_wait(S, LB))) return rc;
+                search_replay(S, LB, mid, R);
+            }
+            bool b_live = any_active(mid, R);
+            if (b_live) {
+                search_expand(S, mid, R);  // overlaps A's device batch
+                if ((rc = search_launch(S, LB, mid, R))) return rc;
+            }
+            b_inflight = b_live;
+            if ((rc = lane_wait(S, LA))) return rc;
+            search_replay(S, LA, 0, mid);
+            bool a_live = any_active(0, mid);
+            if (!a_live && !b_inflight) break;
+            if (a_live && (max_rounds <= 0 || it + 1 < max_rounds)) {
+                search_expand(S, 0, mid);  // overlaps B's device batch
+                if ((rc = search_launch(S, LA, 0, mid))) return rc;
+            } else {
+                LA.n = 0;
+                if (!b_inflight) break;
+            }
+        }
+        if (b_inflight) {
+            if ((rc = lane_wait(S, LB))) return rc;
+            search_replay(S, LB, mid, R);
+        }
+        if ((rc = lane_wait(S, LA))) return rc;
+        if (LA.n) search_replay(S, LA, 0, mid);
+    }
+    if (active_out) *active_out = count_active(S, nullptr);
     return FO_OK;
 }
 
@@ -876,10 +992,15 @@ int fo_search_timing(fo_search *S, double *device_ms, double *expand_ms, int64_t
 
 int fo_search_destroy(fo_search *S) {
     if (!S) return FO_OK;
-    if (S->d_buf) cudaFree(S->d_buf);
-    if (S->h_buf) cudaFreeHost(S->h_buf);
-    if (S->ev0) cudaEventDestroy(S->ev0);
-    if (S->ev1) cudaEventDestroy(S->ev1);
+    for (auto &L : S->lanes) {
+        if (L.d_buf) cudaFree(L.d_buf);
+        if (L.h_buf) cudaFreeHost(L.h_buf);
+        if (L.h_cost) cudaFreeHost(L.h_cost);
+        if (L.h_status) cudaFreeHost(L.h_status);
+        if (L.done) cudaEventDestroy(L.done);
+        if (L.e0) cudaEventDestroy(L.e0);
+        if (L.e1) cudaEventDestroy(L.e1);
+    }
     delete S->eng;
     delete S;
     return FO_OK;

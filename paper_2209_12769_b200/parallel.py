@@ -79,6 +79,15 @@ class ShardedSearch:
         return int(a.item())
 
     def run(self, device, max_rounds: Optional[int] = None):
+        dist = _dist()
+        if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+            # single rank: no per-round exchange, the whole search runs natively
+            if self.s is None:
+                return (float("inf"), -1.0)
+            res = self.s.run(max_rounds)
+            best = min(range(len(res)), key=lambda r: (res[r].best_cost_us, r))
+            self.best_history.append((res[best].best_cost_us, float(self.seed_offset + best)))
+            return self.best_history[-1]
         rounds = 0
         while self.round(device) > 0:
             rounds += 1

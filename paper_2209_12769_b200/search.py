@@ -114,6 +114,13 @@ class LockstepSearch:
         return self.active
 
     def run(self, max_rounds: Optional[int] = None, started: Optional[float] = None):
+        if self.cfg.time_budget_s is None:  # whole search in native code (fo_search_run)
+            a = C.c_int32()
+            st = N.lib().fo_search_run(self.h, int(max_rounds or 0), C.byref(a))
+            _raise(st, "fo_search_run", N.last_error())
+            self.active = a.value
+            self.rounds += 1
+            return [self.result(r) for r in range(self.R)]
         t0 = time.monotonic() if started is None else started
         while self.active > 0:
             if max_rounds is not None and self.rounds >= max_rounds:
