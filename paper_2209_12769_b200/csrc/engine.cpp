@@ -916,11 +916,23 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
             if (S->seeds[r].active) return true;
         return false;
     };
-    if (R == 1) {
-        for (int64_t it = 0; (max_rounds <= 0 || it < max_rounds) && any_active(0, 1); it++) {
-            search_expand(S, 0, 1);
-            if ((rc = search_launch(S, S->lanes[0], 0, 1)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
-            search_replay(S, S->lanes[0], 0, 1);
+    // Probe rounds decide the schedule: splitting the seeds in two halves only
+    // pays when the host expand outweighs a device batch (a batch of search
+    // candidates is latency-bound, so halving it does not halve its time).
+    int64_t it = 0;
+    const int probe = R == 1 ? INT32_MAX : 8;
+    const double d0 = S->device_ms, e0 = S->expand_ms;
+    for (; (max_rounds <= 0 || it < max_rounds) && it < probe && any_active(0, R); it++) {
+        search_expand(S, 0, R);
+        if ((rc = search_launch(S, S->lanes[0], 0, R)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
+        search_replay(S, S->lanes[0], 0, R);
+    }
+    const bool pipeline = R > 1 && (S->expand_ms - e0) > 2.0 * (S->device_ms - d0);
+    if (!pipeline) {
+        for (; (max_rounds <= 0 || it < max_rounds) && any_active(0, R); it++) {
+            search_expand(S, 0, R);
+            if ((rc = search_launch(S, S->lanes[0], 0, R)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
+            search_replay(S, S->lanes[0], 0, R);
         }
     } else {
         const int mid = R / 2;
@@ -928,7 +940,7 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
         bool b_inflight = false;
         search_expand(S, 0, mid);
         if ((rc = search_launch(S, LA, 0, mid))) return rc;
-        for (int64_t it = 0; max_rounds <= 0 || it < max_rounds; it++) {
+        for (; max_rounds <= 0 || it < max_rounds; it++) {
             if (b_inflight) {
                 if ((rc = lane_wait(S, LB))) return rc;
                 search_replay(S, LB, mid, R);
