@@ -1319,6 +1319,8 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
         geo.sm_bytes = 0;
         per_sm = precision == FO_PREC_FP64 ? blocks_per_sm<double>(0) : blocks_per_sm<float>(0);
     }
+    static const char *bps = getenv("FO_BLOCKS_PER_SM");  // tuning override
+    if (bps && atoi(bps) > 0) per_sm = std::min(per_sm, atoi(bps));
     int want = (K + kWarps - 1) / kWarps;
     int maxb = num_sms * std::max(per_sm, 1);
     geo.grid = std::max(1, std::min(want, maxb));
