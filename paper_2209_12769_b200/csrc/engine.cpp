@@ -193,7 +193,7 @@ struct Engine {
         return B;
     }
 
-    void build(const State &s, Index &ix, Scratch &sc) const {
+    void build(const State &s, Index &ix, Scratch &sc, bool buckets = true) const {
         ix.G = number_groups(s, sc.gnode, &ix.gid);
         const int G = ix.G;
         const int32_t *gn = sc.gnode.data();
@@ -247,6 +247,7 @@ struct Engine {
         }
         csr_unique(G, sc.ps, sc.pt, ix.sptr, ix.succ, sc.cur);
         csr_unique(G, sc.pt, sc.ps, ix.pptr, ix.pred, sc.cur);
+        if (!buckets) return;  // op-fusion moves never read the bucket structures
         // buckets: export groups of their members, and the inverse
         ix.B = number_buckets(s, sc.bnode, &ix.bid);
         ix.bki.resize(A);
@@ -416,11 +417,14 @@ struct Engine {
 
     // random_apply (rewrite.py:222-263); state updated in place
     bool random_apply(State &s, int method, int n, PyRng &rng, Scratch &sc) const {
-        bool applied = false;
+        bool applied = false, stale = true;
         for (int it = 0; it < n; it++) {
-            build(s, sc.ix, sc);
-            if (method == M_AR) bucket_pairs(sc.ix, sc, sc.pairs);
-            else fusible_pairs(sc.ix, method == M_DUP, sc.pairs);
+            if (stale) {  // a rejected draw leaves the state, its index and its choice list unchanged
+                build(s, sc.ix, sc, method == M_AR);
+                if (method == M_AR) bucket_pairs(sc.ix, sc, sc.pairs);
+                else fusible_pairs(sc.ix, method == M_DUP, sc.pairs);
+                stale = false;
+            }
             if (sc.pairs.empty()) break;
             auto pr = sc.pairs[rng.below((uint32_t)sc.pairs.size())];
             bool ok = method == M_AR ? fuse_ar(s, sc.ix, pr.first, pr.second, sc.cand, sc)
@@ -428,6 +432,7 @@ struct Engine {
             if (ok) {
                 std::swap(s, sc.cand);
                 applied = true;
+                stale = true;
             }
         }
         return applied;
