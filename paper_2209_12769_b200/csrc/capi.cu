@@ -31,8 +31,8 @@ int fail(int status, const std::string &msg) {
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big) {
-    *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, big ? g->V : kMpCapDefault);
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int nws) {
+    *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, big ? g->V : kMpCapDefault, nws);
     size_t need = (size_t)L->total * (size_t)slots;
     char *&buf = big ? g->d_ws_big : g->d_ws;
     size_t &have = big ? g->ws_big_bytes : g->ws_bytes;
@@ -50,14 +50,16 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
                   double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
     ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
-    WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, kMpCapDefault);
-    // bound the per-warp workspace to a fixed HBM budget (large graphs get
+    const int nws = score_team_warps(geo);
+    WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, kMpCapDefault, nws);
+    // bound the per-slot workspace to a fixed HBM budget (large graphs get
     // fewer resident candidates rather than tens of GB of scratch)
     const size_t budget = (size_t)16 << 30;
-    int max_blocks = (int)std::max<size_t>(1, budget / ((size_t)L.total * score_warps_per_block()));
+    const int per_block = score_slots(geo) / geo.grid;
+    int max_blocks = (int)std::max<size_t>(1, budget / ((size_t)L.total * per_block));
     geo.grid = std::min(geo.grid, max_blocks);
-    int slots = geo.grid * score_warps_per_block();
-    int st = ensure_workspace(g, VB, slots, &L);
+    int slots = score_slots(geo);
+    int st = ensure_workspace(g, VB, slots, &L, false, nws);
     if (st) return st;
     cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws, L, geo, cost, status, ext_dur, tl,
                                  dur_out, bad_out, ngroups_out, stream);
@@ -69,10 +71,11 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
         WsLayout Lb;
         ScoreGeo gb = geo;
         gb.sm_bytes = 0;
+        gb.team = 0;
         gb.grid = std::min(std::max(1, (K + score_warps_per_block() - 1) / score_warps_per_block()), g->num_sms);
         Lb = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, g->V);
         gb.grid = std::min<int>(gb.grid, (int)std::max<size_t>(1, budget / ((size_t)Lb.total * score_warps_per_block())));
-        st = ensure_workspace(g, VB, gb.grid * score_warps_per_block(), &Lb, true);
+        st = ensure_workspace(g, VB, gb.grid * score_warps_per_block(), &Lb, true, 1);
         if (st) return st;
         e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws_big, Lb, gb, cost, status, ext_dur, tl,
                          dur_out, bad_out, ngroups_out, stream, 1);

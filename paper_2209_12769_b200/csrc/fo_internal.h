@@ -76,11 +76,14 @@ __host__ __device__ inline MpLayout mp_layout(int layers) {
 
 // Per-warp workspace (one candidate at a time), byte offsets.
 struct WsLayout {
-    int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, dur, fused, gptr, gmem, msort, lidx, nbptr, nb, H, P, gint, gin, gout, vis, zl, csim, rank, tlid;
+    int64_t gmap, bmap, g2id, b2id, nn, rr, bki, gmin, gcnt, bmin, btot, indeg, scnt, sptr, succ, prank, dur, fused,
+        gptr, gmem, gint, gin, gout, vis, zl, csim, rank, tlid;
+    // per-warp fused-group scratch: copy w at gs0 + w * gs_stride, fields relative to the copy
+    int64_t gs0, gs_stride, g_msort, g_lidx, g_zl, g_nbptr, g_nb, g_mark, g_H, g_P;
     int64_t total;
     int32_t mpcap;
 };
-WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap);
+WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap, int nws = 1);
 constexpr int kMpCapDefault = 2048;  // fused-group size the per-warp MP scratch holds
 
 struct TimelineOut {
@@ -95,6 +98,7 @@ struct TimelineOut {
 // Launch geometry: persistent grid and the per-warp shared-memory arena.
 struct ScoreGeo {
     int grid, blocks_per_sm, sm_nodes, sm_pairs, sm_bytes;
+    int team;  // 1: one 128-thread block per candidate (latency mode)
 };
 ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision);
 // Kernel launch (score.cu).  ext_dur / tl / dur_out / bad_out are optional and
@@ -105,6 +109,8 @@ cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, co
                          double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream,
                          int retry_only = 0);
 int score_warps_per_block();
+int score_slots(const ScoreGeo &geo);       // workspace slots a launch uses
+int score_team_warps(const ScoreGeo &geo);  // warps per candidate
 cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, int64_t id_offset, double *out,
                               cudaStream_t stream, int pairs = 0);
 
@@ -146,7 +152,7 @@ namespace fo {
 void set_error(const std::string &msg);
 int fail(int status, const std::string &msg);
 // Ensure the handle's workspace can hold `slots` warps for gid bound VB.
-int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big = false);
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big = false, int nws = 1);
 // Score K device-resident candidates (used by fo_score and the search engine).
 int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                  int precision, double *cost, int32_t *status, cudaStream_t stream);

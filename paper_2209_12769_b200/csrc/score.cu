@@ -33,7 +33,7 @@ constexpr int kRetryLarge = 100;   // internal status: fused group larger than t
 
 static inline int64_t align8(int64_t x) { return (x + 7) & ~int64_t(7); }
 
-WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap) {
+WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap, int nws) {
     WsLayout L{};
     L.mpcap = mpcap;
     int64_t GM = (int64_t)(VB < 2 * V ? VB : 2 * V) + 1;
@@ -61,12 +61,6 @@ WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap) {
     L.fused = take(4 * GM);
     L.gptr = take(4 * (GM + 1));
     L.gmem = take(4 * (2 * (int64_t)V + 1));
-    L.msort = take(4 * (cap + 1));
-    L.lidx = take(4 * (int64_t)V);
-    L.nbptr = take(4 * (cap + 1));
-    L.nb = take(4 * (2 * (int64_t)E + 1));
-    L.H = take(8 * cap * kHidden);
-    L.P = take(8 * cap * kHidden);
     L.gint = take(8 * GM);
     L.gin = take(8 * GM);
     L.gout = take(8 * GM);
@@ -75,6 +69,19 @@ WsLayout ws_layout(int V, int E, int A, int VB, int pairs_max, int mpcap) {
     L.rank = take(4 * (2 * (int64_t)V + A + 64));
     L.tlid = take(4 * NM);
     L.csim = take(4 * (NM + 2) * 2 + 8 * (int64_t)(pairs_max + 2) + std::max<int64_t>(24 * (GM + A + 4), 16 * 2 * 256) + 64);
+    // per-warp fused-group scratch, one copy per warp of the team
+    int64_t q = 0;
+    auto sub = [&](int64_t bytes) { int64_t r = q; q = align8(q + bytes); return r; };
+    L.g_msort = sub(4 * (cap + 1));
+    L.g_lidx = sub(4 * (int64_t)V);
+    L.g_zl = sub(4 * (cap + 1));
+    L.g_nbptr = sub(4 * (cap + 1));
+    L.g_nb = sub(4 * (2 * (int64_t)E + 1));
+    L.g_mark = sub(4 * (int64_t)V);
+    L.g_H = sub(8 * cap * kHidden);
+    L.g_P = sub(8 * cap * kHidden);
+    L.gs_stride = align8(q) + 128;
+    L.gs0 = take(L.gs_stride * (nws > 0 ? nws : 1));
     L.total = align8(o) + 128;
     return L;
 }
@@ -128,6 +135,130 @@ __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
     return v;
+}
+
+// ---------------------------------------------------------------------------
+// team primitives: a candidate is scored by a team of TEAM threads -- one warp
+// (throughput mode: thousands of candidates in flight) or one 128-thread block
+// (latency mode: search-round batches).  TEAM == 32 compiles to warp intrinsics.
+
+struct TeamShm {
+    int wsum[32];
+    long long wll[32];
+};
+
+template <int TEAM>
+__device__ __forceinline__ void tsync() {
+    if constexpr (TEAM == 32) __syncwarp();
+    else __syncthreads();
+}
+template <int TEAM>
+__device__ __forceinline__ bool tany(bool p) {
+    if constexpr (TEAM == 32) return __any_sync(FULL, p);
+    else return __syncthreads_or(p) != 0;
+}
+// exclusive prefix count of a flag over one chunk of TEAM items; total out
+template <int TEAM>
+__device__ __forceinline__ int tprefix(bool f, int &total, TeamShm *ts, int tid) {
+    unsigned m = __ballot_sync(FULL, f);
+    int pre = __popc(m & lanemask_lt());
+    if constexpr (TEAM == 32) {
+        total = __popc(m);
+        return pre;
+    } else {
+        const int wid = tid >> 5;
+        if ((tid & 31) == 0) ts->wsum[wid] = __popc(m);
+        __syncthreads();
+        int off = 0, tot = 0;
+#pragma unroll
+        for (int i = 0; i < TEAM / 32; i++) {
+            int c = ts->wsum[i];
+            off += i < wid ? c : 0;
+            tot += c;
+        }
+        __syncthreads();
+        total = tot;
+        return off + pre;
+    }
+}
+// exclusive prefix sum of x over one chunk of TEAM items; total out
+template <int TEAM>
+__device__ __forceinline__ int tscan(int x, int &total, TeamShm *ts, int tid) {
+    const int lane = tid & 31;
+    int v = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int y = __shfl_up_sync(FULL, v, d);
+        if (lane >= d) v += y;
+    }
+    int wtot = __shfl_sync(FULL, v, 31);
+    if constexpr (TEAM == 32) {
+        total = wtot;
+        return v - x;
+    } else {
+        const int wid = tid >> 5;
+        if (lane == 0) ts->wsum[wid] = wtot;
+        __syncthreads();
+        int off = 0, tot = 0;
+#pragma unroll
+        for (int i = 0; i < TEAM / 32; i++) {
+            int c = ts->wsum[i];
+            off += i < wid ? c : 0;
+            tot += c;
+        }
+        __syncthreads();
+        total = tot;
+        return off + v - x;
+    }
+}
+template <int TEAM>
+__device__ __forceinline__ long long tmin(long long v, TeamShm *ts, int tid) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v = min(v, __shfl_xor_sync(FULL, v, d));
+    if constexpr (TEAM == 32) {
+        return v;
+    } else {
+        if ((tid & 31) == 0) ts->wll[tid >> 5] = v;
+        __syncthreads();
+        long long r = ts->wll[0];
+#pragma unroll
+        for (int i = 1; i < TEAM / 32; i++) r = min(r, ts->wll[i]);
+        __syncthreads();
+        return r;
+    }
+}
+// flags (0/1) in arr[0..n) -> ranks; inv[rank] = i when inv != nullptr
+template <int TEAM>
+__device__ int team_rank_flags(int *arr, int *inv, int n, TeamShm *ts, int tid) {
+    int carry = 0;
+    for (int base = 0; base < n; base += TEAM) {
+        int i = base + tid;
+        int f = (i < n) ? arr[i] : 0;
+        int tot;
+        int r = carry + tprefix<TEAM>(f != 0, tot, ts, tid);
+        if (f) {
+            arr[i] = r;
+            if (inv) inv[r] = i;
+        }
+        carry += tot;
+    }
+    tsync<TEAM>();
+    return carry;
+}
+// exclusive scan of in[0..n) into out[0..n] (out[n] = total)
+template <int TEAM, typename O>
+__device__ int team_exscan(const int *in, O *out, int n, TeamShm *ts, int tid) {
+    int carry = 0;
+    for (int base = 0; base < n; base += TEAM) {
+        int i = base + tid;
+        int x = (i < n) ? in[i] : 0, tot;
+        int e = tscan<TEAM>(x, tot, ts, tid);
+        if (i < n) out[i] = (O)(carry + e);
+        carry += tot;
+    }
+    if (tid == 0) out[n] = (O)carry;
+    tsync<TEAM>();
+    return carry;
 }
 
 // CPython 3.12 sum() over floats is Neumaier-compensated (bltinmodule.c
@@ -209,10 +340,10 @@ __device__ __forceinline__ void memo_put(MemoEnt *t, unsigned mask, unsigned lon
 // (discard.global.L2): the per-warp scratch of ~4,000 resident candidates
 // exceeds the 126 MB L2, and write-backs of dead setup arrays were most of
 // the kernel's DRAM traffic.  Only whole 128-byte lines inside the range.
-__device__ __forceinline__ void l2_discard(const void *p, int64_t bytes, int lane) {
+__device__ __forceinline__ void l2_discard(const void *p, int64_t bytes, int tid, int nthreads) {
     uintptr_t lo = ((uintptr_t)p + 127) & ~uintptr_t(127);
     uintptr_t hi = ((uintptr_t)p + (uintptr_t)bytes) & ~uintptr_t(127);
-    for (uintptr_t a = lo + (uintptr_t)lane * 128; a < hi; a += 32 * 128) {
+    for (uintptr_t a = lo + (uintptr_t)tid * 128; a < hi; a += (uintptr_t)nthreads * 128) {
         size_t ga = __cvta_generic_to_global((const void *)a);
         asm volatile("discard.global.L2 [%0], 128;" ::"l"(ga) : "memory");
     }
@@ -333,12 +464,6 @@ struct Ws {
     __device__ __forceinline__ int *fused() const { return (int *)(b + L->fused); }
     __device__ __forceinline__ int *gptr() const { return (int *)(b + L->gptr); }
     __device__ __forceinline__ int *gmem() const { return (int *)(b + L->gmem); }
-    __device__ __forceinline__ int *msort() const { return (int *)(b + L->msort); }
-    __device__ __forceinline__ int *lidx() const { return (int *)(b + L->lidx); }
-    __device__ __forceinline__ int *nbptr() const { return (int *)(b + L->nbptr); }
-    __device__ __forceinline__ int *nb() const { return (int *)(b + L->nb); }
-    __device__ __forceinline__ char *H() const { return (char *)(b + L->H); }
-    __device__ __forceinline__ char *P() const { return (char *)(b + L->P); }
     __device__ __forceinline__ long long *gint() const { return (long long *)(b + L->gint); }
     __device__ __forceinline__ long long *gin() const { return (long long *)(b + L->gin); }
     __device__ __forceinline__ long long *gout() const { return (long long *)(b + L->gout); }
@@ -350,6 +475,18 @@ struct Ws {
 };
 
 __device__ __forceinline__ Ws ws_at(char *base, const WsLayout &L) { return Ws{base, &L}; }
+
+// one warp's fused-group scratch (team mode keeps one copy per warp)
+struct GroupScratch {
+    int *msort, *lidx, *zl, *nbptr, *nb, *mark;
+    char *H, *P;
+};
+__device__ __forceinline__ GroupScratch group_scratch(const Ws &w, int wid) {
+    const WsLayout &L = *w.L;
+    char *b = w.b + L.gs0 + (int64_t)wid * L.gs_stride;
+    return GroupScratch{(int *)(b + L.g_msort), (int *)(b + L.g_lidx), (int *)(b + L.g_zl), (int *)(b + L.g_nbptr),
+                        (int *)(b + L.g_nb), (int *)(b + L.g_mark), b + L.g_H, b + L.g_P};
+}
 
 struct ScoreArgs {
     DGraph g;
@@ -575,8 +712,8 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
     return true;
 }
 
-template <typename IT, typename SE>
-__device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lane, int G, int N) {
+template <typename IT, typename SE, int TEAM>
+__device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int tid, int G, int N, TeamShm *ts) {
     // compact copies of the contracted DAG for the serial loop: narrow indices,
     // successor entries carrying the successor's tie-break rank
     IT *sptr = (IT *)w.csim();
@@ -585,39 +722,40 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lan
     const int P = w.sptr()[N];
     ReadyEnt *bufg = (ReadyEnt *)(((uintptr_t)(succ + P + 1) + 15) & ~uintptr_t(15));
     ReadyEnt *bufb = bufg + G + 1;
-    for (int i = lane; i <= N; i += 32) sptr[i] = (IT)w.sptr()[i];
-    for (int i = lane; i < N; i += 32) indeg[i] = (IT)w.indeg()[i];
-    for (int q = lane; q < P; q += 32) {
+    for (int i = tid; i <= N; i += TEAM) sptr[i] = (IT)w.sptr()[i];
+    for (int i = tid; i < N; i += TEAM) indeg[i] = (IT)w.indeg()[i];
+    for (int q = tid; q < P; q += TEAM) {
         int s = w.succ()[q];
         succ[q] = se_make<SE>((unsigned)w.prank()[s], (unsigned)s);
     }
     // setup-only arrays are dead from here on: drop them from L2
     {
         const int V = a.g.V, A = a.g.A;
-        __syncwarp();
-        l2_discard(w.gmap(), 4ll * a.VB, lane);
-        l2_discard(w.nn(), 4ll * V, lane);
-        l2_discard(w.rr(), 4ll * V, lane);
-        l2_discard(w.gmin(), 4ll * G, lane);
-        l2_discard(w.gcnt(), 4ll * G, lane);
-        l2_discard(w.scnt(), 4ll * (N + 1), lane);
-        l2_discard(w.succ(), 4ll * P, lane);
-        l2_discard(w.bki(), 4ll * A, lane);
+        tsync<TEAM>();
+        l2_discard(w.gmap(), 4ll * a.VB, tid, TEAM);
+        l2_discard(w.nn(), 4ll * V, tid, TEAM);
+        l2_discard(w.rr(), 4ll * V, tid, TEAM);
+        l2_discard(w.gmin(), 4ll * G, tid, TEAM);
+        l2_discard(w.gcnt(), 4ll * G, tid, TEAM);
+        l2_discard(w.scnt(), 4ll * (N + 1), tid, TEAM);
+        l2_discard(w.succ(), 4ll * P, tid, TEAM);
+        l2_discard(w.bki(), 4ll * A, tid, TEAM);
     }
     // initial ready set: nodes with no deps at rt = 0.0 (level 0), keys sorted
     int hg = 0, hb = 0;
-    for (int base = 0; base < N; base += 32) {
-        int i = base + lane;
+    for (int base = 0; base < N; base += TEAM) {
+        int i = base + tid;
         bool z = i < N && w.indeg()[i] == 0;
-        bool zg = z && i < G;
-        unsigned mg = __ballot_sync(FULL, zg), mb = __ballot_sync(FULL, z && !zg);
-        if (zg) w.zl()[hg + __popc(mg & lanemask_lt())] = i;
-        if (z && !zg) w.zl()[N + hb + __popc(mb & lanemask_lt())] = i;
-        hg += __popc(mg);
-        hb += __popc(mb);
+        bool zg = z && i < G, zb = z && !zg;
+        int tg, tb;
+        int pg = tprefix<TEAM>(zg, tg, ts, tid), pb = tprefix<TEAM>(zb, tb, ts, tid);
+        if (zg) w.zl()[hg + pg] = i;
+        if (zb) w.zl()[N + hb + pb] = i;
+        hg += tg;
+        hb += tb;
     }
-    __syncwarp();
-    if (lane == 0) {
+    tsync<TEAM>();
+    if (tid == 0) {
         bool done = false;
         if (sizeof(IT) == 2 && !a.tl.c_id && hg <= kRing && hb <= kRing) {
             Ent16 *rg = (Ent16 *)bufg, *rb = rg + kRing;
@@ -653,7 +791,7 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int lan
             else event_loop<false, IT, SE>(a, k, w.dur(), sptr, indeg, succ, bufg, bufb, w, G, N, hg, hb);
         }
     }
-    __syncwarp();
+    tsync<TEAM>();
 }
 
 // Shared-memory simulation.  Nodes are renumbered into tie-break order --
@@ -725,7 +863,8 @@ __device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const doubl
     if (a.bad_out) *a.bad_out = -1;
 }
 
-__device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int lane, int G, int N, char *sm) {
+template <int TEAM>
+__device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int tid, int G, int N, char *sm, TeamShm *ts) {
     const int V = a.g.V, A = a.g.A, B = N - G;
     const int P = w.sptr()[N];
     const int cn = a.sm_nodes, cp = a.sm_pairs;
@@ -737,15 +876,15 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int lane, 
     uint32_t *ready = (uint32_t *)(((uintptr_t)(succ + cp) + 3) & ~uintptr_t(3));
     // sim order: rank of prank among groups / of min AR among buckets
     int *rk = w.rank();  // [0, 2V) group pranks, [2V, 2V + A) bucket pranks
-    for (int i = lane; i < 2 * V + A; i += 32) rk[i] = 0;
-    __syncwarp();
-    for (int i = lane; i < N; i += 32) rk[i < G ? w.prank()[i] : 2 * V + w.prank()[i]] = 1;
-    __syncwarp();
-    warp_rank_flags(rk, w.zl(), 2 * V, lane);
-    warp_rank_flags(rk + 2 * V, w.zl(), A, lane);
+    for (int i = tid; i < 2 * V + A; i += TEAM) rk[i] = 0;
+    tsync<TEAM>();
+    for (int i = tid; i < N; i += TEAM) rk[i < G ? w.prank()[i] : 2 * V + w.prank()[i]] = 1;
+    tsync<TEAM>();
+    team_rank_flags<TEAM>(rk, nullptr, 2 * V, ts, tid);
+    team_rank_flags<TEAM>(rk + 2 * V, nullptr, A, ts, tid);
     int *sim = w.zl();       // [0, N): setup node -> sim node
     int *cnt = w.zl() + N;   // [N, 2N): successor counts in sim order
-    for (int i = lane; i < N; i += 32) {
+    for (int i = tid; i < N; i += TEAM) {
         int j = i < G ? rk[w.prank()[i]] : G + rk[2 * V + w.prank()[i]];
         sim[i] = j;
         cnt[j] = w.sptr()[i + 1] - w.sptr()[i];
@@ -753,53 +892,227 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int lane, 
         indeg[j] = (uint16_t)w.indeg()[i];
         if (a.tl.c_id) w.tlid()[j] = i < G ? w.g2id()[i] : w.b2id()[i - G];
     }
-    __syncwarp();
-    {  // exclusive scan of counts -> sptr (u16)
-        int carry = 0;
-        for (int base = 0; base < N; base += 32) {
-            int i = base + lane;
-            int x = i < N ? cnt[i] : 0, v = x;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                int y = __shfl_up_sync(FULL, v, d);
-                if (lane >= d) v += y;
-            }
-            if (i < N) sptr[i] = (uint16_t)(carry + v - x);
-            carry += __shfl_sync(FULL, v, 31);
-        }
-        if (lane == 0) sptr[N] = (uint16_t)carry;
-    }
-    __syncwarp();
-    for (int i = lane; i < N; i += 32) {
+    tsync<TEAM>();
+    team_exscan<TEAM>(cnt, sptr, N, ts, tid);  // successor counts -> sptr (u16)
+    for (int i = tid; i < N; i += TEAM) {
         int o = sptr[sim[i]];
         for (int q = w.sptr()[i]; q < w.sptr()[i + 1]; q++) succ[o++] = (uint16_t)sim[w.succ()[q]];
     }
     // initial ready runs: indegree-0 nodes at level 0, already in key order
     uint32_t *rg = ready, *rb = ready + G;
     int hg = 0, hb = 0;
-    __syncwarp();
-    for (int base = 0; base < N; base += 32) {
-        int j = base + lane;
+    tsync<TEAM>();
+    for (int base = 0; base < N; base += TEAM) {
+        int j = base + tid;
         bool z = j < N && indeg[j] == 0;
         bool zg = z && j < G, zb = z && j >= G;
-        unsigned mg = __ballot_sync(FULL, zg), mb = __ballot_sync(FULL, zb);
-        if (zg) rg[hg + __popc(mg & lanemask_lt())] = (uint32_t)j;
-        if (zb) rb[hb + __popc(mb & lanemask_lt())] = (uint32_t)(j - G);
-        hg += __popc(mg);
-        hb += __popc(mb);
+        int tg, tb;
+        int pg = tprefix<TEAM>(zg, tg, ts, tid), pb = tprefix<TEAM>(zb, tb, ts, tid);
+        if (zg) rg[hg + pg] = (uint32_t)j;
+        if (zb) rb[hb + pb] = (uint32_t)(j - G);
+        hg += tg;
+        hb += tb;
     }
-    __syncwarp();
-    if (lane == 0) {
+    tsync<TEAM>();
+    if (tid == 0) {
         if (a.tl.c_id) smem_loop<true>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
         else smem_loop<false>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
     }
-    __syncwarp();
+    tsync<TEAM>();
     (void)B;
     return true;
 }
 
+// One fused group (K2), warp-level: lane = hidden channel for message passing.
 template <typename T>
-__device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char *sm) {
+__device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratch &gs, int f, int lane, bool hw,
+                              long long &badk) {
+    const DGraph &g = a.g;
+    const int V = g.V;
+    const int gi = w.fused()[f];
+    const int b0 = w.gptr()[f], n = w.gptr()[f + 1] - b0;
+    int *mem = w.gmem() + b0;
+    unsigned long long mh1 = 0, mh2 = 0;
+    MemoEnt *memo = (!hw && g.variant == FO_EST_MESSAGE_PASSING) ? g.memo[sizeof(T) == 8] : nullptr;
+    if (memo) {
+        set_hash(mem, n, lane, mh1, mh2);
+        double mv = 0.0;
+        bool hit = false;
+        if (lane == 0) hit = memo_get(memo, g.memo_mask, mh1, mh2, &mv);
+        hit = __shfl_sync(FULL, hit, 0);
+        if (hit) {
+            if (lane == 0) w.dur()[gi] = mv;
+            return;
+        }
+    }
+    if (n > a.L.mpcap && !hw && (g.variant == FO_EST_MESSAGE_PASSING || g.variant == FO_EST_LINEAR)) {
+        badk = min(badk, pack_bad(gi, kRetryLarge));
+        return;
+    }
+    // sort members ascending (estimator.py:160, node order = ascending op id)
+    if (n <= 32) {
+        int x = lane < n ? mem[lane] : INT_MAX;
+        for (int kk = 2; kk <= 32; kk <<= 1)
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                int y = __shfl_xor_sync(FULL, x, j);
+                bool up = ((lane & kk) == 0);
+                bool lower = (lane & j) == 0;
+                int lo = min(x, y), hi = max(x, y);
+                x = (lower == up) ? lo : hi;
+            }
+        if (lane < n) mem[lane] = x;
+    } else {  // large groups: mark members, then a ballot scan over ops yields them in order
+        int *mark = gs.mark;
+        for (int v = lane; v < V; v += 32) mark[v] = 0;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) mark[mem[i]] = 1;
+        __syncwarp();
+        int o = 0;
+        for (int base = 0; base < V; base += 32) {
+            int v = base + lane;
+            bool m = v < V && mark[v];
+            unsigned bm = __ballot_sync(FULL, m);
+            if (m) mem[o + __popc(bm & lanemask_lt())] = v;
+            o += __popc(bm);
+        }
+    }
+    __syncwarp();
+    double d = 0.0;
+    if (hw) {  // oracle_time (workloads.py:281-291): sum in ascending member order
+        if (lane == 0) {
+            bool all_param = true;
+            PySum comp;
+            for (int i = 0; i < n; i++) {
+                int v = mem[i];
+                if (g.op_kind[v] != 1) all_param = false;
+                double c = g.op_compute[v];
+                comp.add(isnan(c) ? 0.0 : c);
+            }
+            d = all_param ? 0.0
+                          : __dadd_rn(__dadd_rn(comp.get(), g.launch),
+                                      __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
+        }
+        d = __shfl_sync(FULL, d, 0);
+        if (lane == 0) w.dur()[gi] = d;
+        return;
+    }
+    // featurize -> lookup for every member (estimator.py:170)
+    bool miss = false;
+    for (int i = lane; i < n; i += 32) miss |= isnan(g.op_prof[mem[i]]);
+    if (__any_sync(FULL, miss)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); return; }
+    if (g.variant == FO_EST_ANALYTIC) {  // estimator.py:434-446
+        if (lane == 0) {
+            PySum sum;
+            for (int i = 0; i < n; i++) {
+                int v = mem[i];
+                double raw = __dsub_rn(__dsub_rn(g.op_prof[v], g.launch),
+                                       __dmul_rn(g.mem, (double)(g.op_in[v] + g.op_out[v])));
+                sum.add(raw);
+            }
+            double pred = __dadd_rn(__dadd_rn(sum.get(), g.launch), __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
+            w.dur()[gi] = pred > 1e-9 ? pred : 1e-9;
+        }
+        return;
+    }
+    // member-local undirected neighbour lists (estimator.py:173-177, :348-355)
+    for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = i;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+        int v = mem[i];
+        gs.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
+    }
+    __syncwarp();
+    warp_exscan(gs.zl, gs.nbptr, n, lane);
+    int dirE = 0;  // directed internal edges (linear variant's longest path)
+    for (int i = lane; i < n; i += 32) {
+        int v = mem[i];
+        int o = gs.nbptr[i], c = 0;
+        for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
+            int s = g.e_src[g.in_e[q]];
+            if (!in_grp(w, s, gi)) continue;
+            dirE++;
+            int j = gs.lidx[s];
+            bool dup = false;
+            for (int t = 0; t < c; t++) dup |= (gs.nb[o + t] == j);
+            if (!dup) gs.nb[o + c++] = j;
+        }
+        for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
+            int d2 = g.e_dst[g.out_e[q]];
+            if (!in_grp(w, d2, gi)) continue;
+            int j = gs.lidx[d2];
+            bool dup = false;
+            for (int t = 0; t < c; t++) dup |= (gs.nb[o + t] == j);
+            if (!dup) gs.nb[o + c++] = j;
+        }
+        gs.zl[i] = c;
+    }
+    __syncwarp();
+    // compact rows in place: nbptr -> [start, start + count)
+    // (store counts as end pointers in msort to keep nbptr monotone)
+    for (int i = lane; i < n; i += 32) gs.msort[i] = gs.zl[i];
+    __syncwarp();
+    if (g.variant == FO_EST_MESSAGE_PASSING) {
+        // compact neighbour rows into a dense CSR (msort holds the counts)
+        if (lane == 0) {
+            int o = 0;
+            for (int i = 0; i < n; i++) {
+                int s0 = gs.nbptr[i], c = gs.msort[i];
+                for (int t = 0; t < c; t++) gs.nb[o + t] = gs.nb[s0 + t];
+                gs.nbptr[i] = o;
+                o += c;
+            }
+            gs.nbptr[n] = o;
+        }
+        __syncwarp();
+        double pred = mp_forward<T>(g, mem, n, gs.nbptr, gs.nb, (T *)gs.H, (T *)gs.P, lane);
+        if (lane == 0) {
+            w.dur()[gi] = pred;
+            if (memo) memo_put(memo, g.memo_mask, mh1, mh2, pred);
+        }
+    } else {  // LINEAR (estimator.py:117-128, 341-345, 421-426)
+        dirE = __reduce_add_sync(FULL, dirE);
+        if (lane == 0) {
+            // longest path in nodes over the directed internal edges (estimator.py:131-154)
+            int *depth = gs.msort;  // reuse: counts no longer needed
+            for (int i = 0; i < n; i++) depth[i] = 1;
+            for (int it = 0; it < n; it++) {
+                bool ch = false;
+                for (int i = 0; i < n; i++) {
+                    int v = mem[i];
+                    for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
+                        int s = g.e_src[g.in_e[q]];
+                        if (!in_grp(w, s, gi)) continue;
+                        int j = gs.lidx[s];
+                        if (depth[j] + 1 > depth[i]) { depth[i] = depth[j] + 1; ch = true; }
+                    }
+                }
+                if (!ch) break;
+            }
+            int lp = 0;
+            for (int i = 0; i < n; i++) lp = max(lp, depth[i]);
+            PySum tot;
+            for (int i = 0; i < n; i++) tot.add(g.op_prof[mem[i]]);
+            const double total = tot.get();
+            double agg[6] = {(double)n, total, (double)w.gint()[gi], (double)w.gin()[gi], (double)w.gout()[gi],
+                             (double)lp};
+            double fs[12];
+            for (int q = 0; q < 6; q++) { fs[q] = log1p(agg[q]); fs[6 + q] = agg[q]; }
+            if (g.lin_norm)
+                for (int q = 0; q < 12; q++) fs[q] = __ddiv_rn(__dsub_rn(fs[q], g.agg_mean[q]), g.agg_std[q]);
+            double z = 0.0;
+            for (int q = 0; q < 12; q++) z = __dadd_rn(z, __dmul_rn(g.lin_w[q], fs[q]));
+            z = __dadd_rn(z, g.lin_b);
+            double pred = __dmul_rn(softplus_d(z), g.out_scale);
+            w.dur()[gi] = pred > 1e-9 ? pred : 1e-9;
+        }
+    }
+    __syncwarp();
+}
+
+template <typename T, int TEAM>
+__device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char *sm, TeamShm *ts) {
+    constexpr int NW = TEAM / 32;
+    const int lane = tid & 31, wid = tid >> 5;
     const DGraph &g = a.g;
     const int V = g.V, E = g.E, A = g.A, VB = a.VB;
     // candidate encoding: int32 or int16 ids (the int16 form halves the bytes moved)
@@ -809,11 +1122,11 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     const int64_t ob = (int64_t)k * V, oa = (int64_t)k * A;
 
     // ---- K1: group / bucket numbering (ids -> node order, graph.py:269-273)
-    for (int i = lane; i < VB; i += 32) w.gmap()[i] = 0;
-    for (int i = lane; i < A; i += 32) w.bmap()[i] = 0;
-    __syncwarp();
+    for (int i = tid; i < VB; i += TEAM) w.gmap()[i] = 0;
+    for (int i = tid; i < A; i += TEAM) w.bmap()[i] = 0;
+    tsync<TEAM>();
     bool bad = false;
-    for (int v = lane; v < V; v += 32) {
+    for (int v = tid; v < V; v += TEAM) {
         int x = ldid(a.ngid, ob + v), y = ldid(a.rgid, ob + v);
         if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
         w.gmap()[x] = 1;
@@ -821,51 +1134,51 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
         w.nn()[v] = x;
         w.rr()[v] = y;
     }
-    for (int i = lane; i < A; i += 32) {
+    for (int i = tid; i < A; i += TEAM) {
         int x = ldid(a.bkt, oa + i);
         if (x < 0 || x >= A) { bad = true; continue; }
         w.bmap()[x] = 1;
         w.bki()[i] = x;
     }
-    if (__any_sync(FULL, bad)) {
-        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_INVALID_ARG; }
+    if (tany<TEAM>(bad)) {
+        if (tid == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_INVALID_ARG; }
         return;
     }
-    __syncwarp();
-    const int G = warp_rank_flags(w.gmap(), w.g2id(), VB, lane);
-    const int B = warp_rank_flags(w.bmap(), w.b2id(), A, lane);
+    tsync<TEAM>();
+    const int G = team_rank_flags<TEAM>(w.gmap(), a.tl.c_id ? w.g2id() : nullptr, VB, ts, tid);
+    const int B = team_rank_flags<TEAM>(w.bmap(), a.tl.c_id ? w.b2id() : nullptr, A, ts, tid);
     const int N = G + B;
-    for (int v = lane; v < V; v += 32) {
+    for (int v = tid; v < V; v += TEAM) {
         w.nn()[v] = w.gmap()[w.nn()[v]];
         int y = w.rr()[v];
         w.rr()[v] = y >= 0 ? w.gmap()[y] : -1;
     }
-    for (int i = lane; i < A; i += 32) w.bki()[i] = w.bmap()[w.bki()[i]];
-    for (int i = lane; i < G; i += 32) { w.gmin()[i] = INT_MAX; w.gcnt()[i] = 0; }
-    for (int i = lane; i < B; i += 32) { w.bmin()[i] = INT_MAX; w.btot()[i] = 0; }
-    for (int i = lane; i < N; i += 32) { w.indeg()[i] = 0; w.scnt()[i] = 0; }
-    __syncwarp();
+    for (int i = tid; i < A; i += TEAM) w.bki()[i] = w.bmap()[w.bki()[i]];
+    for (int i = tid; i < G; i += TEAM) { w.gmin()[i] = INT_MAX; w.gcnt()[i] = 0; }
+    for (int i = tid; i < B; i += TEAM) { w.bmin()[i] = INT_MAX; w.btot()[i] = 0; }
+    for (int i = tid; i < N; i += TEAM) { w.indeg()[i] = 0; w.scnt()[i] = 0; }
+    tsync<TEAM>();
 
     // per-group min member / size, per-bucket min AR / total bytes
-    for (int v = lane; v < V; v += 32) {
+    for (int v = tid; v < V; v += TEAM) {
         int x = w.nn()[v], y = w.rr()[v];
         atomicMin(&w.gmin()[x], v);
         atomicAdd(&w.gcnt()[x], 1);
         if (y >= 0) { atomicMin(&w.gmin()[y], v); atomicAdd(&w.gcnt()[y], 1); }
     }
-    for (int i = lane; i < A; i += 32) {
+    for (int i = tid; i < A; i += TEAM) {
         int b = w.bki()[i];
         atomicMin(&w.bmin()[b], i);
         atomicAdd((unsigned long long *)&w.btot()[b], (unsigned long long)g.ar_bytes[i]);
     }
-    __syncwarp();
+    tsync<TEAM>();
 
     // contracted schedule DAG with multiplicities (graph.py:237-274):
     //   non-aggregate edge s->d: every copy C of d not holding s waits for export(s)
     //   aggregate edge s->d:     every copy C of d waits for bucket(a), a in ARs(s)
     //   bucket b:                waits for export(producer(a)), a in b
     for (int pass = 0; pass < 2; pass++) {
-        for (int e = lane; e < E; e += 32) {
+        for (int e = tid; e < E; e += TEAM) {
             int s = g.e_src[e], d = g.e_dst[e];
             int c0 = w.nn()[d], c1 = w.rr()[d];
             if (!g.e_agg[e]) {
@@ -893,43 +1206,43 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                 }
             }
         }
-        for (int i = lane; i < A; i += 32) {
+        for (int i = tid; i < A; i += TEAM) {
             int bn = G + w.bki()[i];
             int ex = export_of(w, g.ar_prod[i]);
             if (pass == 0) { atomicAdd(&w.scnt()[ex], 1); atomicAdd(&w.indeg()[bn], 1); }
             else w.succ()[atomicAdd(&w.scnt()[ex], 1)] = bn;
         }
-        __syncwarp();
+        tsync<TEAM>();
         if (pass == 0) {
-            warp_exscan(w.scnt(), w.sptr(), N, lane);
-            for (int i = lane; i < N; i += 32) w.scnt()[i] = w.sptr()[i];  // fill cursors
-            __syncwarp();
+            team_exscan<TEAM>(w.scnt(), w.sptr(), N, ts, tid);
+            for (int i = tid; i < N; i += TEAM) w.scnt()[i] = w.sptr()[i];  // fill cursors
+            tsync<TEAM>();
         }
     }
 
     // tie-break ranks (simulator.py:63-64): group key (min member, id), bucket key min AR.
     // prank = 2*min_member + (1 if the other group sharing that min member has a smaller id)
-    for (int gi = lane; gi < G; gi += 32) {
+    for (int gi = tid; gi < G; gi += TEAM) {
         int t = w.gmin()[gi];
         int other = (w.nn()[t] == gi) ? w.rr()[t] : w.nn()[t];
         int sub = (other >= 0 && w.gmin()[other] == t && other < gi) ? 1 : 0;
         int pr = 2 * t + sub;
         w.prank()[gi] = pr;
     }
-    for (int b = lane; b < B; b += 32) {
+    for (int b = tid; b < B; b += TEAM) {
         int pr = w.bmin()[b];
         w.prank()[G + b] = pr;
     }
 
     // ---- K2: durations of every node (simulator.py:62)
     long long badk = LLONG_MAX;
-    for (int b = lane; b < B; b += 32) {  // comm.py:45-49
+    for (int b = tid; b < B; b += TEAM) {  // comm.py:45-49
         double d = __dadd_rn(__dmul_rn(g.C, (double)w.btot()[b]), g.D);
         w.dur()[G + b] = d;
         if (d < 0.0) badk = min(badk, pack_bad(G + b, FO_NEGATIVE_DURATION));
     }
     if (a.ext_dur) {
-        for (int i = lane; i < N; i += 32) {
+        for (int i = tid; i < N; i += TEAM) {
             double d = a.ext_dur[i];
             w.dur()[i] = d;
             if (d < 0.0) badk = min(badk, pack_bad(i, FO_NEGATIVE_DURATION));
@@ -938,10 +1251,10 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
         const bool hw = g.provider == FO_PROVIDER_HW_ORACLE;
         const bool need_io = hw || g.variant == FO_EST_ANALYTIC || g.variant == FO_EST_LINEAR;
         if (need_io) {  // group_io (graph.py:181-213)
-            for (int i = lane; i < G; i += 32) { w.gint()[i] = 0; w.gin()[i] = 0; w.gout()[i] = 0; }
-            for (int v = lane; v < V; v += 32) w.vis()[v] = 0;
-            __syncwarp();
-            for (int e = lane; e < E; e += 32) {
+            for (int i = tid; i < G; i += TEAM) { w.gint()[i] = 0; w.gin()[i] = 0; w.gout()[i] = 0; }
+            for (int v = tid; v < V; v += TEAM) w.vis()[v] = 0;
+            tsync<TEAM>();
+            for (int e = tid; e < E; e += TEAM) {
                 int s = g.e_src[e], d = g.e_dst[e];
                 unsigned long long by = (unsigned long long)g.e_bytes[e];
                 int cs[2] = {w.nn()[d], w.rr()[d]};
@@ -952,17 +1265,17 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                     else { atomicAdd((unsigned long long *)&w.gin()[C], by); w.vis()[s] = 1; }
                 }
             }
-            __syncwarp();
-            for (int v = lane; v < V; v += 32) {
+            tsync<TEAM>();
+            for (int v = tid; v < V; v += TEAM) {
                 if (w.vis()[v] || g.out_ptr[v + 1] == g.out_ptr[v] || g.arp_ptr[v + 1] > g.arp_ptr[v])
                     atomicAdd((unsigned long long *)&w.gout()[export_of(w, v)], (unsigned long long)g.op_out[v]);
             }
-            __syncwarp();
+            tsync<TEAM>();
         }
         // singletons (estimator.py:810-814 / workloads.py:276-291) and the fused-group list
         int nf = 0;
-        for (int base = 0; base < G; base += 32) {
-            int gi = base + lane;
+        for (int base = 0; base < G; base += TEAM) {
+            int gi = base + tid;
             bool fused = false;
             if (gi < G) {
                 int n = w.gcnt()[gi];
@@ -988,22 +1301,23 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                     else fused = true;
                 }
             }
-            unsigned m = __ballot_sync(FULL, fused);
-            if (fused) w.fused()[nf + __popc(m & lanemask_lt())] = gi;
-            nf += __popc(m);
+            int tot;
+            int pos = tprefix<TEAM>(fused, tot, ts, tid);
+            if (fused) w.fused()[nf + pos] = gi;
+            nf += tot;
         }
-        __syncwarp();
+        tsync<TEAM>();
         if (nf > 0) {
             // member lists of fused groups (order fixed below by sorting)
-            for (int f = lane; f < nf; f += 32) w.zl()[f] = w.gcnt()[w.fused()[f]];
-            __syncwarp();
-            warp_exscan(w.zl(), w.gptr(), nf, lane);
+            for (int f = tid; f < nf; f += TEAM) w.zl()[f] = w.gcnt()[w.fused()[f]];
+            tsync<TEAM>();
+            team_exscan<TEAM>(w.zl(), w.gptr(), nf, ts, tid);
             // group -> fused position via prank scratch-free map: reuse gcnt as position+1 marker
-            for (int f = lane; f < nf; f += 32) w.gcnt()[w.fused()[f]] = -(f + 1);
-            __syncwarp();
-            for (int f = lane; f < nf; f += 32) w.zl()[f] = w.gptr()[f];
-            __syncwarp();
-            for (int v = lane; v < V; v += 32) {
+            for (int f = tid; f < nf; f += TEAM) w.gcnt()[w.fused()[f]] = -(f + 1);
+            tsync<TEAM>();
+            for (int f = tid; f < nf; f += TEAM) w.zl()[f] = w.gptr()[f];
+            tsync<TEAM>();
+            for (int v = tid; v < V; v += TEAM) {
                 int x = w.nn()[v], y = w.rr()[v];
                 int fx = w.gcnt()[x];
                 if (fx < 0) w.gmem()[atomicAdd(&w.zl()[-fx - 1], 1)] = v;
@@ -1012,199 +1326,21 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
                     if (fy < 0) w.gmem()[atomicAdd(&w.zl()[-fy - 1], 1)] = v;
                 }
             }
-            __syncwarp();
-            for (int f = 0; f < nf; f++) {
-                const int gi = w.fused()[f];
-                const int b0 = w.gptr()[f], n = w.gptr()[f + 1] - b0;
-                int *mem = w.gmem() + b0;
-                unsigned long long mh1 = 0, mh2 = 0;
-                MemoEnt *memo = (!hw && g.variant == FO_EST_MESSAGE_PASSING) ? g.memo[sizeof(T) == 8] : nullptr;
-                if (memo) {
-                    set_hash(mem, n, lane, mh1, mh2);
-                    double mv = 0.0;
-                    bool hit = false;
-                    if (lane == 0) hit = memo_get(memo, g.memo_mask, mh1, mh2, &mv);
-                    hit = __shfl_sync(FULL, hit, 0);
-                    if (hit) {
-                        if (lane == 0) w.dur()[gi] = mv;
-                        continue;
-                    }
-                }
-                if (n > a.L.mpcap && !hw && (g.variant == FO_EST_MESSAGE_PASSING || g.variant == FO_EST_LINEAR)) {
-                    badk = min(badk, pack_bad(gi, kRetryLarge));
-                    continue;
-                }
-                // sort members ascending (estimator.py:160, node order = ascending op id)
-                if (n <= 32) {
-                    int x = lane < n ? mem[lane] : INT_MAX;
-                    for (int kk = 2; kk <= 32; kk <<= 1)
-                        for (int j = kk >> 1; j > 0; j >>= 1) {
-                            int y = __shfl_xor_sync(FULL, x, j);
-                            bool up = ((lane & kk) == 0);
-                            bool lower = (lane & j) == 0;
-                            int lo = min(x, y), hi = max(x, y);
-                            x = (lower == up) ? lo : hi;
-                        }
-                    if (lane < n) mem[lane] = x;
-                } else {  // large groups: mark members, then a ballot scan over ops yields them in order
-                    int *mark = w.vis();
-                    for (int v = lane; v < V; v += 32) mark[v] = 0;
-                    __syncwarp();
-                    for (int i = lane; i < n; i += 32) mark[mem[i]] = 1;
-                    __syncwarp();
-                    int o = 0;
-                    for (int base = 0; base < V; base += 32) {
-                        int v = base + lane;
-                        bool m = v < V && mark[v];
-                        unsigned bm = __ballot_sync(FULL, m);
-                        if (m) mem[o + __popc(bm & lanemask_lt())] = v;
-                        o += __popc(bm);
-                    }
-                }
-                __syncwarp();
-                double d = 0.0;
-                if (hw) {  // oracle_time (workloads.py:281-291): sum in ascending member order
-                    if (lane == 0) {
-                        bool all_param = true;
-                        PySum comp;
-                        for (int i = 0; i < n; i++) {
-                            int v = mem[i];
-                            if (g.op_kind[v] != 1) all_param = false;
-                            double c = g.op_compute[v];
-                            comp.add(isnan(c) ? 0.0 : c);
-                        }
-                        d = all_param ? 0.0
-                                      : __dadd_rn(__dadd_rn(comp.get(), g.launch),
-                                                  __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
-                    }
-                    d = __shfl_sync(FULL, d, 0);
-                    if (lane == 0) w.dur()[gi] = d;
-                    continue;
-                }
-                // featurize -> lookup for every member (estimator.py:170)
-                bool miss = false;
-                for (int i = lane; i < n; i += 32) miss |= isnan(g.op_prof[mem[i]]);
-                if (__any_sync(FULL, miss)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); continue; }
-                if (g.variant == FO_EST_ANALYTIC) {  // estimator.py:434-446
-                    if (lane == 0) {
-                        PySum sum;
-                        for (int i = 0; i < n; i++) {
-                            int v = mem[i];
-                            double raw = __dsub_rn(__dsub_rn(g.op_prof[v], g.launch),
-                                                   __dmul_rn(g.mem, (double)(g.op_in[v] + g.op_out[v])));
-                            sum.add(raw);
-                        }
-                        double pred = __dadd_rn(__dadd_rn(sum.get(), g.launch), __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
-                        w.dur()[gi] = pred > 1e-9 ? pred : 1e-9;
-                    }
-                    continue;
-                }
-                // member-local undirected neighbour lists (estimator.py:173-177, :348-355)
-                for (int i = lane; i < n; i += 32) w.lidx()[mem[i]] = i;
-                __syncwarp();
-                for (int i = lane; i < n; i += 32) {
-                    int v = mem[i];
-                    w.zl()[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
-                }
-                __syncwarp();
-                warp_exscan(w.zl(), w.nbptr(), n, lane);
-                int dirE = 0;  // directed internal edges (linear variant's longest path)
-                for (int i = lane; i < n; i += 32) {
-                    int v = mem[i];
-                    int o = w.nbptr()[i], c = 0;
-                    for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
-                        int s = g.e_src[g.in_e[q]];
-                        if (!in_grp(w, s, gi)) continue;
-                        dirE++;
-                        int j = w.lidx()[s];
-                        bool dup = false;
-                        for (int t = 0; t < c; t++) dup |= (w.nb()[o + t] == j);
-                        if (!dup) w.nb()[o + c++] = j;
-                    }
-                    for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
-                        int d2 = g.e_dst[g.out_e[q]];
-                        if (!in_grp(w, d2, gi)) continue;
-                        int j = w.lidx()[d2];
-                        bool dup = false;
-                        for (int t = 0; t < c; t++) dup |= (w.nb()[o + t] == j);
-                        if (!dup) w.nb()[o + c++] = j;
-                    }
-                    w.zl()[i] = c;
-                }
-                __syncwarp();
-                // compact rows in place: nbptr -> [start, start + count)
-                // (store counts as end pointers in msort to keep nbptr monotone)
-                for (int i = lane; i < n; i += 32) w.msort()[i] = w.zl()[i];
-                __syncwarp();
-                if (g.variant == FO_EST_MESSAGE_PASSING) {
-                    // compact neighbour rows into a dense CSR (msort holds the counts)
-                    if (lane == 0) {
-                        int o = 0;
-                        for (int i = 0; i < n; i++) {
-                            int s0 = w.nbptr()[i], c = w.msort()[i];
-                            for (int t = 0; t < c; t++) w.nb()[o + t] = w.nb()[s0 + t];
-                            w.nbptr()[i] = o;
-                            o += c;
-                        }
-                        w.nbptr()[n] = o;
-                    }
-                    __syncwarp();
-                    double pred = mp_forward<T>(g, mem, n, w.nbptr(), w.nb(), (T *)w.H(), (T *)w.P(), lane);
-                    if (lane == 0) {
-                        w.dur()[gi] = pred;
-                        if (memo) memo_put(memo, g.memo_mask, mh1, mh2, pred);
-                    }
-                } else {  // LINEAR (estimator.py:117-128, 341-345, 421-426)
-                    dirE = __reduce_add_sync(FULL, dirE);
-                    if (lane == 0) {
-                        // longest path in nodes over the directed internal edges (estimator.py:131-154)
-                        int *depth = w.msort();  // reuse: counts no longer needed
-                        for (int i = 0; i < n; i++) depth[i] = 1;
-                        for (int it = 0; it < n; it++) {
-                            bool ch = false;
-                            for (int i = 0; i < n; i++) {
-                                int v = mem[i];
-                                for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
-                                    int s = g.e_src[g.in_e[q]];
-                                    if (!in_grp(w, s, gi)) continue;
-                                    int j = w.lidx()[s];
-                                    if (depth[j] + 1 > depth[i]) { depth[i] = depth[j] + 1; ch = true; }
-                                }
-                            }
-                            if (!ch) break;
-                        }
-                        int lp = 0;
-                        for (int i = 0; i < n; i++) lp = max(lp, depth[i]);
-                        PySum tot;
-                        for (int i = 0; i < n; i++) tot.add(g.op_prof[mem[i]]);
-                        const double total = tot.get();
-                        double agg[6] = {(double)n, total, (double)w.gint()[gi], (double)w.gin()[gi], (double)w.gout()[gi],
-                                         (double)lp};
-                        double fs[12];
-                        for (int q = 0; q < 6; q++) { fs[q] = log1p(agg[q]); fs[6 + q] = agg[q]; }
-                        if (g.lin_norm)
-                            for (int q = 0; q < 12; q++) fs[q] = __ddiv_rn(__dsub_rn(fs[q], g.agg_mean[q]), g.agg_std[q]);
-                        double z = 0.0;
-                        for (int q = 0; q < 12; q++) z = __dadd_rn(z, __dmul_rn(g.lin_w[q], fs[q]));
-                        z = __dadd_rn(z, g.lin_b);
-                        double pred = __dmul_rn(softplus_d(z), g.out_scale);
-                        w.dur()[gi] = pred > 1e-9 ? pred : 1e-9;
-                    }
-                }
-                __syncwarp();
-            }
+            tsync<TEAM>();
+            const GroupScratch gs = group_scratch(w, wid);
+            for (int f = wid; f < nf; f += NW) process_group<T>(a, w, gs, f, lane, hw, badk);
+            tsync<TEAM>();
         }
     }
     // first failing node in node order decides the error (simulator.py:62)
-#pragma unroll
-    for (int d = 16; d; d >>= 1) badk = min(badk, __shfl_xor_sync(FULL, badk, d));
-    __syncwarp();
+    badk = tmin<TEAM>(badk, ts, tid);
+    tsync<TEAM>();
     if (a.dur_out) {
-        for (int i = lane; i < N; i += 32) a.dur_out[i] = w.dur()[i];
-        if (lane == 0) *a.ngroups_out = G;
+        for (int i = tid; i < N; i += TEAM) a.dur_out[i] = w.dur()[i];
+        if (tid == 0) *a.ngroups_out = G;
     }
     if (badk != LLONG_MAX) {
-        if (lane == 0) {
+        if (tid == 0) {
             a.cost_out[k] = 0.0;
             a.status_out[k] = (int)(badk & 0xff);
             if (a.bad_out) *a.bad_out = (int)(badk >> 8);
@@ -1215,12 +1351,12 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int lane, char
     // ---- K3: two-lane discrete-event simulation (simulator.py:66-140)
     const bool small = N < 65536 && w.sptr()[N] < 65536 && 2 * V < 65536;
     if (!small && (N >= (1 << kKeyNodeBits) || 2 * V >= (1 << kKeyNodeBits))) {
-        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_UNSUPPORTED; }
+        if (tid == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_UNSUPPORTED; }
         return;
     }
-    if (simulate_smem(a, k, w, lane, G, N, sm)) return;
-    if (small) simulate_compact<uint16_t, uint32_t>(a, k, w, lane, G, N);
-    else simulate_compact<uint32_t, unsigned long long>(a, k, w, lane, G, N);
+    if (simulate_smem<TEAM>(a, k, w, tid, G, N, sm, ts)) return;
+    if (small) simulate_compact<uint16_t, uint32_t, TEAM>(a, k, w, tid, G, N, ts);
+    else simulate_compact<uint32_t, unsigned long long, TEAM>(a, k, w, tid, G, N, ts);
 }
 
 template <typename T>
@@ -1233,7 +1369,23 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel(const __grid_cons
     char *sm = a.sm_bytes > 0 ? smem_arena + (threadIdx.x >> 5) * a.sm_bytes : nullptr;
     for (int k = wid; k < a.K; k += nw) {
         if (a.retry_only && a.status_out[k] != kRetryLarge) continue;
-        score_one<T>(a, k, w, lane, sm);
+        score_one<T, 32>(a, k, w, lane, sm, nullptr);
+    }
+}
+
+// Latency mode: one 128-thread block scores one candidate (setup loops over
+// 128 threads, fused groups spread over the 4 warps, event loop on thread 0).
+constexpr int kTeam = 128;
+template <typename T>
+__global__ void __launch_bounds__(kTeam, 4) score_kernel_team(const __grid_constant__ ScoreArgs a) {
+    extern __shared__ __align__(16) char smem_arena[];
+    __shared__ TeamShm ts;
+    Ws w = ws_at(a.ws + (int64_t)blockIdx.x * a.L.total, a.L);
+    char *sm = a.sm_bytes > 0 ? smem_arena : nullptr;
+    for (int k = blockIdx.x; k < a.K; k += gridDim.x) {
+        if (a.retry_only && a.status_out[k] != kRetryLarge) continue;
+        score_one<T, kTeam>(a, k, w, threadIdx.x, sm, &ts);
+        __syncthreads();
     }
 }
 
@@ -1288,40 +1440,49 @@ cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, 
 int score_warps_per_block() { return kWarps; }
 
 template <typename T>
-static int blocks_per_sm(int smem_per_block) {
-    if (smem_per_block > 48 * 1024)
-        cudaFuncSetAttribute(score_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
+static int blocks_per_sm(int smem_per_block, bool team) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel<T>, kWarps * 32, smem_per_block);
+    if (team) {
+        if (smem_per_block > 48 * 1024)
+            cudaFuncSetAttribute(score_kernel_team<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel_team<T>, kTeam, smem_per_block);
+    } else {
+        if (smem_per_block > 48 * 1024)
+            cudaFuncSetAttribute(score_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel<T>, kWarps * 32, smem_per_block);
+    }
     return n;
 }
 
 ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
     ScoreGeo geo{};
     const int V = g.V, E = g.E, A = g.A;
+    // small batches (search rounds): one block per candidate
+    const char *tenv = getenv("FO_TEAM");  // tuning override, read per launch
+    geo.team = tenv ? (tenv[0] == '1') : (K <= 2 * num_sms);
+    const int per_block = geo.team ? 1 : kWarps;  // arenas per block
     // arena sized for typical candidates (groups ~ ops); larger ones use the global path
     int64_t n = std::min<int64_t>(2 * (int64_t)V + A + 1, (int64_t)V + V / 8 + A + 32);
     int64_t p = std::min<int64_t>(g.pairs_max, (int64_t)E + E / 4 + A + 32);
     int64_t bytes = (8 * n + 2 * (n + 2) + 2 * n + 2 * p + 4 + 4 * n + 15) & ~int64_t(15);
     geo.sm_nodes = (int)n;
     geo.sm_pairs = (int)p;
-    // The shared-memory arena takes the L1 capacity the global-workspace
-    // setup phase lives on (measured: 2.65 ms vs 1.81 ms per 4096-candidate
-    // ResNet-50 batch), so it is opt-in until setup moves on-chip as well.
-    // Small batches (search rounds: one block per SM at most) are latency-bound
-    // and have L1 to spare, so they always take the arena.
+    // The shared-memory arena takes the L1 capacity the global-workspace setup
+    // phase lives on (measured slower for full batches), so only small batches
+    // (latency-bound, one block per SM at most) take it.
     static const char *env = getenv("FO_SIM_SMEM");
     const bool arena_on = env ? env[0] == '1' : K <= num_sms * kWarps;
-    geo.sm_bytes = (arena_on && bytes * kWarps <= 200 * 1024 && n < 65536) ? (int)bytes : 0;
-    int per_sm = precision == FO_PREC_FP64 ? blocks_per_sm<double>(geo.sm_bytes * kWarps)
-                                           : blocks_per_sm<float>(geo.sm_bytes * kWarps);
+    geo.sm_bytes = (arena_on && bytes * per_block <= 200 * 1024 && n < 65536) ? (int)bytes : 0;
+    const bool fp64 = precision == FO_PREC_FP64;
+    int per_sm = fp64 ? blocks_per_sm<double>(geo.sm_bytes * per_block, geo.team)
+                      : blocks_per_sm<float>(geo.sm_bytes * per_block, geo.team);
     if (per_sm <= 0) {  // arena does not fit: global-memory simulation only
         geo.sm_bytes = 0;
-        per_sm = precision == FO_PREC_FP64 ? blocks_per_sm<double>(0) : blocks_per_sm<float>(0);
+        per_sm = fp64 ? blocks_per_sm<double>(0, geo.team) : blocks_per_sm<float>(0, geo.team);
     }
     static const char *bps = getenv("FO_BLOCKS_PER_SM");  // tuning override
     if (bps && atoi(bps) > 0) per_sm = std::min(per_sm, atoi(bps));
-    int want = (K + kWarps - 1) / kWarps;
+    int want = geo.team ? K : (K + kWarps - 1) / kWarps;
     int maxb = num_sms * std::max(per_sm, 1);
     geo.grid = std::max(1, std::min(want, maxb));
     geo.blocks_per_sm = per_sm;
@@ -1353,12 +1514,20 @@ cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, co
     a.dur_out = dur_out;
     a.bad_out = bad_out;
     a.ngroups_out = ngroups_out;
-    size_t smem = (size_t)geo.sm_bytes * kWarps;
-    if (precision == FO_PREC_FP64)
-        score_kernel<double><<<geo.grid, kWarps * 32, smem, stream>>>(a);
-    else
-        score_kernel<float><<<geo.grid, kWarps * 32, smem, stream>>>(a);
+    const bool fp64 = precision == FO_PREC_FP64;
+    if (geo.team) {
+        size_t smem = (size_t)geo.sm_bytes;
+        if (fp64) score_kernel_team<double><<<geo.grid, kTeam, smem, stream>>>(a);
+        else score_kernel_team<float><<<geo.grid, kTeam, smem, stream>>>(a);
+    } else {
+        size_t smem = (size_t)geo.sm_bytes * kWarps;
+        if (fp64) score_kernel<double><<<geo.grid, kWarps * 32, smem, stream>>>(a);
+        else score_kernel<float><<<geo.grid, kWarps * 32, smem, stream>>>(a);
+    }
     return cudaGetLastError();
 }
+
+int score_slots(const ScoreGeo &geo) { return geo.team ? geo.grid : geo.grid * kWarps; }
+int score_team_warps(const ScoreGeo &geo) { return geo.team ? kTeam / 32 : 1; }
 
 }  // namespace fo

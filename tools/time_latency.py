@@ -1,24 +1,53 @@
-"""Latency of small batches (search-round sized), memo cleared per call."""
-import os, sys, json
+"""Latency of small batches (search-round sized), memo cleared per call.
+
+usage: time_latency.py [fp32|fp64] cfg:K [cfg:K ...]
+FO_TEAM=0/1 is toggled per measurement (warp-per-candidate vs block-per-candidate).
+"""
+import ctypes, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2209_12769_b200 as P
 from paper_2209_12769_b200 import _native as N
-cfg = sys.argv[1] if len(sys.argv) > 1 else "bert"
-K = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-prec = N.FO_PREC_FP32 if (len(sys.argv) > 3 and sys.argv[3] == "fp32") else N.FO_PREC_FP64
+
+args = sys.argv[1:]
+prec = N.FO_PREC_FP64
+if args and args[0] in ("fp32", "fp64"):
+    prec = N.FO_PREC_FP32 if args.pop(0) == "fp32" else N.FO_PREC_FP64
+specs = args or ["bert:1"]
 torch.cuda.set_device(0)
-g, prof, comm, mp, lin = P.load_workload(cfg)
-cp = P.make_cost_providers(prof, comm, mp, precision=prec)
-dg = cp.device_graph(g)
-ng, rg, bk, gb = dg.make_candidates(np.arange(K, dtype=np.uint64))
-d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
-cost = torch.empty(K, dtype=torch.float64, device="cuda"); st = torch.empty(K, dtype=torch.int32, device="cuda")
 s = torch.cuda.current_stream()
-ts = []
-for i in range(23):
-    N.lib().fo_memo_clear(dg.h, __import__("ctypes").c_void_p(s.cuda_stream))
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); dg.score_device(d[0], d[1], d[2], gb, cost, st, prec); b.record(); torch.cuda.synchronize()
-    if i >= 3: ts.append(a.elapsed_time(b))
-print(json.dumps({"lib": os.environ.get("FO_LIB_PATH", "default"), "config": cfg, "K": K, "ms_median": float(np.median(ts))}))
+cache = {}
+for spec in specs:
+    cfg, K = spec.split(":")
+    K = int(K)
+    if cfg not in cache:
+        g, prof, comm, mp, lin = P.load_workload(cfg)
+        cp = P.make_cost_providers(prof, comm, mp, precision=prec)
+        cache[cfg] = cp.device_graph(g)
+    dg = cache[cfg]
+    ng, rg, bk, gb = dg.make_candidates(np.arange(K, dtype=np.uint64))
+    d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
+    cost = torch.empty(K, dtype=torch.float64, device="cuda")
+    st = torch.empty(K, dtype=torch.int32, device="cuda")
+    out = {"config": cfg, "K": K}
+    ref = None
+    for team in ("0", "1"):
+        os.environ["FO_TEAM"] = team
+        ts = []
+        for i in range(23):
+            N.lib().fo_memo_clear(dg.h, ctypes.c_void_p(s.cuda_stream))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
+            b.record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(a.elapsed_time(b))
+        c = cost.cpu().numpy().copy()
+        if ref is None:
+            ref = c
+        else:
+            out["same_costs"] = bool(np.array_equal(ref, c))
+        out[f"ms_team{team}"] = round(float(np.median(ts)), 4)
+    os.environ.pop("FO_TEAM", None)
+    print(json.dumps(out), flush=True)
