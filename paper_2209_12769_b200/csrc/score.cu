@@ -25,6 +25,9 @@
 
 #include "fo_internal.h"
 
+#include <map>
+#include <mutex>
+
 namespace fo {
 
 #define FULL 0xffffffffu
@@ -291,6 +294,7 @@ __device__ __forceinline__ unsigned long long smix(unsigned long long x) {
 __device__ __forceinline__ void set_hash(const int *mem, int n, int lane, unsigned long long &h1,
                                          unsigned long long &h2) {
     unsigned long long a = 0, b = 0;
+    #pragma unroll 4
     for (int i = lane; i < n; i += 32) {
         a += smix((unsigned long long)mem[i] * 2 + 1);
         b += smix(((unsigned long long)mem[i] << 32) ^ 0x5bd1e995ull);
@@ -722,8 +726,11 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int tid
     const int P = w.sptr()[N];
     ReadyEnt *bufg = (ReadyEnt *)(((uintptr_t)(succ + P + 1) + 15) & ~uintptr_t(15));
     ReadyEnt *bufb = bufg + G + 1;
+    #pragma unroll 4
     for (int i = tid; i <= N; i += TEAM) sptr[i] = (IT)w.sptr()[i];
+    #pragma unroll 4
     for (int i = tid; i < N; i += TEAM) indeg[i] = (IT)w.indeg()[i];
+    #pragma unroll 4
     for (int q = tid; q < P; q += TEAM) {
         int s = w.succ()[q];
         succ[q] = se_make<SE>((unsigned)w.prank()[s], (unsigned)s);
@@ -873,17 +880,20 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int tid, i
     uint16_t *sptr = (uint16_t *)(dur + cn);
     uint16_t *indeg = sptr + cn + 2;
     uint16_t *succ = indeg + cn;
-    uint32_t *ready = (uint32_t *)(((uintptr_t)(succ + cp) + 3) & ~uintptr_t(3));
+    uint32_t *ready = (uint32_t *)(succ + cp);  // cp is even: 4-byte aligned, stays a shared-space pointer
     // sim order: rank of prank among groups / of min AR among buckets
     int *rk = w.rank();  // [0, 2V) group pranks, [2V, 2V + A) bucket pranks
+    #pragma unroll 4
     for (int i = tid; i < 2 * V + A; i += TEAM) rk[i] = 0;
     tsync<TEAM>();
+    #pragma unroll 4
     for (int i = tid; i < N; i += TEAM) rk[i < G ? w.prank()[i] : 2 * V + w.prank()[i]] = 1;
     tsync<TEAM>();
     team_rank_flags<TEAM>(rk, nullptr, 2 * V, ts, tid);
     team_rank_flags<TEAM>(rk + 2 * V, nullptr, A, ts, tid);
     int *sim = w.zl();       // [0, N): setup node -> sim node
     int *cnt = w.zl() + N;   // [N, 2N): successor counts in sim order
+    #pragma unroll 4
     for (int i = tid; i < N; i += TEAM) {
         int j = i < G ? rk[w.prank()[i]] : G + rk[2 * V + w.prank()[i]];
         sim[i] = j;
@@ -894,6 +904,7 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int tid, i
     }
     tsync<TEAM>();
     team_exscan<TEAM>(cnt, sptr, N, ts, tid);  // successor counts -> sptr (u16)
+    #pragma unroll 4
     for (int i = tid; i < N; i += TEAM) {
         int o = sptr[sim[i]];
         for (int q = w.sptr()[i]; q < w.sptr()[i + 1]; q++) succ[o++] = (uint16_t)sim[w.succ()[q]];
@@ -963,8 +974,10 @@ __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratc
         if (lane < n) mem[lane] = x;
     } else {  // large groups: mark members, then a ballot scan over ops yields them in order
         int *mark = gs.mark;
+        #pragma unroll 4
         for (int v = lane; v < V; v += 32) mark[v] = 0;
         __syncwarp();
+        #pragma unroll 4
         for (int i = lane; i < n; i += 32) mark[mem[i]] = 1;
         __syncwarp();
         int o = 0;
@@ -998,6 +1011,7 @@ __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratc
     }
     // featurize -> lookup for every member (estimator.py:170)
     bool miss = false;
+    #pragma unroll 4
     for (int i = lane; i < n; i += 32) miss |= isnan(g.op_prof[mem[i]]);
     if (__any_sync(FULL, miss)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); return; }
     if (g.variant == FO_EST_ANALYTIC) {  // estimator.py:434-446
@@ -1015,8 +1029,10 @@ __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratc
         return;
     }
     // member-local undirected neighbour lists (estimator.py:173-177, :348-355)
+    #pragma unroll 4
     for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = i;
     __syncwarp();
+    #pragma unroll 4
     for (int i = lane; i < n; i += 32) {
         int v = mem[i];
         gs.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
@@ -1024,6 +1040,7 @@ __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratc
     __syncwarp();
     warp_exscan(gs.zl, gs.nbptr, n, lane);
     int dirE = 0;  // directed internal edges (linear variant's longest path)
+    #pragma unroll 4
     for (int i = lane; i < n; i += 32) {
         int v = mem[i];
         int o = gs.nbptr[i], c = 0;
@@ -1049,6 +1066,7 @@ __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratc
     __syncwarp();
     // compact rows in place: nbptr -> [start, start + count)
     // (store counts as end pointers in msort to keep nbptr monotone)
+    #pragma unroll 4
     for (int i = lane; i < n; i += 32) gs.msort[i] = gs.zl[i];
     __syncwarp();
     if (g.variant == FO_EST_MESSAGE_PASSING) {
@@ -1122,10 +1140,13 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
     const int64_t ob = (int64_t)k * V, oa = (int64_t)k * A;
 
     // ---- K1: group / bucket numbering (ids -> node order, graph.py:269-273)
+    #pragma unroll 4
     for (int i = tid; i < VB; i += TEAM) w.gmap()[i] = 0;
+    #pragma unroll 4
     for (int i = tid; i < A; i += TEAM) w.bmap()[i] = 0;
     tsync<TEAM>();
     bool bad = false;
+    #pragma unroll 4
     for (int v = tid; v < V; v += TEAM) {
         int x = ldid(a.ngid, ob + v), y = ldid(a.rgid, ob + v);
         if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
@@ -1134,6 +1155,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         w.nn()[v] = x;
         w.rr()[v] = y;
     }
+    #pragma unroll 4
     for (int i = tid; i < A; i += TEAM) {
         int x = ldid(a.bkt, oa + i);
         if (x < 0 || x >= A) { bad = true; continue; }
@@ -1148,24 +1170,31 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
     const int G = team_rank_flags<TEAM>(w.gmap(), a.tl.c_id ? w.g2id() : nullptr, VB, ts, tid);
     const int B = team_rank_flags<TEAM>(w.bmap(), a.tl.c_id ? w.b2id() : nullptr, A, ts, tid);
     const int N = G + B;
+    #pragma unroll 4
     for (int v = tid; v < V; v += TEAM) {
         w.nn()[v] = w.gmap()[w.nn()[v]];
         int y = w.rr()[v];
         w.rr()[v] = y >= 0 ? w.gmap()[y] : -1;
     }
+    #pragma unroll 4
     for (int i = tid; i < A; i += TEAM) w.bki()[i] = w.bmap()[w.bki()[i]];
+    #pragma unroll 4
     for (int i = tid; i < G; i += TEAM) { w.gmin()[i] = INT_MAX; w.gcnt()[i] = 0; }
+    #pragma unroll 4
     for (int i = tid; i < B; i += TEAM) { w.bmin()[i] = INT_MAX; w.btot()[i] = 0; }
+    #pragma unroll 4
     for (int i = tid; i < N; i += TEAM) { w.indeg()[i] = 0; w.scnt()[i] = 0; }
     tsync<TEAM>();
 
     // per-group min member / size, per-bucket min AR / total bytes
+    #pragma unroll 4
     for (int v = tid; v < V; v += TEAM) {
         int x = w.nn()[v], y = w.rr()[v];
         atomicMin(&w.gmin()[x], v);
         atomicAdd(&w.gcnt()[x], 1);
         if (y >= 0) { atomicMin(&w.gmin()[y], v); atomicAdd(&w.gcnt()[y], 1); }
     }
+    #pragma unroll 4
     for (int i = tid; i < A; i += TEAM) {
         int b = w.bki()[i];
         atomicMin(&w.bmin()[b], i);
@@ -1178,6 +1207,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
     //   aggregate edge s->d:     every copy C of d waits for bucket(a), a in ARs(s)
     //   bucket b:                waits for export(producer(a)), a in b
     for (int pass = 0; pass < 2; pass++) {
+        #pragma unroll 4
         for (int e = tid; e < E; e += TEAM) {
             int s = g.e_src[e], d = g.e_dst[e];
             int c0 = w.nn()[d], c1 = w.rr()[d];
@@ -1206,6 +1236,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
                 }
             }
         }
+        #pragma unroll 4
         for (int i = tid; i < A; i += TEAM) {
             int bn = G + w.bki()[i];
             int ex = export_of(w, g.ar_prod[i]);
@@ -1215,6 +1246,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         tsync<TEAM>();
         if (pass == 0) {
             team_exscan<TEAM>(w.scnt(), w.sptr(), N, ts, tid);
+            #pragma unroll 4
             for (int i = tid; i < N; i += TEAM) w.scnt()[i] = w.sptr()[i];  // fill cursors
             tsync<TEAM>();
         }
@@ -1222,6 +1254,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
 
     // tie-break ranks (simulator.py:63-64): group key (min member, id), bucket key min AR.
     // prank = 2*min_member + (1 if the other group sharing that min member has a smaller id)
+    #pragma unroll 4
     for (int gi = tid; gi < G; gi += TEAM) {
         int t = w.gmin()[gi];
         int other = (w.nn()[t] == gi) ? w.rr()[t] : w.nn()[t];
@@ -1229,6 +1262,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         int pr = 2 * t + sub;
         w.prank()[gi] = pr;
     }
+    #pragma unroll 4
     for (int b = tid; b < B; b += TEAM) {
         int pr = w.bmin()[b];
         w.prank()[G + b] = pr;
@@ -1236,12 +1270,14 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
 
     // ---- K2: durations of every node (simulator.py:62)
     long long badk = LLONG_MAX;
+    #pragma unroll 4
     for (int b = tid; b < B; b += TEAM) {  // comm.py:45-49
         double d = __dadd_rn(__dmul_rn(g.C, (double)w.btot()[b]), g.D);
         w.dur()[G + b] = d;
         if (d < 0.0) badk = min(badk, pack_bad(G + b, FO_NEGATIVE_DURATION));
     }
     if (a.ext_dur) {
+        #pragma unroll 4
         for (int i = tid; i < N; i += TEAM) {
             double d = a.ext_dur[i];
             w.dur()[i] = d;
@@ -1251,9 +1287,12 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         const bool hw = g.provider == FO_PROVIDER_HW_ORACLE;
         const bool need_io = hw || g.variant == FO_EST_ANALYTIC || g.variant == FO_EST_LINEAR;
         if (need_io) {  // group_io (graph.py:181-213)
+            #pragma unroll 4
             for (int i = tid; i < G; i += TEAM) { w.gint()[i] = 0; w.gin()[i] = 0; w.gout()[i] = 0; }
+            #pragma unroll 4
             for (int v = tid; v < V; v += TEAM) w.vis()[v] = 0;
             tsync<TEAM>();
+            #pragma unroll 4
             for (int e = tid; e < E; e += TEAM) {
                 int s = g.e_src[e], d = g.e_dst[e];
                 unsigned long long by = (unsigned long long)g.e_bytes[e];
@@ -1266,6 +1305,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
                 }
             }
             tsync<TEAM>();
+            #pragma unroll 4
             for (int v = tid; v < V; v += TEAM) {
                 if (w.vis()[v] || g.out_ptr[v + 1] == g.out_ptr[v] || g.arp_ptr[v + 1] > g.arp_ptr[v])
                     atomicAdd((unsigned long long *)&w.gout()[export_of(w, v)], (unsigned long long)g.op_out[v]);
@@ -1309,14 +1349,18 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         tsync<TEAM>();
         if (nf > 0) {
             // member lists of fused groups (order fixed below by sorting)
+            #pragma unroll 4
             for (int f = tid; f < nf; f += TEAM) w.zl()[f] = w.gcnt()[w.fused()[f]];
             tsync<TEAM>();
             team_exscan<TEAM>(w.zl(), w.gptr(), nf, ts, tid);
             // group -> fused position via prank scratch-free map: reuse gcnt as position+1 marker
+            #pragma unroll 4
             for (int f = tid; f < nf; f += TEAM) w.gcnt()[w.fused()[f]] = -(f + 1);
             tsync<TEAM>();
+            #pragma unroll 4
             for (int f = tid; f < nf; f += TEAM) w.zl()[f] = w.gptr()[f];
             tsync<TEAM>();
+            #pragma unroll 4
             for (int v = tid; v < V; v += TEAM) {
                 int x = w.nn()[v], y = w.rr()[v];
                 int fx = w.gcnt()[x];
@@ -1336,6 +1380,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
     badk = tmin<TEAM>(badk, ts, tid);
     tsync<TEAM>();
     if (a.dur_out) {
+        #pragma unroll 4
         for (int i = tid; i < N; i += TEAM) a.dur_out[i] = w.dur()[i];
         if (tid == 0) *a.ngroups_out = G;
     }
@@ -1440,7 +1485,7 @@ cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, 
 int score_warps_per_block() { return kWarps; }
 
 template <typename T>
-static int blocks_per_sm(int smem_per_block, bool team) {
+static int blocks_per_sm_query(int smem_per_block, bool team) {
     int n = 0;
     if (team) {
         if (smem_per_block > 48 * 1024)
@@ -1454,17 +1499,45 @@ static int blocks_per_sm(int smem_per_block, bool team) {
     return n;
 }
 
+// occupancy queries are cached: they sit on the per-launch host path
+template <typename T>
+static int blocks_per_sm(int smem_per_block, bool team) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;
+    const std::pair<int, int> key(smem_per_block, team ? 1 : 0);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    int n = blocks_per_sm_query<T>(smem_per_block, team);
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = n;
+    return n;
+}
+
 ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
     ScoreGeo geo{};
     const int V = g.V, E = g.E, A = g.A;
-    // small batches (search rounds): one block per candidate
-    const char *tenv = getenv("FO_TEAM");  // tuning override, read per launch
-    geo.team = tenv ? (tenv[0] == '1') : (K <= 2 * num_sms);
-    const int per_block = geo.team ? 1 : kWarps;  // arenas per block
     // arena sized for typical candidates (groups ~ ops); larger ones use the global path
     int64_t n = std::min<int64_t>(2 * (int64_t)V + A + 1, (int64_t)V + V / 8 + A + 32);
-    int64_t p = std::min<int64_t>(g.pairs_max, (int64_t)E + E / 4 + A + 32);
+    int64_t p = (std::min<int64_t>(g.pairs_max, (int64_t)E + E / 4 + A + 32) + 1) & ~int64_t(1);
     int64_t bytes = (8 * n + 2 * (n + 2) + 2 * n + 2 * p + 4 + 4 * n + 15) & ~int64_t(15);
+    const bool fp64 = precision == FO_PREC_FP64;
+    const bool arena_fits = bytes <= 200 * 1024 && n < 65536;
+    // Batches that fit in one wave of 128-thread blocks (search rounds) take
+    // one block per candidate: the setup phases then run 4x wider, halving
+    // the per-candidate latency; larger batches take one warp per candidate.
+    const char *tenv = getenv("FO_TEAM");  // tuning override, read per launch
+    if (tenv) {
+        geo.team = tenv[0] == '1';
+    } else {
+        int sm_t = arena_fits ? (int)bytes : 0;
+        int per_sm_t = fp64 ? blocks_per_sm<double>(sm_t, true) : blocks_per_sm<float>(sm_t, true);
+        if (per_sm_t <= 0) per_sm_t = fp64 ? blocks_per_sm<double>(0, true) : blocks_per_sm<float>(0, true);
+        geo.team = K <= num_sms * std::max(per_sm_t, 1);
+    }
+    const int per_block = geo.team ? 1 : kWarps;  // arenas per block
     geo.sm_nodes = (int)n;
     geo.sm_pairs = (int)p;
     // The shared-memory arena takes the L1 capacity the global-workspace setup
@@ -1472,8 +1545,7 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
     // (latency-bound, one block per SM at most) take it.
     static const char *env = getenv("FO_SIM_SMEM");
     const bool arena_on = env ? env[0] == '1' : K <= num_sms * kWarps;
-    geo.sm_bytes = (arena_on && bytes * per_block <= 200 * 1024 && n < 65536) ? (int)bytes : 0;
-    const bool fp64 = precision == FO_PREC_FP64;
+    geo.sm_bytes = (arena_on && arena_fits && bytes * per_block <= 200 * 1024) ? (int)bytes : 0;
     int per_sm = fp64 ? blocks_per_sm<double>(geo.sm_bytes * per_block, geo.team)
                       : blocks_per_sm<float>(geo.sm_bytes * per_block, geo.team);
     if (per_sm <= 0) {  // arena does not fit: global-memory simulation only
