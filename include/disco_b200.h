@@ -172,6 +172,21 @@ int fo_random_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int
 int fo_expand_all(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t cap,
                   int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *n_out);
 
+/* ---- heuristic baselines (search.py:228-302) ---------------------------- */
+/* greedy_postorder_fusion (search.py:228-244): every op in reverse contracted
+ * topological order; its normal group is non-duplicate-fused with the first
+ * predecessor group (ascending id) whose rewrite is valid.  FO_CYCLE when the
+ * input's group graph is cyclic. */
+int fo_greedy_postorder(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt,
+                        int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out);
+/* threshold_allreduce_fusion (search.py:247-302): buckets scanned in production
+ * order -- order[n_order] = bucket ids sorted by simulated start (the cp path,
+ * search.py:264-267), or NULL for the contracted topological production key
+ * (search.py:268-281) -- merging consecutive neighbours while the merged size
+ * stays <= threshold_bytes (> 0, else FO_INVALID_ARG). */
+int fo_threshold_ar(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int64_t threshold_bytes,
+                    const int32_t *order, int32_t n_order, int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out);
+
 /* Canonical fusion-state hash (equality semantics of canonical_hash, graph.py:559-580). */
 int fo_state_hash(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t K,
                   uint64_t *hash_out);

@@ -55,7 +55,9 @@ from .search import (
     TraceRecord,
     backtracking_search,
     exhaustive_search,
+    greedy_postorder_fusion,
     lockstep_search,
+    threshold_allreduce_fusion,
 )
 from .simulator import CostProviders, Timeline, cost, cost_batch, fo_bound, format_timeline, simulate
 from .workloads import HardwareParams, load_workload, oracle_providers

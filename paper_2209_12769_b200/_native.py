@@ -69,6 +69,8 @@ SIGNATURES = [
     ("fo_random_apply", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, P(C.c_int32)]),
     ("fo_expand_all", C.c_int, [vp, vp, vp, vp, C.c_int32, vp, vp, vp, P(C.c_int32)]),
     ("fo_state_hash", C.c_int, [vp, vp, vp, vp, C.c_int32, vp]),
+    ("fo_greedy_postorder", C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    ("fo_threshold_ar", C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, vp, vp]),
     ("fo_search_create", C.c_int, [vp, P(SearchCfg), vp, C.c_int32, vp, vp, vp, P(vp)]),
     ("fo_search_round", C.c_int, [vp, P(C.c_int32), vp]),
     ("fo_search_run", C.c_int, [vp, C.c_int64, P(C.c_int32)]),

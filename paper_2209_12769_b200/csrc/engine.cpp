@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cstring>
 #include <queue>
 #include <unordered_map>
@@ -356,6 +357,44 @@ struct Engine {
         }
     }
 
+    // topo_order (graph.py:536-556): Kahn over the contracted group graph,
+    // ties to the smallest (min member op, group id).  False on a cycle.
+    bool topo_groups(const Index &ix, std::vector<int32_t> &order) const {
+        const int G = ix.G;
+        std::vector<int32_t> indeg(G);
+        for (int x = 0; x < G; x++) indeg[x] = ix.pptr[x + 1] - ix.pptr[x];
+        using Key = std::pair<int32_t, int32_t>;  // (min member, dense id == id order)
+        std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap;
+        for (int x = 0; x < G; x++)
+            if (!indeg[x]) heap.emplace(ix.mem[ix.mptr[x]], x);
+        order.clear();
+        while (!heap.empty()) {
+            int x = heap.top().second;
+            heap.pop();
+            order.push_back(x);
+            for (int k = ix.sptr[x]; k < ix.sptr[x + 1]; k++) {
+                int h = ix.succ[k];
+                if (--indeg[h] == 0) heap.emplace(ix.mem[ix.mptr[h]], h);
+            }
+        }
+        return (int)order.size() == G;
+    }
+
+    // o in neighbors_allreduce(b) (rewrite.py:156-178), dense bucket indices
+    bool bucket_neighbor(const Index &ix, Scratch &sc, int b, int o) const {
+        if (o == b) return false;
+        sc.stamp.assign(ix.G, 0);
+        for (int k = ix.bptr[b]; k < ix.bptr[b + 1]; k++) {
+            int x = ix.bex[k];
+            sc.stamp[x] = 1;
+            for (int q = ix.sptr[x]; q < ix.sptr[x + 1]; q++) sc.stamp[ix.succ[q]] = 1;
+            for (int q = ix.pptr[x]; q < ix.pptr[x + 1]; q++) sc.stamp[ix.pred[q]] = 1;
+        }
+        for (int k = ix.bptr[o]; k < ix.bptr[o + 1]; k++)
+            if (sc.stamp[ix.bex[k]]) return true;
+        return false;
+    }
+
     void compact(State &s, Scratch &sc) const {  // monotone relabel of group ids to 0..G-1
         number_groups(s, sc.gnode, nullptr);
         for (int v = 0; v < V; v++) {
@@ -585,6 +624,111 @@ int fo_expand_all(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
         std::copy(out[k].rg.begin(), out[k].rg.end(), rgid_out + k * V);
         std::copy(out[k].bk.begin(), out[k].bk.end(), bkt_out + k * A);
     }
+    return FO_OK;
+}
+
+// greedy_postorder_fusion (search.py:228-244): ops in reverse topological
+// order; each op's current normal group is non-duplicate-fused with its first
+// predecessor group (ascending id) for which the rewrite is valid.
+int fo_greedy_postorder(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt,
+                        int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out) {
+    if (!g || !ngid_out || !rgid_out || !bkt_out) return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State s, cand;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    Scratch sc;
+    Index ix;
+    eng.build(s, ix, sc, false);
+    std::vector<int32_t> topo, ops;
+    if (!eng.topo_groups(ix, topo)) return fail(FO_CYCLE, "contracted group graph is cyclic");
+    for (int x : topo)
+        for (int k = ix.mptr[x]; k < ix.mptr[x + 1]; k++) ops.push_back(ix.mem[k]);
+    for (size_t i = ops.size(); i-- > 0;) {
+        const int x = ix.nn[ops[i]];
+        for (int k = ix.pptr[x]; k < ix.pptr[x + 1]; k++) {
+            if (eng.fuse_ops(s, ix, x, ix.pred[k], false, cand, sc)) {
+                std::swap(s, cand);
+                eng.build(s, ix, sc, false);
+                break;
+            }
+        }
+    }
+    std::copy(s.ng.begin(), s.ng.end(), ngid_out);
+    std::copy(s.rg.begin(), s.rg.end(), rgid_out);
+    std::copy(s.bk.begin(), s.bk.end(), bkt_out);
+    return FO_OK;
+}
+
+// threshold_allreduce_fusion (search.py:247-302): buckets in production order
+// (order[] = bucket ids by simulated start; NULL: contracted topological
+// production order), consecutive neighbours merged while the merged size stays
+// within threshold_bytes.
+int fo_threshold_ar(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int64_t threshold_bytes,
+                    const int32_t *order, int32_t n_order, int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out) {
+    if (!g || !ngid_out || !rgid_out || !bkt_out) return fail(FO_INVALID_ARG, "bad arguments");
+    if (threshold_bytes <= 0) return fail(FO_INVALID_ARG, "threshold must be > 0");
+    Engine eng(g);
+    State s, cand;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    Scratch sc;
+    Index ix;
+    eng.build(s, ix, sc, true);
+    const int A = g->A;
+    std::vector<int32_t> ord;
+    if (order) {
+        if (n_order != ix.B) return fail(FO_INVALID_ARG, "order must list every bucket once");
+        std::vector<uint8_t> seen(A, 0);
+        for (int i = 0; i < n_order; i++) {
+            int b = order[i];
+            if (b < 0 || b >= A || seen[b] || !std::binary_search(ix.bid.begin(), ix.bid.end(), b))
+                return fail(FO_INVALID_ARG, "order must list every bucket once");
+            seen[b] = 1;
+            ord.push_back(b);
+        }
+    } else {  // production key (max topo position of member producers' export groups, min member)
+        std::vector<int32_t> topo, pos(ix.G);
+        if (!eng.topo_groups(ix, topo)) return fail(FO_CYCLE, "contracted group graph is cyclic");
+        for (int i = 0; i < ix.G; i++) pos[topo[i]] = i;
+        std::vector<std::pair<std::pair<int32_t, int32_t>, int32_t>> key(ix.B, {{-1, INT32_MAX}, 0});
+        for (int a = 0; a < A; a++) {
+            const int b = ix.bki[a], pv = g->ar_prod[a];
+            const int ex = ix.rr[pv] >= 0 ? ix.rr[pv] : ix.nn[pv];
+            key[b].first.first = std::max(key[b].first.first, pos[ex]);
+            key[b].first.second = std::min(key[b].first.second, a);
+            key[b].second = ix.bid[b];
+        }
+        std::sort(key.begin(), key.end());
+        for (auto &k : key) ord.push_back(k.second);
+    }
+    std::vector<int64_t> tot(A, 0);
+    for (int a = 0; a < A; a++) tot[s.bk[a]] += g->ar_bytes[a];
+    std::vector<int32_t> alias(A);
+    for (int b : ord) alias[b] = b;
+    auto dense = [&](int b) { return (int)(std::lower_bound(ix.bid.begin(), ix.bid.end(), b) - ix.bid.begin()); };
+    int acc = -1;
+    for (int b : ord) {
+        const int live = alias[b];
+        if (acc < 0) {
+            acc = live;
+            continue;
+        }
+        if (tot[acc] + tot[live] <= threshold_bytes && eng.bucket_neighbor(ix, sc, dense(acc), dense(live)) &&
+            eng.fuse_ar(s, ix, dense(acc), dense(live), cand, sc)) {
+            std::swap(s, cand);
+            eng.build(s, ix, sc, true);
+            const int merged = std::min(acc, live);
+            const int64_t t = tot[acc] + tot[live];
+            for (int k : ord)
+                if (alias[k] == acc || alias[k] == live) alias[k] = merged;
+            tot[merged] = t;
+            acc = merged;
+            continue;
+        }
+        acc = live;
+    }
+    std::copy(s.ng.begin(), s.ng.end(), ngid_out);
+    std::copy(s.rg.begin(), s.rg.end(), rgid_out);
+    std::copy(s.bk.begin(), s.bk.end(), bkt_out);
     return FO_OK;
 }
 

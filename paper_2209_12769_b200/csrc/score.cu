@@ -808,62 +808,75 @@ __device__ void simulate_compact(const ScoreArgs &a, int k, const Ws &w, int tid
 // (rt, tiebreak, id) heap entries (simulator.py:63-77, :95-96).  All hot
 // state (durations, successor CSR, indegrees, ready runs) sits in the warp's
 // shared-memory arena.  Returns false when the candidate does not fit.
+// Per-node record of the shared-memory loop: everything a node needs when it
+// starts (duration) and completes (successor range) in one 16-byte load.
+struct __align__(16) NodeRec {
+    double dur;
+    uint16_t sb, se;
+    uint32_t pad;
+};
+
 template <bool TL>
-__device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const double *dur, const uint16_t *sptr,
-                                          uint16_t *indeg, const uint16_t *succ, uint32_t *rg, uint32_t *rb,
-                                          const int *tlid, int G, int N, int hg, int hb) {
+__device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const NodeRec *rec, uint16_t *indeg,
+                                          const uint16_t *succ, uint32_t *rg, uint32_t *rb, const int *tlid, int G,
+                                          int N, int hg, int hb) {
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
-    int run0 = -1, run1 = -1, done = 0, nc = 0, nb = 0, st = FO_OK;
-    double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
+    int run0 = -1, run1 = -1, done = 0, nc = 0, nb = 0;
+    unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
+    double end0 = 0.0, end1 = 0.0, now = 0.0, mk = 0.0;
     uint32_t level = 0;
-    for (;;) {
-        // start_available (simulator.py:98-115); start = max(now, rt) = now
+    // release the successors of a completed node (finish_node, simulator.py:88-96)
+    auto release = [&](unsigned qb, unsigned qe) {
+        for (unsigned q = qb; q < qe; q++) {
+            const int s = succ[q];
+            const int d = indeg[s] - 1;
+            indeg[s] = (uint16_t)d;
+            if (d == 0) {
+                const bool isg = s < G;
+                uint32_t *r = isg ? rg : rb;
+                const int h = isg ? headg : headb;
+                int i = isg ? tailg++ : tailb++;
+                const uint32_t key = level | (uint32_t)(isg ? s : s - G);
+                while (i > h && r[i - 1] > key) { r[i] = r[i - 1]; i--; }
+                r[i] = key;
+            }
+        }
+    };
+    // start_available (simulator.py:98-115): compute lane then comm lane;
+    // start = max(now, rt) = now because rt is a drained completion time
+    auto start = [&]() {
         if (run0 < 0 && headg < tailg) {
             run0 = (int)(rg[headg++] & 0xffffu);
-            end0 = __dadd_rn(now, dur[run0]);
-            if (end0 > mk) mk = end0;
+            const NodeRec r = rec[run0];
+            end0 = __dadd_rn(now, r.dur);
+            sb0 = r.sb;
+            se0 = r.se;
+            mk = end0 > mk ? end0 : mk;
             if (TL) { a.tl.c_id[nc] = tlid[run0]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
         }
         if (run1 < 0 && headb < tailb) {
             run1 = G + (int)(rb[headb++] & 0xffffu);
-            end1 = __dadd_rn(now, dur[run1]);
-            if (end1 > mk) mk = end1;
+            const NodeRec r = rec[run1];
+            end1 = __dadd_rn(now, r.dur);
+            sb1 = r.sb;
+            se1 = r.se;
+            mk = end1 > mk ? end1 : mk;
             if (TL) { a.tl.b_id[nb] = tlid[run1]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
         }
-        if (run0 < 0 && run1 < 0) {
-            if (done != N) st = FO_CYCLE;  // simulator.py:133
-            break;
-        }
-        // advance to the next completion; drain every lane ending there
-        now = run0 < 0 ? end1 : (run1 < 0 ? end0 : (end0 < end1 ? end0 : end1));
-        if (now > last) { last = now; level += 0x10000u; }
-#pragma unroll
-        for (int t = 0; t < 2; t++) {
-            const int node = t == 0 ? run0 : run1;
-            if (node < 0 || (t == 0 ? end0 : end1) != now) continue;
-            if (t == 0) run0 = -1; else run1 = -1;
-            done++;
-            const int qe = sptr[node + 1];
-            for (int q = sptr[node]; q < qe; q++) {  // finish_node (simulator.py:88-96)
-                const int s = succ[q];
-                const int d = indeg[s] - 1;
-                indeg[s] = (uint16_t)d;
-                if (d == 0) {
-                    if (s < G) {
-                        uint32_t key = level | (uint32_t)s;
-                        int i = tailg++;
-                        while (i > headg && rg[i - 1] > key) { rg[i] = rg[i - 1]; i--; }
-                        rg[i] = key;
-                    } else {
-                        uint32_t key = level | (uint32_t)(s - G);
-                        int i = tailb++;
-                        while (i > headb && rb[i - 1] > key) { rb[i] = rb[i - 1]; i--; }
-                        rb[i] = key;
-                    }
-                }
-            }
-        }
+    };
+    start();
+    while (run0 >= 0 || run1 >= 0) {
+        // next completion; every lane ending then is drained before any start
+        // (simulator.py:122-132).  Equal completion times share one level.
+        const bool c0 = run0 >= 0 && (run1 < 0 || end0 <= end1);
+        const bool c1 = run1 >= 0 && (run0 < 0 || end1 <= end0);
+        const double t = c0 ? end0 : end1;
+        if (t > now) { now = t; level += 0x10000u; }
+        if (c0) { run0 = -1; done++; release(sb0, se0); }
+        if (c1) { run1 = -1; done++; release(sb1, se1); }
+        start();
     }
+    const int st = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
     a.cost_out[k] = st == FO_OK ? mk : 0.0;
     a.status_out[k] = st;
     if (TL) { *a.tl.n_c = nc; *a.tl.n_b = nb; }
@@ -876,8 +889,8 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int tid, i
     const int P = w.sptr()[N];
     const int cn = a.sm_nodes, cp = a.sm_pairs;
     if (sm == nullptr || N > cn || P > cp || N >= 65536 || 2 * V + A >= 65536) return false;
-    double *dur = (double *)sm;
-    uint16_t *sptr = (uint16_t *)(dur + cn);
+    NodeRec *rec = (NodeRec *)sm;
+    uint16_t *sptr = (uint16_t *)(rec + cn);  // exclusive scan scratch (cn + 2)
     uint16_t *indeg = sptr + cn + 2;
     uint16_t *succ = indeg + cn;
     uint32_t *ready = (uint32_t *)(succ + cp);  // cp is even: 4-byte aligned, stays a shared-space pointer
@@ -898,12 +911,14 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int tid, i
         int j = i < G ? rk[w.prank()[i]] : G + rk[2 * V + w.prank()[i]];
         sim[i] = j;
         cnt[j] = w.sptr()[i + 1] - w.sptr()[i];
-        dur[j] = w.dur()[i];
+        rec[j].dur = w.dur()[i];
         indeg[j] = (uint16_t)w.indeg()[i];
         if (a.tl.c_id) w.tlid()[j] = i < G ? w.g2id()[i] : w.b2id()[i - G];
     }
     tsync<TEAM>();
     team_exscan<TEAM>(cnt, sptr, N, ts, tid);  // successor counts -> sptr (u16)
+#pragma unroll 4
+    for (int j = tid; j < N; j += TEAM) { rec[j].sb = sptr[j]; rec[j].se = sptr[j + 1]; }
     #pragma unroll 4
     for (int i = tid; i < N; i += TEAM) {
         int o = sptr[sim[i]];
@@ -926,8 +941,8 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int tid, i
     }
     tsync<TEAM>();
     if (tid == 0) {
-        if (a.tl.c_id) smem_loop<true>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
-        else smem_loop<false>(a, k, dur, sptr, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
+        if (a.tl.c_id) smem_loop<true>(a, k, rec, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
+        else smem_loop<false>(a, k, rec, indeg, succ, rg, rb, w.tlid(), G, N, hg, hb);
     }
     tsync<TEAM>();
     (void)B;
@@ -1522,7 +1537,7 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
     // arena sized for typical candidates (groups ~ ops); larger ones use the global path
     int64_t n = std::min<int64_t>(2 * (int64_t)V + A + 1, (int64_t)V + V / 8 + A + 32);
     int64_t p = (std::min<int64_t>(g.pairs_max, (int64_t)E + E / 4 + A + 32) + 1) & ~int64_t(1);
-    int64_t bytes = (8 * n + 2 * (n + 2) + 2 * n + 2 * p + 4 + 4 * n + 15) & ~int64_t(15);
+    int64_t bytes = (16 * n + 2 * (n + 2) + 2 * n + 2 * p + 4 + 4 * n + 15) & ~int64_t(15);
     const bool fp64 = precision == FO_PREC_FP64;
     const bool arena_fits = bytes <= 200 * 1024 && n < 65536;
     // Batches that fit in one wave of 128-thread blocks (search rounds) take

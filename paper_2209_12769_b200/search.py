@@ -21,7 +21,7 @@ import numpy as np
 from . import _native as N
 from .errors import InvalidConfig, LimitExceeded, _raise
 from .graph import HloGraph, canonical_hash, state_arrays, state_from_arrays
-from .rewrite import ALL_METHODS, METHOD_INDEX, OptimizationMethod, expand_all
+from .rewrite import ALL_METHODS, METHOD_INDEX, OptimizationMethod, engine_graph, expand_all
 
 METHOD_NAMES = ("nondup", "dup", "ar")
 
@@ -206,3 +206,45 @@ def exhaustive_search(g0: HloGraph, cp, max_ops: int = 8, max_tensors: int = 4) 
                 best, best_cost = x, float(cost[i])
         frontier = level
     return SearchResult(state_from_arrays(g0, *best), best_cost, steps, evaluated, len(seen) - 1)
+
+
+# --- heuristic baselines (search.py:228-302) ---------------------------------
+
+
+def greedy_postorder_fusion(g: HloGraph) -> HloGraph:
+    """Walk ops in post order (reverse topological) and non-duplicate-fuse each
+    op's current group with its first fusible predecessor when the rewrite is
+    valid (search.py:228-244), in the native engine."""
+    dg = engine_graph(g)
+    ng, rg, bk, _, _, _ = state_arrays(g)
+    on, orr, ob = np.empty_like(ng), np.empty_like(rg), np.empty_like(bk)
+    st = N.lib().fo_greedy_postorder(dg.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), N.ptr(on), N.ptr(orr), N.ptr(ob))
+    _raise(st, "greedy_postorder_fusion", N.last_error())
+    return state_from_arrays(g, on, orr, ob)
+
+
+def threshold_allreduce_fusion(g: HloGraph, threshold_bytes: int, cp=None) -> HloGraph:
+    """Scan buckets in tensor production order and merge consecutive neighbours
+    while the merged size stays within the threshold (search.py:247-302).
+    With cost providers the order is the simulated start order (the device
+    simulator), otherwise the contracted topological production order."""
+    if threshold_bytes <= 0:
+        raise InvalidConfig("threshold must be > 0")
+    if not g.buckets:
+        return g
+    dg = engine_graph(g)
+    ng, rg, bk, _, _, bids = state_arrays(g)
+    order = None
+    if cp is not None:
+        from .simulator import simulate
+
+        tl = simulate(g, cp)
+        start_of = {bid: (start, bid) for bid, start, _ in tl.comm_events}
+        rank = {b: i for i, b in enumerate(bids)}
+        order = np.array([rank[b] for b in sorted(bids, key=lambda b: start_of[b])], np.int32)
+    on, orr, ob = np.empty_like(ng), np.empty_like(rg), np.empty_like(bk)
+    st = N.lib().fo_threshold_ar(dg.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), int(threshold_bytes),
+                                 None if order is None else N.ptr(order), 0 if order is None else len(order),
+                                 N.ptr(on), N.ptr(orr), N.ptr(ob))
+    _raise(st, "threshold_allreduce_fusion", N.last_error())
+    return state_from_arrays(g, on, orr, ob)

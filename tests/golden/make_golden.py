@@ -7,7 +7,8 @@ imports the reference, and it only ever runs in the build container
 (/root/reference does not exist on the GPU box); its outputs are committed.
 
 Usage:  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [section ...]
-Sections: workloads rng cases search   (default: all)
+Sections: workloads rng cases search exhaustive sweep baselines
+(default: the first five)
 
 Inputs follow SURVEY.md section 8(d) / BASELINE.md section 3:
   * graphs   gen_workload(WorkloadSpec(family, V, A, seed=0))      (workloads.py:131)
@@ -382,14 +383,43 @@ def section_sweep(_=None):
         _dump_gz(os.path.join(OUT, "sweep_gpt2m.json.gz"), out)
 
 
+def section_baselines(names=None):
+    """Heuristic baselines (search.py:228-302) on the small configs: the greedy
+    post-order op fusion, threshold AllReduce fusion without cost providers
+    (contracted production order) and with the MP providers (simulated start
+    order), each from the unfused graph, from the greedy result and from a
+    random-batch candidate (which holds replica groups)."""
+    from fuseopt import greedy_postorder_fusion, threshold_allreduce_fusion
+
+    out = {}
+    for name in list(SMALL) + ["vgg16", "resnet50", "bert"]:
+        if names and name not in names:
+            continue
+        t0 = time.time()
+        g, profile, comm, mp, lin = load_workload(name)
+        cp = make_cost_providers(profile, comm, mp)
+        starts = {"unfused": g, "cand3": make_candidate(g, 3)}
+        greedy = {k: greedy_postorder_fusion(x) for k, x in starts.items()}
+        ent = {"greedy": {k: state_doc(x) for k, x in greedy.items()}, "threshold": []}
+        starts["greedy"] = greedy["unfused"]
+        for T in (64 * 1024, 4 * 1024 * 1024, 256 * 1024 * 1024):
+            for k, x in starts.items():
+                ent["threshold"].append({"T": T, "start": k, "topo": state_doc(threshold_allreduce_fusion(x, T)),
+                                         "sim": state_doc(threshold_allreduce_fusion(x, T, cp))})
+        ent["starts"] = {k: state_doc(x) for k, x in starts.items()}
+        out[name] = ent
+        print(f"baselines {name}: {time.time() - t0:.0f}s", flush=True)
+        _dump_gz(os.path.join(OUT, "baselines.json.gz"), out)
+
+
 def main(argv):
-    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep")]
+    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep", "baselines")]
     names = [a for a in argv if a not in sections]
     if not sections:
         sections = ["workloads", "rng", "cases", "search", "exhaustive"]
     for s in sections:
         {"workloads": section_workloads, "rng": lambda _: section_rng(), "exhaustive": section_exhaustive,
-         "sweep": section_sweep,
+         "sweep": section_sweep, "baselines": section_baselines,
          "cases": section_cases, "search": section_search}[s](names or None)
 
 

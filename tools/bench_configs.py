@@ -3,9 +3,10 @@ is configs[1]).
 
   python tools/bench_configs.py gpt2-sweep [--batch 256]
       GPT-2-medium proxy (V=5000): the 13 bucket-size thresholds x {AR-only,
-      greedy op fusion + AR} parents from the reference's own baselines
-      (tests/golden/sweep_gpt2m.json.gz), each scored and then used as the
-      parent of a random-candidate batch.
+      greedy op fusion + AR} parents, built by this package's
+      greedy_postorder_fusion / threshold_allreduce_fusion and checked against
+      the reference's own (tests/golden/sweep_gpt2m.json.gz), each scored and
+      then used as the parent of a random-candidate batch.
   python tools/bench_configs.py synth50k [--batch 8192]
       synthetic 50k-op DAG: one round of random candidates per GPU
       (64k per round on 8 GPUs = 8192 per GPU).
@@ -51,17 +52,30 @@ def gpt2_sweep(args):
     from _golden import graph_with_state, read
 
     torch.cuda.set_device(0)
-    prec = N.FO_PREC_FP32
+    prec = N.FO_PREC_FP64 if args.precision == "fp64" else N.FO_PREC_FP32
     g, prof, comm, mp, lin = P.load_workload("gpt2m")
     cp = P.make_cost_providers(prof, comm, mp, precision=prec)
+    cp64 = P.make_cost_providers(prof, comm, mp, precision=N.FO_PREC_FP64)  # decision-exact parents
     dg = cp.device_graph(g)
     sweep = read("sweep_gpt2m.json.gz")
     rows, worst, total_c, total_ms, gen_s = [], 0.0, 0, 0.0, 0.0
     from paper_2209_12769_b200.graph import state_arrays
+    from _golden import canon_doc, canon_graph
 
+    # parents built by this package (greedy op fusion, then the threshold scan
+    # in simulated production order); the reference's parents are the check
+    t0 = time.perf_counter()
+    greedy = P.greedy_postorder_fusion(g)
+    parents_s = time.perf_counter() - t0
+    match = canon_graph(greedy) == canon_doc(g, sweep["greedy"]["state"])
     for ent in sweep["sweep"]:
+        t0 = time.perf_counter()
+        built = {"ar_only": P.threshold_allreduce_fusion(g, ent["T"], cp64),
+                 "both": P.threshold_allreduce_fusion(greedy, ent["T"], cp64)}
+        parents_s += time.perf_counter() - t0
         for kind in ("ar_only", "both"):
-            parent = graph_with_state(g, ent[kind]["state"])
+            parent = built[kind]
+            match &= canon_graph(parent) == canon_doc(g, ent[kind]["state"])
             c_dev = P.cost(parent, cp)
             rel = abs(c_dev - ent[kind]["cost"]) / ent[kind]["cost"]
             worst = max(worst, rel)
@@ -78,7 +92,8 @@ def gpt2_sweep(args):
     line = {"metric": "fusion candidates scored/sec (GNN est.+sim)", "config": "gpt2m bucket-size sweep",
             "value": total_c / (total_ms / 1e3), "unit": "candidates/s", "n_gpus": 1,
             "thresholds": len(sweep["sweep"]), "batch_per_parent": args.batch, "parents": len(rows),
-            "parent_cost_max_rel_err_vs_reference": worst, "candidate_generation_s": gen_s,
+            "parent_cost_max_rel_err_vs_reference": worst, "parents_match_reference": bool(match),
+            "parents_build_s": parents_s, "candidate_generation_s": gen_s,
             "best": min(rows, key=lambda r: r["batch_best_us"]), "rows": rows}
     print(json.dumps(line))
 
@@ -131,6 +146,7 @@ if __name__ == "__main__":
     ap.add_argument("--beta", type=int, default=10)
     ap.add_argument("--check", type=int, default=2)
     ap.add_argument("--distinct", type=int, default=1024)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     a = ap.parse_args()
     if a.what == "gpt2-sweep":
         a.batch = a.batch or 256
