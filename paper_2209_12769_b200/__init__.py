@@ -37,6 +37,7 @@ from .graph import (
     FusionGroup,
     GraphMeta,
     HloGraph,
+    ModuleStats,
     OpNode,
     TensorBucket,
     build_graph,
@@ -44,6 +45,7 @@ from .graph import (
     graph_from_doc,
     graph_to_doc,
     load_graph,
+    module_stats,
     save_graph,
     with_fusion_state,
 )
@@ -59,7 +61,7 @@ from .search import (
     lockstep_search,
     threshold_allreduce_fusion,
 )
-from .simulator import CostProviders, Timeline, cost, cost_batch, fo_bound, format_timeline, simulate
+from .simulator import CostProviders, Timeline, cost, cost_batch, fo_bound, format_timeline, report_lines, simulate
 from .workloads import HardwareParams, load_workload, oracle_providers
 
 __version__ = "0.1.0"

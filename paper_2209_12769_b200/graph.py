@@ -13,7 +13,7 @@ import gzip
 import hashlib
 import json
 from dataclasses import dataclass
-from typing import Iterable, Optional, Sequence
+from typing import Iterable, NamedTuple, Optional, Sequence
 
 from .errors import GraphFormatError
 
@@ -305,3 +305,30 @@ def state_from_arrays(g: HloGraph, ngid, rgid, bkt) -> HloGraph:
     new_ars = tuple(AllReduceInstr(a.id, a.producer_op, a.tensor_bytes, owner[a.id]) for a in ars)
     bks = tuple(TensorBucket(bid, tuple(ms), sum(size[m] for m in ms)) for bid, ms in sorted(buckets))
     return HloGraph(g.meta, g.ops, g.edges, new_ars, tuple(sorted(groups, key=lambda x: x.id)), bks)
+
+
+class ModuleStats(NamedTuple):
+    total_compute_us: float
+    total_comm_us: float
+    op_count: int
+    bucket_count: int
+
+
+def module_stats(g: HloGraph, costs, comm) -> ModuleStats:
+    """Exact compute/communication totals from per-group and per-bucket
+    durations (graph.py:583-601); builtin sum in group/bucket order, as the
+    reference sums them."""
+    from .errors import MissingCost
+
+    for gr in g.groups:
+        if gr.id not in costs:
+            raise MissingCost(f"no duration for group {gr.id}")
+    for b in g.buckets:
+        if b.id not in comm:
+            raise MissingCost(f"no duration for bucket {b.id}")
+    return ModuleStats(
+        total_compute_us=float(sum(costs[gr.id] for gr in g.groups)),
+        total_comm_us=float(sum(comm[b.id] for b in g.buckets)),
+        op_count=len(g.groups),
+        bucket_count=len(g.buckets),
+    )

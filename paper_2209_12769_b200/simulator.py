@@ -135,3 +135,25 @@ def format_timeline(tl: Timeline) -> str:
     out = ["kind id start_us end_us"] + [f"{k} {i} {s:.6f} {e:.6f}" for k, i, s, e in rows]
     out.append(f"makespan_us {tl.makespan_us:.6f}")
     return "\n".join(out) + "\n"
+
+
+def report_lines(g: HloGraph, cp, label: str) -> list:
+    """The compare/report verb's per-graph summary (cli.py:227-238): makespan,
+    fo_bound and module totals, from one device simulate and one device
+    durations pass."""
+    from .graph import module_stats
+
+    tl = simulate(g, cp)
+    if _is_device(cp):
+        costs, comms = cp.node_durations(g)
+    else:
+        costs = {gr.id: cp.op_cost(g, gr) for gr in g.groups}
+        comms = {b.id: cp.comm_cost(g, b) for b in g.buckets}
+    stats = module_stats(g, costs, comms)
+    return [
+        f"[{label}] makespan_us {tl.makespan_us:.6f}",
+        f"[{label}] fo_bound_us {fo_bound(g, cp):.6f}",
+        f"[{label}] total_compute_us {stats.total_compute_us:.6f}",
+        f"[{label}] total_comm_us {stats.total_comm_us:.6f}",
+        f"[{label}] groups {stats.op_count} buckets {stats.bucket_count}",
+    ]

@@ -140,3 +140,25 @@ def test_gpt2_sweep_parents_built_natively():
         assert canon_graph(a) == canon_doc(g, ent["ar_only"]["state"]), ent["T"]
         assert canon_graph(b) == canon_doc(g, ent["both"]["state"]), ent["T"]
         np.testing.assert_allclose(P.cost(b, cp), ent["both"]["cost"], rtol=1e-12)
+
+
+def test_module_stats_matches_reference_semantics():
+    g = comm_heavy_graph(3, 1 * MB)
+    costs = {x.id: 0.1 * (x.id + 1) for x in g.groups}
+    comm = {b.id: 2.5 for b in g.buckets}
+    st = P.module_stats(g, costs, comm)
+    assert st == (sum(costs[x.id] for x in g.groups), 7.5, 3, 3)
+    with pytest.raises(P.MissingCost):
+        P.module_stats(g, {}, comm)
+
+
+@pytest.mark.gpu
+def test_report_lines_device_providers():
+    from paper_2209_12769_b200 import make_cost_providers
+    import paper_2209_12769_b200._native as N
+
+    g, prof, comm, mp, lin = P.load_workload("vgg16")
+    cp = make_cost_providers(prof, comm, mp, precision=N.FO_PREC_FP64)
+    lines = P.report_lines(g, cp, "x")
+    assert lines[0] == f"[x] makespan_us {P.cost(g, cp):.6f}"
+    assert lines[-1] == f"[x] groups {len(g.groups)} buckets {len(g.buckets)}"
