@@ -18,8 +18,8 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",  # schedule arithmetic must stay plain IEEE add/mul (bit-exact vs the reference)
     "-Xcompiler", "-fPIC,-fopenmp,-O3",
-    "-shared",
 ]
+HEADERS = [os.path.join(CSRC, "fo_internal.h"), os.path.join(os.path.dirname(HERE), "include", "disco_b200.h")]
 
 
 def needs_build() -> bool:
@@ -31,14 +31,34 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _stale(obj: str, src: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(d) > t for d in [src, *HEADERS])
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Per-source objects (rebuilt when the source or a shared header changed),
+    then one shared library."""
     if not force and not needs_build():
         return OUT
     os.makedirs(OUT_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *(os.path.join(CSRC, s) for s in SOURCES), "-o", OUT + ".tmp", "-lgomp"]
+    objs = []
+    for src in SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
+        objs.append(obj)
+        if force or _stale(obj, path):
+            cmd = [nvcc, *NVCC_FLAGS, "-c", path, "-o", obj + ".tmp"]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+            os.replace(obj + ".tmp", obj)
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", OUT + ".tmp", "-lgomp"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)

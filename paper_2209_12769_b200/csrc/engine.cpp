@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <unordered_map>
@@ -538,6 +539,716 @@ struct Engine {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Incremental rewrite engine.  Engine::random_apply
+// rebuilds the whole index after every accepted rewrite and runs a full Kahn
+// pass per draw: O(V + E) per draw, ~50 ms per candidate at 50k ops.  Inc
+// keeps the index live instead:
+//   * per group id: members, flags, and four sorted-unique rows -- contracted
+//     preds / succs over all edges (graph.py:161-179) and joint schedule
+//     preds / succs with the bucket nodes (graph.py:215-274); bucket nodes
+//     carry their joint rows too.  A merge recomputes only the rows of the
+//     merged node and of its neighbours, from their member ops' edges.
+//   * the fusible-pair list (rewrite.py:49-61) as per-group counts in a
+//     Fenwick tree over group ids, so the k-th pair in the reference's order
+//     is found without materialising the list.
+//   * a topological order of the joint graph.  A merge of u and v is cyclic
+//     iff a node reachable from the merged node's successors can reach it,
+//     and every such node lies strictly between pos(u) and pos(v): the
+//     validity test is a DFS bounded to that window (rewrite_candidate_ok,
+//     graph.py:505-512), and an accepted merge reorders only that window
+//     (Pearce-Kelly: the window's ancestors of the merged node, then the
+//     merged node, then its descendants).
+//   * a duplicate fusion that leaves a replica never needs the test: the
+//     merged group takes the consumer's position and the replica the
+//     producer's, and every new dependency runs forward in the old order.
+// Draw sequence, accept/reject decisions and ids equal Engine::random_apply
+// (cross-checked by tests/test_native_cpu.py with FO_ENGINE=full).
+
+struct Inc {
+    const fo_graph *g = nullptr;
+    int V = 0, E = 0, A = 0, VB = 0, NJ = 0;
+    std::vector<int32_t> ng, rg, bk;  // fusion state (engine ids)
+    int maxid = -1;                   // largest live group id
+    // groups by id
+    std::vector<uint8_t> alive, cok, hdup, far, hrep;
+    std::vector<int32_t> moff, mlen, mpool;  // members (op << 1 | dup), ascending op
+    // rows: kind 0 contracted preds, 1 contracted succs (groups only),
+    // 2 joint preds, 3 joint succs (groups [0, VB), bucket b at VB + b)
+    std::vector<int32_t> roff[4], rlen[4], rpool;
+    std::vector<int32_t> pos;  // topological position in the joint graph
+    // buckets by id: member ARs ascending, total bytes
+    std::vector<int32_t> boff, blen, bpool;
+    std::vector<int64_t> btot;
+    // fusible-pair counts per group id for the nondup (0) and dup (1) rules,
+    // Fenwick trees over ids, kept current across every rewrite
+    int method = -1;
+    std::vector<int32_t> cnt[2], fen[2];
+    int64_t tot[2] = {0, 0};
+    int64_t total = 0;
+    // AR method: materialised bucket pairs
+    std::vector<std::pair<int32_t, int32_t>> arpairs;
+    // scratch
+    std::vector<int32_t> t0, t1, t2, t3, mark, stk, F, Bk, nb, gen, ihead;
+    std::vector<std::pair<int32_t, int32_t>> iv;
+    int32_t gen_no = 0;
+
+    const int32_t *row(int k, int n) const { return rpool.data() + roff[k][n]; }
+    int rowlen(int k, int n) const { return rlen[k][n]; }
+    bool member(int s, int c) const { return ng[s] == c || rg[s] == c; }
+    int exportg(int s) const { return rg[s] >= 0 ? rg[s] : ng[s]; }
+
+    void store(int k, int n, std::vector<int32_t> &t) {
+        std::sort(t.begin(), t.end());
+        t.erase(std::unique(t.begin(), t.end()), t.end());
+        if ((int)t.size() <= rlen[k][n]) {  // shrinking rows rewrite in place
+            std::copy(t.begin(), t.end(), rpool.begin() + roff[k][n]);
+        } else {
+            roff[k][n] = (int32_t)rpool.size();
+            rpool.insert(rpool.end(), t.begin(), t.end());
+        }
+        rlen[k][n] = (int32_t)t.size();
+    }
+
+    // the four rows of group x from its member ops' edges
+    void rows_group(int x) {
+        t0.clear();
+        t1.clear();
+        const int32_t *m = mpool.data() + moff[x];
+        for (int i = 0; i < mlen[x]; i++) {
+            const int d = m[i] >> 1;
+            for (int q = g->in_ptr[d]; q < g->in_ptr[d + 1]; q++) {
+                const int e = g->in_e[q], s = g->e_src[e];
+                const bool inside = member(s, x);
+                if (!inside) t0.push_back(exportg(s));
+                if (!g->agg[e]) {
+                    if (!inside) t1.push_back(exportg(s));
+                } else {
+                    for (int r = g->arp_ptr[s]; r < g->arp_ptr[s + 1]; r++) t1.push_back(VB + bk[g->arp[r]]);
+                }
+            }
+        }
+        store(0, x, t0);
+        store(2, x, t1);
+        t0.clear();
+        t1.clear();
+        for (int i = 0; i < mlen[x]; i++) {
+            const int s = m[i] >> 1;
+            if (exportg(s) != x) continue;
+            const int ns = ng[s], rs = rg[s];
+            for (int q = g->out_ptr[s]; q < g->out_ptr[s + 1]; q++) {
+                const int e = g->out_e[q], d = g->e_dst[e];
+                const int c0 = ng[d], c1 = rg[d];
+                if (c0 != ns && c0 != rs) {
+                    t0.push_back(c0);
+                    if (!g->agg[e]) t1.push_back(c0);
+                }
+                if (c1 >= 0 && c1 != ns && c1 != rs) {
+                    t0.push_back(c1);
+                    if (!g->agg[e]) t1.push_back(c1);
+                }
+            }
+            for (int r = g->arp_ptr[s]; r < g->arp_ptr[s + 1]; r++) t1.push_back(VB + bk[g->arp[r]]);
+        }
+        store(1, x, t0);
+        store(3, x, t1);
+    }
+
+    // joint rows of bucket b: producers' export groups in, aggregate consumers out
+    void rows_bucket(int b) {
+        t0.clear();
+        t1.clear();
+        const int32_t *m = bpool.data() + boff[b];
+        for (int i = 0; i < blen[b]; i++) {
+            const int s = g->ar_prod[m[i]];
+            t0.push_back(exportg(s));
+            for (int q = g->out_ptr[s]; q < g->out_ptr[s + 1]; q++) {
+                const int e = g->out_e[q];
+                if (!g->agg[e]) continue;
+                const int d = g->e_dst[e];
+                t1.push_back(ng[d]);
+                if (rg[d] >= 0) t1.push_back(rg[d]);
+            }
+        }
+        store(2, VB + b, t0);
+        store(3, VB + b, t1);
+    }
+
+    void group_flags(int x) {
+        cok[x] = 1;
+        hdup[x] = far[x] = hrep[x] = 0;
+        const int32_t *m = mpool.data() + moff[x];
+        for (int i = 0; i < mlen[x]; i++) {
+            const int v = m[i] >> 1;
+            if (g->op_kind[v] != 0) cok[x] = 0;
+            if (g->arp_ptr[v + 1] > g->arp_ptr[v]) far[x] = 1;
+            if (m[i] & 1) hdup[x] = 1;
+            if (rg[v] >= 0) hrep[x] = 1;
+        }
+    }
+
+    // full build from a state (ids < VB); false when the joint graph is cyclic
+    bool build(const fo_graph *gr, const State &s, int vb) {
+        g = gr;
+        V = gr->V;
+        E = gr->E;
+        A = gr->A;
+        VB = vb;
+        NJ = VB + A;
+        ng = s.ng;
+        rg = s.rg;
+        bk = s.bk;
+        alive.assign(VB, 0);
+        cok.assign(VB, 0);
+        hdup.assign(VB, 0);
+        far.assign(VB, 0);
+        hrep.assign(VB, 0);
+        moff.assign(VB, 0);
+        mlen.assign(VB, 0);
+        for (int v = 0; v < V; v++) {
+            mlen[ng[v]]++;
+            if (rg[v] >= 0) mlen[rg[v]]++;
+        }
+        int o = 0;
+        maxid = -1;
+        for (int x = 0; x < VB; x++) {
+            moff[x] = o;
+            o += mlen[x];
+            if (mlen[x]) {
+                alive[x] = 1;
+                maxid = x;
+            }
+            mlen[x] = 0;
+        }
+        mpool.assign(o, 0);
+        for (int v = 0; v < V; v++) {  // ascending op: member lists come out sorted
+            mpool[moff[ng[v]] + mlen[ng[v]]++] = v << 1;
+            if (rg[v] >= 0) mpool[moff[rg[v]] + mlen[rg[v]]++] = (v << 1) | 1;
+        }
+        for (int x = 0; x < VB; x++)
+            if (alive[x]) group_flags(x);
+        boff.assign(A, 0);
+        blen.assign(A, 0);
+        btot.assign(A, 0);
+        for (int a = 0; a < A; a++) {
+            blen[bk[a]]++;
+            btot[bk[a]] += g->ar_bytes[a];
+        }
+        o = 0;
+        for (int b = 0; b < A; b++) {
+            boff[b] = o;
+            o += blen[b];
+            blen[b] = 0;
+        }
+        bpool.assign(o, 0);
+        for (int a = 0; a < A; a++) bpool[boff[bk[a]] + blen[bk[a]]++] = a;
+        for (int k = 0; k < 4; k++) {
+            roff[k].assign(NJ, 0);
+            rlen[k].assign(NJ, 0);
+        }
+        rpool.clear();
+        rpool.reserve(4 * (size_t)E + 4 * (size_t)A + 1024);
+        for (int x = 0; x < VB; x++)
+            if (alive[x]) rows_group(x);
+        for (int b = 0; b < A; b++)
+            if (blen[b]) rows_bucket(b);
+        // topological positions of the joint graph (Kahn, LIFO: chains stay contiguous)
+        pos.assign(NJ, 0);
+        std::vector<int32_t> indeg(NJ, 0);
+        stk.clear();
+        int nodes = 0;
+        for (int n = 0; n < NJ; n++) {
+            const bool live = n < VB ? alive[n] : blen[n - VB] > 0;
+            if (!live) continue;
+            nodes++;
+            indeg[n] = rlen[2][n];
+            if (!indeg[n]) stk.push_back(n);
+        }
+        int p = 0;
+        while (!stk.empty()) {
+            const int u = stk.back();
+            stk.pop_back();
+            pos[u] = p++;
+            const int32_t *r = row(3, u);
+            for (int i = 0; i < rlen[3][u]; i++)
+                if (--indeg[r[i]] == 0) stk.push_back(r[i]);
+        }
+        mark.assign(NJ, 0);
+        gen.assign(NJ, 0);
+        gen_no = 0;
+        method = -1;
+        init_counts();
+        return p == nodes;
+    }
+
+    // ---- fusible pairs in the reference's order (rewrite.py:49-61, :242-247)
+    bool qual(int p, int r) const { return cok[p] && !(r == 1 && hdup[p]); }
+    void count_of(int x, int c[2]) const {
+        c[0] = c[1] = 0;
+        if (!alive[x] || !cok[x]) return;
+        const int32_t *r = row(0, x);
+        for (int i = 0; i < rlen[0][x]; i++) {
+            const int p = r[i];
+            if (cok[p]) {
+                c[0]++;
+                c[1] += !hdup[p];
+            }
+        }
+    }
+    void fen_add(int r, int x, int d) {
+        for (int i = x + 1; i <= VB; i += i & -i) fen[r][i] += d;
+        tot[r] += d;
+    }
+    void recount(int x) {
+        int c[2];
+        count_of(x, c);
+        for (int r = 0; r < 2; r++)
+            if (c[r] != cnt[r][x]) {
+                fen_add(r, x, c[r] - cnt[r][x]);
+                cnt[r][x] = c[r];
+            }
+        if (method == M_NONDUP || method == M_DUP) total = tot[method == M_DUP];
+    }
+    void init_counts() {
+        for (int r = 0; r < 2; r++) {
+            cnt[r].assign(VB, 0);
+            fen[r].assign(VB + 1, 0);
+            tot[r] = 0;
+        }
+        for (int x = 0; x < VB; x++) {
+            int c[2];
+            count_of(x, c);
+            for (int r = 0; r < 2; r++) {
+                cnt[r][x] = c[r];
+                tot[r] += c[r];
+                fen[r][x + 1] += c[r];
+            }
+        }
+        for (int r = 0; r < 2; r++)
+            for (int i = 1; i <= VB; i++) {
+                const int j = i + (i & -i);
+                if (j <= VB) fen[r][j] += fen[r][i];
+            }
+    }
+    void prepare_op_pairs(int m) {
+        method = m;
+        total = tot[m == M_DUP];
+    }
+    std::pair<int, int> select(int64_t k) const {  // k-th pair, 0-based
+        const int rr = method == M_DUP;
+        const std::vector<int32_t> &f = fen[rr];
+        int x = 0;
+        int step = 1;
+        while (step * 2 <= VB) step *= 2;
+        for (; step; step >>= 1)
+            if (x + step <= VB && f[x + step] <= k) {
+                x += step;
+                k -= f[x];
+            }
+        // group x (0-based) holds the pair; k-th qualifying pred
+        const int32_t *r = row(0, x);
+        for (int i = 0; i < rlen[0][x]; i++)
+            if (qual(r[i], rr) && k-- == 0) return {x, r[i]};
+        return {-1, -1};
+    }
+
+    // ---- bucket pairs (rewrite.py:156-178, :212-219)
+    void prepare_ar_pairs() {
+        method = M_AR;
+        arpairs.clear();
+        // inverse: group -> buckets exporting from it (bex = joint preds of a
+        // bucket), as (group, bucket) pairs sorted by group; ihead[x] (stamped
+        // by gen == gi) is the first pair of group x
+        iv.clear();
+        for (int b = 0; b < A; b++)
+            if (blen[b]) {
+                const int32_t *r = row(2, VB + b);
+                for (int i = 0; i < rlen[2][VB + b]; i++) iv.emplace_back(r[i], b);
+            }
+        std::sort(iv.begin(), iv.end());
+        if ((int)ihead.size() < VB) ihead.assign(VB, 0);
+        const int32_t gi = ++gen_no;
+        for (int i = (int)iv.size() - 1; i >= 0; i--) {
+            ihead[iv[i].first] = i;
+            gen[iv[i].first] = gi;
+        }
+        for (int b = 0; b < A; b++) {
+            if (!blen[b]) continue;
+            t0.clear();
+            const int32_t *r = row(2, VB + b);
+            // nearby groups
+            for (int i = 0; i < rlen[2][VB + b]; i++) {
+                const int x = r[i];
+                t0.push_back(x);
+                const int32_t *s1 = row(1, x);
+                t0.insert(t0.end(), s1, s1 + rlen[1][x]);
+                const int32_t *p1 = row(0, x);
+                t0.insert(t0.end(), p1, p1 + rlen[0][x]);
+            }
+            t1.clear();
+            for (int x : t0) {
+                if (gen[x] != gi) continue;  // no bucket exports from x
+                for (int q = ihead[x]; q < (int)iv.size() && iv[q].first == x; q++)
+                    if (iv[q].second != b) t1.push_back(iv[q].second);
+            }
+            std::sort(t1.begin(), t1.end());
+            t1.erase(std::unique(t1.begin(), t1.end()), t1.end());
+            for (int o : t1) arpairs.emplace_back(b, o);
+        }
+        total = (int64_t)arpairs.size();
+    }
+
+    // ---- validity of merging joint nodes u, v (rewrite_candidate_ok)
+    // IN marks (gen == gin) the merged node's in-neighbours; the DFS from its
+    // successors, bounded to positions < max(pos u, pos v), fails on reaching
+    // one.  F collects the visited window.
+    bool acyclic_merge(int u, int v, int32_t gin) {
+        const int P = std::max(pos[u], pos[v]);
+        const int32_t gv = ++gen_no;
+        F.clear();
+        stk.clear();
+        for (int w : {u, v}) {
+            const int32_t *r = row(3, w);
+            for (int i = 0; i < rlen[3][w]; i++) {
+                const int y = r[i];
+                if (y == u || y == v || pos[y] >= P || gen[y] == gv) continue;
+                gen[y] = gv;
+                stk.push_back(y);
+            }
+        }
+        while (!stk.empty()) {
+            const int y = stk.back();
+            stk.pop_back();
+            if (mark[y] == gin) return false;
+            F.push_back(y);
+            const int32_t *r = row(3, y);
+            for (int i = 0; i < rlen[3][y]; i++) {
+                const int z = r[i];
+                if (z == u || z == v || pos[z] >= P || gen[z] == gv) continue;
+                gen[z] = gv;
+                stk.push_back(z);
+            }
+        }
+        return true;
+    }
+    // reorder the window after merging u, v into keep (Pearce-Kelly): the
+    // merged node's ancestors inside the window (Bk), then it, then F
+    void reorder(int u, int v, int keep, int32_t gin) {
+        const int L = std::min(pos[u], pos[v]);
+        const int32_t gb = ++gen_no;
+        Bk.clear();
+        stk.clear();
+        for (int n : t2)  // in-neighbours of the merged node
+            if (pos[n] > L && gen[n] != gb) {
+                gen[n] = gb;
+                stk.push_back(n);
+            }
+        while (!stk.empty()) {
+            const int y = stk.back();
+            stk.pop_back();
+            Bk.push_back(y);
+            const int32_t *r = row(2, y);
+            for (int i = 0; i < rlen[2][y]; i++) {
+                const int z = r[i];
+                if (z == u || z == v || pos[z] <= L || gen[z] == gb) continue;
+                gen[z] = gb;
+                stk.push_back(z);
+            }
+        }
+        (void)gin;
+        auto by_pos = [&](int a, int b) { return pos[a] < pos[b]; };
+        std::sort(Bk.begin(), Bk.end(), by_pos);
+        std::sort(F.begin(), F.end(), by_pos);
+        t3.clear();
+        for (int n : Bk) t3.push_back(pos[n]);
+        for (int n : F) t3.push_back(pos[n]);
+        t3.push_back(pos[u]);
+        t3.push_back(pos[v]);
+        std::sort(t3.begin(), t3.end());
+        int i = 0;
+        for (int n : Bk) pos[n] = t3[i++];
+        pos[keep] = t3[i++];
+        for (int n : F) pos[n] = t3[i++];
+    }
+
+    // in-neighbours of the group merging og and pg (exclusion relative to the
+    // merged member set, graph.py:245-262), marked with a fresh generation; the
+    // list lands in t2
+    int32_t mark_in_groups(int og, int pg) {
+        const int32_t gi = ++gen_no;
+        t2.clear();
+        auto add = [&](int n) {
+            if (mark[n] != gi) {
+                mark[n] = gi;
+                t2.push_back(n);
+            }
+        };
+        for (int x : {og, pg}) {
+            const int32_t *m = mpool.data() + moff[x];
+            for (int i = 0; i < mlen[x]; i++) {
+                const int d = m[i] >> 1;
+                for (int q = g->in_ptr[d]; q < g->in_ptr[d + 1]; q++) {
+                    const int e = g->in_e[q], s = g->e_src[e];
+                    if (g->agg[e]) {
+                        for (int r = g->arp_ptr[s]; r < g->arp_ptr[s + 1]; r++) add(VB + bk[g->arp[r]]);
+                    } else if (!member(s, og) && !member(s, pg)) {
+                        add(exportg(s));
+                    }
+                }
+            }
+        }
+        return gi;
+    }
+
+    // neighbours of nodes (all row kinds), excluding the nodes themselves -> nb
+    void collect_neighbours(std::initializer_list<int> nodes) {
+        const int32_t gg = ++gen_no;
+        nb.clear();
+        for (int n : nodes) gen[n] = gg;
+        for (int n : nodes)
+            for (int k = 0; k < 4; k++) {
+                if (k < 2 && n >= VB) continue;
+                const int32_t *r = row(k, n);
+                for (int i = 0; i < rlen[k][n]; i++)
+                    if (gen[r[i]] != gg) {
+                        gen[r[i]] = gg;
+                        nb.push_back(r[i]);
+                    }
+            }
+    }
+    void refresh(int n) {
+        if (n < VB) {
+            if (alive[n]) rows_group(n);
+        } else if (blen[n - VB]) {
+            rows_bucket(n - VB);
+        }
+    }
+    void kill_group(int x) {
+        alive[x] = 0;
+        mlen[x] = 0;
+        for (int k = 0; k < 4; k++) rlen[k][x] = 0;
+        while (maxid >= 0 && !alive[maxid]) maxid--;
+    }
+    // merge member lists of x and y into a fresh slot for id keep
+    void merge_members(int x, int y, int keep, bool y_normal_only) {
+        t0.clear();
+        const int32_t *a = mpool.data() + moff[x], *b = mpool.data() + moff[y];
+        int i = 0, j = 0;
+        while (i < mlen[x] || j < mlen[y]) {
+            if (j >= mlen[y] || (i < mlen[x] && (a[i] >> 1) < (b[j] >> 1))) t0.push_back(a[i++]);
+            else t0.push_back(y_normal_only ? (b[j++] & ~1) : b[j++]);
+        }
+        moff[keep] = (int32_t)mpool.size();
+        mlen[keep] = (int32_t)t0.size();
+        mpool.insert(mpool.end(), t0.begin(), t0.end());
+    }
+
+    // non-duplicate fusion of pg into og (rewrite.py:64-96); false if rejected
+    bool try_nondup(int og, int pg) {
+        if (og == pg) return false;
+        {
+            const int32_t *m = mpool.data() + moff[pg];
+            for (int i = 0; i < mlen[pg]; i++)
+                if (member(m[i] >> 1, og)) return false;  // groups share a member
+        }
+        if (!cok[og] || !cok[pg]) return false;
+        const int32_t gin = mark_in_groups(og, pg);
+        if (!acyclic_merge(og, pg, gin)) return false;
+        const int keep = std::min(og, pg), dead = std::max(og, pg);
+        reorder(og, pg, keep, gin);
+        collect_neighbours({og, pg});
+        // state: every membership of og / pg moves to keep (duplicated stays duplicated)
+        for (int x : {og, pg}) {
+            const int32_t *m = mpool.data() + moff[x];
+            for (int i = 0; i < mlen[x]; i++) {
+                const int v = m[i] >> 1;
+                if (m[i] & 1) rg[v] = keep; else ng[v] = keep;
+            }
+        }
+        merge_members(og, pg, keep, false);
+        const uint8_t fd = hdup[og] | hdup[pg], ff = far[og] | far[pg], fr = hrep[og] | hrep[pg];
+        kill_group(dead);
+        alive[keep] = 1;
+        cok[keep] = 1;
+        hdup[keep] = fd;
+        far[keep] = ff;
+        hrep[keep] = fr;
+        if (keep > maxid) maxid = keep;
+        rows_group(keep);
+        for (int n : nb) refresh(n);
+        recount(keep);
+        recount(dead);
+        for (int n : nb)
+            if (n < VB) recount(n);
+        return true;
+    }
+    // relabel group ids to 0..G-1 in id order (Engine::compact) and rebuild;
+    // og / pg follow their groups
+    void compact_rebuild(int &og, int &pg) {
+        std::vector<int32_t> rank(VB, -1);
+        int G = 0;
+        for (int x = 0; x < VB; x++)
+            if (alive[x]) rank[x] = G++;
+        State s;
+        s.ng.resize(V);
+        s.rg.resize(V);
+        for (int v = 0; v < V; v++) {
+            s.ng[v] = rank[ng[v]];
+            s.rg[v] = rg[v] >= 0 ? rank[rg[v]] : -1;
+        }
+        s.bk = bk;
+        og = rank[og];
+        pg = rank[pg];
+        const int m = method;
+        build(g, s, VB);
+        if (m >= 0 && m != M_AR) prepare_op_pairs(m);
+        else method = m;
+    }
+
+    // duplicate fusion (rewrite.py:99-153); degrades to nondup without other
+    // consumers.  The replica path needs no acyclicity test (see above).
+    bool try_dup(int og, int pg) {
+        if (og == pg) return false;
+        {
+            const int32_t *m = mpool.data() + moff[pg];
+            for (int i = 0; i < mlen[pg]; i++)
+                if (member(m[i] >> 1, og)) return false;
+        }
+        if (!cok[og] || !cok[pg]) return false;
+        if (hrep[pg]) return false;  // rewrite.py:116-118
+        bool other = far[pg] != 0;
+        {
+            const int32_t *r = row(1, pg);
+            for (int i = 0; i < rlen[1][pg]; i++) other |= r[i] != og;
+        }
+        if (!other) return try_nondup(og, pg);
+        if (maxid + 1 >= VB) compact_rebuild(og, pg);
+        const int R = maxid + 1;  // rewrite.py:138
+        const int keep = std::min(og, pg), dead = std::max(og, pg);
+        const int po = pos[og], pp = pos[pg];
+        collect_neighbours({og, pg});
+        // replica member list first (pg's slot may be reused by keep)
+        {
+            const int32_t *m = mpool.data() + moff[pg];
+            t1.clear();
+            for (int i = 0; i < mlen[pg]; i++) t1.push_back(m[i] | 1);
+            moff[R] = (int32_t)mpool.size();
+            mlen[R] = (int32_t)t1.size();
+            mpool.insert(mpool.end(), t1.begin(), t1.end());
+        }
+        {
+            const int32_t *m = mpool.data() + moff[og];
+            for (int i = 0; i < mlen[og]; i++) {
+                const int v = m[i] >> 1;
+                if (m[i] & 1) rg[v] = keep; else ng[v] = keep;
+            }
+            m = mpool.data() + moff[pg];
+            for (int i = 0; i < mlen[pg]; i++) {
+                const int v = m[i] >> 1;
+                ng[v] = keep;
+                rg[v] = R;
+            }
+        }
+        merge_members(og, pg, keep, true);
+        const uint8_t fd = hdup[og], ff = far[og] | far[pg], fr_p = far[pg];
+        kill_group(dead);
+        alive[keep] = 1;
+        cok[keep] = 1;
+        hdup[keep] = fd;
+        far[keep] = ff;
+        hrep[keep] = 1;
+        alive[R] = 1;
+        cok[R] = 1;
+        hdup[R] = 1;
+        far[R] = fr_p;
+        hrep[R] = 1;
+        maxid = std::max(maxid, R);
+        pos[keep] = po;
+        pos[R] = pp;
+        rows_group(keep);
+        rows_group(R);
+        for (int n : nb) refresh(n);
+        recount(keep);
+        recount(dead);
+        recount(R);
+        for (int n : nb)
+            if (n < VB) recount(n);
+        return true;
+    }
+
+    // AllReduce fusion of buckets bo, bn (rewrite.py:181-209)
+    bool try_ar(int bo, int bn) {
+        const int u = VB + bo, v = VB + bn;
+        const int32_t gi = ++gen_no;
+        t2.clear();
+        for (int w : {u, v}) {
+            const int32_t *r = row(2, w);
+            for (int i = 0; i < rlen[2][w]; i++)
+                if (mark[r[i]] != gi) {
+                    mark[r[i]] = gi;
+                    t2.push_back(r[i]);
+                }
+        }
+        if (!acyclic_merge(u, v, gi)) return false;
+        const int keep = std::min(bo, bn), dead = std::max(bo, bn);
+        reorder(u, v, VB + keep, gi);
+        collect_neighbours({u, v});
+        t0.clear();
+        const int32_t *a = bpool.data() + boff[bo], *b = bpool.data() + boff[bn];
+        int i = 0, j = 0;
+        while (i < blen[bo] || j < blen[bn]) {
+            if (j >= blen[bn] || (i < blen[bo] && a[i] < b[j])) t0.push_back(a[i++]);
+            else t0.push_back(b[j++]);
+        }
+        for (int x : t0) bk[x] = keep;
+        btot[keep] = btot[bo] + btot[bn];
+        btot[dead] = 0;
+        blen[dead] = 0;
+        rlen[2][VB + dead] = rlen[3][VB + dead] = 0;
+        boff[keep] = (int32_t)bpool.size();
+        blen[keep] = (int32_t)t0.size();
+        bpool.insert(bpool.end(), t0.begin(), t0.end());
+        rows_bucket(keep);
+        for (int n : nb) refresh(n);
+        return true;
+    }
+
+    // random_apply (rewrite.py:222-263) on the live state
+    bool random_apply(int m, int n, PyRng &rng) {
+        if (n <= 0) return false;
+        if (m == M_AR) prepare_ar_pairs();
+        else prepare_op_pairs(m);
+        bool applied = false;
+        for (int it = 0; it < n; it++) {
+            if (total == 0) break;
+            const uint32_t k = rng.below((uint32_t)total);
+            bool ok;
+            if (m == M_AR) {
+                const auto pr = arpairs[k];
+                ok = try_ar(pr.first, pr.second);
+                if (ok) prepare_ar_pairs();
+            } else {
+                const auto pr = select(k);
+                ok = m == M_DUP ? try_dup(pr.first, pr.second) : try_nondup(pr.first, pr.second);
+            }
+            applied |= ok;
+        }
+        return applied;
+    }
+
+    void to_state(State &s) const {
+        s.ng = ng;
+        s.rg = rg;
+        s.bk = bk;
+    }
+};
+
+// FO_ENGINE=full selects the full-rebuild Engine path (cross-checking only)
+static bool use_full_engine() {
+    const char *e = getenv("FO_ENGINE");
+    return e && std::strcmp(e, "full") == 0;
+}
+
 }  // namespace fo
 
 using namespace fo;
@@ -553,19 +1264,34 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
     if (!eng.load_state(base_ngid, base_rgid, base_bkt, base)) return fail(FO_INVALID_ARG, "bad base state");
     if (n_threads <= 0) n_threads = omp_get_max_threads();
     const int V = g->V, A = g->A;
+    Inc inc0;
+    const bool full = use_full_engine() || !inc0.build(g, base, eng.VB);
 #pragma omp parallel for num_threads(n_threads) schedule(dynamic, 1)
     for (int k = 0; k < K; k++) {
-        thread_local Scratch sc;
         PyRng rng(seeds[k]);
-        State s = base;
+        if (full) {
+            thread_local Scratch sc;
+            State s = base;
+            for (int m = 0; m < 3; m++) {
+                if (!(methods_mask & (1 << m))) continue;
+                int n = (int)rng.below((uint32_t)beta + 1);
+                eng.random_apply(s, m, n, rng, sc);
+            }
+            std::copy(s.ng.begin(), s.ng.end(), ngid_out + (int64_t)k * V);
+            std::copy(s.rg.begin(), s.rg.end(), rgid_out + (int64_t)k * V);
+            std::copy(s.bk.begin(), s.bk.end(), bkt_out + (int64_t)k * A);
+            continue;
+        }
+        thread_local Inc w;
+        w = inc0;
         for (int m = 0; m < 3; m++) {
             if (!(methods_mask & (1 << m))) continue;
             int n = (int)rng.below((uint32_t)beta + 1);
-            eng.random_apply(s, m, n, rng, sc);
+            w.random_apply(m, n, rng);
         }
-        std::copy(s.ng.begin(), s.ng.end(), ngid_out + (int64_t)k * V);
-        std::copy(s.rg.begin(), s.rg.end(), rgid_out + (int64_t)k * V);
-        std::copy(s.bk.begin(), s.bk.end(), bkt_out + (int64_t)k * A);
+        std::copy(w.ng.begin(), w.ng.end(), ngid_out + (int64_t)k * V);
+        std::copy(w.rg.begin(), w.rg.end(), rgid_out + (int64_t)k * V);
+        std::copy(w.bk.begin(), w.bk.end(), bkt_out + (int64_t)k * A);
     }
     if (gid_bound_out) *gid_bound_out = eng.VB;
     return FO_OK;
@@ -581,8 +1307,15 @@ int fo_random_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int
     PyRng rng(0);
     std::copy(mt_state, mt_state + 624, rng.mt);
     rng.mti = (int)mt_state[624];
-    Scratch sc;
-    bool applied = eng.random_apply(s, method, n, rng, sc);
+    bool applied;
+    Inc w;
+    if (use_full_engine() || !w.build(g, s, eng.VB)) {
+        Scratch sc;
+        applied = eng.random_apply(s, method, n, rng, sc);
+    } else {
+        applied = w.random_apply(method, n, rng);
+        w.to_state(s);
+    }
     std::copy(rng.mt, rng.mt + 624, mt_state);
     mt_state[624] = (uint32_t)rng.mti;
     std::copy(s.ng.begin(), s.ng.end(), ngid);
@@ -782,6 +1515,7 @@ struct fo_search {
         uint64_t h[3];
         int64_t batch_pos[3];
         Scratch sc;
+        Inc inc0, inc;  // incremental index of the popped state / working copy
     };
     // one in-flight device batch: pinned staging, device buffers, results
     struct Lane {
@@ -901,6 +1635,7 @@ static int search_start(fo_search *S) {
 static void search_expand(fo_search *S, int lo, int hi) {
     auto t0 = std::chrono::steady_clock::now();
     const Engine &eng = *S->eng;
+    const bool full = use_full_engine();
     int nthreads = S->cfg.n_threads > 0 ? S->cfg.n_threads : omp_get_max_threads();
 #pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
     for (int r = lo; r < hi; r++) {
@@ -911,12 +1646,26 @@ static void search_expand(fo_search *S, int lo, int hi) {
         sd.cur = sd.queue.top();
         sd.queue.pop();
         sd.steps++;
+        bool built = false, inc_ok = !full;
         for (int m = 0; m < 3; m++) {
             if (!(S->cfg.methods_mask & (1 << m))) continue;
             int n = (int)sd.rng.below((uint32_t)S->cfg.beta + 1);
             int j = sd.ncand++;
-            sd.cand[j] = sd.pool[sd.cur.slot];
-            bool applied = eng.random_apply(sd.cand[j], m, n, sd.rng, sd.sc);
+            const State &H = sd.pool[sd.cur.slot];
+            bool applied = false;
+            if (inc_ok && n > 0 && !built) {  // one index of the popped state serves all methods
+                inc_ok = sd.inc0.build(S->g, H, eng.VB);
+                built = true;
+            }
+            if (inc_ok && n > 0) {
+                sd.inc = sd.inc0;
+                applied = sd.inc.random_apply(m, n, sd.rng);
+                if (applied) sd.inc.to_state(sd.cand[j]);
+                else sd.cand[j] = H;
+            } else {
+                sd.cand[j] = H;
+                applied = eng.random_apply(sd.cand[j], m, n, sd.rng, sd.sc);
+            }
             sd.meth[j] = m;
             sd.h[j] = applied ? eng.hash(sd.cand[j]) : sd.cur.h;
         }

@@ -149,3 +149,22 @@ def test_host_only_handle_refuses_device_work():
     ng, rg, bk, vb = dg.make_candidates([1, 2])
     with pytest.raises(P.DeviceError):
         dg.score_host(ng, rg, bk, vb)
+
+
+@pytest.mark.parametrize("name", SMALL + ["gpt2m"])
+def test_incremental_engine_matches_full_rebuild(name, monkeypatch):
+    """The incremental engine (Inc) draws, accepts and labels exactly like the
+    full-rebuild engine (FO_ENGINE=full), also from deep base states."""
+    g = P.load_workload(name)[0]
+    dg = engine_graph(g)
+    base = None
+    rounds = 3 if name == "gpt2m" else 4
+    for rnd in range(rounds):
+        seeds = np.arange(rnd * 1000, rnd * 1000 + 96, dtype=np.uint64)
+        monkeypatch.delenv("FO_ENGINE", raising=False)
+        a = dg.make_candidates(seeds, 30, 7, base, 4)
+        monkeypatch.setenv("FO_ENGINE", "full")
+        b = dg.make_candidates(seeds, 30, 7, base, 4)
+        for x, y in zip(a[:3], b[:3]):
+            assert np.array_equal(x, y), (name, rnd)
+        base = (a[0][rnd].copy(), a[1][rnd].copy(), a[2][rnd].copy())
