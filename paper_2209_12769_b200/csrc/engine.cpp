@@ -13,6 +13,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cstdlib>
@@ -592,6 +593,56 @@ struct Inc {
     std::vector<int32_t> t0, t1, t2, t3, mark, stk, F, Bk, nb, gen, ihead;
     std::vector<std::pair<int32_t, int32_t>> iv;
     int32_t gen_no = 0;
+    // undo journal: a candidate is applied to a shared index and rolled back
+    // (checkpoint / undo), so per-candidate cost is the rewrites' footprint,
+    // not a copy of the index
+    bool jon = false, rebuilt = false;
+    std::vector<std::pair<int32_t *, int32_t>> j32;
+    std::vector<std::pair<uint8_t *, uint8_t>> j8;
+    std::vector<std::pair<int64_t *, int64_t>> j64;
+    size_t cp_m = 0, cp_r = 0, cp_b = 0;
+    int cp_maxid = -1;
+    int64_t cp_tot[2] = {0, 0};
+    void S(int32_t &r, int32_t v) {
+        if (jon) j32.emplace_back(&r, r);
+        r = v;
+    }
+    void S(uint8_t &r, uint8_t v) {
+        if (jon) j8.emplace_back(&r, r);
+        r = v;
+    }
+    void S(int64_t &r, int64_t v) {
+        if (jon) j64.emplace_back(&r, r);
+        r = v;
+    }
+    void checkpoint() {
+        jon = true;
+        rebuilt = false;
+        j32.clear();
+        j8.clear();
+        j64.clear();
+        cp_m = mpool.size();
+        cp_r = rpool.size();
+        cp_b = bpool.size();
+        cp_maxid = maxid;
+        cp_tot[0] = tot[0];
+        cp_tot[1] = tot[1];
+    }
+    // false when a rebuild (id compaction) happened: the caller recopies the base
+    bool undo() {
+        jon = false;
+        if (rebuilt) return false;
+        for (size_t i = j32.size(); i-- > 0;) *j32[i].first = j32[i].second;
+        for (size_t i = j8.size(); i-- > 0;) *j8[i].first = j8[i].second;
+        for (size_t i = j64.size(); i-- > 0;) *j64[i].first = j64[i].second;
+        mpool.resize(cp_m);
+        rpool.resize(cp_r);
+        bpool.resize(cp_b);
+        maxid = cp_maxid;
+        tot[0] = cp_tot[0];
+        tot[1] = cp_tot[1];
+        return true;
+    }
 
     const int32_t *row(int k, int n) const { return rpool.data() + roff[k][n]; }
     int rowlen(int k, int n) const { return rlen[k][n]; }
@@ -601,13 +652,13 @@ struct Inc {
     void store(int k, int n, std::vector<int32_t> &t) {
         std::sort(t.begin(), t.end());
         t.erase(std::unique(t.begin(), t.end()), t.end());
-        if ((int)t.size() <= rlen[k][n]) {  // shrinking rows rewrite in place
+        if (!jon && (int)t.size() <= rlen[k][n]) {  // shrinking rows rewrite in place
             std::copy(t.begin(), t.end(), rpool.begin() + roff[k][n]);
         } else {
-            roff[k][n] = (int32_t)rpool.size();
+            S(roff[k][n], (int32_t)rpool.size());
             rpool.insert(rpool.end(), t.begin(), t.end());
         }
-        rlen[k][n] = (int32_t)t.size();
+        S(rlen[k][n], (int32_t)t.size());
     }
 
     // the four rows of group x from its member ops' edges
@@ -796,7 +847,7 @@ struct Inc {
         }
     }
     void fen_add(int r, int x, int d) {
-        for (int i = x + 1; i <= VB; i += i & -i) fen[r][i] += d;
+        for (int i = x + 1; i <= VB; i += i & -i) S(fen[r][i], fen[r][i] + d);
         tot[r] += d;
     }
     void recount(int x) {
@@ -805,7 +856,7 @@ struct Inc {
         for (int r = 0; r < 2; r++)
             if (c[r] != cnt[r][x]) {
                 fen_add(r, x, c[r] - cnt[r][x]);
-                cnt[r][x] = c[r];
+                S(cnt[r][x], c[r]);
             }
         if (method == M_NONDUP || method == M_DUP) total = tot[method == M_DUP];
     }
@@ -966,9 +1017,9 @@ struct Inc {
         t3.push_back(pos[v]);
         std::sort(t3.begin(), t3.end());
         int i = 0;
-        for (int n : Bk) pos[n] = t3[i++];
-        pos[keep] = t3[i++];
-        for (int n : F) pos[n] = t3[i++];
+        for (int n : Bk) S(pos[n], t3[i++]);
+        S(pos[keep], t3[i++]);
+        for (int n : F) S(pos[n], t3[i++]);
     }
 
     // in-neighbours of the group merging og and pg (exclusion relative to the
@@ -1024,9 +1075,9 @@ struct Inc {
         }
     }
     void kill_group(int x) {
-        alive[x] = 0;
-        mlen[x] = 0;
-        for (int k = 0; k < 4; k++) rlen[k][x] = 0;
+        S(alive[x], 0);
+        S(mlen[x], 0);
+        for (int k = 0; k < 4; k++) S(rlen[k][x], 0);
         while (maxid >= 0 && !alive[maxid]) maxid--;
     }
     // merge member lists of x and y into a fresh slot for id keep
@@ -1038,8 +1089,8 @@ struct Inc {
             if (j >= mlen[y] || (i < mlen[x] && (a[i] >> 1) < (b[j] >> 1))) t0.push_back(a[i++]);
             else t0.push_back(y_normal_only ? (b[j++] & ~1) : b[j++]);
         }
-        moff[keep] = (int32_t)mpool.size();
-        mlen[keep] = (int32_t)t0.size();
+        S(moff[keep], (int32_t)mpool.size());
+        S(mlen[keep], (int32_t)t0.size());
         mpool.insert(mpool.end(), t0.begin(), t0.end());
     }
 
@@ -1062,17 +1113,17 @@ struct Inc {
             const int32_t *m = mpool.data() + moff[x];
             for (int i = 0; i < mlen[x]; i++) {
                 const int v = m[i] >> 1;
-                if (m[i] & 1) rg[v] = keep; else ng[v] = keep;
+                if (m[i] & 1) S(rg[v], keep); else S(ng[v], keep);
             }
         }
         merge_members(og, pg, keep, false);
         const uint8_t fd = hdup[og] | hdup[pg], ff = far[og] | far[pg], fr = hrep[og] | hrep[pg];
         kill_group(dead);
-        alive[keep] = 1;
-        cok[keep] = 1;
-        hdup[keep] = fd;
-        far[keep] = ff;
-        hrep[keep] = fr;
+        S(alive[keep], 1);
+        S(cok[keep], 1);
+        S(hdup[keep], fd);
+        S(far[keep], ff);
+        S(hrep[keep], fr);
         if (keep > maxid) maxid = keep;
         rows_group(keep);
         for (int n : nb) refresh(n);
@@ -1100,7 +1151,10 @@ struct Inc {
         og = rank[og];
         pg = rank[pg];
         const int m = method;
+        const bool j = jon;
         build(g, s, VB);
+        jon = j;
+        rebuilt = true;
         if (m >= 0 && m != M_AR) prepare_op_pairs(m);
         else method = m;
     }
@@ -1132,39 +1186,39 @@ struct Inc {
             const int32_t *m = mpool.data() + moff[pg];
             t1.clear();
             for (int i = 0; i < mlen[pg]; i++) t1.push_back(m[i] | 1);
-            moff[R] = (int32_t)mpool.size();
-            mlen[R] = (int32_t)t1.size();
+            S(moff[R], (int32_t)mpool.size());
+            S(mlen[R], (int32_t)t1.size());
             mpool.insert(mpool.end(), t1.begin(), t1.end());
         }
         {
             const int32_t *m = mpool.data() + moff[og];
             for (int i = 0; i < mlen[og]; i++) {
                 const int v = m[i] >> 1;
-                if (m[i] & 1) rg[v] = keep; else ng[v] = keep;
+                if (m[i] & 1) S(rg[v], keep); else S(ng[v], keep);
             }
             m = mpool.data() + moff[pg];
             for (int i = 0; i < mlen[pg]; i++) {
                 const int v = m[i] >> 1;
-                ng[v] = keep;
-                rg[v] = R;
+                S(ng[v], keep);
+                S(rg[v], R);
             }
         }
         merge_members(og, pg, keep, true);
         const uint8_t fd = hdup[og], ff = far[og] | far[pg], fr_p = far[pg];
         kill_group(dead);
-        alive[keep] = 1;
-        cok[keep] = 1;
-        hdup[keep] = fd;
-        far[keep] = ff;
-        hrep[keep] = 1;
-        alive[R] = 1;
-        cok[R] = 1;
-        hdup[R] = 1;
-        far[R] = fr_p;
-        hrep[R] = 1;
+        S(alive[keep], 1);
+        S(cok[keep], 1);
+        S(hdup[keep], fd);
+        S(far[keep], ff);
+        S(hrep[keep], 1);
+        S(alive[R], 1);
+        S(cok[R], 1);
+        S(hdup[R], 1);
+        S(far[R], fr_p);
+        S(hrep[R], 1);
         maxid = std::max(maxid, R);
-        pos[keep] = po;
-        pos[R] = pp;
+        S(pos[keep], po);
+        S(pos[R], pp);
         rows_group(keep);
         rows_group(R);
         for (int n : nb) refresh(n);
@@ -1200,13 +1254,15 @@ struct Inc {
             if (j >= blen[bn] || (i < blen[bo] && a[i] < b[j])) t0.push_back(a[i++]);
             else t0.push_back(b[j++]);
         }
-        for (int x : t0) bk[x] = keep;
-        btot[keep] = btot[bo] + btot[bn];
-        btot[dead] = 0;
-        blen[dead] = 0;
-        rlen[2][VB + dead] = rlen[3][VB + dead] = 0;
-        boff[keep] = (int32_t)bpool.size();
-        blen[keep] = (int32_t)t0.size();
+        for (int x : t0) S(bk[x], keep);
+        const int64_t bt = btot[bo] + btot[bn];
+        S(btot[dead], 0);
+        S(btot[keep], bt);
+        S(blen[dead], 0);
+        S(rlen[2][VB + dead], 0);
+        S(rlen[3][VB + dead], 0);
+        S(boff[keep], (int32_t)bpool.size());
+        S(blen[keep], (int32_t)t0.size());
         bpool.insert(bpool.end(), t0.begin(), t0.end());
         rows_bucket(keep);
         for (int n : nb) refresh(n);
@@ -1266,6 +1322,8 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
     const int V = g->V, A = g->A;
     Inc inc0;
     const bool full = use_full_engine() || !inc0.build(g, base, eng.VB);
+    static std::atomic<uint64_t> calls{0};
+    const uint64_t epoch = ++calls;
 #pragma omp parallel for num_threads(n_threads) schedule(dynamic, 1)
     for (int k = 0; k < K; k++) {
         PyRng rng(seeds[k]);
@@ -1282,8 +1340,14 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
             std::copy(s.bk.begin(), s.bk.end(), bkt_out + (int64_t)k * A);
             continue;
         }
+        // one copy of the base index per thread and call; candidates roll back
         thread_local Inc w;
-        w = inc0;
+        thread_local uint64_t w_epoch = 0;
+        if (w_epoch != epoch) {
+            w = inc0;
+            w_epoch = epoch;
+        }
+        w.checkpoint();
         for (int m = 0; m < 3; m++) {
             if (!(methods_mask & (1 << m))) continue;
             int n = (int)rng.below((uint32_t)beta + 1);
@@ -1292,6 +1356,7 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
         std::copy(w.ng.begin(), w.ng.end(), ngid_out + (int64_t)k * V);
         std::copy(w.rg.begin(), w.rg.end(), rgid_out + (int64_t)k * V);
         std::copy(w.bk.begin(), w.bk.end(), bkt_out + (int64_t)k * A);
+        if (!w.undo()) w = inc0;
     }
     if (gid_bound_out) *gid_bound_out = eng.VB;
     return FO_OK;
@@ -1515,7 +1580,7 @@ struct fo_search {
         uint64_t h[3];
         int64_t batch_pos[3];
         Scratch sc;
-        Inc inc0, inc;  // incremental index of the popped state / working copy
+        Inc inc0;  // incremental index of the popped state (methods roll back)
     };
     // one in-flight device batch: pinned staging, device buffers, results
     struct Lane {
@@ -1658,10 +1723,11 @@ static void search_expand(fo_search *S, int lo, int hi) {
                 built = true;
             }
             if (inc_ok && n > 0) {
-                sd.inc = sd.inc0;
-                applied = sd.inc.random_apply(m, n, sd.rng);
-                if (applied) sd.inc.to_state(sd.cand[j]);
+                sd.inc0.checkpoint();
+                applied = sd.inc0.random_apply(m, n, sd.rng);
+                if (applied) sd.inc0.to_state(sd.cand[j]);
                 else sd.cand[j] = H;
+                if (!sd.inc0.undo()) sd.inc0.build(S->g, H, eng.VB);
             } else {
                 sd.cand[j] = H;
                 applied = eng.random_apply(sd.cand[j], m, n, sd.rng, sd.sc);
