@@ -664,51 +664,66 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
                                           const uint32_t *__restrict__ succ, Ent16 *__restrict__ rg,
                                           Ent16 *__restrict__ rb, int G, int N, int hg, int hb) {
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
-    int run0 = -1, run1 = -1, done = 0;
+    int done = 0;
+    bool run0 = false, run1 = false;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
-    double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
+    double end0 = 0.0, end1 = 0.0, now = 0.0, mk = 0.0;
     uint32_t level = 0;
-    for (;;) {
-        if (run0 < 0 && headg < tailg) {  // start_available (simulator.py:98-115)
-            Ent16 x = rg[(headg++) & (kRing - 1)];
-            run0 = 1;
+    // finish_node (simulator.py:88-96); false on ring overflow
+    auto release = [&](unsigned qb, unsigned qe) -> bool {
+        for (unsigned q = qb; q < qe; q++) {
+            const uint32_t e = succ[q];
+            const unsigned s = e & 0xffffu;
+            const int d = indeg[s] - 1;
+            Ent16 x;  // release-time loads issued with the indegree load
+            x.dur = dur[s];
+            x.sb = sptr[s];
+            x.se = sptr[s + 1];
+            indeg[s] = (uint16_t)d;
+            if (d == 0) {
+                x.key = level | (e >> 16);
+                if (!((int)s < G ? ring_push(rg, headg, tailg, x) : ring_push(rb, headb, tailb, x))) return false;
+            }
+        }
+        return true;
+    };
+    // start_available (simulator.py:98-115): compute lane, then comm lane
+    auto start = [&]() {
+        if (!run0 && headg < tailg) {
+            const Ent16 x = rg[(headg++) & (kRing - 1)];
+            run0 = true;
             end0 = __dadd_rn(now, x.dur);
             sb0 = x.sb;
             se0 = x.se;
-            if (end0 > mk) mk = end0;
+            mk = end0 > mk ? end0 : mk;
         }
-        if (run1 < 0 && headb < tailb) {
-            Ent16 x = rb[(headb++) & (kRing - 1)];
-            run1 = 1;
+        if (!run1 && headb < tailb) {
+            const Ent16 x = rb[(headb++) & (kRing - 1)];
+            run1 = true;
             end1 = __dadd_rn(now, x.dur);
             sb1 = x.sb;
             se1 = x.se;
-            if (end1 > mk) mk = end1;
+            mk = end1 > mk ? end1 : mk;
         }
-        if (run0 < 0 && run1 < 0) break;
-        now = run0 < 0 ? end1 : (run1 < 0 ? end0 : (end0 < end1 ? end0 : end1));
-        if (now > last) { last = now; level += 0x10000u; }
-#pragma unroll
-        for (int t = 0; t < 2; t++) {
-            if ((t == 0 ? run0 : run1) < 0 || (t == 0 ? end0 : end1) != now) continue;
-            const unsigned qb = t == 0 ? sb0 : sb1, qe = t == 0 ? se0 : se1;
-            if (t == 0) run0 = -1; else run1 = -1;
+    };
+    start();
+    while (run0 || run1) {
+        // next completion; every lane ending then drains before any start
+        const bool c0 = run0 && (!run1 || end0 <= end1);
+        const bool c1 = run1 && (!run0 || end1 <= end0);
+        const double t = c0 ? end0 : end1;
+        if (t > now) { now = t; level += 0x10000u; }
+        if (c0) {
+            run0 = false;
             done++;
-            for (unsigned q = qb; q < qe; q++) {  // finish_node (simulator.py:88-96)
-                const uint32_t e = succ[q];
-                const unsigned s = e & 0xffffu;
-                const int d = indeg[s] - 1;
-                Ent16 x;
-                x.dur = dur[s];
-                x.sb = sptr[s];
-                x.se = sptr[s + 1];
-                indeg[s] = (uint16_t)d;
-                if (d == 0) {
-                    x.key = level | (e >> 16);
-                    if (!((int)s < G ? ring_push(rg, headg, tailg, x) : ring_push(rb, headb, tailb, x))) return false;
-                }
-            }
+            if (!release(sb0, se0)) return false;
         }
+        if (c1) {
+            run1 = false;
+            done++;
+            if (!release(sb1, se1)) return false;
+        }
+        start();
     }
     a.cost_out[k] = done == N ? mk : 0.0;
     a.status_out[k] = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
