@@ -162,6 +162,29 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
                        const uint64_t *seeds, int32_t K, int32_t beta, int32_t methods_mask, int32_t n_threads,
                        int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *gid_bound_out);
 
+/* Sparse (delta) candidates.  A candidate of a search or batch usually
+ * differs from its parent in a handful of entries (13 of 1,505 at ResNet-50,
+ * 10 of 101,000 at 50k ops), so the parent state stays resident on the
+ * device and each candidate travels as (index, value) int32 pairs over the
+ * concatenated ngid[V] | rgid[V] | bkt[A] index space.
+ *   fo_set_parent         parent state (host arrays, any ids; ranked like the
+ *                         engine's base state; NULL = unfused default)
+ *   fo_make_candidates_delta   fo_make_candidates' batch as changes against
+ *                         the same base: offsets_out[K+1], changes_out[2 * n]
+ *                         (capacity cap_pairs pairs; offsets_out[K] = n even
+ *                         when the capacity is too small -> FO_INVALID_ARG)
+ *   fo_score_delta        device offsets / changes / outputs, async on stream
+ *   fo_score_delta_host   host (pinned) buffers, synchronous
+ * Indices within one candidate must be distinct. */
+int fo_set_parent(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt);
+int fo_make_candidates_delta(fo_graph *g, const int32_t *base_ngid, const int32_t *base_rgid, const int32_t *base_bkt,
+                             const uint64_t *seeds, int32_t K, int32_t beta, int32_t methods_mask, int32_t n_threads,
+                             int32_t *offsets_out, int32_t *changes_out, int64_t cap_pairs);
+int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
+                   double *cost_out, int32_t *status_out, void *stream);
+int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
+                        double *cost_out, int32_t *status_out);
+
 /* random_apply (rewrite.py:222-263) on one state in place, driven by a
  * CPython random.Random state: mt_state = getstate()[1] (624 words + index). */
 int fo_random_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int32_t method, int32_t n,

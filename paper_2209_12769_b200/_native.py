@@ -70,6 +70,11 @@ SIGNATURES = [
     ("fo_expand_all", C.c_int, [vp, vp, vp, vp, C.c_int32, vp, vp, vp, P(C.c_int32)]),
     ("fo_state_hash", C.c_int, [vp, vp, vp, vp, C.c_int32, vp]),
     ("fo_greedy_postorder", C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    ("fo_set_parent", C.c_int, [vp, vp, vp, vp]),
+    ("fo_make_candidates_delta", C.c_int, [vp, vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp,
+                                           C.c_int64]),
+    ("fo_score_delta", C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp]),
+    ("fo_score_delta_host", C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp, vp]),
     ("fo_threshold_ar", C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, vp, vp]),
     ("fo_search_create", C.c_int, [vp, P(SearchCfg), vp, C.c_int32, vp, vp, vp, P(vp)]),
     ("fo_search_round", C.c_int, [vp, P(C.c_int32), vp]),

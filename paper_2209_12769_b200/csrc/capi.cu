@@ -48,7 +48,8 @@ int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int 
 
 static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
-                  double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream) {
+                  double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream,
+                  const DeltaIn *delta = nullptr) {
     ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
     const int nws = score_team_warps(geo);
     WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, kMpCapDefault, nws);
@@ -62,7 +63,7 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
     int st = ensure_workspace(g, VB, slots, &L, false, nws);
     if (st) return st;
     cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws, L, geo, cost, status, ext_dur, tl,
-                                 dur_out, bad_out, ngroups_out, stream);
+                                 dur_out, bad_out, ngroups_out, stream, 0, delta);
     g_launches++;
     if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score kernel launch: ") + cudaGetErrorString(e));
     if (g->V > kMpCapDefault) {
@@ -78,7 +79,7 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
         st = ensure_workspace(g, VB, gb.grid * score_warps_per_block(), &Lb, true, 1);
         if (st) return st;
         e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws_big, Lb, gb, cost, status, ext_dur, tl,
-                         dur_out, bad_out, ngroups_out, stream, 1);
+                         dur_out, bad_out, ngroups_out, stream, 1, delta);
         g_launches++;
         if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score retry launch: ") + cudaGetErrorString(e));
     }
@@ -96,6 +97,23 @@ int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bk
     TimelineOut tl{};
     return launch(g, ngid, rgid, bkt, idx16, K, VB, precision, cost, status, nullptr, tl, nullptr, nullptr, nullptr,
                   stream);
+}
+
+// sparse candidates against the resident parent (fo_set_parent)
+int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int K, int precision, double *cost,
+                       int32_t *status, cudaStream_t stream) {
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set (fo_graph_set_cost_model)");
+    if (!g->d_parent) return fail(FO_INVALID_ARG, "no parent state set (fo_set_parent)");
+    if (K <= 0) return FO_OK;
+    CUDA_TRY(cudaSetDevice(g->device));
+    TimelineOut tl{};
+    DeltaIn d;
+    d.base = g->d_parent;
+    d.off = off;
+    d.chg = chg;
+    return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
+                  nullptr, nullptr, stream, &d);
 }
 
 }  // namespace fo
@@ -219,6 +237,7 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_ws_big) cudaFree(g->d_ws_big);
     if (g->d_memo) cudaFree(g->d_memo);
     if (g->d_io) cudaFree(g->d_io);
+    if (g->d_parent) cudaFree(g->d_parent);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
@@ -427,6 +446,37 @@ int fo_score_host(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
 int fo_score_host_i16(fo_graph *g, const int16_t *ngid, const int16_t *rgid, const int16_t *bkt, int32_t K,
                       int32_t gid_bound, int32_t precision, double *cost_out, int32_t *status_out) {
     return score_host_impl(g, ngid, rgid, bkt, 2, K, gid_bound, precision, cost_out, status_out);
+}
+
+int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
+                   double *cost_out, int32_t *status_out, void *stream) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    return score_delta_device(g, offsets, changes, K, precision, cost_out, status_out, (cudaStream_t)stream);
+}
+
+int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
+                        double *cost_out, int32_t *status_out) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (K <= 0) return FO_OK;
+    if (!offsets || offsets[0] != 0 || offsets[K] < 0) return fail(FO_INVALID_ARG, "bad offsets");
+    CUDA_TRY(cudaSetDevice(g->device));
+    const size_t nc = (size_t)offsets[K];
+    size_t o_c = al256(4 * ((size_t)K + 1)), o_cost = o_c + al256(8 * nc + 8), o_s = o_cost + al256((size_t)K * 8);
+    int st = ensure_io(g, o_s + al256((size_t)K * 4));
+    if (st) return st;
+    char *b = (char *)g->d_io;
+    cudaStream_t s = g->stream;
+    CUDA_TRY(cudaMemcpyAsync(b, offsets, 4 * ((size_t)K + 1), cudaMemcpyHostToDevice, s));
+    if (nc) CUDA_TRY(cudaMemcpyAsync(b + o_c, changes, 8 * nc, cudaMemcpyHostToDevice, s));
+    st = score_delta_device(g, (const int32_t *)b, (const int32_t *)(b + o_c), K, precision, (double *)(b + o_cost),
+                            (int32_t *)(b + o_s), s);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpyAsync(cost_out, b + o_cost, (size_t)K * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(status_out, b + o_s, (size_t)K * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return FO_OK;
 }
 
 // single candidate through device temporaries (simulate / timeline / durations)

@@ -1311,15 +1311,14 @@ using namespace fo;
 
 extern "C" {
 
-int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *base_rgid, const int32_t *base_bkt,
-                       const uint64_t *seeds, int32_t K, int32_t beta, int32_t methods_mask, int32_t n_threads,
-                       int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *gid_bound_out) {
-    if (!g || !seeds || K < 0 || beta < 0) return fail(FO_INVALID_ARG, "bad arguments");
-    Engine eng(g);
-    State base;
-    if (!eng.load_state(base_ngid, base_rgid, base_bkt, base)) return fail(FO_INVALID_ARG, "bad base state");
+extern "C++" {
+// Candidate k: random.Random(seeds[k]) then, per enabled method, n =
+// randint(0, beta) accumulating random_apply steps from the base state;
+// emit(k, state) runs on the generating thread.
+template <typename Emit>
+static int generate(fo_graph *g, const State &base, const Engine &eng, const uint64_t *seeds, int32_t K, int32_t beta,
+                    int32_t methods_mask, int32_t n_threads, Emit emit) {
     if (n_threads <= 0) n_threads = omp_get_max_threads();
-    const int V = g->V, A = g->A;
     Inc inc0;
     const bool full = use_full_engine() || !inc0.build(g, base, eng.VB);
     static std::atomic<uint64_t> calls{0};
@@ -1335,9 +1334,7 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
                 int n = (int)rng.below((uint32_t)beta + 1);
                 eng.random_apply(s, m, n, rng, sc);
             }
-            std::copy(s.ng.begin(), s.ng.end(), ngid_out + (int64_t)k * V);
-            std::copy(s.rg.begin(), s.rg.end(), rgid_out + (int64_t)k * V);
-            std::copy(s.bk.begin(), s.bk.end(), bkt_out + (int64_t)k * A);
+            emit(k, s.ng.data(), s.rg.data(), s.bk.data());
             continue;
         }
         // one copy of the base index per thread and call; candidates roll back
@@ -1353,12 +1350,84 @@ int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *bas
             int n = (int)rng.below((uint32_t)beta + 1);
             w.random_apply(m, n, rng);
         }
-        std::copy(w.ng.begin(), w.ng.end(), ngid_out + (int64_t)k * V);
-        std::copy(w.rg.begin(), w.rg.end(), rgid_out + (int64_t)k * V);
-        std::copy(w.bk.begin(), w.bk.end(), bkt_out + (int64_t)k * A);
+        emit(k, w.ng.data(), w.rg.data(), w.bk.data());
         if (!w.undo()) w = inc0;
     }
+    return FO_OK;
+}
+}  // extern "C++"
+
+int fo_make_candidates(fo_graph *g, const int32_t *base_ngid, const int32_t *base_rgid, const int32_t *base_bkt,
+                       const uint64_t *seeds, int32_t K, int32_t beta, int32_t methods_mask, int32_t n_threads,
+                       int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *gid_bound_out) {
+    if (!g || !seeds || K < 0 || beta < 0) return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State base;
+    if (!eng.load_state(base_ngid, base_rgid, base_bkt, base)) return fail(FO_INVALID_ARG, "bad base state");
+    const int V = g->V, A = g->A;
+    generate(g, base, eng, seeds, K, beta, methods_mask, n_threads,
+             [&](int k, const int32_t *ng, const int32_t *rg, const int32_t *bk) {
+                 std::copy(ng, ng + V, ngid_out + (int64_t)k * V);
+                 std::copy(rg, rg + V, rgid_out + (int64_t)k * V);
+                 std::copy(bk, bk + A, bkt_out + (int64_t)k * A);
+             });
     if (gid_bound_out) *gid_bound_out = eng.VB;
+    return FO_OK;
+}
+
+// Sparse form: changes of each candidate against the (id-ranked) base state as
+// (index, value) pairs over ngid | rgid | bkt -- the fo_score_delta input.
+int fo_make_candidates_delta(fo_graph *g, const int32_t *base_ngid, const int32_t *base_rgid, const int32_t *base_bkt,
+                             const uint64_t *seeds, int32_t K, int32_t beta, int32_t methods_mask, int32_t n_threads,
+                             int32_t *offsets_out, int32_t *changes_out, int64_t cap_pairs) {
+    if (!g || !seeds || K < 0 || beta < 0 || !offsets_out) return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State base;
+    if (!eng.load_state(base_ngid, base_rgid, base_bkt, base)) return fail(FO_INVALID_ARG, "bad base state");
+    const int V = g->V, A = g->A;
+    std::vector<std::vector<int32_t>> per(K);
+    generate(g, base, eng, seeds, K, beta, methods_mask, n_threads,
+             [&](int k, const int32_t *ng, const int32_t *rg, const int32_t *bk) {
+                 auto &d = per[k];
+                 d.clear();
+                 for (int v = 0; v < V; v++)
+                     if (ng[v] != base.ng[v]) { d.push_back(v); d.push_back(ng[v]); }
+                 for (int v = 0; v < V; v++)
+                     if (rg[v] != base.rg[v]) { d.push_back(V + v); d.push_back(rg[v]); }
+                 for (int a = 0; a < A; a++)
+                     if (bk[a] != base.bk[a]) { d.push_back(2 * V + a); d.push_back(bk[a]); }
+             });
+    int64_t n = 0;
+    offsets_out[0] = 0;
+    for (int k = 0; k < K; k++) {
+        n += (int64_t)per[k].size() / 2;
+        if (n > INT32_MAX) return fail(FO_INVALID_ARG, "too many changes");
+        offsets_out[k + 1] = (int32_t)n;
+    }
+    if (n > cap_pairs || (n > 0 && !changes_out)) return fail(FO_INVALID_ARG, "changes capacity too small");
+    for (int k = 0; k < K; k++) std::copy(per[k].begin(), per[k].end(), changes_out + 2 * (int64_t)offsets_out[k]);
+    return FO_OK;
+}
+
+// Resident parent of sparse candidates: ids ranked like the engine's base state.
+int fo_set_parent(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    Engine eng(g);
+    State s;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad parent state");
+    const int V = g->V, A = g->A;
+    g->h_parent.resize(2 * (size_t)V + A);
+    std::copy(s.ng.begin(), s.ng.end(), g->h_parent.begin());
+    std::copy(s.rg.begin(), s.rg.end(), g->h_parent.begin() + V);
+    std::copy(s.bk.begin(), s.bk.end(), g->h_parent.begin() + 2 * V);
+    if (g->device < 0) return FO_OK;
+    if (cudaSetDevice(g->device) != cudaSuccess) return fail(FO_CUDA_ERROR, "cudaSetDevice");
+    if (!g->d_parent && cudaMalloc(&g->d_parent, 4 * g->h_parent.size() + 4) != cudaSuccess)
+        return fail(FO_CUDA_ERROR, "parent alloc");
+    if (cudaMemcpyAsync(g->d_parent, g->h_parent.data(), 4 * g->h_parent.size(), cudaMemcpyHostToDevice, g->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(g->stream) != cudaSuccess)
+        return fail(FO_CUDA_ERROR, "parent upload");
     return FO_OK;
 }
 

@@ -101,13 +101,19 @@ struct ScoreGeo {
     int team;  // 1: one 128-thread block per candidate (latency mode)
 };
 ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision);
+// Sparse candidates: a resident parent state (ngid[V] | rgid[V] | bkt[A],
+// int32) and, per candidate k, changes [off[k], off[k+1]) of (index, value)
+// pairs over that concatenated index space.
+struct DeltaIn {
+    const int32_t *base = nullptr, *off = nullptr, *chg = nullptr;
+};
 // Kernel launch (score.cu).  ext_dur / tl / dur_out / bad_out are optional and
 // only used with K == 1.
 cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K,
                          int VB, int precision, char *ws, const WsLayout &L, const ScoreGeo &geo,
                          double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
                          double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream,
-                         int retry_only = 0);
+                         int retry_only = 0, const DeltaIn *delta = nullptr);
 int score_warps_per_block();
 int score_slots(const ScoreGeo &geo);       // workspace slots a launch uses
 int score_team_warps(const ScoreGeo &geo);  // warps per candidate
@@ -140,6 +146,9 @@ struct fo_graph {
     size_t ws_big_bytes = 0;
     // host API staging
     void *d_io = nullptr;
+    // resident parent of sparse (delta) candidates, engine ids
+    int32_t *d_parent = nullptr;
+    std::vector<int32_t> h_parent;
     size_t io_bytes = 0;
     void *h_pinned = nullptr;
     size_t pinned_bytes = 0;

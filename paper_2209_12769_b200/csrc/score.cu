@@ -495,6 +495,7 @@ __device__ __forceinline__ GroupScratch group_scratch(const Ws &w, int wid) {
 struct ScoreArgs {
     DGraph g;
     const void *ngid, *rgid, *bkt;  // int32, or int16 when idx16
+    const int32_t *dbase, *doff, *dchg;  // sparse candidates (DeltaIn) when dbase != nullptr
     int idx16;
     int retry_only;  // second pass: only candidates a first pass flagged kRetryLarge
     int K, VB;
@@ -1176,21 +1177,56 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
     for (int i = tid; i < A; i += TEAM) w.bmap()[i] = 0;
     tsync<TEAM>();
     bool bad = false;
-    #pragma unroll 4
-    for (int v = tid; v < V; v += TEAM) {
-        int x = ldid(a.ngid, ob + v), y = ldid(a.rgid, ob + v);
-        if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
-        w.gmap()[x] = 1;
-        if (y >= 0) w.gmap()[y] = 1;
-        w.nn()[v] = x;
-        w.rr()[v] = y;
-    }
-    #pragma unroll 4
-    for (int i = tid; i < A; i += TEAM) {
-        int x = ldid(a.bkt, oa + i);
-        if (x < 0 || x >= A) { bad = true; continue; }
-        w.bmap()[x] = 1;
-        w.bki()[i] = x;
+    if (a.dbase) {
+        // sparse candidate: the resident parent (read by every candidate of the
+        // batch, so it is served from L2) with this candidate's changes applied
+        const int32_t *pb = a.dbase;
+        #pragma unroll 4
+        for (int v = tid; v < V; v += TEAM) {
+            w.nn()[v] = pb[v];
+            w.rr()[v] = pb[V + v];
+        }
+        #pragma unroll 4
+        for (int i = tid; i < A; i += TEAM) w.bki()[i] = pb[2 * V + i];
+        tsync<TEAM>();
+        for (int c = a.doff[k] + tid; c < a.doff[k + 1]; c += TEAM) {
+            const int idx = a.dchg[2 * c], val = a.dchg[2 * c + 1];
+            if (idx < 0 || idx >= 2 * V + A) { bad = true; continue; }
+            if (idx < V) w.nn()[idx] = val;
+            else if (idx < 2 * V) w.rr()[idx - V] = val;
+            else w.bki()[idx - 2 * V] = val;
+        }
+        tsync<TEAM>();
+        #pragma unroll 4
+        for (int v = tid; v < V; v += TEAM) {
+            const int x = w.nn()[v], y = w.rr()[v];
+            if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
+            w.gmap()[x] = 1;
+            if (y >= 0) w.gmap()[y] = 1;
+        }
+        #pragma unroll 4
+        for (int i = tid; i < A; i += TEAM) {
+            const int x = w.bki()[i];
+            if (x < 0 || x >= A) { bad = true; continue; }
+            w.bmap()[x] = 1;
+        }
+    } else {
+        #pragma unroll 4
+        for (int v = tid; v < V; v += TEAM) {
+            int x = ldid(a.ngid, ob + v), y = ldid(a.rgid, ob + v);
+            if (x < 0 || x >= VB || y < -1 || y >= VB || x == y) { bad = true; continue; }
+            w.gmap()[x] = 1;
+            if (y >= 0) w.gmap()[y] = 1;
+            w.nn()[v] = x;
+            w.rr()[v] = y;
+        }
+        #pragma unroll 4
+        for (int i = tid; i < A; i += TEAM) {
+            int x = ldid(a.bkt, oa + i);
+            if (x < 0 || x >= A) { bad = true; continue; }
+            w.bmap()[x] = 1;
+            w.bki()[i] = x;
+        }
     }
     if (tany<TEAM>(bad)) {
         if (tid == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_INVALID_ARG; }
@@ -1594,9 +1630,13 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
 cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K,
                          int VB, int precision, char *ws, const WsLayout &L, const ScoreGeo &geo,
                          double *cost_out, int32_t *status_out, const double *ext_dur, TimelineOut tl,
-                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream, int retry_only) {
+                         double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream, int retry_only,
+                         const DeltaIn *delta) {
     ScoreArgs a;
     a.retry_only = retry_only;
+    a.dbase = delta ? delta->base : nullptr;
+    a.doff = delta ? delta->off : nullptr;
+    a.dchg = delta ? delta->chg : nullptr;
     a.g = g;
     a.ngid = ngid;
     a.rgid = rgid;

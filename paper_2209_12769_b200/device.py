@@ -168,6 +168,54 @@ class DeviceGraph:
         _raise(st, "fo_make_candidates", N.last_error())
         return ng, rg, bk, vb.value
 
+    # -- sparse (delta) candidates against a resident parent -----------------------
+    def set_parent(self, ng=None, rg=None, bk=None):
+        """Make (ng, rg, bk) -- any ids; None = unfused default -- the resident
+        parent of sparse candidates (fo_set_parent)."""
+        b0 = (None, None, None) if ng is None else tuple(np.ascontiguousarray(x, np.int32) for x in (ng, rg, bk))
+        st = N.lib().fo_set_parent(self.h, N.ptr(b0[0]), N.ptr(b0[1]), N.ptr(b0[2]))
+        _raise(st, "fo_set_parent", N.last_error())
+
+    def make_candidates_delta(self, seeds, beta=10, methods_mask=7, base=None, n_threads=0):
+        """make_candidates' batch as changes against the base: (offsets[K+1],
+        changes[n, 2] of (index, value) over ngid | rgid | bkt)."""
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        K = len(seeds)
+        b0 = (None, None, None) if base is None else tuple(np.ascontiguousarray(x, np.int32) for x in base)
+        off = np.zeros(K + 1, np.int32)
+        cap = max(64, 48 * K)
+        for _ in range(2):
+            chg = np.zeros((cap, 2), np.int32)
+            st = N.lib().fo_make_candidates_delta(self.h, N.ptr(b0[0]), N.ptr(b0[1]), N.ptr(b0[2]), N.ptr(seeds), K,
+                                                  beta, methods_mask, n_threads, N.ptr(off), N.ptr(chg), cap)
+            if st == 0 or int(off[K]) <= cap:
+                break
+            cap = int(off[K])
+        _raise(st, "fo_make_candidates_delta", N.last_error())
+        return off, chg[: int(off[K])]
+
+    def score_delta_host(self, offsets, changes, precision=N.FO_PREC_FP32):
+        """cost() of sparse candidates held in host arrays (fo_score_delta_host)."""
+        off = np.ascontiguousarray(offsets, np.int32)
+        chg = np.ascontiguousarray(changes, np.int32)
+        K = len(off) - 1
+        cost = np.zeros(K, np.float64)
+        status = np.zeros(K, np.int32)
+        st = N.lib().fo_score_delta_host(self.h, N.ptr(off), N.ptr(chg), K, precision, N.ptr(cost), N.ptr(status))
+        _raise(st, "fo_score_delta_host", N.last_error())
+        return cost, status
+
+    def score_delta_device(self, offsets, changes, cost, status, precision=N.FO_PREC_FP32, stream=None):
+        """Asynchronous scoring of device-resident sparse candidates (torch tensors)."""
+        import torch
+
+        K = int(cost.shape[0])
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        st = N.lib().fo_score_delta(self.h, N.ptr(offsets), N.ptr(changes), K, precision, N.ptr(cost), N.ptr(status),
+                                    C.c_void_p(stream))
+        _raise(st, "fo_score_delta", N.last_error())
+
     def state_hash(self, ng, rg, bk):
         ng = np.ascontiguousarray(np.atleast_2d(ng), np.int32)
         rg = np.ascontiguousarray(np.atleast_2d(rg), np.int32)

@@ -339,3 +339,44 @@ def test_batch_best_and_pairs_best():
     N.lib().fo_pairs_best(N.ptr(pairs), 4, N.ptr(out), None)
     torch.cuda.synchronize()
     assert out.tolist() == [1.0, 12.0]
+
+
+@pytest.mark.parametrize("name", ["resnet50", "bert", "gpt2m"])
+def test_delta_scoring_equals_dense(name):
+    """Sparse candidates against the resident parent score bit-identically to
+    the dense encoding, from the unfused parent and from a fused one (the GPT-2
+    greedy sweep parent holds groups of thousands of ops)."""
+    import torch
+
+    doc = read("sweep_gpt2m.json.gz") if name == "gpt2m" else None
+    for precision in (N.FO_PREC_FP32, N.FO_PREC_FP64):
+        g, cps = providers(name, precision)
+        dg = cps["mp"].device_graph(g)
+        bases = [None]
+        if doc is not None:
+            from paper_2209_12769_b200.graph import state_arrays
+
+            x = graph_with_state(g, doc["sweep"][3]["both"]["state"])
+            bases.append(state_arrays(x)[:3])
+        for base in bases:
+            seeds = np.arange(300, dtype=np.uint64)
+            ng, rg, bk, gb = dg.make_candidates(seeds, base=base)
+            dense, st0 = dg.score_host(ng, rg, bk, gb, precision)
+            dg.set_parent(*(base if base is not None else (None, None, None)))
+            off, chg = dg.make_candidates_delta(seeds, base=base)
+            sparse, st1 = dg.score_delta_host(off, chg, precision)
+            assert np.array_equal(st0, st1) and np.array_equal(dense, sparse), (name, precision)
+            c = torch.empty(len(seeds), dtype=torch.float64, device="cuda")
+            s = torch.empty(len(seeds), dtype=torch.int32, device="cuda")
+            dg.score_delta_device(torch.from_numpy(off).cuda(), torch.from_numpy(chg).cuda(), c, s, precision)
+            torch.cuda.synchronize()
+            assert np.array_equal(c.cpu().numpy(), dense)
+
+
+def test_delta_scoring_rejects_bad_input():
+    g, cps = providers("vgg16", N.FO_PREC_FP32)
+    dg = cps["mp"].device_graph(g)
+    dg.set_parent()
+    off = np.array([0, 1], np.int32)
+    cost, st = dg.score_delta_host(off, np.array([[2 * dg.V + dg.A, 0]], np.int32))
+    assert st[0] == N.FO_INVALID_ARG

@@ -168,3 +168,35 @@ def test_incremental_engine_matches_full_rebuild(name, monkeypatch):
         for x, y in zip(a[:3], b[:3]):
             assert np.array_equal(x, y), (name, rnd)
         base = (a[0][rnd].copy(), a[1][rnd].copy(), a[2][rnd].copy())
+
+
+def _ranked(ng, rg):
+    ids = np.unique(np.concatenate([ng, rg[rg >= 0]]))
+    r = {int(x): i for i, x in enumerate(ids)}
+    return (np.array([r[int(x)] for x in ng], np.int32),
+            np.array([r[int(x)] if x >= 0 else -1 for x in rg], np.int32))
+
+
+@pytest.mark.parametrize("name", ["vgg16", "resnet50", "bert", "gpt2m"])
+def test_delta_candidates_reconstruct_dense(name):
+    """fo_make_candidates_delta = fo_make_candidates as (index, value) changes
+    against the id-ranked base, for the unfused base and a fused one."""
+    g = P.load_workload(name)[0]
+    dg = engine_graph(g)
+    V, A = dg.V, dg.A
+    seeds = np.arange(64, dtype=np.uint64)
+    first = dg.make_candidates(np.array([7], np.uint64))
+    for base in (None, (first[0][0], first[1][0], first[2][0])):
+        ng, rg, bk, _ = dg.make_candidates(seeds, base=base)
+        off, chg = dg.make_candidates_delta(seeds, base=base)
+        if base is None:
+            b = np.concatenate([np.arange(V), -np.ones(V), np.arange(A)]).astype(np.int32)
+        else:
+            bn, br = _ranked(base[0], base[1])
+            b = np.concatenate([bn, br, base[2]]).astype(np.int32)
+        for k in range(len(seeds)):
+            x = b.copy()
+            c = chg[off[k]:off[k + 1]]
+            assert len(np.unique(c[:, 0])) == len(c)
+            x[c[:, 0]] = c[:, 1]
+            assert np.array_equal(x, np.concatenate([ng[k], rg[k], bk[k]])), (name, k)
