@@ -92,6 +92,15 @@ typedef struct {
     const double *norm_mean; /* node_norm (MP, F entries) or agg_norm (LINEAR, 12); NULL = none */
     const double *norm_std;
     double out_scale;
+    /* hardware-oracle jitter (workloads.py:254-291), used when provider ==
+     * FO_PROVIDER_HW_ORACLE and hw_noise > 0: every group's oracle time is
+     * multiplied by 1 + noise * (2u - 1), u = blake2b-64("{seed}|{content key}")
+     * / 2^64 with the content key of _group_content_key (workloads.py:267-273). */
+    double hw_noise;              /* HardwareParams.noise in [0, 0.5] */
+    const char *hw_key_prefix;    /* UTF-8 "{seed}|" */
+    int32_t hw_key_prefix_len;
+    const char *op_key_bytes;     /* per op, UTF-8 "{op_code}:{input_shape_key}:{compute_us}" (Python str()) */
+    const int64_t *op_key_off;    /* [V + 1] offsets into op_key_bytes */
 } fo_cost_model;
 
 typedef struct fo_graph fo_graph;

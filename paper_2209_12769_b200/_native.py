@@ -35,7 +35,9 @@ class CostModel(C.Structure):
                 ("launch_us", C.c_double), ("mem_us_per_byte", C.c_double), ("layers", C.c_int32),
                 ("hidden", C.c_int32), ("feat_dim", C.c_int32), ("op_vocab_slot", P(C.c_int32)),
                 ("params", P(C.c_double)), ("n_params", C.c_int64), ("norm_mean", P(C.c_double)),
-                ("norm_std", P(C.c_double)), ("out_scale", C.c_double)]
+                ("norm_std", P(C.c_double)), ("out_scale", C.c_double), ("hw_noise", C.c_double),
+                ("hw_key_prefix", C.c_char_p), ("hw_key_prefix_len", C.c_int32), ("op_key_bytes", C.c_char_p),
+                ("op_key_off", P(C.c_int64))]
 
 
 class SearchCfg(C.Structure):

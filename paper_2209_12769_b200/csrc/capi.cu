@@ -236,6 +236,7 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_ws) cudaFree(g->d_ws);
     if (g->d_ws_big) cudaFree(g->d_ws_big);
     if (g->d_memo) cudaFree(g->d_memo);
+    if (g->d_keys) cudaFree(g->d_keys);
     if (g->d_io) cudaFree(g->d_io);
     if (g->d_parent) cudaFree(g->d_parent);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
@@ -261,6 +262,33 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         return fail(FO_INVALID_ARG, "unknown provider");
     if (!(m->comm_C >= 0) || !(m->comm_D >= 0)) return fail(FO_INVALID_ARG, "C and D must be non-negative");
     const int V = g->V;
+    dg.noise = 0.0;
+    dg.kpre = dg.okb = nullptr;
+    dg.oko = nullptr;
+    dg.kpre_len = 0;
+    if (m->provider == FO_PROVIDER_HW_ORACLE && m->hw_noise != 0.0) {
+        // jitter keys (workloads.py:254-273): prefix | per-op fragments | offsets
+        if (!(m->hw_noise >= 0.0 && m->hw_noise <= 0.5)) return fail(FO_INVALID_ARG, "noise fraction must lie in [0, 0.5]");
+        if (!m->hw_key_prefix || m->hw_key_prefix_len < 0 || !m->op_key_bytes || !m->op_key_off)
+            return fail(FO_INVALID_ARG, "jitter needs the key prefix and per-op key fragments");
+        const int64_t nb = m->op_key_off[V];
+        size_t o_off = al256((size_t)m->hw_key_prefix_len + 8), o_b = o_off + al256(8 * ((size_t)V + 1));
+        size_t tot = o_b + al256((size_t)nb + 8);
+        dg.noise = m->hw_noise;
+        dg.kpre_len = m->hw_key_prefix_len;
+        if (g->device >= 0) {
+            CUDA_TRY(cudaSetDevice(g->device));
+            if (g->d_keys) { cudaFree(g->d_keys); g->d_keys = nullptr; }
+            CUDA_TRY(cudaMalloc(&g->d_keys, tot));
+            char *b = (char *)g->d_keys;
+            CUDA_TRY(cudaMemcpy(b, m->hw_key_prefix, m->hw_key_prefix_len, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(b + o_off, m->op_key_off, 8 * ((size_t)V + 1), cudaMemcpyHostToDevice));
+            if (nb) CUDA_TRY(cudaMemcpy(b + o_b, m->op_key_bytes, nb, cudaMemcpyHostToDevice));
+            dg.kpre = (const uint8_t *)b;
+            dg.oko = (const int64_t *)(b + o_off);
+            dg.okb = (const uint8_t *)(b + o_b);
+        }
+    }
     if (m->provider == FO_PROVIDER_PROFILE && m->variant == FO_EST_LINEAR) {
         if (!m->params || m->n_params != 13) return fail(FO_DIM_MISMATCH, "linear model needs w[12] and b");
         for (int i = 0; i < 12; i++) dg.lin_w[i] = m->params[i];

@@ -53,6 +53,13 @@ struct DGraph {
     int32_t pairs_max;          // bound on contracted dependency pairs per candidate
     MemoEnt *memo[2];           // MP predictions by member set: [fp32, fp64]
     uint32_t memo_mask;
+    // hardware-oracle jitter (workloads.py:254-291): noise, "{seed}|" prefix,
+    // per-op content-key fragments (CSR over ops)
+    double noise;
+    const uint8_t *kpre;
+    int32_t kpre_len;
+    const uint8_t *okb;
+    const int64_t *oko;
 };
 
 // Packed message-passing weights (float or double), all transposed so lane c
@@ -137,6 +144,7 @@ struct fo_graph {
     void *d_static = nullptr;  // one allocation for the static graph
     void *d_model = nullptr;   // H0 + weights
     void *d_memo = nullptr;    // estimator memo tables
+    void *d_keys = nullptr;    // hardware-oracle jitter key bytes
     fo::DGraph dg{};
     bool model_set = false;
     // scoring workspace

@@ -340,6 +340,108 @@ __device__ __forceinline__ void memo_put(MemoEnt *t, unsigned mask, unsigned lon
     }
 }
 
+// ---------------------------------------------------------------------------
+// Hardware-oracle jitter (workloads.py:254-273): blake2b with an 8-byte
+// digest over "{seed}|{content key}", where the key is the members' fragments
+// "{op_code}:{input_shape_key}:{compute_us}" in ascending op order joined by
+// ';', then "|{internal},{external_in},{external_out}".  One thread streams the
+// message through a 128-byte block buffer (RFC 7693).
+__device__ __constant__ uint64_t kB2bIv[8] = {0x6a09e667f3bcc908ull, 0xbb67ae8584caa73bull, 0x3c6ef372fe94f82bull,
+                                              0xa54ff53a5f1d36f1ull, 0x510e527fade682d1ull, 0x9b05688c2b3e6c1full,
+                                              0x1f83d9abfb41bd6bull, 0x5be0cd19137e2179ull};
+__device__ __constant__ uint8_t kB2bSigma[12][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+
+struct Blake2b64 {
+    uint64_t h[8];
+    uint64_t m[16];  // current block as little-endian words
+    uint64_t t;      // bytes compressed so far
+    int n;           // bytes in the current block
+
+    __device__ __forceinline__ static uint64_t rotr(uint64_t x, int r) { return (x >> r) | (x << (64 - r)); }
+    __device__ void init() {
+        for (int i = 0; i < 8; i++) h[i] = kB2bIv[i];
+        h[0] ^= 0x01010000ull ^ 8ull;  // digest_size 8, no key
+        for (int i = 0; i < 16; i++) m[i] = 0;
+        t = 0;
+        n = 0;
+    }
+    __device__ void compress(bool last) {
+        uint64_t v[16];
+        for (int i = 0; i < 8; i++) { v[i] = h[i]; v[i + 8] = kB2bIv[i]; }
+        v[12] ^= t;
+        if (last) v[14] = ~v[14];
+        for (int r = 0; r < 12; r++) {
+            const uint8_t *sg = kB2bSigma[r];
+#define FO_B2B_G(a, b, c, d, x, y)               \
+    a = a + b + x; d = rotr(d ^ a, 32);          \
+    c = c + d; b = rotr(b ^ c, 24);              \
+    a = a + b + y; d = rotr(d ^ a, 16);          \
+    c = c + d; b = rotr(b ^ c, 63);
+            FO_B2B_G(v[0], v[4], v[8], v[12], m[sg[0]], m[sg[1]]);
+            FO_B2B_G(v[1], v[5], v[9], v[13], m[sg[2]], m[sg[3]]);
+            FO_B2B_G(v[2], v[6], v[10], v[14], m[sg[4]], m[sg[5]]);
+            FO_B2B_G(v[3], v[7], v[11], v[15], m[sg[6]], m[sg[7]]);
+            FO_B2B_G(v[0], v[5], v[10], v[15], m[sg[8]], m[sg[9]]);
+            FO_B2B_G(v[1], v[6], v[11], v[12], m[sg[10]], m[sg[11]]);
+            FO_B2B_G(v[2], v[7], v[8], v[13], m[sg[12]], m[sg[13]]);
+            FO_B2B_G(v[3], v[4], v[9], v[14], m[sg[14]], m[sg[15]]);
+#undef FO_B2B_G
+        }
+        for (int i = 0; i < 8; i++) h[i] ^= v[i] ^ v[i + 8];
+    }
+    __device__ void put(uint8_t c) {
+        if (n == 128) {  // a full block is compressed only once more data follows
+            t += 128;
+            compress(false);
+            for (int i = 0; i < 16; i++) m[i] = 0;
+            n = 0;
+        }
+        m[n >> 3] |= (uint64_t)c << (8 * (n & 7));
+        n++;
+    }
+    __device__ void put(const uint8_t *p, int64_t len) {
+        for (int64_t i = 0; i < len; i++) put(p[i]);
+    }
+    __device__ void put_uint(unsigned long long x) {  // decimal, like str(int)
+        char d[20];
+        int k = 0;
+        do { d[k++] = (char)('0' + x % 10); x /= 10; } while (x);
+        while (k) put((uint8_t)d[--k]);
+    }
+    __device__ uint64_t digest() {
+        t += n;
+        compress(true);
+        return h[0];  // the 8-byte digest, read little-endian
+    }
+};
+
+// 1 + noise * (2u - 1), u = digest / 2^64 (workloads.py:256-264); ops[] ascending
+__device__ double hw_jitter(const DGraph &g, const int *ops, int n, long long internal, long long ext_in,
+                            long long ext_out) {
+    Blake2b64 b;
+    b.init();
+    b.put(g.kpre, g.kpre_len);
+    for (int i = 0; i < n; i++) {
+        if (i) b.put((uint8_t)';');
+        const int v = ops[i];
+        b.put(g.okb + g.oko[v], g.oko[v + 1] - g.oko[v]);
+    }
+    b.put((uint8_t)'|');
+    b.put_uint((unsigned long long)internal);
+    b.put((uint8_t)',');
+    b.put_uint((unsigned long long)ext_in);
+    b.put((uint8_t)',');
+    b.put_uint((unsigned long long)ext_out);
+    const double u = __dmul_rn(__ull2double_rn(b.digest()), 0x1p-64);
+    return __dadd_rn(1.0, __dmul_rn(g.noise, __dsub_rn(__dmul_rn(2.0, u), 1.0)));
+}
+
 // Drop dead workspace lines from L2 without writing them back
 // (discard.global.L2): the per-warp scratch of ~4,000 resident candidates
 // exceeds the 126 MB L2, and write-backs of dead setup arrays were most of
@@ -1035,6 +1137,8 @@ __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratc
             d = all_param ? 0.0
                           : __dadd_rn(__dadd_rn(comp.get(), g.launch),
                                       __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
+            if (!all_param && g.noise != 0.0)
+                d = __dmul_rn(d, hw_jitter(g, mem, n, w.gint()[gi], w.gin()[gi], w.gout()[gi]));
         }
         d = __shfl_sync(FULL, d, 0);
         if (lane == 0) w.dur()[gi] = d;
@@ -1393,6 +1497,8 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
                         d = g.op_kind[v] == 1 ? 0.0
                                               : __dadd_rn(__dadd_rn(isnan(c) ? 0.0 : c, g.launch),
                                                           __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
+                        if (g.noise != 0.0 && g.op_kind[v] != 1)
+                            d = __dmul_rn(d, hw_jitter(g, &v, 1, w.gint()[gi], w.gin()[gi], w.gout()[gi]));
                     } else if (g.op_kind[v] == 1) {
                         d = 0.0;
                     } else {

@@ -50,6 +50,8 @@ class StaticArrays:
         self.ar_prod = np.array([self.op_index[a.producer_op] for a in ars], np.int32)
         self.ar_bytes = np.array([a.tensor_bytes for a in ars], np.int64)
         self.op_codes = [o.op_code for o in ops]
+        # _group_content_key fragments (workloads.py:267-273), for the jittered oracle
+        self.op_keys = [f"{o.op_code}:{o.input_shape_key}:{o.compute_us}" for o in ops]
 
     def desc(self):
         d = N.GraphDesc()

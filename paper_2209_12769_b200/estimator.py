@@ -164,6 +164,17 @@ class DeviceCostProviders:
             cm.variant = N.FO_EST_NONE
             cm.comm_C, cm.comm_D = hw.comm_params.C, hw.comm_params.D
             cm.launch_us, cm.mem_us_per_byte = hw.launch_overhead_us, hw.mem_us_per_byte
+            if hw.noise != 0:  # jitter keys (workloads.py:254-273)
+                frags = [k.encode() for k in static.op_keys]
+                off = np.zeros(len(frags) + 1, np.int64)
+                off[1:] = np.cumsum([len(f) for f in frags])
+                blob = b"".join(frags) or b"\0"
+                prefix = f"{hw.seed}|".encode()
+                keep += [off, blob, prefix]
+                cm.hw_noise = float(hw.noise)
+                cm.hw_key_prefix, cm.hw_key_prefix_len = prefix, len(prefix)
+                cm.op_key_bytes = blob
+                cm.op_key_off = N.tptr(off, C.c_int64)
             return cm
         cm.provider = N.FO_PROVIDER_PROFILE
         cm.comm_C, cm.comm_D = self.comm_params.C, self.comm_params.D

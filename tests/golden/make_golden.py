@@ -7,7 +7,7 @@ imports the reference, and it only ever runs in the build container
 (/root/reference does not exist on the GPU box); its outputs are committed.
 
 Usage:  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [section ...]
-Sections: workloads rng cases search exhaustive sweep baselines
+Sections: workloads rng cases search exhaustive sweep baselines jitter
 (default: the first five)
 
 Inputs follow SURVEY.md section 8(d) / BASELINE.md section 3:
@@ -412,14 +412,39 @@ def section_baselines(names=None):
         _dump_gz(os.path.join(OUT, "baselines.json.gz"), out)
 
 
+def section_jitter(names=None):
+    """oracle_providers with noise > 0 (workloads.py:254-291): candidate costs
+    and per-group durations under the reference's blake2b jitter."""
+    out = {}
+    for name in ["chain24", "residual40", "attention36", "vgg16", "resnet50", "bert"]:
+        if names and name not in names:
+            continue
+        g = load_workload(name)[0]
+        ent = []
+        for noise, seed in ((0.05, 42), (0.3, 7)):
+            hw = HardwareParams(noise=noise, seed=seed)
+            cp = oracle_providers(hw)
+            rows = []
+            for i in range(10):
+                c = make_candidate(g, i)
+                row = {"i": i, "cost": cost(c, cp)}
+                if i < 2:
+                    row["groups"] = [[gr.id, cp.op_cost(c, gr)] for gr in c.groups]
+                rows.append(row)
+            ent.append({"noise": noise, "seed": seed, "rows": rows})
+        out[name] = ent
+        print(f"jitter {name}", flush=True)
+    _dump_gz(os.path.join(OUT, "jitter.json.gz"), out)
+
+
 def main(argv):
-    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep", "baselines")]
+    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep", "baselines", "jitter")]
     names = [a for a in argv if a not in sections]
     if not sections:
         sections = ["workloads", "rng", "cases", "search", "exhaustive"]
     for s in sections:
         {"workloads": section_workloads, "rng": lambda _: section_rng(), "exhaustive": section_exhaustive,
-         "sweep": section_sweep, "baselines": section_baselines,
+         "sweep": section_sweep, "baselines": section_baselines, "jitter": section_jitter,
          "cases": section_cases, "search": section_search}[s](names or None)
 
 

@@ -380,3 +380,40 @@ def test_delta_scoring_rejects_bad_input():
     off = np.array([0, 1], np.int32)
     cost, st = dg.score_delta_host(off, np.array([[2 * dg.V + dg.A, 0]], np.int32))
     assert st[0] == N.FO_INVALID_ARG
+
+
+@pytest.mark.parametrize("name", ["chain24", "residual40", "attention36", "vgg16", "resnet50", "bert"])
+def test_hw_oracle_jitter_matches_reference(name):
+    """oracle_providers with noise > 0: the reference's blake2b content-key
+    jitter (workloads.py:254-291) reproduced on the device, per candidate cost
+    and per group duration."""
+    doc = read("jitter.json.gz")[name]
+    g = P.load_workload(name)[0]
+    cs = {c["i"]: c for c in cases(name)["candidates"]}
+    for ent in doc:
+        hw = P.HardwareParams(noise=ent["noise"], seed=ent["seed"])
+        cp = P.oracle_providers(hw, precision=N.FO_PREC_FP64)
+        graphs = [graph_with_state(g, cs[r["i"]]["state"]) for r in ent["rows"]]
+        got = P.cost_batch(graphs, cp)
+        ref = np.array([r["cost"] for r in ent["rows"]])
+        np.testing.assert_allclose(got, ref, rtol=1e-15, atol=0)
+        for r, x in zip(ent["rows"], graphs):
+            if "groups" not in r:
+                continue
+            groups, _ = cp.node_durations(x)
+            for gid, d in r["groups"]:
+                assert groups[gid] == d, (name, ent["seed"], r["i"], gid)
+
+
+def test_hw_oracle_jitter_is_deterministic_and_bounded():
+    """test_workloads.py:134-145: jitter is a pure function of group content and
+    stays within [1 - noise, 1 + noise] of the noise-free time."""
+    g = P.load_workload("vgg16")[0]
+    base = P.oracle_providers(P.HardwareParams(noise=0.0), precision=N.FO_PREC_FP64)
+    noisy = P.oracle_providers(P.HardwareParams(noise=0.05, seed=77), precision=N.FO_PREC_FP64)
+    a, _ = noisy.node_durations(g)
+    b, _ = noisy.node_durations(g)
+    c, _ = base.node_durations(g)
+    assert a == b
+    for gid, d in c.items():
+        assert abs(a[gid] - d) <= 0.05 * d + 1e-12
