@@ -52,8 +52,10 @@ def global_best(cost, ids, group=None):
 
 
 class ShardedSearch:
-    """R lock-stepped Alg. 1 seeds sharded across ranks; every round each rank
-    advances its seeds and the global (best cost, seed) pair is exchanged."""
+    """R lock-stepped Alg. 1 seeds sharded across ranks.  Each rank advances its
+    seeds; the global (best cost, seed) pair is exchanged over the process
+    group at the end of the run, or every M rounds (run(exchange_every=M)), or
+    every round when driven through round()."""
 
     def __init__(self, g0, cfg, cp, seeds: Sequence[int], rank: int, world: int, precision=None, n_threads=0):
         from .search import LockstepSearch
@@ -78,19 +80,46 @@ class ShardedSearch:
             dist.all_reduce(a)
         return int(a.item())
 
-    def run(self, device, max_rounds: Optional[int] = None):
+    def run(self, device, max_rounds: Optional[int] = None, exchange_every: Optional[int] = None):
+        """Advance every local seed to completion.  Seeds are independent, so by
+        default each rank runs its shard natively (fo_search_run) and the global
+        best is exchanged once at the end; exchange_every=M steps the shard M
+        rounds at a time with an exchange after each block (progress reports)."""
+        import torch
+
         dist = _dist()
-        if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
-            # single rank: no per-round exchange, the whole search runs natively
-            if self.s is None:
-                return (float("inf"), -1.0)
-            res = self.s.run(max_rounds)
-            best = min(range(len(res)), key=lambda r: (res[r].best_cost_us, r))
-            self.best_history.append((res[best].best_cost_us, float(self.seed_offset + best)))
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        if exchange_every is None:
+            if self.s is not None:
+                res = self.s.run(max_rounds)
+                best = np.array([r.best_cost_us for r in res], np.float64)
+            else:
+                best = np.zeros(0)
+            if not multi:
+                if self.s is None:
+                    return (float("inf"), -1.0)
+                r = min(range(len(best)), key=lambda i: (best[i], i))
+                self.best_history.append((float(best[r]), float(self.seed_offset + r)))
+                return self.best_history[-1]
+            cost = torch.as_tensor(best, dtype=torch.float64, device=device)
+            ids = torch.arange(self.seed_offset, self.seed_offset + len(best), dtype=torch.float64, device=device)
+            self.best_history.append(global_best(cost, ids))
             return self.best_history[-1]
         rounds = 0
-        while self.round(device) > 0:
-            rounds += 1
-            if max_rounds is not None and rounds >= max_rounds:
+        while True:
+            active = 0
+            for _ in range(exchange_every):
+                active = self.s.round() if self.s is not None else 0
+                rounds += 1
+                if active == 0 or (max_rounds is not None and rounds >= max_rounds):
+                    break
+            best = self.s.best if self.s is not None else np.zeros(0)
+            cost = torch.as_tensor(best, dtype=torch.float64, device=device)
+            ids = torch.arange(self.seed_offset, self.seed_offset + len(best), dtype=torch.float64, device=device)
+            self.best_history.append(global_best(cost, ids))
+            a = torch.tensor([active], dtype=torch.int64, device=device)
+            if multi:
+                dist.all_reduce(a)
+            if int(a.item()) == 0 or (max_rounds is not None and rounds >= max_rounds):
                 break
         return self.best_history[-1] if self.best_history else (float("inf"), -1.0)
