@@ -489,8 +489,10 @@ struct Engine {
     }
     uint64_t hash(const State &s) const {
         // group content hashes accumulated per group id (ops visited ascending)
-        std::vector<uint64_t> acc(VB, 0);
-        std::vector<uint8_t> used(VB, 0);
+        thread_local std::vector<uint64_t> acc, bacc;
+        thread_local std::vector<uint8_t> used, bused;
+        acc.assign(VB, 0);
+        used.assign(VB, 0);
         for (int v = 0; v < V; v++) {
             int x = s.ng[v];
             acc[x] = mix(acc[x] ^ (uint64_t)(2 * v + 2));
@@ -504,8 +506,8 @@ struct Engine {
         uint64_t h = 0x6a09e667f3bcc909ull;
         for (int i = 0; i < VB; i++)
             if (used[i]) h += mix(acc[i] + 0x3c6ef372fe94f82bull);
-        std::vector<uint64_t> bacc(A, 0);
-        std::vector<uint8_t> bused(A, 0);
+        bacc.assign(A, 0);
+        bused.assign(A, 0);
         for (int a = 0; a < A; a++) {
             int b = s.bk[a];
             bacc[b] = mix(bacc[b] ^ (uint64_t)(a + 1));
