@@ -16,6 +16,7 @@
 #include <atomic>
 #include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <queue>
@@ -1652,6 +1653,17 @@ struct fo_search {
         int64_t batch_pos[3];
         Scratch sc;
         Inc inc0;  // incremental index of the popped state (methods roll back)
+        // speculation (one step ahead): costs of the candidates of every state
+        // the next step may pop, scored in the same device batch.  They enter
+        // the reference-visible cache only when that step really evaluates them.
+        std::unordered_map<uint64_t, std::pair<double, int32_t>> spec;
+        int nbr = 0;
+        State br_cand[4][3];
+        uint64_t br_h[4][3];
+        int br_n[4];
+        int64_t br_pos[4][3];
+        const State *br_state[4];
+        uint64_t br_hs[4];
     };
     // one in-flight device batch: pinned staging, device buffers, results
     struct Lane {
@@ -1668,8 +1680,11 @@ struct fo_search {
     std::vector<Seed> seeds;
     Lane lanes[2];
     double device_ms = 0, expand_ms = 0;
-    int64_t scored = 0;
+    double launch_ms = 0, wait_ms = 0, replay_ms = 0;  // host-side split (FO_SEARCH_PROFILE)
+    double put_ms = 0, issue_ms = 0;
+    int64_t scored = 0, host_steps = 0;
     bool started = false;
+    bool spec = false;  // one-step speculation (latency-bound rounds: few seeds)
 };
 
 static int lane_reserve(fo_search *S, fo_search::Lane &L, int n) {
@@ -1690,9 +1705,10 @@ static int lane_reserve(fo_search *S, fo_search::Lane &L, int n) {
         L.hc_cap = cap;
     }
     size_t need = ((W * n * 4 + 255) & ~size_t(255)) + 16 * (size_t)n + 256;
-    if (need > L.d_cap) {
+    if (need > L.d_cap) {  // geometric: cudaFree synchronises the device
         if (L.d_buf) cudaFree(L.d_buf);
         L.d_buf = nullptr;
+        need = std::max(need, 2 * L.d_cap);
         if (cudaMalloc(&L.d_buf, need) != cudaSuccess) return fail(FO_CUDA_ERROR, "search batch alloc");
         L.d_cap = need;
     }
@@ -1767,44 +1783,98 @@ static int search_start(fo_search *S) {
     return FO_OK;
 }
 
-// every active seed in [lo, hi) pops and generates its step's candidates
+// one Alg. 1 step's batch-expand from state H (search.py:112-119): for each
+// enabled method, n = randint(0, beta) rewrites from H (rewrite.py:222-263)
+static void expand_step(const fo_search *S, const State &H, uint64_t hH, PyRng &rng, Inc &inc, Scratch &sc,
+                        State *cand, int *meth, uint64_t *h, int &ncand) {
+    const Engine &eng = *S->eng;
+    bool built = false, inc_ok = !use_full_engine();
+    ncand = 0;
+    for (int m = 0; m < 3; m++) {
+        if (!(S->cfg.methods_mask & (1 << m))) continue;
+        int n = (int)rng.below((uint32_t)S->cfg.beta + 1);
+        int j = ncand++;
+        bool applied = false;
+        if (inc_ok && n > 0 && !built) {  // one index of the popped state serves all methods
+            inc_ok = inc.build(S->g, H, eng.VB);
+            built = true;
+        }
+        if (inc_ok && n > 0) {
+            inc.checkpoint();
+            applied = inc.random_apply(m, n, rng);
+            if (applied) inc.to_state(cand[j]);
+            else cand[j] = H;
+            if (!inc.undo()) inc.build(S->g, H, eng.VB);
+        } else {
+            cand[j] = H;
+            applied = eng.random_apply(cand[j], m, n, rng, sc);
+        }
+        if (meth) meth[j] = m;
+        h[j] = applied ? eng.hash(cand[j]) : hH;
+    }
+}
+
+static bool step_known(const fo_search::Seed &sd) {
+    for (int j = 0; j < sd.ncand; j++)
+        if (!sd.cache.count(sd.h[j]) && !sd.spec.count(sd.h[j])) return false;
+    return true;
+}
+
+static void replay_seed(fo_search *S, fo_search::Seed &sd, const fo_search::Lane *L);
+
+// every active seed in [lo, hi) pops and generates its step's candidates.
+// With speculation, steps whose candidates were all scored speculatively are
+// replayed on the host at once, and the pending step's successors are expanded
+// for every state the next pop can return.
 static void search_expand(fo_search *S, int lo, int hi) {
     auto t0 = std::chrono::steady_clock::now();
-    const Engine &eng = *S->eng;
-    const bool full = use_full_engine();
     int nthreads = S->cfg.n_threads > 0 ? S->cfg.n_threads : omp_get_max_threads();
 #pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
     for (int r = lo; r < hi; r++) {
         auto &sd = S->seeds[r];
         sd.ncand = 0;
-        if (!sd.active) continue;
-        if (sd.queue.empty() || sd.unchanged >= S->cfg.max_unchanged) { sd.active = false; continue; }
-        sd.cur = sd.queue.top();
-        sd.queue.pop();
-        sd.steps++;
-        bool built = false, inc_ok = !full;
-        for (int m = 0; m < 3; m++) {
-            if (!(S->cfg.methods_mask & (1 << m))) continue;
-            int n = (int)sd.rng.below((uint32_t)S->cfg.beta + 1);
-            int j = sd.ncand++;
-            const State &H = sd.pool[sd.cur.slot];
-            bool applied = false;
-            if (inc_ok && n > 0 && !built) {  // one index of the popped state serves all methods
-                inc_ok = sd.inc0.build(S->g, H, eng.VB);
-                built = true;
+        sd.nbr = 0;
+        for (;;) {
+            if (!sd.active) break;
+            if (sd.queue.empty() || sd.unchanged >= S->cfg.max_unchanged) { sd.active = false; break; }
+            sd.cur = sd.queue.top();
+            sd.queue.pop();
+            sd.steps++;
+            expand_step(S, sd.pool[sd.cur.slot], sd.cur.h, sd.rng, sd.inc0, sd.sc, sd.cand, sd.meth, sd.h, sd.ncand);
+            if (S->spec && step_known(sd)) {
+                replay_seed(S, sd, nullptr);
+#pragma omp atomic
+                S->host_steps++;
+                continue;
             }
-            if (inc_ok && n > 0) {
-                sd.inc0.checkpoint();
-                applied = sd.inc0.random_apply(m, n, sd.rng);
-                if (applied) sd.inc0.to_state(sd.cand[j]);
-                else sd.cand[j] = H;
-                if (!sd.inc0.undo()) sd.inc0.build(S->g, H, eng.VB);
-            } else {
-                sd.cand[j] = H;
-                applied = eng.random_apply(sd.cand[j], m, n, sd.rng, sd.sc);
-            }
-            sd.meth[j] = m;
-            sd.h[j] = applied ? eng.hash(sd.cand[j]) : sd.cur.h;
+            break;
+        }
+        if (!S->spec || sd.ncand == 0) continue;
+        // the next pop is the queue's current top or one of this step's candidates
+        int nb = 0;
+        auto add = [&](const State *st, uint64_t hs) {
+            for (int q = 0; q < nb; q++)
+                if (sd.br_hs[q] == hs) return;
+            sd.br_state[nb] = st;
+            sd.br_hs[nb++] = hs;
+        };
+        for (int j = 0; j < sd.ncand; j++) add(&sd.cand[j], sd.h[j]);
+        if (!sd.queue.empty()) add(&sd.pool[sd.queue.top().slot], sd.queue.top().h);
+        sd.nbr = nb;
+    }
+    if (S->spec) {  // branch expansions, flattened over (seed, branch)
+        std::vector<std::pair<int, int>> work;
+        for (int r = lo; r < hi; r++)
+            for (int q = 0; q < S->seeds[r].nbr; q++) work.emplace_back(r, q);
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
+        for (int w = 0; w < (int)work.size(); w++) {
+            auto &sd = S->seeds[work[w].first];
+            const int q = work[w].second;
+            thread_local Inc inc;
+            thread_local Scratch sc;
+            PyRng rng = sd.rng;  // the next step continues this seed's draws
+            expand_step(S, *sd.br_state[q], sd.br_hs[q], rng, inc, sc, sd.br_cand[q], nullptr, sd.br_h[q],
+                        sd.br_n[q]);
         }
     }
     S->expand_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1815,68 +1885,105 @@ static int search_launch(fo_search *S, fo_search::Lane &L, int lo, int hi) {
     int n = 0;
     for (int r = lo; r < hi; r++) {
         auto &sd = S->seeds[r];
+        std::unordered_map<uint64_t, int64_t> inb;  // hash -> batch position (this seed)
         for (int j = 0; j < sd.ncand; j++) {
             sd.batch_pos[j] = -1;
-            if (sd.cache.count(sd.h[j])) continue;
-            bool dup = false;
-            for (int q = 0; q < j; q++)
-                if (sd.h[q] == sd.h[j] && sd.batch_pos[q] >= 0) { sd.batch_pos[j] = sd.batch_pos[q]; dup = true; }
-            if (!dup) sd.batch_pos[j] = n++;
+            if (sd.cache.count(sd.h[j]) || sd.spec.count(sd.h[j])) continue;
+            auto it = inb.find(sd.h[j]);
+            if (it != inb.end()) sd.batch_pos[j] = it->second;
+            else inb[sd.h[j]] = sd.batch_pos[j] = n++;
         }
+        for (int q = 0; q < sd.nbr; q++)
+            for (int j = 0; j < sd.br_n[q]; j++) {
+                const uint64_t hh = sd.br_h[q][j];
+                sd.br_pos[q][j] = -1;
+                if (sd.cache.count(hh) || sd.spec.count(hh) || inb.count(hh)) continue;
+                inb[hh] = sd.br_pos[q][j] = n++;
+            }
     }
+    auto t0 = std::chrono::steady_clock::now();
     if (n > 0) {
         int rc = lane_reserve(S, L, n);
         if (rc) return rc;
         for (int r = lo; r < hi; r++) {
             auto &sd = S->seeds[r];
-            for (int j = 0; j < sd.ncand; j++)
+            for (int j = 0; j < sd.ncand; j++)  // duplicates write the same state twice
                 if (sd.batch_pos[j] >= 0) lane_put(S, L, n, (int)sd.batch_pos[j], sd.cand[j]);
+            for (int q = 0; q < sd.nbr; q++)
+                for (int j = 0; j < sd.br_n[q]; j++)
+                    if (sd.br_pos[q][j] >= 0) lane_put(S, L, n, (int)sd.br_pos[q][j], sd.br_cand[q][j]);
         }
     }
-    return lane_launch(S, L, n);
+    auto t1 = std::chrono::steady_clock::now();
+    int rc = lane_launch(S, L, n);
+    auto t2 = std::chrono::steady_clock::now();
+    S->put_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    S->issue_ms += std::chrono::duration<double, std::milli>(t2 - t1).count();
+    return rc;
 }
 
-// replay the accept / prune bookkeeping in method order (search.py:120-146)
+// replay the accept / prune bookkeeping of a seed's pending step in method
+// order (search.py:120-146).  Costs come from the cache, the batch, or the
+// speculation table -- the last two count as this step's evaluations.
+static void replay_seed(fo_search *S, fo_search::Seed &sd, const fo_search::Lane *L) {
+    bool requeued = false;
+    for (int j = 0; j < sd.ncand; j++) {
+        double c;
+        auto it = sd.cache.find(sd.h[j]);
+        if (it != sd.cache.end()) c = it->second;
+        else {
+            int32_t st;
+            if (L && sd.batch_pos[j] >= 0) {
+                const int p = (int)sd.batch_pos[j];
+                st = L->h_status[p];
+                c = L->h_cost[p];
+            } else {
+                const auto &e = sd.spec.at(sd.h[j]);
+                c = e.first;
+                st = e.second;
+            }
+            if (st) { sd.status = st; sd.active = false; break; }
+            sd.cache[sd.h[j]] = c;
+            sd.evaluated++;
+        }
+        int slot = -1;
+        if (c < sd.best) {
+            sd.best = c;
+            sd.pool.push_back(sd.cand[j]);
+            slot = (int)sd.pool.size() - 1;
+            sd.best_slot = slot;
+            sd.unchanged = 0;
+        } else sd.unchanged++;
+        int entered = 0;
+        if (c <= S->cfg.alpha * sd.best) {
+            bool push = false;
+            if (!sd.seen.count(sd.h[j])) { sd.seen.insert(sd.h[j]); push = true; sd.enqueued++; }
+            else if (sd.h[j] == sd.cur.h && !requeued) { push = true; requeued = true; }
+            if (push) {
+                if (slot < 0) {
+                    if (sd.h[j] == sd.cur.h) slot = sd.cur.slot;
+                    else { sd.pool.push_back(sd.cand[j]); slot = (int)sd.pool.size() - 1; }
+                }
+                sd.queue.push({c, sd.seq++, sd.h[j], slot});
+                entered = 1;
+            }
+        }
+        sd.trace.push_back({(int32_t)sd.steps, sd.meth[j], c, sd.best, (int32_t)sd.queue.size(), entered});
+    }
+    sd.ncand = 0;
+}
+
 static void search_replay(fo_search *S, fo_search::Lane &L, int lo, int hi) {
     for (int r = lo; r < hi; r++) {
         auto &sd = S->seeds[r];
-        bool requeued = false;
-        for (int j = 0; j < sd.ncand; j++) {
-            double c;
-            auto it = sd.cache.find(sd.h[j]);
-            if (it != sd.cache.end()) c = it->second;
-            else {
-                int p = (int)sd.batch_pos[j];
-                if (L.h_status[p]) { sd.status = L.h_status[p]; sd.active = false; break; }
-                c = L.h_cost[p];
-                sd.cache[sd.h[j]] = c;
-                sd.evaluated++;
-            }
-            int slot = -1;
-            if (c < sd.best) {
-                sd.best = c;
-                sd.pool.push_back(sd.cand[j]);
-                slot = (int)sd.pool.size() - 1;
-                sd.best_slot = slot;
-                sd.unchanged = 0;
-            } else sd.unchanged++;
-            int entered = 0;
-            if (c <= S->cfg.alpha * sd.best) {
-                bool push = false;
-                if (!sd.seen.count(sd.h[j])) { sd.seen.insert(sd.h[j]); push = true; sd.enqueued++; }
-                else if (sd.h[j] == sd.cur.h && !requeued) { push = true; requeued = true; }
-                if (push) {
-                    if (slot < 0) {
-                        if (sd.h[j] == sd.cur.h) slot = sd.cur.slot;
-                        else { sd.pool.push_back(sd.cand[j]); slot = (int)sd.pool.size() - 1; }
-                    }
-                    sd.queue.push({c, sd.seq++, sd.h[j], slot});
-                    entered = 1;
+        for (int q = 0; q < sd.nbr; q++)  // speculative results first (not yet evaluations)
+            for (int j = 0; j < sd.br_n[q]; j++)
+                if (sd.br_pos[q][j] >= 0) {
+                    const int p = (int)sd.br_pos[q][j];
+                    sd.spec.emplace(sd.br_h[q][j], std::make_pair(L.h_cost[p], L.h_status[p]));
                 }
-            }
-            sd.trace.push_back({(int32_t)sd.steps, sd.meth[j], c, sd.best, (int32_t)sd.queue.size(), entered});
-        }
-        sd.ncand = 0;
+        sd.nbr = 0;
+        if (sd.ncand) replay_seed(S, sd, &L);
     }
 }
 
@@ -1912,6 +2019,10 @@ int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seed
         sd.seen.insert(h0);
         sd.cur.h = h0;
     }
+    // speculation pays while a round is latency-bound (few seeds): each round
+    // then advances a seed by two steps.  FO_SEARCH_SPEC=0/1 overrides.
+    const char *sp = getenv("FO_SEARCH_SPEC");
+    S->spec = sp ? sp[0] == '1' : R <= 32;
     cudaSetDevice(g->device);
     *out = S;
     return FO_OK;
@@ -1963,11 +2074,21 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
         search_replay(S, S->lanes[0], 0, R);
     }
     const bool pipeline = R > 1 && (S->expand_ms - e0) > 2.0 * (S->device_ms - d0);
+    if (pipeline) S->spec = false;  // halves overlap instead
     if (!pipeline) {
+        using clk = std::chrono::steady_clock;
+        auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
         for (; (max_rounds <= 0 || it < max_rounds) && any_active(0, R); it++) {
             search_expand(S, 0, R);
-            if ((rc = search_launch(S, S->lanes[0], 0, R)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
+            const auto t0 = clk::now();
+            if ((rc = search_launch(S, S->lanes[0], 0, R))) return rc;
+            const auto t1 = clk::now();
+            if ((rc = lane_wait(S, S->lanes[0]))) return rc;
+            const auto t2 = clk::now();
             search_replay(S, S->lanes[0], 0, R);
+            S->launch_ms += ms(t0, t1);
+            S->wait_ms += ms(t1, t2);
+            S->replay_ms += ms(t2, clk::now());
         }
     } else {
         const int mid = R / 2;
@@ -2006,6 +2127,10 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
         if (LA.n) search_replay(S, LA, 0, mid);
     }
     if (active_out) *active_out = count_active(S, nullptr);
+    if (getenv("FO_SEARCH_PROFILE"))
+        fprintf(stderr, "fo_search_run: rounds %lld pipeline %d spec %d (host-only steps %lld) device %.1f ms expand %.1f ms launch %.1f ms (put %.1f, issue %.1f) wait %.1f ms replay %.1f ms\n",
+                (long long)it, (int)pipeline, (int)S->spec, (long long)S->host_steps, S->device_ms, S->expand_ms,
+                S->launch_ms, S->put_ms, S->issue_ms, S->wait_ms, S->replay_ms);
     return FO_OK;
 }
 

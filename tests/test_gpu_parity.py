@@ -417,3 +417,19 @@ def test_hw_oracle_jitter_is_deterministic_and_bounded():
     assert a == b
     for gid, d in c.items():
         assert abs(a[gid] - d) <= 0.05 * d + 1e-12
+
+
+@pytest.mark.parametrize("name", ["vgg16", "bert"])
+def test_speculative_search_equals_plain(name, monkeypatch):
+    """One-step speculation (FO_SEARCH_SPEC) changes only how many device round
+    trips a search takes: traces, counters and results are identical."""
+    g, cps = providers(name, N.FO_PREC_FP64)
+    cfg = P.SearchConfig(alpha=1.05, beta=10, max_unchanged=60 if name == "bert" else 200)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FO_SEARCH_SPEC", mode)
+        res = P.lockstep_search(g, cfg, cps["mp"], [0, 1, 2])
+        out[mode] = [(r.steps, r.candidates_evaluated, r.candidates_enqueued, r.best_cost_us,
+                      [(t.step, t.action, t.cost_us, t.best_cost_us, t.queue_len, t.enqueued) for t in r.trace])
+                     for r in res]
+    assert out["0"] == out["1"]
