@@ -262,6 +262,10 @@ int fo_search_destroy(fo_search *s);
 const char *fo_last_error(void);
 /* Device kernel launches issued by this process (for the bench's gpu_launches). */
 int64_t fo_kernel_launches(void);
+/* Measurement hook (phase timing in bench.py): subsequent launches on g return
+ * after K1 contraction (phase 1) or K2 estimation (phase 2) with cost 0 /
+ * status OK; 0 restores full scoring. */
+int fo_set_phase_stop(fo_graph *g, int32_t phase);
 
 #ifdef __cplusplus
 }

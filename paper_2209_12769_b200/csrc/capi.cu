@@ -125,6 +125,12 @@ extern "C" {
 const char *fo_last_error(void) { return fo::g_last_error.c_str(); }
 int64_t fo_kernel_launches(void) { return fo::g_launches.load(); }
 
+int fo_set_phase_stop(fo_graph *g, int32_t phase) {
+    if (!g || phase < 0 || phase > 2) return fail(FO_INVALID_ARG, "phase must be 0, 1 or 2");
+    g->dg.phase_stop = phase;
+    return FO_OK;
+}
+
 int fo_graph_create(const fo_graph_desc *d, int32_t device, fo_graph **out) {
     if (!d || !out) return fail(FO_INVALID_ARG, "null argument");
     const int V = d->n_ops, E = d->n_edges, A = d->n_allreduces;

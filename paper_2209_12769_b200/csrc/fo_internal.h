@@ -53,6 +53,7 @@ struct DGraph {
     int32_t pairs_max;          // bound on contracted dependency pairs per candidate
     MemoEnt *memo[2];           // MP predictions by member set: [fp32, fp64]
     uint32_t memo_mask;
+    int32_t phase_stop;         // measurement hook: launches stop after K1 (1) or K2 (2); 0 = full
     // hardware-oracle jitter (workloads.py:254-291): noise, "{seed}|" prefix,
     // per-op content-key fragments (CSR over ops)
     double noise;

@@ -600,6 +600,7 @@ struct ScoreArgs {
     const int32_t *dbase, *doff, *dchg;  // sparse candidates (DeltaIn) when dbase != nullptr
     int idx16;
     int retry_only;  // second pass: only candidates a first pass flagged kRetryLarge
+    int stop_after;  // measurement hook (fo_set_phase_stop): 1 = after K1, 2 = after K2, 0 = full
     int K, VB;
     int sm_nodes, sm_pairs, sm_bytes;  // per-warp shared-memory simulation arena
     char *ws;
@@ -1438,6 +1439,10 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         w.prank()[G + b] = pr;
     }
 
+    if (a.stop_after == 1) {  // phase timing only (fo_set_phase_stop)
+        if (tid == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
+        return;
+    }
     // ---- K2: durations of every node (simulator.py:62)
     long long badk = LLONG_MAX;
     #pragma unroll 4
@@ -1565,6 +1570,10 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         return;
     }
 
+    if (a.stop_after == 2) {  // phase timing only (fo_set_phase_stop)
+        if (tid == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
+        return;
+    }
     // ---- K3: two-lane discrete-event simulation (simulator.py:66-140)
     const bool small = N < 65536 && w.sptr()[N] < 65536 && 2 * V < 65536;
     if (!small && (N >= (1 << kKeyNodeBits) || 2 * V >= (1 << kKeyNodeBits))) {
@@ -1740,6 +1749,7 @@ cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, co
                          const DeltaIn *delta) {
     ScoreArgs a;
     a.retry_only = retry_only;
+    a.stop_after = g.phase_stop;
     a.dbase = delta ? delta->base : nullptr;
     a.doff = delta ? delta->off : nullptr;
     a.dchg = delta ? delta->chg : nullptr;

@@ -12,10 +12,19 @@ torch.cuda.set_device(0)
 g, prof, comm, mp, lin = P.load_workload(cfg)
 cp = P.make_cost_providers(prof, comm, mp, precision=prec)
 dg = cp.device_graph(g)
-ng, rg, bk, gb = dg.make_candidates(np.arange(K, dtype=np.uint64))
-d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
+delta = os.environ.get("FO_PROF_ENCODING", "delta") == "delta"  # bench.py's default encoding
 cost = torch.empty(K, dtype=torch.float64, device="cuda"); st = torch.empty(K, dtype=torch.int32, device="cuda")
+if delta:
+    dg.set_parent()
+    off, chg = dg.make_candidates_delta(np.arange(K, dtype=np.uint64))
+    d_off, d_chg = torch.from_numpy(off).cuda(), torch.from_numpy(chg).cuda()
+else:
+    ng, rg, bk, gb = dg.make_candidates(np.arange(K, dtype=np.uint64))
+    d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
 for _ in range(reps):
-    dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
+    if delta:
+        dg.score_delta_device(d_off, d_chg, cost, st, prec)
+    else:
+        dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
 torch.cuda.synchronize()
 print("ok", float(cost.mean()), int(st.max()))
