@@ -433,3 +433,17 @@ def test_speculative_search_equals_plain(name, monkeypatch):
                       [(t.step, t.action, t.cost_us, t.best_cost_us, t.queue_len, t.enqueued) for t in r.trace])
                      for r in res]
     assert out["0"] == out["1"]
+
+
+def test_delta_scoring_needs_parent_and_handles_empty():
+    g, prof, comm, mp, lin = P.load_workload("chain24")
+    dg = P.make_cost_providers(prof, comm, mp).device_graph(g)  # fresh handle: no parent yet
+    with pytest.raises(P.GraphFormatError):
+        dg.score_delta_host(np.array([0, 0], np.int32), np.zeros((0, 2), np.int32))
+    dg.set_parent()
+    cost, st = dg.score_delta_host(np.zeros(1, np.int32), np.zeros((0, 2), np.int32))  # K = 0
+    assert cost.shape == (0,)
+    base, _ = dg.score_delta_host(np.array([0, 0], np.int32), np.zeros((0, 2), np.int32))  # the parent itself
+    ng, rg, bk, vb, _, _ = __import__("paper_2209_12769_b200.graph", fromlist=["x"]).state_arrays(g)
+    ref, _ = dg.score_host(ng[None], rg[None], bk[None], vb)
+    assert base[0] == ref[0] and base[0] > 0

@@ -200,3 +200,12 @@ def test_delta_candidates_reconstruct_dense(name):
             assert len(np.unique(c[:, 0])) == len(c)
             x[c[:, 0]] = c[:, 1]
             assert np.array_equal(x, np.concatenate([ng[k], rg[k], bk[k]])), (name, k)
+
+
+def test_delta_candidates_edge_cases():
+    g = P.load_workload("chain24")[0]
+    dg = engine_graph(g)
+    off, chg = dg.make_candidates_delta(np.zeros(0, np.uint64))
+    assert off.tolist() == [0] and chg.shape == (0, 2)
+    off, chg = dg.make_candidates_delta(np.arange(5, dtype=np.uint64), beta=0)  # n = 0 rewrites: no changes
+    assert off.tolist() == [0] * 6
