@@ -447,3 +447,66 @@ def test_delta_scoring_needs_parent_and_handles_empty():
     ng, rg, bk, vb, _, _ = __import__("paper_2209_12769_b200.graph", fromlist=["x"]).state_arrays(g)
     ref, _ = dg.score_host(ng[None], rg[None], bk[None], vb)
     assert base[0] == ref[0] and base[0] > 0
+
+
+# ---- the reference's estimator known answers (test_estimator.py:101-139, :351-418)
+
+KB = 1024
+
+
+def _two_op_worked_example():
+    """test_estimator.py:101-118: external 10 KB input -> op 1 (raw 100 us,
+    50 KB out) -> op 2 (raw 200 us, 20 KB out); launch 5 us, 1 us per KB."""
+    ops = [op(0, code="Src", out=10 * KB, us=1.0, key="src"), op(1, code="Mul", out=50 * KB, us=100.0, key="m1"),
+           op(2, code="Mul", out=20 * KB, us=200.0, key="m2")]
+    g = build_graph(ops, [DataEdge(0, 1, 10 * KB), DataEdge(1, 2, 50 * KB)])
+    prof = P.Profile({("Src", "src"): 16.0, ("Mul", "m1"): 165.0, ("Mul", "m2"): 275.0})
+    return g, prof
+
+
+@pytest.mark.parametrize("precision", [N.FO_PREC_FP32, N.FO_PREC_FP64])
+def test_analytic_worked_example(precision):
+    g, prof = _two_op_worked_example()
+    cp = P.make_cost_providers(prof, P.CommModelParams(0.0, 1.0), P.analytic_model(5.0, 1.0 / KB), precision)
+    fused = build_graph(g.ops, g.edges, groups=[FusionGroup(0, frozenset({0})), FusionGroup(1, frozenset({1, 2}))])
+    # unfused 165 + 275 = 440; fused keeps the 50 KB tensor on chip: 300 + 5 + 30 = 335
+    assert P.predict_fused_groups(cp, fused)[1] == pytest.approx(335.0, rel=1e-12)
+    # a singleton group is the profile lookup itself (estimator.py:810-814)
+    assert cp.node_durations(g)[0][1] == 165.0
+
+
+def _zero_mp_model(vocab=("Mul", "<other>"), hidden=4, layers=2, c3=1.7):
+    feat = 6 + len(vocab)
+    p = {"W_emb": np.zeros((hidden, feat)), "W_r": np.zeros((hidden, hidden)), "A1": np.zeros((hidden, hidden)),
+         "c1": np.zeros(hidden), "A2": np.zeros((hidden, hidden)), "c2": np.zeros(hidden), "a3": np.zeros(hidden),
+         "c3": np.array(c3)}
+    for layer in range(1, layers + 1):
+        p[f"W_{layer}"] = np.zeros((hidden, hidden))
+    return P.EstimatorModel(P.EstimatorVariant.MESSAGE_PASSING, p, vocab=vocab, layers=layers, hidden=hidden)
+
+
+@pytest.mark.parametrize("precision", [N.FO_PREC_FP32, N.FO_PREC_FP64])
+def test_mp_zero_weights_constant_output(precision):
+    """test_estimator.py:376-382: all-zero weights give softplus(c3) for any group."""
+    rng = random.Random(6)
+    expected = float(np.logaddexp(0, 1.7))
+    for _ in range(5):
+        n = rng.randrange(3, 9)
+        g = build_graph([op(i, code=rng.choice(["Mul", "Conv2D"]), us=rng.uniform(1, 50)) for i in range(n)],
+                        [DataEdge(i, i + 1, 64) for i in range(n - 1)])
+        prof = P.Profile({(o.op_code, o.input_shape_key): o.compute_us for o in g.ops})
+        cp = P.make_cost_providers(prof, P.CommModelParams(0.0, 1.0), _zero_mp_model(), precision)
+        fused = build_graph(g.ops, g.edges, groups=[FusionGroup(0, frozenset(range(n)))])
+        assert P.predict_fused_groups(cp, fused)[0] == pytest.approx(expected, rel=1e-6 if precision == N.FO_PREC_FP32 else 1e-15)
+
+
+def test_mp_dimension_mismatch():
+    """test_estimator.py:413-418: a W_emb that does not match the feature width
+    raises DimensionMismatch for fused groups."""
+    g, prof = _two_op_worked_example()
+    m = _zero_mp_model(vocab=("Mul", "<other>"))
+    m.params["W_emb"] = np.zeros((4, 99))
+    cp = P.make_cost_providers(prof, P.CommModelParams(0.0, 1.0), m)
+    fused = build_graph(g.ops, g.edges, groups=[FusionGroup(0, frozenset({0})), FusionGroup(1, frozenset({1, 2}))])
+    with pytest.raises(P.DimensionMismatch):
+        P.cost(fused, cp)
