@@ -31,11 +31,11 @@ int fail(int status, const std::string &msg) {
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int nws) {
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int nws, int alt) {
     *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, big ? g->V : kMpCapDefault, nws);
     size_t need = (size_t)L->total * (size_t)slots;
-    char *&buf = big ? g->d_ws_big : g->d_ws;
-    size_t &have = big ? g->ws_big_bytes : g->ws_bytes;
+    char *&buf = big ? g->d_ws_big : (alt ? g->d_ws_alt : g->d_ws);
+    size_t &have = big ? g->ws_big_bytes : (alt ? g->ws_alt_bytes : g->ws_bytes);
     if (need > have) {
         if (buf) cudaFree(buf);
         buf = nullptr;
@@ -49,7 +49,7 @@ int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int 
 static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
                   double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream,
-                  const DeltaIn *delta = nullptr) {
+                  const DeltaIn *delta = nullptr, int alt_ws = 0) {
     ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
     const int nws = score_team_warps(geo);
     WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, kMpCapDefault, nws);
@@ -60,9 +60,10 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
     int max_blocks = (int)std::max<size_t>(1, budget / ((size_t)L.total * per_block));
     geo.grid = std::min(geo.grid, max_blocks);
     int slots = score_slots(geo);
-    int st = ensure_workspace(g, VB, slots, &L, false, nws);
+    int st = ensure_workspace(g, VB, slots, &L, false, nws, alt_ws);
     if (st) return st;
-    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws, L, geo, cost, status, ext_dur, tl,
+    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, alt_ws ? g->d_ws_alt : g->d_ws, L, geo,
+                                 cost, status, ext_dur, tl,
                                  dur_out, bad_out, ngroups_out, stream, 0, delta);
     g_launches++;
     if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score kernel launch: ") + cudaGetErrorString(e));
@@ -87,7 +88,7 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
 }
 
 int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
-                 int precision, double *cost, int32_t *status, cudaStream_t stream) {
+                 int precision, double *cost, int32_t *status, cudaStream_t stream, int alt_ws) {
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
     if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set (fo_graph_set_cost_model)");
     if (K <= 0) return FO_OK;
@@ -96,7 +97,7 @@ int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bk
     CUDA_TRY(cudaSetDevice(g->device));
     TimelineOut tl{};
     return launch(g, ngid, rgid, bkt, idx16, K, VB, precision, cost, status, nullptr, tl, nullptr, nullptr, nullptr,
-                  stream);
+                  stream, nullptr, alt_ws);
 }
 
 // sparse candidates against the resident parent (fo_set_parent)
@@ -241,6 +242,7 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_model) cudaFree(g->d_model);
     if (g->d_ws) cudaFree(g->d_ws);
     if (g->d_ws_big) cudaFree(g->d_ws_big);
+    if (g->d_ws_alt) cudaFree(g->d_ws_alt);
     if (g->d_memo) cudaFree(g->d_memo);
     if (g->d_keys) cudaFree(g->d_keys);
     if (g->d_io) cudaFree(g->d_io);

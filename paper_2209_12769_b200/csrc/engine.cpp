@@ -1676,6 +1676,8 @@ struct fo_search {
         size_t hc_cap = 0;
         int n = 0;
         cudaEvent_t done = nullptr, e0 = nullptr, e1 = nullptr;
+        cudaStream_t stream = nullptr;  // lane 1: its own stream and workspace (concurrent halves)
+        int alt = 0;
     };
     std::vector<Seed> seeds;
     Lane lanes[2];
@@ -1720,9 +1722,19 @@ static int lane_reserve(fo_search *S, fo_search::Lane &L, int n) {
     return FO_OK;
 }
 
+// bytes per id in the staged batch: int16 whenever the ids fit (half the H2D)
+static size_t id_bytes(const fo_search *S) { return (S->eng->VB <= 32767 && S->g->A <= 32767) ? 2 : 4; }
+
 // write candidate j of an n-candidate batch (SoA [ng * n | rg * n | bk * n])
 static void lane_put(fo_search *S, fo_search::Lane &L, int n, int j, const State &s) {
     const int V = S->g->V, A = S->g->A;
+    if (id_bytes(S) == 2) {
+        int16_t *b = (int16_t *)L.h_buf;
+        std::copy(s.ng.begin(), s.ng.end(), b + (size_t)j * V);
+        std::copy(s.rg.begin(), s.rg.end(), b + (size_t)V * n + (size_t)j * V);
+        std::copy(s.bk.begin(), s.bk.end(), b + (size_t)2 * V * n + (size_t)j * A);
+        return;
+    }
     std::copy(s.ng.begin(), s.ng.end(), L.h_buf + (size_t)j * V);
     std::copy(s.rg.begin(), s.rg.end(), L.h_buf + (size_t)V * n + (size_t)j * V);
     std::copy(s.bk.begin(), s.bk.end(), L.h_buf + (size_t)2 * V * n + (size_t)j * A);
@@ -1736,15 +1748,16 @@ static int lane_launch(fo_search *S, fo_search::Lane &L, int n) {
     L.n = n;
     if (n == 0) return FO_OK;
     char *db = L.d_buf;
-    size_t cost_off = (W * n * 4 + 255) & ~size_t(255);
-    int32_t *dn = (int32_t *)db, *dr = dn + (size_t)V * n, *dk = dr + (size_t)V * n;
+    const size_t eb = id_bytes(S);
+    size_t cost_off = (W * n * eb + 255) & ~size_t(255);
+    const char *dn = db, *dr = dn + (size_t)V * n * eb, *dk = dr + (size_t)V * n * eb;
     double *dc = (double *)(db + cost_off);
     int32_t *ds = (int32_t *)(dc + n);
-    cudaStream_t st = g->stream;
-    if (cudaMemcpyAsync(db, L.h_buf, W * n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    cudaStream_t st = L.stream ? L.stream : g->stream;
+    if (cudaMemcpyAsync(db, L.h_buf, W * n * eb, cudaMemcpyHostToDevice, st) != cudaSuccess)
         return fail(FO_CUDA_ERROR, "search batch H2D");
     cudaEventRecord(L.e0, st);
-    int rc = score_device(g, dn, dr, dk, 0, n, S->eng->VB, S->cfg.precision, dc, ds, st);
+    int rc = score_device(g, dn, dr, dk, eb == 2, n, S->eng->VB, S->cfg.precision, dc, ds, st, L.alt);
     if (rc) return rc;
     cudaEventRecord(L.e1, st);
     cudaMemcpyAsync(L.h_cost, dc, 8 * (size_t)n, cudaMemcpyDeviceToHost, st);
@@ -1905,6 +1918,8 @@ static int search_launch(fo_search *S, fo_search::Lane &L, int lo, int hi) {
     if (n > 0) {
         int rc = lane_reserve(S, L, n);
         if (rc) return rc;
+        const int nthreads = S->cfg.n_threads > 0 ? S->cfg.n_threads : omp_get_max_threads();
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 4) if (hi - lo > 8)
         for (int r = lo; r < hi; r++) {
             auto &sd = S->seeds[r];
             for (int j = 0; j < sd.ncand; j++)  // duplicates write the same state twice
@@ -1974,6 +1989,9 @@ static void replay_seed(fo_search *S, fo_search::Seed &sd, const fo_search::Lane
 }
 
 static void search_replay(fo_search *S, fo_search::Lane &L, int lo, int hi) {
+    const int nthreads = S->cfg.n_threads > 0 ? S->cfg.n_threads : omp_get_max_threads();
+    // seeds are independent: their bookkeeping replays in parallel
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 4) if (hi - lo > 8)
     for (int r = lo; r < hi; r++) {
         auto &sd = S->seeds[r];
         for (int q = 0; q < sd.nbr; q++)  // speculative results first (not yet evaluations)
@@ -2049,6 +2067,95 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
 // code.  With R >= 2 the seeds are split in two halves whose device batches
 // alternate with the other half's host-side expand, so host and device
 // overlap; each seed's own step sequence is unchanged.
+static bool any_active(const fo_search *S, int lo, int hi) {
+    for (int r = lo; r < hi; r++)
+        if (S->seeds[r].active) return true;
+    return false;
+}
+
+// up to `limit` rounds (< 0: no limit), one batch in flight; returns rounds run
+static int run_single(fo_search *S, int64_t limit, int &rc) {
+    using clk = std::chrono::steady_clock;
+    auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const int R = (int)S->seeds.size();
+    int64_t it = 0;
+    rc = FO_OK;
+    for (; (limit < 0 || it < limit) && any_active(S, 0, R); it++) {
+        search_expand(S, 0, R);
+        const auto t0 = clk::now();
+        if ((rc = search_launch(S, S->lanes[0], 0, R))) return (int)it;
+        const auto t1 = clk::now();
+        if ((rc = lane_wait(S, S->lanes[0]))) return (int)it;
+        const auto t2 = clk::now();
+        search_replay(S, S->lanes[0], 0, R);
+        S->launch_ms += ms(t0, t1);
+        S->wait_ms += ms(t1, t2);
+        S->replay_ms += ms(t2, clk::now());
+    }
+    return (int)it;
+}
+
+// seeds split in two halves whose host expand overlaps the other half's device
+// batch; up to `limit` rounds, both lanes drained on return
+static int run_pipelined(fo_search *S, int64_t limit, int &rc) {
+    const int R = (int)S->seeds.size(), mid = R / 2;
+    auto &LA = S->lanes[0], &LB = S->lanes[1];
+    // the halves' batches are latency-bound: on two streams with two workspaces
+    // they run concurrently (not when a second pass would share its scratch)
+    if (!LB.stream && S->g->V <= kMpCapDefault) {
+        if (cudaStreamCreateWithFlags(&LB.stream, cudaStreamNonBlocking) == cudaSuccess) LB.alt = 1;
+        else LB.stream = nullptr;
+    }
+    bool b_inflight = false;
+    int64_t it = 0;
+    rc = FO_OK;
+    if (!any_active(S, 0, R)) return 0;
+    search_expand(S, 0, mid);
+    if ((rc = search_launch(S, LA, 0, mid))) return 0;
+    using clk = std::chrono::steady_clock;
+    auto ms = [](clk::time_point x, clk::time_point y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+    for (; limit < 0 || it < limit; it++) {
+        auto t0 = clk::now();
+        if (b_inflight) {
+            if ((rc = lane_wait(S, LB))) return (int)it;
+            search_replay(S, LB, mid, R);
+        }
+        auto t1 = clk::now();
+        S->wait_ms += ms(t0, t1);
+        bool b_live = any_active(S, mid, R);
+        if (b_live) {
+            search_expand(S, mid, R);  // overlaps A's device batch
+            auto t2 = clk::now();
+            if ((rc = search_launch(S, LB, mid, R))) return (int)it;
+            S->launch_ms += ms(t2, clk::now());
+        }
+        b_inflight = b_live;
+        auto t3 = clk::now();
+        if ((rc = lane_wait(S, LA))) return (int)it;
+        search_replay(S, LA, 0, mid);
+        S->wait_ms += ms(t3, clk::now());
+        bool a_live = any_active(S, 0, mid);
+        if (!a_live && !b_inflight) { it++; break; }
+        if (a_live && (limit < 0 || it + 1 < limit)) {
+            search_expand(S, 0, mid);  // overlaps B's device batch
+            auto t4 = clk::now();
+            if ((rc = search_launch(S, LA, 0, mid))) return (int)it;
+            S->launch_ms += ms(t4, clk::now());
+        } else {
+            LA.n = 0;
+            if (!b_inflight) { it++; break; }
+        }
+    }
+    if (b_inflight) {
+        if ((rc = lane_wait(S, LB))) return (int)it;
+        search_replay(S, LB, mid, R);
+    }
+    if ((rc = lane_wait(S, LA))) return (int)it;
+    if (LA.n) search_replay(S, LA, 0, mid);
+    LA.n = LB.n = 0;
+    return (int)it;
+}
+
 int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
     if (!S) return fail(FO_INVALID_ARG, "null search");
     fo_graph *g = S->g;
@@ -2057,74 +2164,33 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
     int rc = search_start(S);
     if (rc) return rc;
     const int R = (int)S->seeds.size();
-    auto any_active = [&](int lo, int hi) {
-        for (int r = lo; r < hi; r++)
-            if (S->seeds[r].active) return true;
-        return false;
-    };
-    // Probe rounds decide the schedule: splitting the seeds in two halves only
-    // pays when the host expand outweighs a device batch (a batch of search
-    // candidates is latency-bound, so halving it does not halve its time).
+    using clk = std::chrono::steady_clock;
+    auto left = [&](int64_t it) { return max_rounds <= 0 ? (int64_t)-1 : std::max<int64_t>(0, max_rounds - it); };
+    auto cap = [](int64_t l, int64_t n) { return l < 0 ? n : std::min(l, n); };
+    // Probe rounds pick the schedule by measured wall time per round: one batch
+    // of all seeds, or two halves whose host expand overlaps the other half's
+    // device batch (a half batch is not half the time: search batches are
+    // latency-bound).  Speculating drivers (few seeds) keep one batch.
     int64_t it = 0;
-    const int probe = R == 1 ? INT32_MAX : 8;
-    const double d0 = S->device_ms, e0 = S->expand_ms;
-    for (; (max_rounds <= 0 || it < max_rounds) && it < probe && any_active(0, R); it++) {
-        search_expand(S, 0, R);
-        if ((rc = search_launch(S, S->lanes[0], 0, R)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
-        search_replay(S, S->lanes[0], 0, R);
+    bool pipeline = false;
+    if (R > 1 && !S->spec) {
+        const int probe = 8;
+        auto t0 = clk::now();
+        int n1 = run_single(S, cap(left(it), probe), rc);
+        if (rc) return rc;
+        it += n1;
+        const double w1 = std::chrono::duration<double>(clk::now() - t0).count() / std::max(n1, 1);
+        t0 = clk::now();
+        int n2 = run_pipelined(S, cap(left(it), probe), rc);
+        if (rc) return rc;
+        it += n2;
+        const double w2 = std::chrono::duration<double>(clk::now() - t0).count() / std::max(n2, 1);
+        pipeline = n1 > 0 && n2 > 0 && w2 < w1;
     }
-    const bool pipeline = R > 1 && (S->expand_ms - e0) > 2.0 * (S->device_ms - d0);
-    if (pipeline) S->spec = false;  // halves overlap instead
-    if (!pipeline) {
-        using clk = std::chrono::steady_clock;
-        auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-        for (; (max_rounds <= 0 || it < max_rounds) && any_active(0, R); it++) {
-            search_expand(S, 0, R);
-            const auto t0 = clk::now();
-            if ((rc = search_launch(S, S->lanes[0], 0, R))) return rc;
-            const auto t1 = clk::now();
-            if ((rc = lane_wait(S, S->lanes[0]))) return rc;
-            const auto t2 = clk::now();
-            search_replay(S, S->lanes[0], 0, R);
-            S->launch_ms += ms(t0, t1);
-            S->wait_ms += ms(t1, t2);
-            S->replay_ms += ms(t2, clk::now());
-        }
-    } else {
-        const int mid = R / 2;
-        auto &LA = S->lanes[0], &LB = S->lanes[1];
-        bool b_inflight = false;
-        search_expand(S, 0, mid);
-        if ((rc = search_launch(S, LA, 0, mid))) return rc;
-        for (; max_rounds <= 0 || it < max_rounds; it++) {
-            if (b_inflight) {
-                if ((rc = lane_wait(S, LB))) return rc;
-                search_replay(S, LB, mid, R);
-            }
-            bool b_live = any_active(mid, R);
-            if (b_live) {
-                search_expand(S, mid, R);  // overlaps A's device batch
-                if ((rc = search_launch(S, LB, mid, R))) return rc;
-            }
-            b_inflight = b_live;
-            if ((rc = lane_wait(S, LA))) return rc;
-            search_replay(S, LA, 0, mid);
-            bool a_live = any_active(0, mid);
-            if (!a_live && !b_inflight) break;
-            if (a_live && (max_rounds <= 0 || it + 1 < max_rounds)) {
-                search_expand(S, 0, mid);  // overlaps B's device batch
-                if ((rc = search_launch(S, LA, 0, mid))) return rc;
-            } else {
-                LA.n = 0;
-                if (!b_inflight) break;
-            }
-        }
-        if (b_inflight) {
-            if ((rc = lane_wait(S, LB))) return rc;
-            search_replay(S, LB, mid, R);
-        }
-        if ((rc = lane_wait(S, LA))) return rc;
-        if (LA.n) search_replay(S, LA, 0, mid);
+    const int64_t rest = left(it);
+    if (rest != 0) {
+        it += pipeline ? run_pipelined(S, rest, rc) : run_single(S, rest, rc);
+        if (rc) return rc;
     }
     if (active_out) *active_out = count_active(S, nullptr);
     if (getenv("FO_SEARCH_PROFILE"))
@@ -2166,6 +2232,7 @@ int fo_search_destroy(fo_search *S) {
     if (!S) return FO_OK;
     for (auto &L : S->lanes) {
         if (L.d_buf) cudaFree(L.d_buf);
+        if (L.stream) cudaStreamDestroy(L.stream);
         if (L.h_buf) cudaFreeHost(L.h_buf);
         if (L.h_cost) cudaFreeHost(L.h_cost);
         if (L.h_status) cudaFreeHost(L.h_status);

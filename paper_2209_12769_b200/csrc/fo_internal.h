@@ -153,6 +153,8 @@ struct fo_graph {
     size_t ws_bytes = 0;
     char *d_ws_big = nullptr;  // second-pass workspace for fused groups beyond kMpCapDefault
     size_t ws_big_bytes = 0;
+    char *d_ws_alt = nullptr;  // a second first-pass workspace: concurrent batches on another stream
+    size_t ws_alt_bytes = 0;
     // host API staging
     void *d_io = nullptr;
     // resident parent of sparse (delta) candidates, engine ids
@@ -170,8 +172,8 @@ namespace fo {
 void set_error(const std::string &msg);
 int fail(int status, const std::string &msg);
 // Ensure the handle's workspace can hold `slots` warps for gid bound VB.
-int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big = false, int nws = 1);
+int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big = false, int nws = 1, int alt = 0);
 // Score K device-resident candidates (used by fo_score and the search engine).
 int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
-                 int precision, double *cost, int32_t *status, cudaStream_t stream);
+                 int precision, double *cost, int32_t *status, cudaStream_t stream, int alt_ws = 0);
 }  // namespace fo
