@@ -23,20 +23,55 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def timed_score(dg, ng, rg, bk, gb, prec, reps=5):
+    """Dense candidates resident on the device; memo emptied before each rep."""
+    import ctypes
+
     import numpy as np
     import torch
+
+    from paper_2209_12769_b200 import _native as N
 
     d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
     K = ng.shape[0]
     cost = torch.empty(K, dtype=torch.float64, device="cuda")
     st = torch.empty(K, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
     dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
+        N.lib().fo_memo_clear(dg.h, ctypes.c_void_p(s.cuda_stream))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return cost.cpu().numpy(), st.cpu().numpy(), float(np.median(ts))
+
+
+def timed_score_delta(dg, off, chg, prec, reps=5):
+    """Sparse candidates against the handle's resident parent (fo_score_delta)."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2209_12769_b200 import _native as N
+
+    K = len(off) - 1
+    d_off, d_chg = torch.from_numpy(off).cuda(), torch.from_numpy(chg).cuda()
+    cost = torch.empty(K, dtype=torch.float64, device="cuda")
+    st = torch.empty(K, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
+    dg.score_delta_device(d_off, d_chg, cost, st, prec)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        N.lib().fo_memo_clear(dg.h, ctypes.c_void_p(s.cuda_stream))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dg.score_delta_device(d_off, d_chg, cost, st, prec)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
@@ -58,7 +93,7 @@ def gpt2_sweep(args):
     cp64 = P.make_cost_providers(prof, comm, mp, precision=N.FO_PREC_FP64)  # decision-exact parents
     dg = cp.device_graph(g)
     sweep = read("sweep_gpt2m.json.gz")
-    rows, worst, total_c, total_ms, gen_s = [], 0.0, 0, 0.0, 0.0
+    rows, worst, total_c, total_ms, gen_s, total_ms_dense = [], 0.0, 0, 0.0, 0.0, 0.0
     from paper_2209_12769_b200.graph import state_arrays
     from _golden import canon_doc, canon_graph
 
@@ -81,16 +116,21 @@ def gpt2_sweep(args):
             worst = max(worst, rel)
             ng0, rg0, bk0, _, _, _ = state_arrays(parent)
             t0 = time.perf_counter()
-            ng, rg, bk, gb = dg.make_candidates(np.arange(args.batch, dtype=np.uint64), base=(ng0, rg0, bk0))
+            dg.set_parent(ng0, rg0, bk0)  # the parent stays resident; candidates are its changes
+            off, chg = dg.make_candidates_delta(np.arange(args.batch, dtype=np.uint64), base=(ng0, rg0, bk0))
             gen_s += time.perf_counter() - t0
-            cost, st, ms = timed_score(dg, ng, rg, bk, gb, prec)
-            assert (st == 0).all()
+            cost, st, ms = timed_score_delta(dg, off, chg, prec)
+            ng, rg, bk, gb = dg.make_candidates(np.arange(args.batch, dtype=np.uint64), base=(ng0, rg0, bk0))
+            c2, st2, ms_d = timed_score(dg, ng, rg, bk, gb, prec, reps=3)
+            assert (st == 0).all() and np.array_equal(c2, cost)
             total_c += args.batch
             total_ms += ms
+            total_ms_dense += ms_d
             rows.append({"T": ent["T"], "parent": kind, "parent_cost_us": c_dev, "ref_parent_cost_us": ent[kind]["cost"],
                          "batch_best_us": float(cost.min()), "batch_ms": ms})
     line = {"metric": "fusion candidates scored/sec (GNN est.+sim)", "config": "gpt2m bucket-size sweep",
             "value": total_c / (total_ms / 1e3), "unit": "candidates/s", "n_gpus": 1,
+            "encoding": "sparse changes vs each resident parent", "value_dense_int32": total_c / (total_ms_dense / 1e3),
             "thresholds": len(sweep["sweep"]), "batch_per_parent": args.batch, "parents": len(rows),
             "parent_cost_max_rel_err_vs_reference": worst, "parents_match_reference": bool(match),
             "parents_build_s": parents_s, "candidate_generation_s": gen_s,
@@ -110,19 +150,36 @@ def synth50k(args):
     g, prof, comm, mp, lin = P.load_workload("synth50k")
     cp = P.make_cost_providers(prof, comm, mp, precision=prec)
     dg = cp.device_graph(g)
-    # the host rewrite engine rebuilds the full index per rewrite (~0.2 s per
-    # rewrite at 50k ops), so a bounded set of distinct candidates is generated
-    # and tiled to the round size; every tile is scored independently
-    t0 = time.perf_counter()
+    # every candidate distinct (the incremental engine: ~0.5 ms per candidate
+    # per thread at 50k ops), in the sparse form the round is scored in
     nd = min(args.distinct, args.batch)
-    ng, rg, bk, gb = dg.make_candidates(np.arange(nd, dtype=np.uint64), beta=args.beta)
+    t0 = time.perf_counter()
+    dg.set_parent()
+    off, chg = dg.make_candidates_delta(np.arange(nd, dtype=np.uint64), beta=args.beta)
     gen_s = time.perf_counter() - t0
-    reps_ = (args.batch + nd - 1) // nd
-    ng, rg, bk = (np.ascontiguousarray(np.tile(x, (reps_, 1))[: args.batch]) for x in (ng, rg, bk))
-    cost, st, ms = timed_score(dg, ng, rg, bk, gb, prec, reps=3)
+    if nd < args.batch:  # tile the distinct set to the round size
+        reps_ = (args.batch + nd - 1) // nd
+        sizes = np.diff(off)
+        sizes = np.tile(sizes, reps_)[: args.batch]
+        chg = np.concatenate([chg] * reps_)[: int(sizes.sum())]
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    cost, st, ms = timed_score_delta(dg, off, chg, prec, reps=3)
+    # the same round with dense int32 encodings, for comparison
+    V, A = dg.V, dg.A
+    base = np.concatenate([np.arange(V), -np.ones(V), np.arange(A)]).astype(np.int32)
+    dense = np.tile(base, (args.batch, 1))
+    for k in range(args.batch):
+        c = chg[off[k]:off[k + 1]]
+        dense[k, c[:, 0]] = c[:, 1]
+    c2, st2, ms_dense = timed_score(dg, np.ascontiguousarray(dense[:, :V]), np.ascontiguousarray(dense[:, V:2 * V]),
+                                    np.ascontiguousarray(dense[:, 2 * V:]), 2 * V + 2, prec, reps=3)
+    assert np.array_equal(c2, cost) and np.array_equal(st2, st)
     line = {"metric": "fusion candidates scored/sec (GNN est.+sim)", "config": "synthetic 50k-op DAG, one round",
             "value": args.batch / (ms / 1e3), "unit": "candidates/s", "n_gpus": 1, "batch": args.batch,
-            "beta": args.beta, "ms_per_round": ms, "candidate_generation_s": gen_s, "distinct_candidates": nd,
+            "beta": args.beta, "ms_per_round": ms, "encoding": "sparse changes vs resident parent",
+            "changes_per_candidate": float(off[-1]) / args.batch, "bytes_per_candidate_sparse": 8 * float(off[-1]) / args.batch + 4,
+            "bytes_per_candidate_dense": 4 * (2 * V + A), "ms_per_round_dense_int32": ms_dense,
+            "candidate_generation_s": gen_s, "distinct_candidates": nd,
             "statuses": {str(k): int(v) for k, v in zip(*np.unique(st, return_counts=True))},
             "best_us": float(cost[st == 0].min()) if (st == 0).any() else None}
     if args.check > 0:
@@ -145,7 +202,7 @@ if __name__ == "__main__":
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--beta", type=int, default=10)
     ap.add_argument("--check", type=int, default=2)
-    ap.add_argument("--distinct", type=int, default=1024)
+    ap.add_argument("--distinct", type=int, default=8192)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     a = ap.parse_args()
     if a.what == "gpt2-sweep":
