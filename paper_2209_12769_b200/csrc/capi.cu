@@ -73,11 +73,16 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
         WsLayout Lb;
         ScoreGeo gb = geo;
         gb.sm_bytes = 0;
-        gb.team = 0;
-        gb.grid = std::min(std::max(1, (K + score_warps_per_block() - 1) / score_warps_per_block()), g->num_sms);
+        // latency geometry: a block per candidate, so the very large MP groups
+        // (the reason for this pass) run on the whole team (FO_RETRY_TEAM=0: a warp each)
+        const char *rt = getenv("FO_RETRY_TEAM");
+        gb.team = rt ? rt[0] == '1' : 1;
+        const int per_block = gb.team ? 1 : score_warps_per_block();
+        gb.grid = gb.team ? std::min(K, 4 * g->num_sms)
+                          : std::min(std::max(1, (K + per_block - 1) / per_block), g->num_sms);
         Lb = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, g->V);
-        gb.grid = std::min<int>(gb.grid, (int)std::max<size_t>(1, budget / ((size_t)Lb.total * score_warps_per_block())));
-        st = ensure_workspace(g, VB, gb.grid * score_warps_per_block(), &Lb, true, 1);
+        gb.grid = std::min<int>(gb.grid, (int)std::max<size_t>(1, budget / ((size_t)Lb.total * per_block)));
+        st = ensure_workspace(g, VB, gb.grid * per_block, &Lb, true, 1);
         if (st) return st;
         e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, g->d_ws_big, Lb, gb, cost, status, ext_dur, tl,
                          dur_out, bad_out, ngroups_out, stream, 1, delta);

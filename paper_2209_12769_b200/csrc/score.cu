@@ -148,6 +148,9 @@ __device__ __forceinline__ T warp_sum(T v) {
 struct TeamShm {
     int wsum[32];
     long long wll[32];
+    double part[4][32];  // per-warp partial readouts (team MP forward)
+    double bcast;
+    int flag;
 };
 
 template <int TEAM>
@@ -422,7 +425,7 @@ struct Blake2b64 {
 };
 
 // 1 + noise * (2u - 1), u = digest / 2^64 (workloads.py:256-264); ops[] ascending
-__device__ double hw_jitter(const DGraph &g, const int *ops, int n, long long internal, long long ext_in,
+__device__ __noinline__ double hw_jitter(const DGraph &g, const int *ops, int n, long long internal, long long ext_in,
                             long long ext_out) {
     Blake2b64 b;
     b.init();
@@ -1068,6 +1071,163 @@ __device__ bool simulate_smem(const ScoreArgs &a, int k, const Ws &w, int tid, i
     return true;
 }
 
+// Team-level MP forward for very large fused groups (second pass, latency
+// geometry): lane = hidden channel within a warp, nodes split across the
+// team's warps, a team barrier between the aggregation and transform halves of
+// each layer.  The readout sums each warp's nodes, then the warps in order.
+template <typename T, int TEAM>
+__device__ double mp_forward_team(const DGraph &g, const int *mem, int n, const int *nbptr, const int *nb, T *H, T *P,
+                                  int tid, TeamShm *ts) {
+    constexpr int NW = TEAM / 32;
+    const int lane = tid & 31, wid = tid >> 5;
+    const MpLayout ml = mp_layout(g.layers);
+    const T *W = MpW<T>::W(g);
+    const T *H0 = MpW<T>::H0(g);
+    for (int i = wid; i < n; i += NW) H[i * 32 + lane] = __ldg(&H0[(int64_t)mem[i] * 32 + lane]);
+    tsync<TEAM>();
+    for (int l = 0; l < g.layers; l++) {
+        const T *Wt = W + ml.wl + (int64_t)l * 1024;
+        for (int i = wid; i < n; i += NW) {  // mean aggregation (estimator.py:348-355, :374)
+            int b = nbptr[i], e = nbptr[i + 1];
+            T acc = H[i * 32 + lane];
+            for (int q = b; q < e; q++) acc += H[nb[q] * 32 + lane];
+            P[i * 32 + lane] = acc / T(1 + e - b);
+        }
+        tsync<TEAM>();
+        for (int i = wid; i < n; i += 2 * NW) {  // relu(P @ W_l^T), two nodes per weight load
+            const int i1 = i + NW;
+            const bool two = i1 < n;
+            T p0 = P[i * 32 + lane], p1 = two ? P[i1 * 32 + lane] : T(0);
+            T a0 = T(0), a1 = T(0);
+#pragma unroll 8
+            for (int k = 0; k < 32; k++) {
+                T wk = __ldg(&Wt[k * 32 + lane]);
+                a0 = fmaT<T>(__shfl_sync(FULL, p0, k), wk, a0);
+                a1 = fmaT<T>(__shfl_sync(FULL, p1, k), wk, a1);
+            }
+            H[i * 32 + lane] = a0 > T(0) ? a0 : T(0);
+            if (two) H[i1 * 32 + lane] = a1 > T(0) ? a1 : T(0);
+        }
+        tsync<TEAM>();
+    }
+    T part = T(0);
+    for (int i = wid; i < n; i += NW) part += H[i * 32 + lane];
+    ts->part[wid][lane] = (double)part;
+    tsync<TEAM>();
+    double pred = 0.0;
+    if (wid == 0) {
+        T s = T(0);
+        for (int q = 0; q < NW; q++) s += (T)ts->part[q][lane];
+        T r = mat32<T>(W + ml.wr, s, lane);
+        r = r > T(0) ? r : T(0);
+        T d1 = mat32<T>(W + ml.a1, r, lane) + __ldg(&W[ml.c1 + lane]);
+        d1 = d1 > T(0) ? d1 : T(0);
+        T d2 = mat32<T>(W + ml.a2, d1, lane) + __ldg(&W[ml.c2 + lane]);
+        d2 = d2 > T(0) ? d2 : T(0);
+        T z = warp_sum<T>(__ldg(&W[ml.a3 + lane]) * d2) + __ldg(&W[ml.c3]);
+        pred = __dmul_rn(softplus_d((double)z), g.out_scale);
+        pred = pred > 1e-9 ? pred : 1e-9;
+        if (tid == 0) ts->bcast = pred;
+    }
+    tsync<TEAM>();
+    return ts->bcast;
+}
+
+// One very large MP fused group (n > the per-warp scratch), the whole team:
+// canonical member order, member-local undirected neighbour lists, memo,
+// team MP forward (estimator.py:157-191, :363-389).  Scratch: copy 0.
+template <typename T, int TEAM>
+__device__ void process_group_team(const ScoreArgs &a, const Ws &w, const GroupScratch &gs, int f, int tid,
+                                   long long &badk, TeamShm *ts) {
+    const DGraph &g = a.g;
+    const int V = g.V, lane = tid & 31, wid = tid >> 5;
+    const int gi = w.fused()[f];
+    const int b0 = w.gptr()[f], n = w.gptr()[f + 1] - b0;
+    int *mem = w.gmem() + b0;
+    // members ascending: mark, then a team prefix scan over ops
+    for (int v = tid; v < V; v += TEAM) gs.mark[v] = 0;
+    tsync<TEAM>();
+    for (int i = tid; i < n; i += TEAM) gs.mark[mem[i]] = 1;
+    tsync<TEAM>();
+    int o = 0;
+    for (int base = 0; base < V; base += TEAM) {
+        const int v = base + tid;
+        const bool m = v < V && gs.mark[v];
+        int tot;
+        const int pos = tprefix<TEAM>(m, tot, ts, tid);
+        if (m) mem[o + pos] = v;
+        o += tot;
+    }
+    tsync<TEAM>();
+    // memo (member-set hash, as the warp path)
+    MemoEnt *memo = g.memo[sizeof(T) == 8];
+    unsigned long long mh1 = 0, mh2 = 0;
+    if (wid == 0) {
+        set_hash(mem, n, lane, mh1, mh2);
+        double mv = 0.0;
+        bool hit = false;
+        if (lane == 0 && memo) hit = memo_get(memo, g.memo_mask, mh1, mh2, &mv);
+        if (lane == 0) { ts->flag = hit; ts->bcast = mv; }
+    }
+    tsync<TEAM>();
+    if (ts->flag) {
+        if (tid == 0) w.dur()[gi] = ts->bcast;
+        tsync<TEAM>();
+        return;
+    }
+    bool miss = false;
+    for (int i = tid; i < n; i += TEAM) miss |= isnan(g.op_prof[mem[i]]);
+    if (tany<TEAM>(miss)) { badk = min(badk, pack_bad(gi, FO_MISSING_COST)); return; }
+    for (int i = tid; i < n; i += TEAM) gs.lidx[mem[i]] = i;
+    tsync<TEAM>();
+    for (int i = tid; i < n; i += TEAM) {
+        const int v = mem[i];
+        gs.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
+    }
+    tsync<TEAM>();
+    team_exscan<TEAM>(gs.zl, gs.nbptr, n, ts, tid);
+    for (int i = tid; i < n; i += TEAM) {  // unique neighbours inside the group
+        const int v = mem[i];
+        const int o2 = gs.nbptr[i];
+        int c = 0;
+        for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
+            const int s2 = g.e_src[g.in_e[q]];
+            if (!in_grp(w, s2, gi)) continue;
+            const int j = gs.lidx[s2];
+            bool dup = false;
+            for (int t = 0; t < c; t++) dup |= (gs.nb[o2 + t] == j);
+            if (!dup) gs.nb[o2 + c++] = j;
+        }
+        for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
+            const int d2 = g.e_dst[g.out_e[q]];
+            if (!in_grp(w, d2, gi)) continue;
+            const int j = gs.lidx[d2];
+            bool dup = false;
+            for (int t = 0; t < c; t++) dup |= (gs.nb[o2 + t] == j);
+            if (!dup) gs.nb[o2 + c++] = j;
+        }
+        gs.msort[i] = c;
+    }
+    tsync<TEAM>();
+    if (tid == 0) {  // compact rows into a dense CSR
+        int oo = 0;
+        for (int i = 0; i < n; i++) {
+            const int s0 = gs.nbptr[i], c = gs.msort[i];
+            for (int t = 0; t < c; t++) gs.nb[oo + t] = gs.nb[s0 + t];
+            gs.nbptr[i] = oo;
+            oo += c;
+        }
+        gs.nbptr[n] = oo;
+    }
+    tsync<TEAM>();
+    const double pred = mp_forward_team<T, TEAM>(g, mem, n, gs.nbptr, gs.nb, (T *)gs.H, (T *)gs.P, tid, ts);
+    if (tid == 0) {
+        w.dur()[gi] = pred;
+        if (memo) memo_put(memo, g.memo_mask, mh1, mh2, pred);
+    }
+    tsync<TEAM>();
+}
+
 // One fused group (K2), warp-level: lane = hidden channel for message passing.
 template <typename T>
 __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratch &gs, int f, int lane, bool hw,
@@ -1138,8 +1298,6 @@ __device__ void process_group(const ScoreArgs &a, const Ws &w, const GroupScratc
             d = all_param ? 0.0
                           : __dadd_rn(__dadd_rn(comp.get(), g.launch),
                                       __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
-            if (!all_param && g.noise != 0.0)
-                d = __dmul_rn(d, hw_jitter(g, mem, n, w.gint()[gi], w.gin()[gi], w.gout()[gi]));
         }
         d = __shfl_sync(FULL, d, 0);
         if (lane == 0) w.dur()[gi] = d;
@@ -1502,8 +1660,6 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
                         d = g.op_kind[v] == 1 ? 0.0
                                               : __dadd_rn(__dadd_rn(isnan(c) ? 0.0 : c, g.launch),
                                                           __dmul_rn(g.mem, (double)(w.gin()[gi] + w.gout()[gi])));
-                        if (g.noise != 0.0 && g.op_kind[v] != 1)
-                            d = __dmul_rn(d, hw_jitter(g, &v, 1, w.gint()[gi], w.gin()[gi], w.gout()[gi]));
                     } else if (g.op_kind[v] == 1) {
                         d = 0.0;
                     } else {
@@ -1548,10 +1704,39 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
                 }
             }
             tsync<TEAM>();
-            const GroupScratch gs = group_scratch(w, wid);
-            for (int f = wid; f < nf; f += NW) process_group<T>(a, w, gs, f, lane, hw, badk);
+            if (TEAM > 32 && a.retry_only) {
+                // second pass (whole-graph scratch, one copy): groups one at a
+                // time; the very large MP groups use the whole team
+                const GroupScratch gs = group_scratch(w, 0);
+                for (int f = 0; f < nf; f++) {
+                    const int nn_f = w.gptr()[f + 1] - w.gptr()[f];
+                    if (!hw && g.variant == FO_EST_MESSAGE_PASSING && nn_f > kMpCapDefault) {
+                        process_group_team<T, TEAM>(a, w, gs, f, tid, badk, ts);
+                    } else {
+                        if (wid == 0) process_group<T>(a, w, gs, f, lane, hw, badk);
+                        tsync<TEAM>();
+                    }
+                }
+            } else {
+                const GroupScratch gs = group_scratch(w, wid);
+                for (int f = wid; f < nf; f += NW) process_group<T>(a, w, gs, f, lane, hw, badk);
+            }
             tsync<TEAM>();
         }
+    }
+    // hardware-oracle jitter (noise > 0): one cold pass over the groups once
+    // their base times exist; members ascending (fused lists are sorted)
+    if (g.provider == FO_PROVIDER_HW_ORACLE && g.noise != 0.0 && !a.ext_dur) {
+        tsync<TEAM>();
+        for (int gi = tid; gi < G; gi += TEAM) {
+            const double d = w.dur()[gi];
+            if (d == 0.0) continue;  // all-parameter group (workloads.py:282-283)
+            const int c = w.gcnt()[gi];
+            const int *ops = c < 0 ? w.gmem() + w.gptr()[-c - 1] : w.gmin() + gi;
+            const int n = c < 0 ? w.gptr()[-c] - w.gptr()[-c - 1] : 1;
+            w.dur()[gi] = __dmul_rn(d, hw_jitter(g, ops, n, w.gint()[gi], w.gin()[gi], w.gout()[gi]));
+        }
+        tsync<TEAM>();
     }
     // first failing node in node order decides the error (simulator.py:62)
     badk = tmin<TEAM>(badk, ts, tid);
