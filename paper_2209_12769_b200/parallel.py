@@ -91,8 +91,8 @@ class ShardedSearch:
         multi = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
         if exchange_every is None:
             if self.s is not None:
-                res = self.s.run(max_rounds)
-                best = np.array([r.best_cost_us for r in res], np.float64)
+                self.s.run(max_rounds, results=False)  # results on demand (s.result / s.best_costs)
+                best = self.s.best_costs()
             else:
                 best = np.zeros(0)
             if not multi:

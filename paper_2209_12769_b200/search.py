@@ -113,14 +113,16 @@ class LockstepSearch:
         self.rounds += 1
         return self.active
 
-    def run(self, max_rounds: Optional[int] = None, started: Optional[float] = None):
+    def run(self, max_rounds: Optional[int] = None, started: Optional[float] = None, results: bool = True):
+        """Run to completion; results=False skips building the per-seed
+        SearchResult objects (graphs and traces) -- see best_costs()."""
         if self.cfg.time_budget_s is None:  # whole search in native code (fo_search_run)
             a = C.c_int32()
             st = N.lib().fo_search_run(self.h, int(max_rounds or 0), C.byref(a))
             _raise(st, "fo_search_run", N.last_error())
             self.active = a.value
             self.rounds += 1
-            return [self.result(r) for r in range(self.R)]
+            return [self.result(r) for r in range(self.R)] if results else None
         t0 = time.monotonic() if started is None else started
         while self.active > 0:
             if max_rounds is not None and self.rounds >= max_rounds:
@@ -129,6 +131,23 @@ class LockstepSearch:
                 break
             self.round()
         return [self.result(r) for r in range(self.R)]
+
+    def best_costs(self) -> np.ndarray:
+        """Best cost found by every seed (no graph or trace reconstruction)."""
+        out = np.zeros(self.R)
+        for r in range(self.R):
+            c = C.c_double()
+            st = N.lib().fo_search_result(self.h, r, C.byref(c), None, None, None, None, None, 0)
+            _raise(st, "search", N.last_error())
+            out[r] = c.value
+        return out
+
+    def counters(self, r: int):
+        """(steps, candidates_evaluated, candidates_enqueued, trace length) of seed r."""
+        cnt = np.zeros(4, np.int64)
+        st = N.lib().fo_search_result(self.h, r, None, N.ptr(cnt), None, None, None, None, 0)
+        _raise(st, "search", N.last_error())
+        return tuple(int(x) for x in cnt)
 
     def timing(self):
         d, e, s = C.c_double(), C.c_double(), C.c_int64()

@@ -60,9 +60,11 @@ def main():
     best_cost, best_seed = sh.run(dev)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    res = [sh.s.result(r, with_trace=False) for r in range(len(sh.local_seeds))]
-    local_evals = sum(r.candidates_evaluated for r in res)
-    local_steps = max((r.steps for r in res), default=0)
+    # per-seed counters straight from the native search (no graph reconstruction)
+    cnt = [sh.s.counters(r) for r in range(len(sh.local_seeds))] if sh.s else []
+    bests = sh.s.best_costs() if sh.s else []
+    local_evals = sum(c[1] for c in cnt)
+    local_steps = max((c[0] for c in cnt), default=0)
     tm = sh.s.timing()
     t = torch.tensor([wall, local_evals, tm["device_ms"], tm["expand_ms"], tm["scored"]], dtype=torch.float64,
                      device=dev)
@@ -91,15 +93,14 @@ def main():
 
             o = Oracle(load_workload(args.config), "mp")
             ev, tt, match = 0, 0.0, True
-            for s in range(min(args.oracle_seeds, len(res))):
+            for s in range(min(args.oracle_seeds, len(cnt))):
                 t1 = time.perf_counter()
                 r = o.search(alpha=args.alpha, beta=args.beta, max_unchanged=args.max_unchanged, seed=s)
                 tt += time.perf_counter() - t1
                 ev += r["candidates_evaluated"]
-                match &= (r["steps"], r["candidates_evaluated"], r["candidates_enqueued"]) == (
-                    res[s].steps, res[s].candidates_evaluated, res[s].candidates_enqueued)
-                match &= abs(r["best_cost_us"] - res[s].best_cost_us) <= 1e-9 * r["best_cost_us"]
-            line["oracle_port_1thread"] = {"seeds": min(args.oracle_seeds, len(res)), "wall_s": tt,
+                match &= (r["steps"], r["candidates_evaluated"], r["candidates_enqueued"]) == cnt[s][:3]
+                match &= abs(r["best_cost_us"] - bests[s]) <= 1e-9 * r["best_cost_us"]
+            line["oracle_port_1thread"] = {"seeds": min(args.oracle_seeds, len(cnt)), "wall_s": tt,
                                            "cand_per_s": ev / tt, "trajectories_match": bool(match)}
         print(json.dumps(line), flush=True)
     if ws > 1:
