@@ -510,3 +510,27 @@ def test_mp_dimension_mismatch():
     fused = build_graph(g.ops, g.edges, groups=[FusionGroup(0, frozenset({0})), FusionGroup(1, frozenset({1, 2}))])
     with pytest.raises(P.DimensionMismatch):
         P.cost(fused, cp)
+
+
+def test_graph_beyond_16bit_nodes_matches_oracle():
+    """A 70,000-op graph: schedule nodes exceed the 16-bit fast paths (ring
+    buffers, shared-memory arena), so the 32-bit event loop runs; costs match
+    the oracle under the hardware-oracle provider."""
+    from oracle.oracle import Oracle, Workload
+    from paper_2209_12769_b200.graph import graph_to_doc
+
+    n = 70000
+    ops = [op(i, code="GradW" if i % 70 == 0 else "Mul", us=1.0 + (i % 7)) for i in range(n)]
+    edges = [DataEdge(i, i + 1, 256) for i in range(n - 1)] + [DataEdge(i, i + 3, 64) for i in range(0, n - 3, 5)]
+    ars = [(t, 70 * t, 4096 + t) for t in range(n // 70)]
+    g = build_graph(ops, edges, ars)
+    hw = P.HardwareParams()
+    cp = P.oracle_providers(hw, precision=N.FO_PREC_FP64)
+    dg = cp.device_graph(g)
+    ng, rg, bk, gb = dg.make_candidates(np.arange(3, dtype=np.uint64))
+    got, st = dg.score_host(ng, rg, bk, gb, N.FO_PREC_FP64)
+    assert (st == 0).all()
+    o = Oracle(Workload("big", graph_to_doc(g), {}, (hw.comm_params.C, hw.comm_params.D), {}, {}), "oracle")
+    for k in range(3):
+        _, ref = o.cost(ng[k], rg[k], bk[k])
+        assert got[k] == pytest.approx(ref, rel=1e-12)
