@@ -204,6 +204,77 @@ def synth50k(args):
     print(json.dumps(line))
 
 
+def synth50k_sharded(args):
+    """BASELINE configs[4] on N GPUs of one box (torchrun): rank r scores its
+    own `batch` candidates (seeds r*batch..), then the round's best (cost,
+    candidate id) is exchanged (device argmin, 16-byte all-gather, argmin over
+    the pairs).  Time = max over ranks of the device-timed round."""
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2209_12769_b200 as P
+    from paper_2209_12769_b200 import _native as N
+
+    ws, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    prec = N.FO_PREC_FP32
+    g, prof, comm, mp, lin = P.load_workload("synth50k")
+    dg = P.make_cost_providers(prof, comm, mp, precision=prec).device_graph(g)
+    B = args.batch
+    t0 = time.perf_counter()
+    dg.set_parent()
+    off, chg = dg.make_candidates_delta(np.arange(rank * B, (rank + 1) * B, dtype=np.uint64), beta=args.beta,
+                                        n_threads=max(1, (os.cpu_count() or 1) // local_ws))
+    gen_s = time.perf_counter() - t0
+    d_off, d_chg = torch.from_numpy(off).to(dev), torch.from_numpy(chg).to(dev)
+    cost = torch.empty(B, dtype=torch.float64, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    pair = torch.empty(2, dtype=torch.float64, device=dev)
+    gathered = torch.empty(2 * ws, dtype=torch.float64, device=dev)
+    final = torch.empty(2, dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream()
+    cs = ctypes.c_void_p(s.cuda_stream)
+
+    def round_():
+        dg.score_delta_device(d_off, d_chg, cost, st, prec, s.cuda_stream)
+        N.lib().fo_batch_best(N.ptr(cost), N.ptr(st), B, rank * B, N.ptr(pair), cs)
+        dist.all_gather_into_tensor(gathered, pair)
+        N.lib().fo_pairs_best(N.ptr(gathered), ws, N.ptr(final), cs)
+
+    round_()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        N.lib().fo_memo_clear(dg.h, cs)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        round_()
+        e1.record(s)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = torch.tensor([float(np.median(ts)), gen_s], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    best = final.cpu().numpy()
+    if rank == 0:
+        print(json.dumps({"metric": "fusion candidates scored/sec (GNN est.+sim)",
+                          "config": "synthetic 50k-op DAG, one round, candidates sharded over GPUs",
+                          "value": B * ws / (float(t[0]) / 1e3), "unit": "candidates/s", "n_gpus": ws,
+                          "candidates_per_round": B * ws, "ms_per_round_max_over_ranks": float(t[0]),
+                          "candidate_generation_s_max": float(t[1]), "best": {"cost_us": float(best[0]),
+                                                                            "candidate": int(best[1])},
+                          "scaling": "weak"}), flush=True)
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("what", choices=["gpt2-sweep", "synth50k"])
@@ -213,7 +284,10 @@ if __name__ == "__main__":
     ap.add_argument("--distinct", type=int, default=8192)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     a = ap.parse_args()
-    if a.what == "gpt2-sweep":
+    if a.what == "synth50k" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        a.batch = a.batch or 8192
+        synth50k_sharded(a)
+    elif a.what == "gpt2-sweep":
         a.batch = a.batch or 256
         gpt2_sweep(a)
     else:
