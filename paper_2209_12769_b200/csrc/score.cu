@@ -1603,11 +1603,13 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
     }
     // ---- K2: durations of every node (simulator.py:62)
     long long badk = LLONG_MAX;
-    #pragma unroll 4
-    for (int b = tid; b < B; b += TEAM) {  // comm.py:45-49
-        double d = __dadd_rn(__dmul_rn(g.C, (double)w.btot()[b]), g.D);
-        w.dur()[G + b] = d;
-        if (d < 0.0) badk = min(badk, pack_bad(G + b, FO_NEGATIVE_DURATION));
+    if (!a.ext_dur) {  // (external durations replace these; the two must not race)
+        #pragma unroll 4
+        for (int b = tid; b < B; b += TEAM) {  // comm.py:45-49
+            double d = __dadd_rn(__dmul_rn(g.C, (double)w.btot()[b]), g.D);
+            w.dur()[G + b] = d;
+            if (d < 0.0) badk = min(badk, pack_bad(G + b, FO_NEGATIVE_DURATION));
+        }
     }
     if (a.ext_dur) {
         #pragma unroll 4

@@ -171,8 +171,75 @@ class LockstepSearch:
                             trace)
 
 
+def _is_device(cp) -> bool:
+    from .estimator import DeviceCostProviders
+
+    return isinstance(cp, DeviceCostProviders)
+
+
+def _host_driven_search(g0: HloGraph, cfg: SearchConfig, cp) -> SearchResult:
+    """Alg. 1 (search.py:84-155) for arbitrary Python CostProviders: the same
+    bookkeeping, one candidate at a time -- the rewrites run in the native
+    engine on the caller's random.Random, each cost() evaluates the
+    callbacks in Python and simulates on the device (simulator.simulate)."""
+    import random
+
+    from .rewrite import random_apply
+    from .simulator import cost
+
+    rng = random.Random(cfg.seed)
+    t0 = time.monotonic()
+    cache = {}
+    evaluated = 0
+
+    def eval_cost(g, h):
+        nonlocal evaluated
+        if h not in cache:
+            cache[h] = cost(g, cp)
+            evaluated += 1
+        return cache[h]
+
+    h0 = canonical_hash(g0)
+    best, best_cost = g0, eval_cost(g0, h0)
+    seen = {h0}
+    queue = [(best_cost, 0, h0, g0)]
+    seq, enqueued, unchanged, steps = 1, 0, 0, 0
+    trace = []
+    methods = [m for m in ALL_METHODS if m in cfg.methods]
+    while queue and unchanged < cfg.max_unchanged:
+        if cfg.time_budget_s is not None and time.monotonic() - t0 > cfg.time_budget_s:
+            break
+        _, _, cur_h, cur = heapq.heappop(queue)
+        steps += 1
+        requeued = False
+        for m in methods:
+            n = rng.randint(0, cfg.beta)
+            out = random_apply(cur, m, n, rng)
+            h = canonical_hash(out.graph) if out.applied else cur_h
+            c = eval_cost(out.graph, h)
+            if c < best_cost:
+                best, best_cost, unchanged = out.graph, c, 0
+            else:
+                unchanged += 1
+            entered = False
+            if c <= cfg.alpha * best_cost:
+                if h not in seen:  # a new state
+                    seen.add(h)
+                    heapq.heappush(queue, (c, seq, h, out.graph))
+                    seq, enqueued, entered = seq + 1, enqueued + 1, True
+                elif h == cur_h and not requeued:  # the state came back: one copy stays in rotation
+                    heapq.heappush(queue, (c, seq, h, out.graph))
+                    seq, requeued, entered = seq + 1, True, True
+            trace.append(TraceRecord(steps, m.value, c, best_cost, len(queue), entered))
+    return SearchResult(best, best_cost, steps, evaluated, enqueued, trace)
+
+
 def backtracking_search(g0: HloGraph, cfg: SearchConfig, cp, precision=None) -> SearchResult:
-    """Best fusion state found from g0; never worse than g0 (search.py:84-155)."""
+    """Best fusion state found from g0; never worse than g0 (search.py:84-155).
+    Device providers run the native lock-stepped driver; arbitrary Python
+    CostProviders run the same algorithm one candidate at a time."""
+    if not _is_device(cp):
+        return _host_driven_search(g0, cfg, cp)
     return LockstepSearch(g0, cfg, cp, [cfg.seed], precision).run()[0]
 
 
@@ -184,11 +251,12 @@ def lockstep_search(g0: HloGraph, cfg: SearchConfig, cp, seeds: Sequence[int], p
 def exhaustive_search(g0: HloGraph, cp, max_ops: int = 8, max_tensors: int = 4) -> SearchResult:
     """BFS closure of the three rewrites with state dedupe (search.py:158-225);
     each BFS level is scored as one device batch."""
-    _require_device(cp)
     if len(g0.ops) > max_ops:
         raise LimitExceeded(f"{len(g0.ops)} ops exceeds limit {max_ops}")
     if len(g0.allreduces) > max_tensors:
         raise LimitExceeded(f"{len(g0.allreduces)} tensors exceeds limit {max_tensors}")
+    if not _is_device(cp):
+        return _host_exhaustive(g0, cp)
     dg = cp.device_graph(g0)
     ng, rg, bk, vb, _, _ = state_arrays(g0)
     h0 = int(dg.state_hash(ng, rg, bk)[0])
@@ -267,3 +335,39 @@ def threshold_allreduce_fusion(g: HloGraph, threshold_bytes: int, cp=None) -> Hl
                                  N.ptr(on), N.ptr(orr), N.ptr(ob))
     _raise(st, "threshold_allreduce_fusion", N.last_error())
     return state_from_arrays(g, on, orr, ob)
+
+
+def _host_exhaustive(g0: HloGraph, cp) -> SearchResult:
+    """exhaustive_search (search.py:158-225) for arbitrary Python CostProviders:
+    BFS over the native engine's single rewrites, cost() per new state."""
+    from .rewrite import engine_graph
+    from .simulator import cost
+
+    dg = engine_graph(g0)
+    ng, rg, bk, _, _, _ = state_arrays(g0)
+    seen = {int(dg.state_hash(ng, rg, bk)[0])}
+    best, best_cost = g0, cost(g0, cp)
+    evaluated, steps = 1, 0
+    frontier = [(ng, rg, bk)]
+    while frontier:
+        level = []
+        for st in frontier:
+            steps += 1
+            cn, cr, cb = expand_all(g0, *st)
+            if len(cn) == 0:
+                continue
+            hs = dg.state_hash(cn, cr, cb)
+            for i in range(len(cn)):
+                h = int(hs[i])
+                if h in seen:
+                    continue
+                seen.add(h)
+                level.append((cn[i], cr[i], cb[i]))
+        for x in level:
+            gx = state_from_arrays(g0, *x)
+            c = cost(gx, cp)
+            evaluated += 1
+            if c < best_cost:  # strict: the first in enumeration order wins (search.py:214-215)
+                best, best_cost = gx, c
+        frontier = level
+    return SearchResult(best, best_cost, steps, evaluated, len(seen) - 1)
