@@ -1911,7 +1911,7 @@ ScoreGeo score_geometry(const DGraph &g, int K, int num_sms, int precision) {
     // The shared-memory arena takes the L1 capacity the global-workspace setup
     // phase lives on (measured slower for full batches), so only small batches
     // (latency-bound, one block per SM at most) take it.
-    static const char *env = getenv("FO_SIM_SMEM");
+    const char *env = getenv("FO_SIM_SMEM");  // tuning override, read per launch
     const bool arena_on = env ? env[0] == '1' : K <= num_sms * kWarps;
     geo.sm_bytes = (arena_on && arena_fits && bytes * per_block <= 200 * 1024) ? (int)bytes : 0;
     int per_sm = fp64 ? blocks_per_sm<double>(geo.sm_bytes * per_block, geo.team)

@@ -534,3 +534,26 @@ def test_graph_beyond_16bit_nodes_matches_oracle():
     for k in range(3):
         _, ref = o.cost(ng[k], rg[k], bk[k])
         assert got[k] == pytest.approx(ref, rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["residual40", "vgg16", "resnet50", "bert", "gpt2m"])
+def test_block_and_warp_geometries_agree(name, monkeypatch):
+    """The block-per-candidate and warp-per-candidate geometries (FO_TEAM)
+    give bit-identical costs and statuses for every provider, with the
+    shared-memory arena on and off, and the jittered oracle."""
+    g, cps = providers(name, N.FO_PREC_FP64)
+    cps = dict(cps)
+    cps["oracle_noise"] = P.oracle_providers(P.HardwareParams(noise=0.1, seed=3), precision=N.FO_PREC_FP64)
+    K = 200
+    for pname, cp in cps.items():
+        dg = cp.device_graph(g)
+        ng, rg, bk, gb = dg.make_candidates(np.arange(K, dtype=np.uint64))
+        out = {}
+        for team in ("0", "1"):
+            for arena in ("0", "1"):
+                monkeypatch.setenv("FO_TEAM", team)
+                monkeypatch.setenv("FO_SIM_SMEM", arena)
+                out[(team, arena)] = dg.score_host(ng, rg, bk, gb, N.FO_PREC_FP64)
+        ref = out[("0", "0")]
+        for key, (c, s) in out.items():
+            assert np.array_equal(s, ref[1]) and np.array_equal(c, ref[0]), (name, pname, key)
