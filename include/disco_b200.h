@@ -247,6 +247,9 @@ int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seed
  * candidates are scored in ONE device batch.  active_out = searches still
  * running; best_out[R] / best_cost_out: per-search best costs after the round. */
 int fo_search_round(fo_search *s, int32_t *active_out, double *best_cost_out);
+/* The initial evaluation of the start state for every seed (search.py:101-102)
+ * without a step -- idempotent; fo_search_round / _run call it too. */
+int fo_search_start(fo_search *s, double *best_cost_out);
 /* Run every search to completion (max_rounds <= 0: unbounded) natively.  With
  * R >= 2 the seeds run in two halves whose device batches overlap the other
  * half's host-side expand; each seed's step sequence is unchanged. */

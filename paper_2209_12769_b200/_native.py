@@ -81,6 +81,7 @@ SIGNATURES = [
     ("fo_threshold_ar", C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, vp, vp]),
     ("fo_search_create", C.c_int, [vp, P(SearchCfg), vp, C.c_int32, vp, vp, vp, P(vp)]),
     ("fo_search_round", C.c_int, [vp, P(C.c_int32), vp]),
+    ("fo_search_start", C.c_int, [vp, vp]),
     ("fo_search_run", C.c_int, [vp, C.c_int64, P(C.c_int32)]),
     ("fo_search_result", C.c_int, [vp, C.c_int32, P(C.c_double), vp, vp, vp, vp, P(TraceRec), C.c_int64]),
     ("fo_search_timing", C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int64)]),

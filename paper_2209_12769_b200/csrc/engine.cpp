@@ -2048,6 +2048,18 @@ int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seed
 
 // One round: every active search does one step of Alg. 1; all of their
 // candidates are scored in ONE device batch.
+// eval_cost(g0) for every seed (search.py:101-102) without a step: what a
+// search whose time budget is already spent reports
+int fo_search_start(fo_search *S, double *best_cost_out) {
+    if (!S) return fail(FO_INVALID_ARG, "null search");
+    std::lock_guard<std::mutex> lk(S->g->mu);
+    cudaSetDevice(S->g->device);
+    int rc = search_start(S);
+    if (rc) return rc;
+    count_active(S, best_cost_out);
+    return FO_OK;
+}
+
 int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
     if (!S) return fail(FO_INVALID_ARG, "null search");
     fo_graph *g = S->g;

@@ -124,6 +124,8 @@ class LockstepSearch:
             self.rounds += 1
             return [self.result(r) for r in range(self.R)] if results else None
         t0 = time.monotonic() if started is None else started
+        st = N.lib().fo_search_start(self.h, N.ptr(self.best))  # eval_cost(g0) precedes the budget check
+        _raise(st, "fo_search_start", N.last_error())
         while self.active > 0:
             if max_rounds is not None and self.rounds >= max_rounds:
                 break

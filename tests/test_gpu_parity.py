@@ -557,3 +557,23 @@ def test_block_and_warp_geometries_agree(name, monkeypatch):
         ref = out[("0", "0")]
         for key, (c, s) in out.items():
             assert np.array_equal(s, ref[1]) and np.array_equal(c, ref[0]), (name, pname, key)
+
+
+def test_per_round_driver_equals_native_run():
+    """The per-round path (fo_search_round, used with a time budget and by the
+    sharded exchange every M rounds) walks the same trajectories as
+    fo_search_run, speculation included; a tiny budget stops early."""
+    g, cps = providers("chain24", N.FO_PREC_FP64)
+    seeds = [0, 1, 2, 3]
+    base = P.SearchConfig(alpha=1.05, beta=6, max_unchanged=40)
+    native = P.LockstepSearch(g, base, cps["mp"], seeds).run()
+    timed = P.SearchConfig(alpha=1.05, beta=6, max_unchanged=40, time_budget_s=600.0)
+    rounds = P.LockstepSearch(g, timed, cps["mp"], seeds).run()
+    for a, b in zip(native, rounds):
+        assert (a.steps, a.candidates_evaluated, a.candidates_enqueued, a.best_cost_us) == (
+            b.steps, b.candidates_evaluated, b.candidates_enqueued, b.best_cost_us)
+        assert a.trace == b.trace
+    short = P.LockstepSearch(g, P.SearchConfig(alpha=1.05, beta=6, max_unchanged=40, time_budget_s=0.0),
+                             cps["mp"], seeds).run()
+    for a, b in zip(native, short):
+        assert b.steps <= 1 and b.best_cost_us >= a.best_cost_us
