@@ -7,7 +7,7 @@ imports the reference, and it only ever runs in the build container
 (/root/reference does not exist on the GPU box); its outputs are committed.
 
 Usage:  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [section ...]
-Sections: workloads rng cases search exhaustive sweep baselines jitter
+Sections: workloads rng cases search exhaustive sweep baselines jitter acceptance
 (default: the first five)
 
 Inputs follow SURVEY.md section 8(d) / BASELINE.md section 3:
@@ -437,14 +437,46 @@ def section_jitter(names=None):
     _dump_gz(os.path.join(OUT, "jitter.json.gz"), out)
 
 
+def section_acceptance(names=None):
+    """The reference's acceptance criteria 1-3 inputs (test_acceptance.py:59-149):
+    generated workloads with their oracle-provider costs / bounds, and the
+    small criterion-2 workloads with their exhaustive optimum."""
+    from fuseopt import exhaustive_search, fo_bound
+    from fuseopt.workloads import FAMILIES
+
+    hw = HardwareParams()
+    cp = oracle_providers(hw)
+    rng = random.Random(0)
+    c1 = []
+    for i in range(1000):
+        spec = WorkloadSpec(family=FAMILIES[i % 4], op_count=rng.randrange(10, 201), tensor_count=rng.randrange(0, 31),
+                            seed=i)
+        if i % 5:  # every fifth workload of the criterion-1 sweep (same generator stream)
+            continue
+        g = gen_workload(spec, hw)
+        total = sum(cp.op_cost(g, gr) for gr in g.groups) + sum(cp.comm_cost(g, b) for b in g.buckets)
+        c1.append({"i": i, "graph": graph_to_doc(g), "cost": cost(g, cp), "fo_bound": fo_bound(g, cp),
+                   "total": total})
+    rng = random.Random(0)
+    c2 = []
+    for k in range(50):
+        spec = WorkloadSpec(family=FAMILIES[k % 4], op_count=rng.randrange(4, 9), tensor_count=rng.randrange(0, 4),
+                            seed=k)
+        g = gen_workload(spec, hw)
+        c2.append({"k": k, "graph": graph_to_doc(g), "exact": exhaustive_search(g, cp).best_cost_us})
+    _dump_gz(os.path.join(OUT, "acceptance.json.gz"), {"criterion1": c1, "criterion2": c2})
+    print(f"acceptance: {len(c1)} + {len(c2)} workloads", flush=True)
+
+
 def main(argv):
-    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep", "baselines", "jitter")]
+    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep", "baselines", "jitter", "acceptance")]
     names = [a for a in argv if a not in sections]
     if not sections:
         sections = ["workloads", "rng", "cases", "search", "exhaustive"]
     for s in sections:
         {"workloads": section_workloads, "rng": lambda _: section_rng(), "exhaustive": section_exhaustive,
          "sweep": section_sweep, "baselines": section_baselines, "jitter": section_jitter,
+         "acceptance": section_acceptance,
          "cases": section_cases, "search": section_search}[s](names or None)
 
 
