@@ -464,7 +464,12 @@ def section_acceptance(names=None):
                             seed=k)
         g = gen_workload(spec, hw)
         c2.append({"k": k, "graph": graph_to_doc(g), "exact": exhaustive_search(g, cp).best_cost_us})
-    _dump_gz(os.path.join(OUT, "acceptance.json.gz"), {"criterion1": c1, "criterion2": c2})
+    # criteria 8 / 9 (test_acceptance.py:250-322): the two generated graphs
+    g8 = gen_workload(WorkloadSpec(family="recurrent", op_count=40, tensor_count=10, min_tensor_bytes=8 * 1024,
+                                   max_tensor_bytes=64 * 1024, seed=21))
+    g9 = gen_workload(WorkloadSpec(family="attention", op_count=100, tensor_count=12, seed=33))
+    _dump_gz(os.path.join(OUT, "acceptance.json.gz"), {"criterion1": c1, "criterion2": c2,
+                                                      "criterion8": graph_to_doc(g8), "criterion9": graph_to_doc(g9)})
     print(f"acceptance: {len(c1)} + {len(c2)} workloads", flush=True)
 
 

@@ -57,3 +57,51 @@ def test_criteria_02_03_oracle_equivalence_and_search_invariants():
         hits += best / exact.best_cost_us <= 1.05 + 1e-12
     assert runs == 1000
     assert hits >= 45, f"only {hits}/50 within 5%"
+
+
+def _cp_c8():
+    hw = P.HardwareParams(comm_params=P.CommModelParams(C=0.0008, D=400.0))
+    return P.oracle_providers(hw, precision=N.FO_PREC_FP64)
+
+
+def _checked(results, g, cp, cfg):
+    initial = P.cost(g, cp)
+    for r in results:
+        assert r.best_cost_us <= initial + 1e-9
+        assert all(t.cost_us <= cfg.alpha * t.best_cost_us + 1e-9 for t in r.trace if t.enqueued)
+    return results
+
+
+def test_criterion_08_ablation_direction():
+    """Median best cost is non-increasing as methods are added."""
+    from paper_2209_12769_b200.rewrite import OptimizationMethod as M
+
+    g = graph_from_doc(read("acceptance.json.gz")["criterion8"])
+    cp = _cp_c8()
+    masks = [(M.NON_DUPLICATE_FUSION,), (M.NON_DUPLICATE_FUSION, M.DUPLICATE_FUSION),
+             (M.NON_DUPLICATE_FUSION, M.DUPLICATE_FUSION, M.ALLREDUCE_FUSION)]
+    medians = []
+    for mask in masks:
+        cfg = P.SearchConfig(alpha=1.05, beta=10, max_unchanged=100, methods=mask)
+        res = _checked(P.lockstep_search(g, cfg, cp, list(range(10))), g, cp, cfg)
+        medians.append(float(np.median([r.best_cost_us for r in res])))
+    assert medians[0] >= medians[1] - 1e-9 and medians[1] >= medians[2] - 1e-9
+
+
+def test_criterion_09_alpha_beta_tradeoff():
+    """A looser alpha costs more evaluations and finds no worse; a larger beta
+    (more rewrites per step) needs fewer evaluations."""
+    g = graph_from_doc(read("acceptance.json.gz")["criterion9"])
+    cp = _cp_c8()
+
+    def sweep(alpha, beta, max_unchanged):
+        cfg = P.SearchConfig(alpha=alpha, beta=beta, max_unchanged=max_unchanged)
+        res = _checked(P.lockstep_search(g, cfg, cp, list(range(10))), g, cp, cfg)
+        return float(np.median([r.best_cost_us for r in res])), float(np.median([r.candidates_evaluated for r in res]))
+
+    cost_tight, evals_tight = sweep(1.0, 10, 200)
+    cost_loose, evals_loose = sweep(1.1, 10, 200)
+    assert cost_loose <= cost_tight + 1e-9 and evals_loose > evals_tight
+    _, evals_beta1 = sweep(1.05, 1, 100)
+    _, evals_beta30 = sweep(1.05, 30, 100)
+    assert evals_beta30 < evals_beta1
