@@ -204,6 +204,21 @@ int fo_random_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int
 int fo_expand_all(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t cap,
                   int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out, int32_t *n_out);
 
+/* ---- rewrite primitives (rewrite.py:49-219) ----------------------------- */
+/* Ids are ranks of the state's group / bucket ids (0..G-1 / 0..B-1 in id
+ * order).  fo_rewrite_pairs: kind 0 fusible_pairs, 1 fusible pairs after the
+ * duplicate-fusion filter, 2 bucket_pairs, 3 every contracted (group,
+ * predecessor) pair (graph.py:161-179); (a, b) pairs in the reference's
+ * order into pairs_out[2 * cap]; n_out = count (FO_INVALID_ARG when cap is
+ * short).  fo_rewrite_apply: method 0 fuse_nondup(a, b), 1 fuse_dup(a, b)
+ * (a consumer, b predecessor group), 2 fuse_allreduce(a, b) (buckets; the
+ * caller checks that b neighbours a); applied_out = 0 for a rejected rewrite,
+ * else the state arrays are rewritten (engine ids). */
+int fo_rewrite_pairs(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t kind,
+                     int32_t *pairs_out, int32_t cap, int32_t *n_out);
+int fo_rewrite_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int32_t method, int32_t a, int32_t b,
+                     int32_t *applied_out);
+
 /* ---- heuristic baselines (search.py:228-302) ---------------------------- */
 /* greedy_postorder_fusion (search.py:228-244): every op in reverse contracted
  * topological order; its normal group is non-duplicate-fused with the first

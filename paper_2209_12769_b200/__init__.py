@@ -49,7 +49,18 @@ from .graph import (
     save_graph,
     with_fusion_state,
 )
-from .rewrite import OptimizationMethod, RewriteOutcome, make_candidates, random_apply
+from .rewrite import (
+    OptimizationMethod,
+    RewriteOutcome,
+    bucket_pairs,
+    fuse_allreduce,
+    fuse_dup,
+    fuse_nondup,
+    fusible_pairs,
+    make_candidates,
+    neighbors_allreduce,
+    random_apply,
+)
 from .search import (
     LockstepSearch,
     SearchConfig,

@@ -1497,6 +1497,66 @@ int fo_expand_all(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
     return FO_OK;
 }
 
+// Rewrite primitives on one state (rewrite.py:49-219), ids as ranks of the
+// state's group / bucket ids.  kind 0: fusible_pairs, 1: the same with the
+// duplicate-fusion filter (rewrite.py:242-247), 2: bucket_pairs, 3: every
+// contracted (group, predecessor) pair.
+int fo_rewrite_pairs(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t kind,
+                     int32_t *pairs_out, int32_t cap, int32_t *n_out) {
+    if (!g || !n_out || kind < 0 || kind > 3) return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State s;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    Scratch sc;
+    Index ix;
+    eng.build(s, ix, sc, kind == 2);
+    std::vector<std::pair<int32_t, int32_t>> v;
+    if (kind == 2) eng.bucket_pairs(ix, sc, v);
+    else if (kind == 3)  // every (group, contracted predecessor) pair (graph.py:161-179)
+        for (int x = 0; x < ix.G; x++)
+            for (int k = ix.pptr[x]; k < ix.pptr[x + 1]; k++) v.emplace_back(x, ix.pred[k]);
+    else eng.fusible_pairs(ix, kind == 1, v);
+    *n_out = (int32_t)v.size();
+    if ((int64_t)v.size() > cap) return fail(FO_INVALID_ARG, "pair capacity too small");
+    for (size_t i = 0; i < v.size(); i++) {
+        pairs_out[2 * i] = v[i].first;
+        pairs_out[2 * i + 1] = v[i].second;
+    }
+    return FO_OK;
+}
+
+// fuse_nondup / fuse_dup (a = consumer group, b = predecessor group) or
+// fuse_allreduce (a = bucket, b = neighbour; the caller checks adjacency,
+// rewrite.py:185-186); the state is rewritten in place when applied.
+int fo_rewrite_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, int32_t method, int32_t a, int32_t b,
+                     int32_t *applied_out) {
+    if (!g || !ngid || !rgid || !bkt || !applied_out || method < 0 || method > 2)
+        return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State s, out;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    Scratch sc;
+    Index ix;
+    eng.build(s, ix, sc, method == M_AR);
+    const int n = method == M_AR ? ix.B : ix.G;
+    if (a < 0 || a >= n || b < 0 || b >= n) return fail(FO_INVALID_ARG, "unknown group or bucket");
+    bool ok = false;
+    if (method == M_AR) {
+        ok = a != b && eng.fuse_ar(s, ix, a, b, out, sc);
+    } else {
+        bool adjacent = false;  // pred_gid in contracted_preds[op_gid] (rewrite.py:72-73)
+        for (int k = ix.pptr[a]; k < ix.pptr[a + 1]; k++) adjacent |= ix.pred[k] == b;
+        ok = adjacent && eng.fuse_ops(s, ix, a, b, method == M_DUP, out, sc);
+    }
+    *applied_out = ok ? 1 : 0;
+    if (ok) {
+        std::copy(out.ng.begin(), out.ng.end(), ngid);
+        std::copy(out.rg.begin(), out.rg.end(), rgid);
+        std::copy(out.bk.begin(), out.bk.end(), bkt);
+    }
+    return FO_OK;
+}
+
 // greedy_postorder_fusion (search.py:228-244): ops in reverse topological
 // order; each op's current normal group is non-duplicate-fused with its first
 // predecessor group (ascending id) for which the rewrite is valid.

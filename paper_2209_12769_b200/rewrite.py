@@ -12,7 +12,7 @@ from enum import Enum
 import numpy as np
 
 from . import _native as N
-from .errors import _raise
+from .errors import NotNeighbors, _raise
 from .graph import HloGraph, state_arrays, state_from_arrays
 
 
@@ -42,6 +42,89 @@ def engine_graph(g: HloGraph):
     from .simulator import _plain_providers
 
     return _plain_providers().device_graph(g)
+
+
+def _pairs(g: HloGraph, kind: int):
+    dg = engine_graph(g)
+    ng, rg, bk, _, gids, bids = state_arrays(g)
+    cap = 4 * (len(g.edges) + len(g.allreduces) ** 2 + 16)
+    out = np.zeros(2 * cap, np.int32)
+    n = C.c_int32()
+    st = N.lib().fo_rewrite_pairs(dg.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), kind, N.ptr(out), cap, C.byref(n))
+    _raise(st, "fo_rewrite_pairs", N.last_error())
+    ids = bids if kind == 2 else gids  # ranks back to the graph's ids
+    return [(ids[out[2 * i]], ids[out[2 * i + 1]]) for i in range(n.value)]
+
+
+def fusible_pairs(g: HloGraph):
+    """(consumer group, predecessor group) pairs eligible for op fusion, in the
+    reference's order (rewrite.py:49-61)."""
+    return _pairs(g, 0)
+
+
+def bucket_pairs(g: HloGraph):
+    """(bucket, neighbour) pairs eligible for AllReduce fusion (rewrite.py:212-219)."""
+    return _pairs(g, 2)
+
+
+def neighbors_allreduce(g: HloGraph, bucket_id: int) -> set:
+    """Buckets whose producing groups touch this bucket's (rewrite.py:156-178)."""
+    g.bucket(bucket_id)  # KeyError for an unknown bucket, as the reference
+    return {o for b, o in _pairs(g, 2) if b == bucket_id}
+
+
+def _apply(g: HloGraph, method: int, a: int, b: int, what: str) -> RewriteOutcome:
+    dg = engine_graph(g)
+    ng, rg, bk, _, gids, bids = state_arrays(g)
+    ids = bids if method == 2 else gids
+    rank = {x: i for i, x in enumerate(ids)}
+    applied = C.c_int32()
+    st = N.lib().fo_rewrite_apply(dg.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), method, rank[a], rank[b], C.byref(applied))
+    _raise(st, "fo_rewrite_apply", N.last_error())
+    if not applied.value:
+        return RewriteOutcome(g, False, "rejected: group contraction (with bucket dependencies) is cyclic")
+    return RewriteOutcome(state_from_arrays(g, ng, rg, bk), True, f"{what}: {b} into {a}")
+
+
+def _op_fusion_checks(g: HloGraph, op_gid: int, pred_gid: int, dup: bool):
+    """The reference's rejection reasons in its order (rewrite.py:70-79,
+    :108-122); None when only the acyclicity test remains."""
+    og, pg = g.group(op_gid), g.group(pred_gid)  # KeyError for unknown groups
+    if op_gid == pred_gid:
+        return "cannot fuse a group with itself"
+    if (op_gid, pred_gid) not in set(_pairs(g, 3)):
+        return f"group {pred_gid} is not a direct predecessor of {op_gid}"
+    if not all(g.op(m).kind == "compute" for m in og.member_ops | pg.member_ops):
+        return "parameter or control op in fusion"
+    if og.member_ops & pg.member_ops:
+        return "groups share a member"
+    if dup and any(m in x.duplicated_ops for x in g.groups for m in pg.member_ops):
+        return "a predecessor member already has a replica"
+    return None
+
+
+def fuse_nondup(g: HloGraph, op_gid: int, pred_gid: int) -> RewriteOutcome:
+    """Merge the predecessor group into the consumer group (rewrite.py:64-96)."""
+    why = _op_fusion_checks(g, op_gid, pred_gid, False)
+    if why:
+        return RewriteOutcome(g, False, f"rejected: {why}")
+    return _apply(g, 0, op_gid, pred_gid, "nondup")
+
+
+def fuse_dup(g: HloGraph, op_gid: int, pred_gid: int) -> RewriteOutcome:
+    """Merge the predecessor into the consumer and leave a replica for its other
+    consumers; degrades to non-duplicate fusion without any (rewrite.py:99-153)."""
+    why = _op_fusion_checks(g, op_gid, pred_gid, True)
+    if why:
+        return RewriteOutcome(g, False, f"rejected: {why}")
+    return _apply(g, 1, op_gid, pred_gid, "dup")
+
+
+def fuse_allreduce(g: HloGraph, bucket_id: int, neighbor_id: int) -> RewriteOutcome:
+    """Merge two neighbouring buckets (rewrite.py:181-209); NotNeighbors otherwise."""
+    if neighbor_id not in neighbors_allreduce(g, bucket_id):
+        raise NotNeighbors(f"bucket {neighbor_id} is not a neighbor of {bucket_id}")
+    return _apply(g, 2, bucket_id, neighbor_id, "ar")
 
 
 def random_apply(g: HloGraph, method: OptimizationMethod, n: int, rng: random.Random) -> RewriteOutcome:
