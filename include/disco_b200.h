@@ -129,6 +129,22 @@ int fo_pairs_best(const double *pairs, int32_t n, double *out_pair, void *stream
 int fo_memo_clear(fo_graph *g, void *stream);
 int fo_memo_enable(fo_graph *g, int32_t enable);
 
+/* ---- feature-level prediction ------------------------------------------ */
+/* predict_fused(model, featurize(g, group, profile)) (estimator.py:462-470,
+ * :157-191) for ONE group given by its features, with the estimator loaded by
+ * fo_graph_set_cost_model (profile provider; any variant).  Host buffers,
+ * synchronous.  n member ops (local ids 0..n-1 in featurize's node order):
+ * op_slot[n] vocab slot (message passing only; else ignored), compute_us[n],
+ * in_bytes[n], out_bytes[n]; m internal edges as (src, dst) local pairs in the
+ * graph's edge order; aggregates[6] = SubgraphFeatures.aggregate_vector()
+ * {member_count, total_compute_us, internal, ext_in, ext_out, longest_path}
+ * (estimator.py:117-128).  The MP variant embeds the node features on the device exactly as
+ * the per-op table is built at fo_graph_set_cost_model, so the result equals
+ * the prediction the scoring kernels make for that group. */
+int fo_predict_features(fo_graph *g, int32_t n, const int32_t *op_slot, const double *compute_us,
+                        const int64_t *in_bytes, const int64_t *out_bytes, int32_t m, const int32_t *edges,
+                        const double *aggregates, int32_t precision, double *pred_out);
+
 /* ---- scoring ----------------------------------------------------------- */
 /* cost() for K candidates (simulator.py:143-145 over K fresh graphs).
  * Device pointers; asynchronous on `stream` (cudaStream_t, NULL = legacy).

@@ -31,6 +31,7 @@ from .estimator import (
     make_cost_providers,
     predict_fused_groups,
 )
+from .features import SubgraphFeatures, featurize, group_io, predict_fused
 from .graph import (
     AllReduceInstr,
     DataEdge,
@@ -73,6 +74,6 @@ from .search import (
     threshold_allreduce_fusion,
 )
 from .simulator import CostProviders, Timeline, cost, cost_batch, fo_bound, format_timeline, report_lines, simulate
-from .workloads import HardwareParams, load_workload, oracle_providers
+from .workloads import HardwareParams, load_workload, oracle_providers, oracle_time
 
 __version__ = "0.1.0"

@@ -58,6 +58,7 @@ SIGNATURES = [
     ("fo_batch_best", C.c_int, [vp, vp, C.c_int32, C.c_int64, vp, vp]),
     ("fo_pairs_best", C.c_int, [vp, C.c_int32, vp, vp]),
     ("fo_memo_clear", C.c_int, [vp, vp]),
+    ("fo_predict_features", C.c_int, [vp, C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, C.c_int32, vp]),
     ("fo_memo_enable", C.c_int, [vp, C.c_int32]),
     ("fo_score", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]),
     ("fo_score_host", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp]),

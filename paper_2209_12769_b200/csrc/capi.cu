@@ -271,6 +271,7 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
     dg.out_scale = m->out_scale;
     dg.layers = 0;
     dg.lin_norm = 0;
+    dg.emb = dg.emb_mean = dg.emb_std = nullptr;
     if (m->provider != FO_PROVIDER_PROFILE && m->provider != FO_PROVIDER_HW_ORACLE)
         return fail(FO_INVALID_ARG, "unknown provider");
     if (!(m->comm_C >= 0) || !(m->comm_D >= 0)) return fail(FO_INVALID_ARG, "C and D must be non-negative");
@@ -360,7 +361,9 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         W[ml.c3] = c3;
         std::vector<float> H0f(H0.begin(), H0.end()), Wf(W.begin(), W.end());
         size_t oH0d = 0, oH0f = al256(H0.size() * 8), oWd = oH0f + al256(H0f.size() * 4 + 4),
-               oWf = oWd + al256(W.size() * 8), tot = oWf + al256(Wf.size() * 4);
+               oWf = oWd + al256(W.size() * 8), oE = oWf + al256(Wf.size() * 4),
+               oNm = oE + al256((size_t)h * F * 8), tot = oNm + al256((size_t)2 * F * 8);
+        const bool has_norm = m->norm_mean && m->norm_std;
         if (g->device < 0) { g->model_set = true; return FO_OK; }
         CUDA_TRY(cudaSetDevice(g->device));
         if (g->d_model) { cudaFree(g->d_model); g->d_model = nullptr; }
@@ -372,6 +375,17 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         }
         CUDA_TRY(cudaMemcpy(b + oWd, W.data(), W.size() * 8, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(b + oWf, Wf.data(), Wf.size() * 4, cudaMemcpyHostToDevice));
+        // W_emb and node_norm for feature-level prediction (fo_predict_features)
+        CUDA_TRY(cudaMemcpy(b + oE, Wemb, (size_t)h * F * 8, cudaMemcpyHostToDevice));
+        if (has_norm) {
+            CUDA_TRY(cudaMemcpy(b + oNm, m->norm_mean, (size_t)F * 8, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(b + oNm + (size_t)F * 8, m->norm_std, (size_t)F * 8, cudaMemcpyHostToDevice));
+        }
+        dg.emb = (const double *)(b + oE);
+        dg.emb_mean = has_norm ? (const double *)(b + oNm) : nullptr;
+        dg.emb_std = has_norm ? (const double *)(b + oNm + (size_t)F * 8) : nullptr;
+        dg.emb_h = h;
+        dg.emb_F = F;
         // estimator memo: 2 x 2^20 slots, cleared whenever the model changes
         const size_t slots = (size_t)1 << 20;
         if (!g->d_memo) CUDA_TRY(cudaMalloc(&g->d_memo, 2 * slots * sizeof(MemoEnt)));
@@ -449,6 +463,66 @@ static int ensure_io(fo_graph *g, size_t bytes) {
         CUDA_TRY(cudaMalloc(&g->d_io, bytes));
         g->io_bytes = bytes;
     }
+    return FO_OK;
+}
+
+int fo_predict_features(fo_graph *g, int32_t n, const int32_t *op_slot, const double *compute_us,
+                        const int64_t *in_bytes, const int64_t *out_bytes, int32_t m, const int32_t *edges,
+                        const double *aggregates, int32_t precision, double *pred_out) {
+    if (!g || !pred_out || n < 0 || m < 0 || (n && (!compute_us || !in_bytes || !out_bytes || !op_slot)) ||
+        (m && !edges) || !aggregates)
+        return fail(FO_INVALID_ARG, "bad arguments");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set");
+    if (g->dg.provider != FO_PROVIDER_PROFILE)
+        return fail(FO_UNSUPPORTED, "feature-level prediction needs a profile-provider estimator");
+    if (precision != FO_PREC_FP64 && precision != FO_PREC_FP32) return fail(FO_INVALID_ARG, "bad precision");
+    if (g->dg.variant != FO_EST_ANALYTIC && g->dg.variant != FO_EST_LINEAR &&
+        (g->dg.variant != FO_EST_MESSAGE_PASSING || !g->dg.emb))
+        return fail(FO_DIM_MISMATCH, "no usable fused-op estimator loaded (parameter shapes do not match)");
+    if (n > 8192) return fail(FO_UNSUPPORTED, "group too large for feature-level prediction (> 8192 ops)");
+    const DGraph &dg = g->dg;
+    if (dg.variant == FO_EST_MESSAGE_PASSING)
+        for (int i = 0; i < n; i++)
+            if (op_slot[i] < 0 || 6 + op_slot[i] >= dg.emb_F) return fail(FO_DIM_MISMATCH, "vocab slot outside W_emb");
+    for (int q = 0; q < m; q++)
+        if (edges[2 * q] < 0 || edges[2 * q] >= n || edges[2 * q + 1] < 0 || edges[2 * q + 1] >= n)
+            return fail(FO_INVALID_ARG, "edge endpoint outside the group");
+    std::lock_guard<std::mutex> lk(g->mu);
+    CUDA_TRY(cudaSetDevice(g->device));
+    const size_t o_slot = 0, o_c = al256((size_t)n * 4 + 4), o_in = o_c + al256((size_t)n * 8 + 8),
+                 o_out = o_in + al256((size_t)n * 8 + 8), o_e = o_out + al256((size_t)n * 8 + 8),
+                 o_ptr = o_e + al256((size_t)m * 8 + 8), o_nb = o_ptr + al256((size_t)n * 4 + 8),
+                 o_H0 = o_nb + al256(((size_t)2 * m + 1 + n) * 4), o_H = o_H0 + al256((size_t)n * 32 * 8 + 8),
+                 o_P = o_H + al256((size_t)n * 32 * 8 + 8), o_pred = o_P + al256((size_t)n * 32 * 8 + 8),
+                 tot = o_pred + 256;
+    int st = ensure_io(g, tot);
+    if (st) return st;
+    char *b = (char *)g->d_io;
+    cudaStream_t s = g->stream;
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(b + o_slot, op_slot, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(b + o_c, compute_us, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(b + o_in, in_bytes, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(b + o_out, out_bytes, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+    }
+    if (m) CUDA_TRY(cudaMemcpyAsync(b + o_e, edges, (size_t)m * 8, cudaMemcpyHostToDevice, s));
+    FeatIn fi;
+    fi.n = n; fi.m = m;
+    for (int q = 0; q < 6; q++) fi.agg[q] = aggregates[q];
+    fi.slot = (const int32_t *)(b + o_slot);
+    fi.edges = (const int32_t *)(b + o_e);
+    fi.c = (const double *)(b + o_c);
+    fi.in = (const long long *)(b + o_in);
+    fi.out = (const long long *)(b + o_out);
+    fi.nbptr = (int32_t *)(b + o_ptr);
+    fi.nb = (int32_t *)(b + o_nb);
+    fi.H0 = b + o_H0; fi.H = b + o_H; fi.P = b + o_P;
+    cudaError_t e = launch_predict_features(dg, fi, precision, (double *)(b + o_pred), s);
+    g_launches++;
+    if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("predict_features launch: ") + cudaGetErrorString(e));
+    CUDA_TRY(cudaMemcpyAsync(pred_out, b + o_pred, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return FO_OK;
 }
 

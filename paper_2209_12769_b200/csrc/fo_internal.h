@@ -54,6 +54,10 @@ struct DGraph {
     MemoEnt *memo[2];           // MP predictions by member set: [fp32, fp64]
     uint32_t memo_mask;
     int32_t phase_stop;         // measurement hook: launches stop after K1 (1) or K2 (2); 0 = full
+    // MP embedding for feature-level prediction (fo_predict_features): W_emb
+    // [h][F] row-major and the node_norm mean / std [F] (nullptr: none)
+    const double *emb, *emb_mean, *emb_std;
+    int32_t emb_h, emb_F;
     // hardware-oracle jitter (workloads.py:254-291): noise, "{seed}|" prefix,
     // per-op content-key fragments (CSR over ops)
     double noise;
@@ -125,6 +129,18 @@ cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, co
 int score_warps_per_block();
 int score_slots(const ScoreGeo &geo);       // workspace slots a launch uses
 int score_team_warps(const ScoreGeo &geo);  // warps per candidate
+// predict_fused (estimator.py:462-470) from one group's features, one warp
+struct FeatIn {
+    int32_t n, m;
+    const int32_t *slot, *edges;  // vocab slot per node; (src, dst) local pairs
+    const double *c;
+    const long long *in, *out;
+    double agg[6];                // SubgraphFeatures.aggregate_vector()
+    int32_t *nbptr, *nb;          // scratch: n + 1, 2m
+    char *H0, *H, *P;             // scratch: n x 32 T each
+};
+cudaError_t launch_predict_features(const DGraph &g, const FeatIn &in, int precision, double *pred_out,
+                                    cudaStream_t stream);
 cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, int64_t id_offset, double *out,
                               cudaStream_t stream, int pairs = 0);
 

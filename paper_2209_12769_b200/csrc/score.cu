@@ -1802,6 +1802,103 @@ __global__ void __launch_bounds__(kTeam, 4) score_kernel_team(const __grid_const
     }
 }
 
+// predict_fused from features (estimator.py:462-470) on one warp: the
+// closed forms as in K2, or the MP forward over embedded node features
+// (estimator.py:321-389) -- the embedding in the host's operation order, the
+// neighbour lists in edge order, like the graph path.
+template <typename T>
+__global__ void predict_features_kernel(DGraph g, FeatIn in, double *pred_out) {
+    const int lane = threadIdx.x;
+    const int n = in.n;
+    if (g.variant == FO_EST_ANALYTIC) {  // estimator.py:434-446
+        if (lane == 0) {
+            PySum sum;
+            for (int i = 0; i < n; i++)
+                sum.add(__dsub_rn(__dsub_rn(in.c[i], g.launch), __dmul_rn(g.mem, (double)(in.in[i] + in.out[i]))));
+            const double pred =
+                __dadd_rn(__dadd_rn(sum.get(), g.launch), __dmul_rn(g.mem, __dadd_rn(in.agg[3], in.agg[4])));
+            *pred_out = pred > 1e-9 ? pred : 1e-9;
+        }
+        return;
+    }
+    if (g.variant == FO_EST_LINEAR) {  // estimator.py:117-128, :341-345, :421-426
+        if (lane == 0) {
+            double fs[12];
+            for (int q = 0; q < 6; q++) { fs[q] = log1p(in.agg[q]); fs[6 + q] = in.agg[q]; }
+            if (g.lin_norm)
+                for (int q = 0; q < 12; q++) fs[q] = __ddiv_rn(__dsub_rn(fs[q], g.agg_mean[q]), g.agg_std[q]);
+            double z = 0.0;
+            for (int q = 0; q < 12; q++) z = __dadd_rn(z, __dmul_rn(g.lin_w[q], fs[q]));
+            z = __dadd_rn(z, g.lin_b);
+            const double pred = __dmul_rn(softplus_d(z), g.out_scale);
+            *pred_out = pred > 1e-9 ? pred : 1e-9;
+        }
+        return;
+    }
+    // message passing: H0 = std(X) @ W_emb^T per node, in double, like the host
+    T *H0 = (T *)in.H0;
+    const int F = g.emb_F, h = g.emb_h;
+    for (int i = 0; i < n; i++) {
+        double acc = 0.0;
+        if (lane < h) {
+            const double c = in.c[i], ib = (double)in.in[i], ob = (double)in.out[i];
+            for (int k = 0; k < F; k++) {
+                double x = k == 0 ? log1p(c) : k == 1 ? c : k == 2 ? log1p(ib) : k == 3 ? ib : k == 4 ? log1p(ob)
+                         : k == 5 ? ob : (k == 6 + in.slot[i] ? 1.0 : 0.0);
+                if (g.emb_mean) x = __ddiv_rn(__dsub_rn(x, g.emb_mean[k]), g.emb_std[k]);
+                acc = __dadd_rn(acc, __dmul_rn(x, g.emb[(int64_t)lane * F + k]));
+            }
+        }
+        H0[i * 32 + lane] = (T)acc;
+    }
+    // unique undirected neighbours: in-edges, then out-edges, in edge order
+    // (warp scan over the edge list per node, ballot-ordered appends)
+    int o = 0;
+    for (int i = 0; i < n; i++) {
+        const int start = o;
+        if (lane == 0) in.nbptr[i] = start;
+        for (int pass = 0; pass < 2; pass++)
+            for (int q0 = 0; q0 < in.m; q0 += 32) {
+                const int q = q0 + lane;
+                int j = -1;
+                if (q < in.m) {
+                    const int s2 = in.edges[2 * q], d2 = in.edges[2 * q + 1];
+                    j = pass == 0 ? (d2 == i ? s2 : -1) : (s2 == i ? d2 : -1);
+                }
+                unsigned hit = __ballot_sync(FULL, j >= 0);
+                while (hit) {
+                    const int src = __ffs(hit) - 1;
+                    hit &= hit - 1;
+                    const int jj = __shfl_sync(FULL, j, src);
+                    bool dup = false;
+                    for (int t = start + lane; t < o; t += 32) dup |= in.nb[t] == jj;
+                    if (!__any_sync(FULL, dup)) {
+                        if (lane == 0) in.nb[o] = jj;
+                        o++;
+                    }
+                    __syncwarp();
+                }
+            }
+    }
+    if (lane == 0) in.nbptr[n] = o;
+    DGraph g2 = g;  // the per-call embeddings stand in for the per-op table
+    if (sizeof(T) == 8) g2.H0d = (const double *)H0;
+    else g2.H0f = (const float *)H0;
+    // mem = identity: node i reads H0[i]
+    int *mem = in.nb + 2 * in.m + 1;
+    for (int i = lane; i < n; i += 32) mem[i] = i;
+    __syncwarp();
+    const double pred = mp_forward<T>(g2, mem, n, in.nbptr, in.nb, (T *)in.H, (T *)in.P, lane);
+    if (lane == 0) *pred_out = pred;
+}
+
+cudaError_t launch_predict_features(const DGraph &g, const FeatIn &in, int precision, double *pred_out,
+                                    cudaStream_t stream) {
+    if (precision == FO_PREC_FP64) predict_features_kernel<double><<<1, 32, 0, stream>>>(g, in, pred_out);
+    else predict_features_kernel<float><<<1, 32, 0, stream>>>(g, in, pred_out);
+    return cudaGetLastError();
+}
+
 // Per-round best (cost, candidate id) of a scored batch: one block, strict-<
 // order (the lowest id wins among equal costs, search.py:124, :214).  Non-OK
 // candidates are skipped.  out = {cost, id}; (inf, -1) for an empty batch.

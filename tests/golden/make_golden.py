@@ -7,7 +7,7 @@ imports the reference, and it only ever runs in the build container
 (/root/reference does not exist on the GPU box); its outputs are committed.
 
 Usage:  PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [section ...]
-Sections: workloads rng cases search exhaustive sweep baselines jitter acceptance
+Sections: workloads rng cases search exhaustive sweep baselines jitter acceptance features
 (default: the first five)
 
 Inputs follow SURVEY.md section 8(d) / BASELINE.md section 3:
@@ -473,15 +473,58 @@ def section_acceptance(names=None):
     print(f"acceptance: {len(c1)} + {len(c2)} workloads", flush=True)
 
 
+def section_features(names=None):
+    """featurize / predict_fused / oracle_time per fused group (estimator.py:157-191,
+    :462-470; workloads.py:276-291) on random candidates, plus group_io."""
+    from fuseopt.graph import group_io
+    from fuseopt.workloads import oracle_time
+
+    out = {}
+    for name in ["chain24", "residual40", "attention36", "recurrent30", "vgg16", "resnet50", "bert"]:
+        if names and name not in names:
+            continue
+        g, profile, comm, mp, lin = load_workload(name)
+        ana = analytic_model(5.0, 1.0 / 1024.0)
+        hws = [HardwareParams(), HardwareParams(noise=0.05, seed=42)]
+        rows = []
+        from fuseopt.search import greedy_postorder_fusion
+
+        for i in range(5):
+            c = make_candidate(g, i) if i < 4 else greedy_postorder_fusion(g)
+            fused = [gr for gr in c.groups if len(gr.member_ops) > 1]
+            fused = fused[:25] if i < 4 else sorted(fused, key=lambda x: (-len(x.member_ops), x.id))[:12]
+            singles = [gr for gr in c.groups if len(gr.member_ops) == 1][:3]
+            grs = []
+            for gr in fused + singles:
+                f = featurize(c, gr, profile)
+                io = group_io(c, gr.id)
+                grs.append({"gid": gr.id, "io": [io.internal_bytes, io.external_in_bytes, io.external_out_bytes],
+                            "features": {"op_codes": list(f.op_codes), "compute_us": list(f.compute_us),
+                                         "in_bytes": list(f.in_bytes), "out_bytes": list(f.out_bytes),
+                                         "edges": [list(e) for e in f.edges], "member_count": f.member_count,
+                                         "total_compute_us": f.total_compute_us,
+                                         "internal_bytes": f.internal_bytes,
+                                         "external_in_bytes": f.external_in_bytes,
+                                         "external_out_bytes": f.external_out_bytes,
+                                         "longest_path_len": f.longest_path_len},
+                            "mp": predict_fused(mp, f), "lin": predict_fused(lin, f),
+                            "analytic": predict_fused(ana, f),
+                            "oracle": [oracle_time(c, gr, hw) for hw in hws]})
+            rows.append({"i": i, "state": state_doc(c), "groups": grs})
+        out[name] = rows
+        print(f"features {name}", flush=True)
+    _dump_gz(os.path.join(OUT, "features.json.gz"), out)
+
+
 def main(argv):
-    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep", "baselines", "jitter", "acceptance")]
+    sections = [a for a in argv if a in ("workloads", "rng", "cases", "search", "exhaustive", "sweep", "baselines", "jitter", "acceptance", "features")]
     names = [a for a in argv if a not in sections]
     if not sections:
         sections = ["workloads", "rng", "cases", "search", "exhaustive"]
     for s in sections:
         {"workloads": section_workloads, "rng": lambda _: section_rng(), "exhaustive": section_exhaustive,
          "sweep": section_sweep, "baselines": section_baselines, "jitter": section_jitter,
-         "acceptance": section_acceptance,
+         "acceptance": section_acceptance, "features": section_features,
          "cases": section_cases, "search": section_search}[s](names or None)
 
 
