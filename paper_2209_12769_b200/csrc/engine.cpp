@@ -1724,6 +1724,13 @@ struct fo_search {
         int64_t br_pos[4][3];
         const State *br_state[4];
         uint64_t br_hs[4];
+        // the branch expansions stay valid for the next pop: the seed's rng
+        // does not move between them, so a pop of branch q's exact state
+        // reuses its candidates and post-expansion rng instead of expanding again
+        int br_avail = 0;
+        State br_src[4];
+        PyRng br_rng[4]{PyRng(0), PyRng(0), PyRng(0), PyRng(0)};
+        int br_meth[4][3];
     };
     // one in-flight device batch: pinned staging, device buffers, results
     struct Lane {
@@ -1747,6 +1754,7 @@ struct fo_search {
     int64_t scored = 0, host_steps = 0;
     bool started = false;
     bool spec = false;  // one-step speculation (latency-bound rounds: few seeds)
+    int spec_at = -1;   // switch speculation on once this few seeds are active (-1: never)
 };
 
 static int lane_reserve(fo_search *S, fo_search::Lane &L, int n) {
@@ -1913,7 +1921,24 @@ static void search_expand(fo_search *S, int lo, int hi) {
             sd.cur = sd.queue.top();
             sd.queue.pop();
             sd.steps++;
-            expand_step(S, sd.pool[sd.cur.slot], sd.cur.h, sd.rng, sd.inc0, sd.sc, sd.cand, sd.meth, sd.h, sd.ncand);
+            int hit = -1;
+            for (int q = 0; q < sd.br_avail && hit < 0; q++)
+                if (sd.br_hs[q] == sd.cur.h && sd.br_src[q].ng == sd.pool[sd.cur.slot].ng &&
+                    sd.br_src[q].rg == sd.pool[sd.cur.slot].rg && sd.br_src[q].bk == sd.pool[sd.cur.slot].bk)
+                    hit = q;
+            sd.br_avail = 0;
+            if (hit >= 0) {
+                sd.ncand = sd.br_n[hit];
+                for (int j = 0; j < sd.ncand; j++) {
+                    sd.cand[j] = sd.br_cand[hit][j];
+                    sd.h[j] = sd.br_h[hit][j];
+                    sd.meth[j] = sd.br_meth[hit][j];
+                }
+                sd.rng = sd.br_rng[hit];
+            } else {
+                expand_step(S, sd.pool[sd.cur.slot], sd.cur.h, sd.rng, sd.inc0, sd.sc, sd.cand, sd.meth, sd.h,
+                            sd.ncand);
+            }
             if (S->spec && step_known(sd)) {
                 replay_seed(S, sd, nullptr);
 #pragma omp atomic
@@ -1946,9 +1971,12 @@ static void search_expand(fo_search *S, int lo, int hi) {
             thread_local Inc inc;
             thread_local Scratch sc;
             PyRng rng = sd.rng;  // the next step continues this seed's draws
-            expand_step(S, *sd.br_state[q], sd.br_hs[q], rng, inc, sc, sd.br_cand[q], nullptr, sd.br_h[q],
+            expand_step(S, *sd.br_state[q], sd.br_hs[q], rng, inc, sc, sd.br_cand[q], sd.br_meth[q], sd.br_h[q],
                         sd.br_n[q]);
+            sd.br_src[q] = *sd.br_state[q];
+            sd.br_rng[q] = rng;
         }
+        for (int r = lo; r < hi; r++) S->seeds[r].br_avail = S->seeds[r].nbr;
     }
     S->expand_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -2099,8 +2127,12 @@ int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seed
     }
     // speculation pays while a round is latency-bound (few seeds): each round
     // then advances a seed by two steps.  FO_SEARCH_SPEC=0/1 overrides.
+    // Long searches end with a tail of few active seeds, so speculation also
+    // switches on when the active count falls to FO_SEARCH_SPEC_AT (default 32).
     const char *sp = getenv("FO_SEARCH_SPEC");
     S->spec = sp ? sp[0] == '1' : R <= 32;
+    const char *sa = getenv("FO_SEARCH_SPEC_AT");
+    S->spec_at = sp ? -1 : (sa ? atoi(sa) : 32);
     cudaSetDevice(g->device);
     *out = S;
     return FO_OK;
@@ -2128,6 +2160,7 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
     int rc = search_start(S);
     if (rc) return rc;
     const int R = (int)S->seeds.size();
+    if (!S->spec && S->spec_at >= 0 && count_active(S, nullptr) <= S->spec_at) S->spec = true;
     search_expand(S, 0, R);
     if ((rc = search_launch(S, S->lanes[0], 0, R)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
     search_replay(S, S->lanes[0], 0, R);
@@ -2259,10 +2292,16 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
         const double w2 = std::chrono::duration<double>(clk::now() - t0).count() / std::max(n2, 1);
         pipeline = n1 > 0 && n2 > 0 && w2 < w1;
     }
-    const int64_t rest = left(it);
-    if (rest != 0) {
-        it += pipeline ? run_pipelined(S, rest, rc) : run_single(S, rest, rc);
+    // the rest in chunks, so speculation can switch on for the tail
+    for (;;) {
+        const int64_t rest = left(it);
+        if (rest == 0 || !any_active(S, 0, R)) break;
+        if (!S->spec && S->spec_at >= 0 && count_active(S, nullptr) <= S->spec_at) S->spec = true;
+        const int64_t chunk = S->spec || S->spec_at < 0 ? rest : cap(rest, 32);
+        const int n = pipeline && !S->spec ? run_pipelined(S, chunk, rc) : run_single(S, chunk, rc);
         if (rc) return rc;
+        it += n;
+        if (n == 0) break;
     }
     if (active_out) *active_out = count_active(S, nullptr);
     if (getenv("FO_SEARCH_PROFILE"))
