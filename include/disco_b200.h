@@ -242,6 +242,14 @@ int fo_rewrite_apply(fo_graph *g, int32_t *ngid, int32_t *rgid, int32_t *bkt, in
  * input's group graph is cyclic. */
 int fo_greedy_postorder(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt,
                         int32_t *ngid_out, int32_t *rgid_out, int32_t *bkt_out);
+
+/* topo_order (graph.py:536-556): the group ids (compact, as in ngid) in the
+ * deterministic topological order of the contracted group graph -- Kahn's
+ * algorithm, ties to the group with the smallest member op.  gid_out holds
+ * one entry per group; *n_out receives the count.  FO_CYCLE when the
+ * contracted graph is cyclic. */
+int fo_topo_order(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t *gid_out,
+                  int32_t *n_out);
 /* threshold_allreduce_fusion (search.py:247-302): buckets scanned in production
  * order -- order[n_order] = bucket ids sorted by simulated start (the cp path,
  * search.py:264-267), or NULL for the contracted topological production key

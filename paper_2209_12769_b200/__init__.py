@@ -70,6 +70,7 @@ from .search import (
     backtracking_search,
     exhaustive_search,
     greedy_postorder_fusion,
+    topo_order,
     lockstep_search,
     threshold_allreduce_fusion,
 )

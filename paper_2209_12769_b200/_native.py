@@ -72,6 +72,7 @@ SIGNATURES = [
     ("fo_random_apply", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, P(C.c_int32)]),
     ("fo_expand_all", C.c_int, [vp, vp, vp, vp, C.c_int32, vp, vp, vp, P(C.c_int32)]),
     ("fo_state_hash", C.c_int, [vp, vp, vp, vp, C.c_int32, vp]),
+    ("fo_topo_order", C.c_int, [vp, vp, vp, vp, vp, P(C.c_int32)]),
     ("fo_greedy_postorder", C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     ("fo_rewrite_pairs", C.c_int, [vp, vp, vp, vp, C.c_int32, vp, C.c_int32, P(C.c_int32)]),
     ("fo_rewrite_apply", C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, P(C.c_int32)]),

@@ -1589,6 +1589,24 @@ int fo_greedy_postorder(fo_graph *g, const int32_t *ngid, const int32_t *rgid, c
     return FO_OK;
 }
 
+// topo_order (graph.py:536-556): group ids in the deterministic topological
+// order of the contracted group graph
+int fo_topo_order(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t *gid_out,
+                  int32_t *n_out) {
+    if (!g || !gid_out || !n_out) return fail(FO_INVALID_ARG, "bad arguments");
+    Engine eng(g);
+    State s;
+    if (!eng.load_state(ngid, rgid, bkt, s)) return fail(FO_INVALID_ARG, "bad state");
+    Scratch sc;
+    Index ix;
+    eng.build(s, ix, sc, false);
+    std::vector<int32_t> topo;
+    if (!eng.topo_groups(ix, topo)) return fail(FO_CYCLE, "contracted group graph is cyclic");
+    for (size_t i = 0; i < topo.size(); i++) gid_out[i] = ix.gid[topo[i]];
+    *n_out = (int32_t)topo.size();
+    return FO_OK;
+}
+
 // threshold_allreduce_fusion (search.py:247-302): buckets in production order
 // (order[] = bucket ids by simulated start; NULL: contracted topological
 // production order), consecutive neighbours merged while the merged size stays

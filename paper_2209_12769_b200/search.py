@@ -300,6 +300,19 @@ def exhaustive_search(g0: HloGraph, cp, max_ops: int = 8, max_tensors: int = 4) 
 # --- heuristic baselines (search.py:228-302) ---------------------------------
 
 
+def topo_order(g: HloGraph) -> list:
+    """Deterministic topological order of group ids over the contracted graph,
+    ties to the group with the smallest member op id (graph.py:536-556), from
+    the native engine.  CycleError when the contraction is cyclic."""
+    dg = engine_graph(g)
+    ng, rg, bk, _, gids, _ = state_arrays(g)
+    out = np.empty(max(len(gids), 1), np.int32)
+    n = C.c_int32(0)
+    st = N.lib().fo_topo_order(dg.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), N.ptr(out), C.byref(n))
+    _raise(st, "topo_order", N.last_error())
+    return [gids[int(x)] for x in out[:n.value]]
+
+
 def greedy_postorder_fusion(g: HloGraph) -> HloGraph:
     """Walk ops in post order (reverse topological) and non-duplicate-fuse each
     op's current group with its first fusible predecessor when the rewrite is

@@ -510,7 +510,9 @@ def section_features(names=None):
                             "mp": predict_fused(mp, f), "lin": predict_fused(lin, f),
                             "analytic": predict_fused(ana, f),
                             "oracle": [oracle_time(c, gr, hw) for hw in hws]})
-            rows.append({"i": i, "state": state_doc(c), "groups": grs})
+            from fuseopt.graph import topo_order
+
+            rows.append({"i": i, "state": state_doc(c), "groups": grs, "topo": topo_order(c)})
         out[name] = rows
         print(f"features {name}", flush=True)
     _dump_gz(os.path.join(OUT, "features.json.gz"), out)

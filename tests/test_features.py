@@ -120,3 +120,23 @@ def test_predict_fused_empty_and_edge_free():
     ana = analytic_model(5.0, 1.0 / 1024.0)
     f0 = P.SubgraphFeatures((), (), (), (), (), 0, 0.0, 0, 0, 0, 0)
     assert P.predict_fused(ana, f0) == pytest.approx(5.0)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_topo_order_matches_reference(name):
+    """topo_order (graph.py:536-556) through the native engine (host only)."""
+    g = P.load_workload(name)[0]
+    for row in _doc()[name]:
+        c = graph_with_state(g, row["state"])
+        assert P.topo_order(c) == row["topo"]
+
+
+def test_topo_order_cyclic_contraction_raises():
+    from paper_2209_12769_b200.graph import DataEdge, FusionGroup, OpNode, build_graph
+
+    ops = [OpNode(i, "Mul", input_shape_key=f"k{i}", out_bytes=8, compute_us=1.0) for i in range(3)]
+    edges = [DataEdge(0, 1, 8), DataEdge(1, 2, 8)]
+    g = build_graph(ops, edges, groups=[FusionGroup(0, frozenset([0, 2])), FusionGroup(1, frozenset([1]))])
+    with pytest.raises(P.CycleError):
+        P.topo_order(g)
+    assert P.topo_order(build_graph(ops, edges)) == [0, 1, 2]
