@@ -387,7 +387,10 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         dg.emb_h = h;
         dg.emb_F = F;
         // estimator memo: 2 x 2^20 slots, cleared whenever the model changes
-        const size_t slots = (size_t)1 << 20;
+        const char *mlog = getenv("FO_MEMO_LOG2");  // tuning override: slots per precision
+        const size_t slots = (size_t)1 << (mlog ? std::max(10, std::min(24, atoi(mlog))) : 20);
+        if (g->d_memo && g->memo_slots != slots) { cudaFree(g->d_memo); g->d_memo = nullptr; }
+        g->memo_slots = slots;
         if (!g->d_memo) CUDA_TRY(cudaMalloc(&g->d_memo, 2 * slots * sizeof(MemoEnt)));
         CUDA_TRY(cudaMemset(g->d_memo, 0, 2 * slots * sizeof(MemoEnt)));
         dg.memo[0] = (MemoEnt *)g->d_memo;

@@ -161,6 +161,7 @@ struct fo_graph {
     void *d_static = nullptr;  // one allocation for the static graph
     void *d_model = nullptr;   // H0 + weights
     void *d_memo = nullptr;    // estimator memo tables
+    size_t memo_slots = 0;     // slots per precision
     void *d_keys = nullptr;    // hardware-oracle jitter key bytes
     fo::DGraph dg{};
     bool model_set = false;
