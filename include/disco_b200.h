@@ -209,6 +209,16 @@ int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, 
                    double *cost_out, int32_t *status_out, void *stream);
 int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
                         double *cost_out, int32_t *status_out);
+/* Pipelined fo_score_delta_host for streams of batches: enqueues H2D of the
+ * candidates (host buffers, pinned for overlap), [if clear_memo, an
+ * fo_memo_clear of this precision's table], the score and the D2H of cost_out / status_out, and returns a
+ * ticket.  Two submissions may be in flight: a third waits for the oldest.
+ * Results are valid, and the input buffers reusable, after
+ * fo_score_wait(g, ticket).  Same semantics per batch as
+ * fo_score_delta_host (simulator.py:143-145 per candidate). */
+int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
+                          int32_t clear_memo, double *cost_out, int32_t *status_out, int64_t *ticket_out);
+int fo_score_wait(fo_graph *g, int64_t ticket);
 
 /* random_apply (rewrite.py:222-263) on one state in place, driven by a
  * CPython random.Random state: mt_state = getstate()[1] (624 words + index). */

@@ -253,6 +253,15 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_io) cudaFree(g->d_io);
     if (g->d_parent) cudaFree(g->d_parent);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
+    for (auto &sl : g->aslot) {
+        if (sl.done) cudaEventSynchronize(sl.done);
+        if (sl.d) cudaFree(sl.d);
+        if (sl.h2d) cudaEventDestroy(sl.h2d);
+        if (sl.kdone) cudaEventDestroy(sl.kdone);
+        if (sl.done) cudaEventDestroy(sl.done);
+    }
+    if (g->hstream) cudaStreamDestroy(g->hstream);
+    if (g->dstream) cudaStreamDestroy(g->dstream);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
     return FO_OK;
@@ -594,6 +603,76 @@ int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *chan
     CUDA_TRY(cudaMemcpyAsync(cost_out, b + o_cost, (size_t)K * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(status_out, b + o_s, (size_t)K * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    return FO_OK;
+}
+
+// Pipelined form of fo_score_delta_host.  Slot t % 2 owns its device
+// staging; H2D runs on one copy stream (then signals the compute stream) and
+// D2H on another (after the kernel), so consecutive submissions overlap
+// transfers with the other batch's kernel.  A slot is reused only after its previous
+// submission's D2H completed.
+int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
+                          int32_t clear_memo, double *cost_out, int32_t *status_out, int64_t *ticket_out) {
+    if (!g || !ticket_out) return fail(FO_INVALID_ARG, "null argument");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (K < 0 || !offsets || offsets[0] != 0 || offsets[K] < 0) return fail(FO_INVALID_ARG, "bad offsets");
+    CUDA_TRY(cudaSetDevice(g->device));
+    if (!g->hstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->hstream, cudaStreamNonBlocking));
+    if (!g->dstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->dstream, cudaStreamNonBlocking));
+    const int64_t t = g->next_ticket;
+    fo_graph::AsyncSlot &sl = g->aslot[t & 1];
+    if (!sl.h2d) {
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.kdone, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
+    if (sl.ticket >= 0) CUDA_TRY(cudaEventSynchronize(sl.done));  // slot free: its last D2H landed
+    const size_t nc = (size_t)offsets[K];
+    const size_t o_c = al256(4 * ((size_t)K + 1)), o_cost = o_c + al256(8 * nc + 8),
+                 o_s = o_cost + al256((size_t)K * 8 + 8), need = o_s + al256((size_t)K * 4 + 4);
+    if (sl.bytes < need) {
+        if (sl.d) CUDA_TRY(cudaFree(sl.d));
+        sl.d = nullptr;
+        sl.bytes = 0;
+        CUDA_TRY(cudaMalloc(&sl.d, need));
+        sl.bytes = need;
+    }
+    char *b = sl.d;
+    cudaStream_t hs = g->hstream, ds = g->dstream, s = g->stream;
+    CUDA_TRY(cudaMemcpyAsync(b, offsets, 4 * ((size_t)K + 1), cudaMemcpyHostToDevice, hs));
+    if (nc) CUDA_TRY(cudaMemcpyAsync(b + o_c, changes, 8 * nc, cudaMemcpyHostToDevice, hs));
+    CUDA_TRY(cudaEventRecord(sl.h2d, hs));
+    CUDA_TRY(cudaStreamWaitEvent(s, sl.h2d, 0));
+    if (clear_memo && g->d_memo) {  // only the table this precision's estimator reads (score.cu K2)
+        const size_t slots = (size_t)g->dg.memo_mask + 1;
+        MemoEnt *tab = (MemoEnt *)g->d_memo + (precision == FO_PREC_FP64 ? slots : 0);
+        CUDA_TRY(cudaMemsetAsync(tab, 0, slots * sizeof(MemoEnt), s));
+    }
+    int st = score_delta_device(g, (const int32_t *)b, (const int32_t *)(b + o_c), K, precision,
+                                (double *)(b + o_cost), (int32_t *)(b + o_s), s);
+    if (st) return st;
+    CUDA_TRY(cudaEventRecord(sl.kdone, s));
+    CUDA_TRY(cudaStreamWaitEvent(ds, sl.kdone, 0));
+    if (K) {
+        CUDA_TRY(cudaMemcpyAsync(cost_out, b + o_cost, (size_t)K * 8, cudaMemcpyDeviceToHost, ds));
+        CUDA_TRY(cudaMemcpyAsync(status_out, b + o_s, (size_t)K * 4, cudaMemcpyDeviceToHost, ds));
+    }
+    CUDA_TRY(cudaEventRecord(sl.done, ds));
+    sl.ticket = t;
+    g->next_ticket = t + 1;
+    *ticket_out = t;
+    return FO_OK;
+}
+
+int fo_score_wait(fo_graph *g, int64_t ticket) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (ticket < 0 || ticket >= g->next_ticket) return fail(FO_INVALID_ARG, "unknown ticket");
+    const fo_graph::AsyncSlot &sl = g->aslot[ticket & 1];
+    // a slot that moved on to a later ticket already waited for this one
+    if (sl.ticket == ticket) CUDA_TRY(cudaEventSynchronize(sl.done));
     return FO_OK;
 }
 

@@ -182,6 +182,16 @@ struct fo_graph {
     size_t pinned_bytes = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 0;
+    // fo_score_delta_submit / fo_score_wait: two in-flight submissions; H2D and
+    // D2H on their own streams so one batch's transfers overlap the other's kernel
+    struct AsyncSlot {
+        char *d = nullptr;
+        size_t bytes = 0;
+        cudaEvent_t h2d = nullptr, kdone = nullptr, done = nullptr;
+        int64_t ticket = -1;
+    } aslot[2];
+    cudaStream_t hstream = nullptr, dstream = nullptr;
+    int64_t next_ticket = 0;
     std::mutex mu;
 };
 

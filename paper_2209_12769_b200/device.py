@@ -207,6 +207,23 @@ class DeviceGraph:
         _raise(st, "fo_score_delta_host", N.last_error())
         return cost, status
 
+    def score_delta_submit(self, offsets, changes, cost, status, precision=N.FO_PREC_FP32, clear_memo=False):
+        """Pipelined fo_score_delta_host: enqueue one batch of sparse candidates
+        held in host arrays (pinned for overlap) and return a ticket; two
+        batches may be in flight.  `cost` / `status` (host, length K) are
+        written once score_wait(ticket) returns; keep every buffer alive until then."""
+        import ctypes
+
+        K = len(offsets) - 1
+        t = ctypes.c_int64(-1)
+        st = N.lib().fo_score_delta_submit(self.h, N.ptr(offsets), N.ptr(changes), K, precision, int(bool(clear_memo)),
+                                           N.ptr(cost), N.ptr(status), ctypes.byref(t))
+        _raise(st, "fo_score_delta_submit", N.last_error())
+        return t.value
+
+    def score_wait(self, ticket):
+        _raise(N.lib().fo_score_wait(self.h, int(ticket)), "fo_score_wait", N.last_error())
+
     def score_delta_device(self, offsets, changes, cost, status, precision=N.FO_PREC_FP32, stream=None):
         """Asynchronous scoring of device-resident sparse candidates (torch tensors)."""
         import torch

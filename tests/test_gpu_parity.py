@@ -373,6 +373,40 @@ def test_delta_scoring_equals_dense(name):
             assert np.array_equal(c.cpu().numpy(), dense)
 
 
+def test_pipelined_delta_submissions_equal_sync():
+    """fo_score_delta_submit / fo_score_wait: several batches in flight (two
+    slots, so the third submission waits for the first) give the synchronous
+    call's results, per batch and in any wait order."""
+    import torch
+
+    g, cps = providers("resnet50", N.FO_PREC_FP32)
+    dg = cps["mp"].device_graph(g)
+    dg.set_parent()
+    batches = []
+    for b in range(5):
+        seeds = np.arange(b * 700, b * 700 + 600 + 37 * b, dtype=np.uint64)
+        off, chg = dg.make_candidates_delta(seeds)
+        ref, st_ref = dg.score_delta_host(off, chg)
+        h = [torch.from_numpy(off).pin_memory(), torch.from_numpy(chg).pin_memory(),
+             torch.zeros(len(seeds), dtype=torch.float64).pin_memory(),
+             torch.full((len(seeds),), -1, dtype=torch.int32).pin_memory()]
+        batches.append((h, ref, st_ref))
+    tickets = [dg.score_delta_submit(*(x for x in h), clear_memo=(i % 2 == 0)) for i, (h, _, _) in enumerate(batches)]
+    for t in reversed(tickets):
+        dg.score_wait(t)
+    for h, ref, st_ref in batches:
+        assert np.array_equal(h[3].numpy(), st_ref) and np.array_equal(h[2].numpy(), ref)
+    # a synchronous call between submissions is ordered with them
+    h, ref, _ = batches[0]
+    h[2].zero_()
+    t = dg.score_delta_submit(*h)
+    mid, _ = dg.score_delta_host(h[0].numpy(), h[1].numpy())
+    dg.score_wait(t)
+    assert np.array_equal(h[2].numpy(), ref) and np.array_equal(mid, ref)
+    with pytest.raises(Exception):
+        dg.score_wait(10**9)
+
+
 def test_delta_scoring_rejects_bad_input():
     g, cps = providers("vgg16", N.FO_PREC_FP32)
     dg = cps["mp"].device_graph(g)
