@@ -149,6 +149,13 @@ def test_host_only_handle_refuses_device_work():
     ng, rg, bk, vb = dg.make_candidates([1, 2])
     with pytest.raises(P.DeviceError):
         dg.score_host(ng, rg, bk, vb)
+    off = np.zeros(3, np.int32)
+    chg = np.zeros((0, 2), np.int32)
+    cost, st = np.zeros(2), np.zeros(2, np.int32)
+    with pytest.raises(P.DeviceError):
+        dg.score_delta_submit(off, chg, cost, st)
+    with pytest.raises(P.DeviceError):
+        dg.score_wait(0)
 
 
 @pytest.mark.parametrize("name", SMALL + ["gpt2m"])
