@@ -682,7 +682,7 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     int run0 = -1, run1 = -1, done = 0, nc = 0, nb = 0, st = FO_OK;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
-    double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0, mk = 0.0;
+    double end0 = 0.0, end1 = 0.0, now = 0.0, last = 0.0;
     unsigned long long level = 0;
     for (;;) {
         // start_available (simulator.py:98-115): compute lane, then comm lane;
@@ -693,7 +693,6 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
             end0 = __dadd_rn(now, x.dur);
             sb0 = x.sb;
             se0 = x.se;
-            if (end0 > mk) mk = end0;
             if (TL) { a.tl.c_id[nc] = w.g2id()[run0]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
         }
         if (run1 < 0 && headb < tailb) {
@@ -702,7 +701,6 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
             end1 = __dadd_rn(now, x.dur);
             sb1 = x.sb;
             se1 = x.se;
-            if (end1 > mk) mk = end1;
             if (TL) { a.tl.b_id[nb] = w.b2id()[run1 - G]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
         }
         if (run0 < 0 && run1 < 0) {
@@ -737,7 +735,7 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
             }
         }
     }
-    a.cost_out[k] = st == FO_OK ? mk : 0.0;
+    a.cost_out[k] = st == FO_OK ? now : 0.0;  // makespan = last completion time
     a.status_out[k] = st;
     if (TL) { *a.tl.n_c = nc; *a.tl.n_b = nb; }
     if (a.bad_out) *a.bad_out = -1;
@@ -766,6 +764,18 @@ __device__ __forceinline__ bool ring_push(Ent16 *buf, int head, int &tail, const
     return true;
 }
 
+// append without reading the ring when the key is not below the last one
+// pushed (the common case: levels only grow); lastkey is the ring's max key
+__device__ __forceinline__ bool ring_push_t(Ent16 *buf, int head, int &tail, uint32_t &lastkey, const Ent16 &x) {
+    if (tail - head >= kRing) return false;
+    if (tail == head || x.key >= lastkey) {
+        buf[(tail++) & (kRing - 1)] = x;
+        lastkey = x.key;
+        return true;
+    }
+    return ring_push(buf, head, tail, x);
+}
+
 __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const double *__restrict__ dur,
                                           const uint16_t *__restrict__ sptr, uint16_t *__restrict__ indeg,
                                           const uint32_t *__restrict__ succ, Ent16 *__restrict__ rg,
@@ -774,8 +784,10 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
     int done = 0;
     bool run0 = false, run1 = false;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
-    double end0 = 0.0, end1 = 0.0, now = 0.0, mk = 0.0;
+    double end0 = 0.0, end1 = 0.0, now = 0.0;
     uint32_t level = 0;
+    uint32_t lastg = hg > 0 ? rg[(hg - 1) & (kRing - 1)].key : 0u;
+    uint32_t lastb = hb > 0 ? rb[(hb - 1) & (kRing - 1)].key : 0u;
     // finish_node (simulator.py:88-96); false on ring overflow
     auto release = [&](unsigned qb, unsigned qe) -> bool {
         for (unsigned q = qb; q < qe; q++) {
@@ -789,7 +801,8 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
             indeg[s] = (uint16_t)d;
             if (d == 0) {
                 x.key = level | (e >> 16);
-                if (!((int)s < G ? ring_push(rg, headg, tailg, x) : ring_push(rb, headb, tailb, x))) return false;
+                if (!((int)s < G ? ring_push_t(rg, headg, tailg, lastg, x) : ring_push_t(rb, headb, tailb, lastb, x)))
+                    return false;
             }
         }
         return true;
@@ -802,7 +815,6 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
             end0 = __dadd_rn(now, x.dur);
             sb0 = x.sb;
             se0 = x.se;
-            mk = end0 > mk ? end0 : mk;
         }
         if (!run1 && headb < tailb) {
             const Ent16 x = rb[(headb++) & (kRing - 1)];
@@ -810,7 +822,6 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
             end1 = __dadd_rn(now, x.dur);
             sb1 = x.sb;
             se1 = x.se;
-            mk = end1 > mk ? end1 : mk;
         }
     };
     start();
@@ -832,7 +843,7 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
         }
         start();
     }
-    a.cost_out[k] = done == N ? mk : 0.0;
+    a.cost_out[k] = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
     a.status_out[k] = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
     if (a.bad_out) *a.bad_out = -1;
     return true;
@@ -945,8 +956,9 @@ __device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const NodeR
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     int run0 = -1, run1 = -1, done = 0, nc = 0, nb = 0;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
-    double end0 = 0.0, end1 = 0.0, now = 0.0, mk = 0.0;
+    double end0 = 0.0, end1 = 0.0, now = 0.0;
     uint32_t level = 0;
+    uint32_t lastg = hg > 0 ? rg[hg - 1] : 0u, lastb = hb > 0 ? rb[hb - 1] : 0u;  // max key in each run
     // release the successors of a completed node (finish_node, simulator.py:88-96)
     auto release = [&](unsigned qb, unsigned qe) {
         for (unsigned q = qb; q < qe; q++) {
@@ -959,7 +971,12 @@ __device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const NodeR
                 const int h = isg ? headg : headb;
                 int i = isg ? tailg++ : tailb++;
                 const uint32_t key = level | (uint32_t)(isg ? s : s - G);
-                while (i > h && r[i - 1] > key) { r[i] = r[i - 1]; i--; }
+                uint32_t &last = isg ? lastg : lastb;
+                if (i == h || key >= last) {
+                    last = key;
+                } else {
+                    while (i > h && r[i - 1] > key) { r[i] = r[i - 1]; i--; }
+                }
                 r[i] = key;
             }
         }
@@ -973,7 +990,6 @@ __device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const NodeR
             end0 = __dadd_rn(now, r.dur);
             sb0 = r.sb;
             se0 = r.se;
-            mk = end0 > mk ? end0 : mk;
             if (TL) { a.tl.c_id[nc] = tlid[run0]; a.tl.c_start[nc] = now; a.tl.c_end[nc] = end0; nc++; }
         }
         if (run1 < 0 && headb < tailb) {
@@ -982,7 +998,6 @@ __device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const NodeR
             end1 = __dadd_rn(now, r.dur);
             sb1 = r.sb;
             se1 = r.se;
-            mk = end1 > mk ? end1 : mk;
             if (TL) { a.tl.b_id[nb] = tlid[run1]; a.tl.b_start[nb] = now; a.tl.b_end[nb] = end1; nb++; }
         }
     };
@@ -999,7 +1014,7 @@ __device__ __forceinline__ void smem_loop(const ScoreArgs &a, int k, const NodeR
         start();
     }
     const int st = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
-    a.cost_out[k] = st == FO_OK ? mk : 0.0;
+    a.cost_out[k] = st == FO_OK ? now : 0.0;
     a.status_out[k] = st;
     if (TL) { *a.tl.n_c = nc; *a.tl.n_b = nb; }
     if (a.bad_out) *a.bad_out = -1;
