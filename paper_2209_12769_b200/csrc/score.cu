@@ -674,11 +674,21 @@ __device__ __forceinline__ unsigned long long se_make<unsigned long long>(unsign
     return ((unsigned long long)prank << 20) | node;
 }
 
+// hide a pointer's derivation from the compiler, so it stays one register
+// pair instead of a base plus a spilled offset re-read at every use
+template <typename T>
+__device__ __forceinline__ T *opaque_ptr(T *p) {
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
+}
+
 template <bool TL, typename IT, typename SE>
 __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const double *__restrict__ dur,
-                                           const IT *__restrict__ sptr, IT *__restrict__ indeg,
-                                           const SE *__restrict__ succ, ReadyEnt *__restrict__ bufg,
+                                           const IT *__restrict__ sptr, IT *__restrict__ indeg_,
+                                           const SE *__restrict__ succ_, ReadyEnt *__restrict__ bufg,
                                            ReadyEnt *__restrict__ bufb, const Ws &w, int G, int N, int hg, int hb) {
+    IT *__restrict__ indeg = opaque_ptr(indeg_);
+    const SE *__restrict__ succ = opaque_ptr(succ_);
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     int run0 = -1, run1 = -1, done = 0, nc = 0, nb = 0, st = FO_OK;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
@@ -777,9 +787,10 @@ __device__ __forceinline__ bool ring_push_t(Ent16 *buf, int head, int &tail, uin
 }
 
 __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const double *__restrict__ dur,
-                                          const uint16_t *__restrict__ sptr, uint16_t *__restrict__ indeg,
+                                          const uint16_t *__restrict__ sptr, uint16_t *__restrict__ indeg_,
                                           const uint32_t *__restrict__ succ, Ent16 *__restrict__ rg,
                                           Ent16 *__restrict__ rb, int G, int N, int hg, int hb) {
+    uint16_t *__restrict__ indeg = opaque_ptr(indeg_);  // measured: a spilled offset otherwise
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     int done = 0;
     bool run0 = false, run1 = false;
