@@ -792,8 +792,7 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
                                           Ent16 *__restrict__ rb, int G, int N, int hg, int hb) {
     uint16_t *__restrict__ indeg = opaque_ptr(indeg_);  // measured: a spilled offset otherwise
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
-    int done = 0;
-    bool run0 = false, run1 = false;
+    int run0 = 0, run1 = 0;  // lane busy flags as full registers (bools get byte-packed)
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
     double end0 = 0.0, end1 = 0.0, now = 0.0;
     uint32_t level = 0;
@@ -822,14 +821,14 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
     auto start = [&]() {
         if (!run0 && headg < tailg) {
             const Ent16 x = rg[(headg++) & (kRing - 1)];
-            run0 = true;
+            run0 = 1;
             end0 = __dadd_rn(now, x.dur);
             sb0 = x.sb;
             se0 = x.se;
         }
         if (!run1 && headb < tailb) {
             const Ent16 x = rb[(headb++) & (kRing - 1)];
-            run1 = true;
+            run1 = 1;
             end1 = __dadd_rn(now, x.dur);
             sb1 = x.sb;
             se1 = x.se;
@@ -843,17 +842,16 @@ __device__ __forceinline__ bool ring_loop(const ScoreArgs &a, int k, const doubl
         const double t = c0 ? end0 : end1;
         if (t > now) { now = t; level += 0x10000u; }
         if (c0) {
-            run0 = false;
-            done++;
+            run0 = 0;
             if (!release(sb0, se0)) return false;
         }
         if (c1) {
-            run1 = false;
-            done++;
+            run1 = 0;
             if (!release(sb1, se1)) return false;
         }
         start();
     }
+    const int done = headg + headb;  // every started node has completed once both lanes are idle
     a.cost_out[k] = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
     a.status_out[k] = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
     if (a.bad_out) *a.bad_out = -1;
