@@ -308,6 +308,9 @@ int fo_search_result(fo_search *s, int32_t r, double *best_cost, int64_t *counte
                      int32_t *best_rgid, int32_t *best_bkt, fo_trace_rec *trace, int64_t trace_cap);
 /* Per-round device time (ms) of the scoring kernels and host expand time (ms). */
 int fo_search_timing(fo_search *s, double *device_ms, double *expand_ms, int64_t *scored);
+/* Rounds (device batches of lock-stepped steps) executed so far by
+ * fo_search_round / fo_search_run. */
+int fo_search_rounds(fo_search *s, int64_t *rounds_out);
 int fo_search_destroy(fo_search *s);
 
 /* ---- misc -------------------------------------------------------------- */

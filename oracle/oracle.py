@@ -150,8 +150,11 @@ class Workload:
     lin: dict
 
 
-def load_workload(name, root=GOLDEN) -> Workload:
-    base = os.path.join(root, "workloads", name)
+WORKLOADS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "workloads")
+
+
+def load_workload(name, root=WORKLOADS) -> Workload:
+    base = os.path.join(root, name)
     graph = _read_json(base + ".graph.json.gz")
     prof = _read_json(base + ".profile.json.gz")
     profile = {(e["op_code"], e["input_shape_key"]): float(e["time_us"]) for e in prof["entries"]}
@@ -159,7 +162,7 @@ def load_workload(name, root=GOLDEN) -> Workload:
     src = name
     if os.path.exists(base + ".model_from.json"):
         src = _read_json(base + ".model_from.json")["model_from"]
-    sbase = os.path.join(root, "workloads", src)
+    sbase = os.path.join(root, src)
     mp = _read_json(sbase + ".mp.model.json.gz")
     lin = _read_json(sbase + ".lin.model.json")
     return Workload(name, graph, profile, (float(comm["C"]), float(comm["D"])), mp, lin)

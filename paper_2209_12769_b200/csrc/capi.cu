@@ -581,13 +581,23 @@ int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, 
     return score_delta_device(g, offsets, changes, K, precision, cost_out, status_out, (cudaStream_t)stream);
 }
 
+// sparse-candidate offsets: offsets[0] == 0 and non-decreasing, so every
+// candidate's change range lies inside the staged changes buffer.  (Indices
+// inside one candidate must be distinct: duplicates race in K1.)
+static bool offsets_ok(const int32_t *offsets, int32_t K) {
+    if (!offsets || offsets[0] != 0) return false;
+    for (int32_t k = 0; k < K; k++)
+        if (offsets[k + 1] < offsets[k]) return false;
+    return true;
+}
+
 int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
                         double *cost_out, int32_t *status_out) {
     if (!g) return fail(FO_INVALID_ARG, "null graph");
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
     std::lock_guard<std::mutex> lk(g->mu);
     if (K <= 0) return FO_OK;
-    if (!offsets || offsets[0] != 0 || offsets[K] < 0) return fail(FO_INVALID_ARG, "bad offsets");
+    if (!offsets_ok(offsets, K)) return fail(FO_INVALID_ARG, "bad offsets (offsets[0] != 0 or decreasing)");
     CUDA_TRY(cudaSetDevice(g->device));
     const size_t nc = (size_t)offsets[K];
     size_t o_c = al256(4 * ((size_t)K + 1)), o_cost = o_c + al256(8 * nc + 8), o_s = o_cost + al256((size_t)K * 8);
@@ -616,7 +626,7 @@ int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *ch
     if (!g || !ticket_out) return fail(FO_INVALID_ARG, "null argument");
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
     std::lock_guard<std::mutex> lk(g->mu);
-    if (K < 0 || !offsets || offsets[0] != 0 || offsets[K] < 0) return fail(FO_INVALID_ARG, "bad offsets");
+    if (K < 0 || !offsets_ok(offsets, K)) return fail(FO_INVALID_ARG, "bad offsets (offsets[0] != 0 or decreasing)");
     CUDA_TRY(cudaSetDevice(g->device));
     if (!g->hstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->hstream, cudaStreamNonBlocking));
     if (!g->dstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->dstream, cudaStreamNonBlocking));

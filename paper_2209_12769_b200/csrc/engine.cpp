@@ -1770,6 +1770,7 @@ struct fo_search {
     double launch_ms = 0, wait_ms = 0, replay_ms = 0;  // host-side split (FO_SEARCH_PROFILE)
     double put_ms = 0, issue_ms = 0;
     int64_t scored = 0, host_steps = 0;
+    int64_t rounds = 0;  // device rounds run (fo_search_rounds)
     bool started = false;
     bool spec = false;  // one-step speculation (latency-bound rounds: few seeds)
     int spec_at = -1;   // switch speculation on once this few seeds are active (-1: never)
@@ -2182,6 +2183,7 @@ int fo_search_round(fo_search *S, int32_t *active_out, double *best_cost_out) {
     search_expand(S, 0, R);
     if ((rc = search_launch(S, S->lanes[0], 0, R)) || (rc = lane_wait(S, S->lanes[0]))) return rc;
     search_replay(S, S->lanes[0], 0, R);
+    S->rounds++;
     *active_out = count_active(S, best_cost_out);
     return FO_OK;
 }
@@ -2321,6 +2323,7 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
         it += n;
         if (n == 0) break;
     }
+    S->rounds += it;
     if (active_out) *active_out = count_active(S, nullptr);
     if (getenv("FO_SEARCH_PROFILE"))
         fprintf(stderr, "fo_search_run: rounds %lld pipeline %d spec %d (host-only steps %lld) device %.1f ms expand %.1f ms launch %.1f ms (put %.1f, issue %.1f) wait %.1f ms replay %.1f ms\n",
@@ -2354,6 +2357,12 @@ int fo_search_timing(fo_search *S, double *device_ms, double *expand_ms, int64_t
     if (device_ms) *device_ms = S->device_ms;
     if (expand_ms) *expand_ms = S->expand_ms;
     if (scored) *scored = S->scored;
+    return FO_OK;
+}
+
+int fo_search_rounds(fo_search *S, int64_t *rounds_out) {
+    if (!S || !rounds_out) return fail(FO_INVALID_ARG, "null argument");
+    *rounds_out = S->rounds;
     return FO_OK;
 }
 

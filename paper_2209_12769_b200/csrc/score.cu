@@ -1476,7 +1476,9 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         #pragma unroll 4
         for (int i = tid; i < A; i += TEAM) w.bki()[i] = pb[2 * V + i];
         tsync<TEAM>();
-        for (int c = a.doff[k] + tid; c < a.doff[k + 1]; c += TEAM) {
+        const int c0 = a.doff[k], c1 = a.doff[k + 1];
+        if (c0 < 0 || c1 < c0 || c1 > a.doff[a.K]) bad = true;  // offsets must be non-decreasing
+        else for (int c = c0 + tid; c < c1; c += TEAM) {
             const int idx = a.dchg[2 * c], val = a.dchg[2 * c + 1];
             if (idx < 0 || idx >= 2 * V + A) { bad = true; continue; }
             if (idx < V) w.nn()[idx] = val;
@@ -1640,7 +1642,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
         for (int i = tid; i < N; i += TEAM) {
             double d = a.ext_dur[i];
             w.dur()[i] = d;
-            if (d < 0.0) badk = min(badk, pack_bad(i, FO_NEGATIVE_DURATION));
+            if (!(d >= 0.0)) badk = min(badk, pack_bad(i, FO_NEGATIVE_DURATION));
         }
     } else {
         const bool hw = g.provider == FO_PROVIDER_HW_ORACLE;

@@ -27,6 +27,30 @@ def current_device() -> int:
     return -1
 
 
+def _host_array(x, dtype, name, ndim, writable=False):
+    """A host buffer that can cross the C-ABI by pointer: numpy arrays or CPU
+    torch tensors of exactly ``dtype``, C-contiguous (no silent copy -- the
+    library writes into / reads from this very memory asynchronously)."""
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            if x.device.type != "cpu":
+                raise ValueError(f"{name} must be a host buffer, got a {x.device} tensor")
+            x = x.numpy()
+    except ImportError:
+        pass
+    if not isinstance(x, np.ndarray):
+        raise TypeError(f"{name} must be a numpy array or a CPU tensor")
+    if x.dtype != dtype:
+        raise TypeError(f"{name} must be {np.dtype(dtype).name}, got {x.dtype}")
+    if x.ndim != ndim or not x.flags.c_contiguous:
+        raise ValueError(f"{name} must be a C-contiguous {ndim}-D array")
+    if writable and not x.flags.writeable:
+        raise ValueError(f"{name} must be writable")
+    return x
+
+
 class StaticArrays:
     """A graph's static part in build_graph order (graph.py:314-316)."""
 
@@ -82,6 +106,7 @@ class DeviceGraph:
         _raise(st, "fo_graph_create", N.last_error())
         self.h = h
         self._keep = []
+        self._inflight = {}  # ticket -> host buffers of a pipelined submission
         cm = cost_model_fn(self.static, self._keep)
         st = L.fo_graph_set_cost_model(self.h, C.byref(cm))
         _raise(st, "fo_graph_set_cost_model", N.last_error())
@@ -210,19 +235,36 @@ class DeviceGraph:
     def score_delta_submit(self, offsets, changes, cost, status, precision=N.FO_PREC_FP32, clear_memo=False):
         """Pipelined fo_score_delta_host: enqueue one batch of sparse candidates
         held in host arrays (pinned for overlap) and return a ticket; two
-        batches may be in flight.  `cost` / `status` (host, length K) are
-        written once score_wait(ticket) returns; keep every buffer alive until then."""
+        batches may be in flight.  `cost` (float64) / `status` (int32), host,
+        length >= K, are written once score_wait(ticket) returns.  The handle
+        keeps references to all four buffers until then."""
         import ctypes
 
-        K = len(offsets) - 1
+        offsets_a = _host_array(offsets, np.int32, "offsets", ndim=1)
+        K = offsets_a.shape[0] - 1
+        if K < 0:
+            raise ValueError("offsets must hold K + 1 entries")
+        changes_a = _host_array(changes, np.int32, "changes", ndim=2)
+        n = int(offsets_a[K])
+        if changes_a.shape[1] != 2 or changes_a.shape[0] < n:
+            raise ValueError(f"changes must have shape (offsets[K], 2) = ({n}, 2), got {changes_a.shape}")
+        cost_a = _host_array(cost, np.float64, "cost", ndim=1, writable=True)
+        status_a = _host_array(status, np.int32, "status", ndim=1, writable=True)
+        if cost_a.shape[0] < K or status_a.shape[0] < K:
+            raise ValueError(f"cost / status must hold K = {K} entries")
         t = ctypes.c_int64(-1)
-        st = N.lib().fo_score_delta_submit(self.h, N.ptr(offsets), N.ptr(changes), K, precision, int(bool(clear_memo)),
-                                           N.ptr(cost), N.ptr(status), ctypes.byref(t))
+        st = N.lib().fo_score_delta_submit(self.h, N.ptr(offsets_a), N.ptr(changes_a), K, precision,
+                                           int(bool(clear_memo)), N.ptr(cost_a), N.ptr(status_a), ctypes.byref(t))
         _raise(st, "fo_score_delta_submit", N.last_error())
+        # the device copies read / write these until score_wait: keep them alive
+        self._inflight[t.value] = (offsets, changes, cost, status, offsets_a, changes_a, cost_a, status_a)
         return t.value
 
     def score_wait(self, ticket):
-        _raise(N.lib().fo_score_wait(self.h, int(ticket)), "fo_score_wait", N.last_error())
+        try:
+            _raise(N.lib().fo_score_wait(self.h, int(ticket)), "fo_score_wait", N.last_error())
+        finally:
+            self._inflight.pop(int(ticket), None)
 
     def score_delta_device(self, offsets, changes, cost, status, precision=N.FO_PREC_FP32, stream=None):
         """Asynchronous scoring of device-resident sparse candidates (torch tensors)."""

@@ -28,10 +28,12 @@ def shard_range(total: int, rank: int, world: int):
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def global_best(cost, ids, group=None):
+def global_best(cost, ids, group=None, active=None):
     """Argmin over every rank's (cost, id) pairs; returns (cost, id) as Python
     numbers, identical on all ranks.  ``cost``/``ids`` are 1-D tensors on the
-    rank's device (float64 / any numeric id)."""
+    rank's device (float64 / any numeric id).  With ``active`` (this rank's
+    count of live seeds) the same single all-gather also carries the counts,
+    and (cost, id, total active) is returned."""
     import torch
 
     dist = _dist()
@@ -40,22 +42,31 @@ def global_best(cost, ids, group=None):
     else:
         j = torch.argmin(cost)  # first minimum -> lowest local id among ties
         pair = torch.stack([cost[j].to(torch.float64), ids[j].to(torch.float64)])
+    if active is not None:
+        pair = torch.cat([pair, torch.tensor([float(active)], dtype=torch.float64, device=cost.device)])
     if not (dist.is_available() and dist.is_initialized()):
-        return float(pair[0]), float(pair[1])
+        out = (float(pair[0]), float(pair[1]))
+        return out + (int(active),) if active is not None else out
     world = dist.get_world_size(group)
-    out = [torch.empty_like(pair) for _ in range(world)]
-    dist.all_gather(out, pair, group=group)
-    allp = torch.stack(out).cpu().numpy()
+    gathered = torch.empty(world * pair.numel(), dtype=torch.float64, device=pair.device)
+    dist.all_gather_into_tensor(gathered, pair, group=group)
+    allp = gathered.view(world, -1).cpu().numpy()
     order = np.lexsort((allp[:, 1], allp[:, 0]))
-    c, i = allp[order[0]]
+    c, i = allp[order[0], 0], allp[order[0], 1]
+    if active is not None:
+        return float(c), float(i), int(round(allp[:, 2].sum()))
     return float(c), float(i)
 
 
 class ShardedSearch:
     """R lock-stepped Alg. 1 seeds sharded across ranks.  Each rank advances its
     seeds; the global (best cost, seed) pair is exchanged over the process
-    group at the end of the run, or every M rounds (run(exchange_every=M)), or
-    every round when driven through round()."""
+    group every round (run() default, or round()), every M rounds
+    (run(exchange_every=M)), or once at the end (run(exchange_every=None)).
+
+    Lock-stepped seeds are independent searches, so the wall time of a run is
+    bounded by its longest seed at any GPU count: sharding adds seeds per
+    second, not speed to one seed."""
 
     def __init__(self, g0, cfg, cp, seeds: Sequence[int], rank: int, world: int, precision=None, n_threads=0):
         from .search import LockstepSearch
@@ -67,24 +78,33 @@ class ShardedSearch:
         self.best_history = []
 
     def round(self, device) -> int:
+        """One lock-stepped round on this rank's seeds, then the per-round
+        exchange: one all-gather of (best cost, seed id, active seeds) per
+        rank.  Returns the active-seed count over all ranks."""
+        active = self.s.round() if self.s is not None else 0
+        c, i, total = self._exchange(device, active)
+        self.best_history.append((c, i))
+        return total
+
+    def _exchange(self, device, active):
         import torch
 
-        dist = _dist()
-        active = self.s.round() if self.s is not None else 0
         best = self.s.best if self.s is not None else np.zeros(0)
         cost = torch.as_tensor(best, dtype=torch.float64, device=device)
         ids = torch.arange(self.seed_offset, self.seed_offset + len(best), dtype=torch.float64, device=device)
-        self.best_history.append(global_best(cost, ids))
-        a = torch.tensor([active], dtype=torch.int64, device=device)
-        if dist.is_available() and dist.is_initialized():
-            dist.all_reduce(a)
-        return int(a.item())
+        return global_best(cost, ids, active=active)
 
-    def run(self, device, max_rounds: Optional[int] = None, exchange_every: Optional[int] = None):
-        """Advance every local seed to completion.  Seeds are independent, so by
-        default each rank runs its shard natively (fo_search_run) and the global
-        best is exchanged once at the end; exchange_every=M steps the shard M
-        rounds at a time with an exchange after each block (progress reports)."""
+    def run(self, device, max_rounds: Optional[int] = None, exchange_every: Optional[int] = 1):
+        """Advance every local seed to completion, exchanging the global best
+        (cost, seed) pair every ``exchange_every`` rounds (default 1: every
+        round, as the north star states).  ``exchange_every=None`` runs each
+        shard natively to the end (fo_search_run, with its speculation and
+        host/device pipelining) and exchanges once.
+
+        The stop decision is collective: every rank counts rounds in whole
+        blocks and the blocks' active-seed counts are all-reduced, so all ranks
+        leave after the same number of exchanges (a rank whose seeds finished
+        keeps joining the exchanges with an empty shard)."""
         import torch
 
         dist = _dist()
@@ -105,21 +125,19 @@ class ShardedSearch:
             ids = torch.arange(self.seed_offset, self.seed_offset + len(best), dtype=torch.float64, device=device)
             self.best_history.append(global_best(cost, ids))
             return self.best_history[-1]
+        if exchange_every < 1:
+            raise ValueError("exchange_every must be >= 1")
         rounds = 0
+        local_active = self.s.R if self.s is not None else 0
         while True:
-            active = 0
-            for _ in range(exchange_every):
-                active = self.s.round() if self.s is not None else 0
-                rounds += 1
-                if active == 0 or (max_rounds is not None and rounds >= max_rounds):
+            block = exchange_every if max_rounds is None else min(exchange_every, max_rounds - rounds)
+            for _ in range(block):
+                if local_active == 0:
                     break
-            best = self.s.best if self.s is not None else np.zeros(0)
-            cost = torch.as_tensor(best, dtype=torch.float64, device=device)
-            ids = torch.arange(self.seed_offset, self.seed_offset + len(best), dtype=torch.float64, device=device)
-            self.best_history.append(global_best(cost, ids))
-            a = torch.tensor([active], dtype=torch.int64, device=device)
-            if multi:
-                dist.all_reduce(a)
-            if int(a.item()) == 0 or (max_rounds is not None and rounds >= max_rounds):
+                local_active = self.s.round()
+            rounds += block  # identical on every rank
+            c, i, total = self._exchange(device, local_active)
+            self.best_history.append((c, i))
+            if total == 0 or (max_rounds is not None and rounds >= max_rounds):
                 break
         return self.best_history[-1] if self.best_history else (float("inf"), -1.0)

@@ -25,6 +25,23 @@ class OptimizationMethod(Enum):
 METHOD_INDEX = {OptimizationMethod.NON_DUPLICATE_FUSION: 0, OptimizationMethod.DUPLICATE_FUSION: 1,
                 OptimizationMethod.ALLREDUCE_FUSION: 2}
 ALL_METHODS = tuple(METHOD_INDEX)
+_VALUE_INDEX = {m.value: i for m, i in METHOD_INDEX.items()}
+
+
+def method_index(method) -> int:
+    """Engine slot of a method.  Keyed by the enum's value, so the reference's
+    own ``fuseopt.OptimizationMethod`` members (same values, rewrite.py:28-33
+    of the reference) and plain value strings work as well as this package's."""
+    value = getattr(method, "value", method)
+    try:
+        return _VALUE_INDEX[value]
+    except (KeyError, TypeError):
+        raise KeyError(method) from None
+
+
+def methods_mask(methods) -> int:
+    """Bit mask of a method collection (SearchConfig.methods)."""
+    return sum(1 << method_index(m) for m in set(methods))
 
 
 @dataclass(frozen=True)
@@ -137,13 +154,13 @@ def random_apply(g: HloGraph, method: OptimizationMethod, n: int, rng: random.Ra
     version, internal, gauss = rng.getstate()
     mt = np.array(internal, dtype=np.uint32)
     applied = C.c_int32()
-    st = N.lib().fo_random_apply(dg.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), METHOD_INDEX[method], n, N.ptr(mt),
+    st = N.lib().fo_random_apply(dg.h, N.ptr(ng), N.ptr(rg), N.ptr(bk), method_index(method), n, N.ptr(mt),
                                  C.byref(applied))
     _raise(st, "fo_random_apply", N.last_error())
     rng.setstate((version, tuple(int(x) for x in mt), gauss))
     if not applied.value:
-        return RewriteOutcome(g, False, f"{method.value}: no change")
-    return RewriteOutcome(state_from_arrays(g, ng, rg, bk), True, f"{method.value}: applied")
+        return RewriteOutcome(g, False, f"{getattr(method, 'value', method)}: no change")
+    return RewriteOutcome(state_from_arrays(g, ng, rg, bk), True, f"{getattr(method, 'value', method)}: applied")
 
 
 def expand_all(g: HloGraph, ng, rg, bk):
@@ -167,5 +184,5 @@ def make_candidates(g: HloGraph, seeds, beta: int = 10, methods=ALL_METHODS, bas
     """Random batch: candidate k = Random(seeds[k]) then accumulating
     random_apply for each method with n = randint(0, beta).
     Returns (ngid[K,V], rgid[K,V], bkt[K,A], gid_bound) with engine ids."""
-    mask = sum(1 << METHOD_INDEX[m] for m in methods)
+    mask = methods_mask(methods)
     return engine_graph(g).make_candidates(seeds, beta, mask, base, n_threads)

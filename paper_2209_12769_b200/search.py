@@ -21,7 +21,7 @@ import numpy as np
 from . import _native as N
 from .errors import InvalidConfig, LimitExceeded, _raise
 from .graph import HloGraph, canonical_hash, state_arrays, state_from_arrays
-from .rewrite import ALL_METHODS, METHOD_INDEX, OptimizationMethod, engine_graph, expand_all
+from .rewrite import ALL_METHODS, OptimizationMethod, engine_graph, expand_all, method_index, methods_mask
 
 METHOD_NAMES = ("nondup", "dup", "ar")
 
@@ -83,7 +83,7 @@ class LockstepSearch:
         self.R = len(seeds)
         c = N.SearchCfg()
         c.alpha, c.beta, c.max_unchanged = cfg.alpha, cfg.beta, cfg.max_unchanged
-        c.methods_mask = sum(1 << METHOD_INDEX[m] for m in cfg.methods)
+        c.methods_mask = methods_mask(cfg.methods)
         c.precision = N.FO_PREC_FP64 if precision is None else precision
         c.n_threads = n_threads
         ng, rg, bk, _, _, _ = state_arrays(g0)
@@ -121,7 +121,9 @@ class LockstepSearch:
             st = N.lib().fo_search_run(self.h, int(max_rounds or 0), C.byref(a))
             _raise(st, "fo_search_run", N.last_error())
             self.active = a.value
-            self.rounds += 1
+            n = C.c_int64()
+            N.lib().fo_search_rounds(self.h, C.byref(n))
+            self.rounds = int(n.value)
             return [self.result(r) for r in range(self.R)] if results else None
         t0 = time.monotonic() if started is None else started
         st = N.lib().fo_search_start(self.h, N.ptr(self.best))  # eval_cost(g0) precedes the budget check
@@ -207,7 +209,8 @@ def _host_driven_search(g0: HloGraph, cfg: SearchConfig, cp) -> SearchResult:
     queue = [(best_cost, 0, h0, g0)]
     seq, enqueued, unchanged, steps = 1, 0, 0, 0
     trace = []
-    methods = [m for m in ALL_METHODS if m in cfg.methods]
+    chosen = {method_index(m) for m in cfg.methods}
+    methods = [m for m in ALL_METHODS if method_index(m) in chosen]
     while queue and unchanged < cfg.max_unchanged:
         if cfg.time_budget_s is not None and time.monotonic() - t0 > cfg.time_budget_s:
             break

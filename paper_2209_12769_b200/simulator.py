@@ -60,6 +60,8 @@ def _duration(cp, g, kind, ident) -> float:
     value = float(value)
     if value < 0:
         raise ValueError(f"negative duration {value} for {kind} {ident}")
+    if value != value:  # NaN: no schedule order exists (every comparison is false)
+        raise ValueError(f"NaN duration for {kind} {ident}")
     return value
 
 

@@ -1,7 +1,9 @@
 """The hardware-oracle cost providers (workloads.py:53-74, :276-304 of the
 reference) on the device, and loading of the committed synthetic workload
-fixtures (tests/golden/workloads, generated by the reference's own
-gen_workload / make_profile / train, see tests/golden/make_golden.py)."""
+inputs (workloads/ at the repository root: graphs, profiles, comm params and
+random-init estimator models made by the reference's own gen_workload /
+make_profile / train, see tests/golden/make_golden.py).  They are inputs, not
+expected outputs: the expected outputs live under tests/golden."""
 
 from __future__ import annotations
 
@@ -15,7 +17,7 @@ from .estimator import DeviceCostProviders, load_model, load_profile
 from .graph import load_graph
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-FIXTURES = os.path.join(ROOT, "tests", "golden", "workloads")
+FIXTURES = os.path.join(ROOT, "workloads")
 
 # BASELINE.json configs -> fixture names
 CONFIGS = {

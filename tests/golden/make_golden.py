@@ -62,7 +62,7 @@ from fuseopt.estimator import analytic_model, save_model, save_profile  # noqa: 
 from fuseopt.graph import DataEdge, OpNode, graph_to_doc  # noqa: E402
 
 OUT = HERE
-WL = os.path.join(OUT, "workloads")
+WL = os.path.join(os.path.dirname(os.path.dirname(HERE)), "workloads")  # inputs: <repo>/workloads
 
 # name -> (family, V, A, comm C, comm D, model source)
 CONFIGS = {
@@ -277,7 +277,7 @@ def _case(name, g, profile, comm, mp, lin, n_cand, n_timeline):
 
 CASE_COUNTS = {
     "chain24": (64, 8), "residual40": (64, 8), "attention36": (64, 8), "recurrent30": (64, 8),
-    "vgg16": (64, 4), "resnet50": (48, 4), "bert": (48, 4), "gpt2m": (6, 1), "synth50k": (1, 0),
+    "vgg16": (64, 4), "resnet50": (48, 4), "bert": (48, 4), "gpt2m": (48, 1), "synth50k": (16, 0),
 }
 
 
@@ -306,13 +306,14 @@ SEARCHES = [
     ("recurrent30", "mp", dict(alpha=1.2, beta=10, seed=7, max_unchanged=80)),
     ("vgg16", "mp", dict()),  # reference defaults (BASELINE config 0)
     ("bert", "mp", dict(seed=0, max_unchanged=60)),
+    ("bert", "mp", dict(), "default"),  # reference defaults (BASELINE config 2, one seed)
 ]
 
 
 def section_search(only=None):
     os.makedirs(os.path.join(OUT, "search"), exist_ok=True)
-    for wl, prov, kw in SEARCHES:
-        tag = f"{wl}.{prov}.s{kw.get('seed', 0)}"
+    for wl, prov, kw, *suffix in SEARCHES:
+        tag = f"{wl}.{prov}.s{kw.get('seed', 0)}" + "".join("." + x for x in suffix)
         if only and tag not in only and wl not in only:
             continue
         g, profile, comm, mp, lin = load_workload(wl)
@@ -451,8 +452,6 @@ def section_acceptance(names=None):
     for i in range(1000):
         spec = WorkloadSpec(family=FAMILIES[i % 4], op_count=rng.randrange(10, 201), tensor_count=rng.randrange(0, 31),
                             seed=i)
-        if i % 5:  # every fifth workload of the criterion-1 sweep (same generator stream)
-            continue
         g = gen_workload(spec, hw)
         total = sum(cp.op_cost(g, gr) for gr in g.groups) + sum(cp.comm_cost(g, b) for b in g.buckets)
         c1.append({"i": i, "graph": graph_to_doc(g), "cost": cost(g, cp), "fo_bound": fo_bound(g, cp),

@@ -158,6 +158,30 @@ def test_host_only_handle_refuses_device_work():
         dg.score_wait(0)
 
 
+def test_score_delta_submit_validates_host_buffers():
+    """The pipelined submission writes into the caller's buffers after it
+    returns, so it refuses anything it could not write safely: wrong dtypes,
+    short or non-contiguous buffers, a changes array that does not cover
+    offsets[K] (before any device work, so this runs on a host-only handle)."""
+    g = P.load_workload("chain24")[0]
+    dg = engine_graph(g)
+    off = np.array([0, 1, 2], np.int32)
+    chg = np.zeros((2, 2), np.int32)
+    cost, st = np.zeros(2), np.zeros(2, np.int32)
+    with pytest.raises(TypeError):
+        dg.score_delta_submit(off, chg, cost.astype(np.float32), st)
+    with pytest.raises(TypeError):
+        dg.score_delta_submit(off, chg, cost, st.astype(np.int64))
+    with pytest.raises(ValueError):
+        dg.score_delta_submit(off, chg, cost, st[:1])
+    with pytest.raises(ValueError):
+        dg.score_delta_submit(off, chg, np.zeros(4)[::2], st)
+    with pytest.raises(ValueError):
+        dg.score_delta_submit(off, chg[:1], cost, st)
+    with pytest.raises(TypeError):
+        dg.score_delta_submit(off.astype(np.int64), chg, cost, st)
+
+
 @pytest.mark.parametrize("name", SMALL + ["gpt2m"])
 def test_incremental_engine_matches_full_rebuild(name, monkeypatch):
     """The incremental engine (Inc) draws, accepts and labels exactly like the

@@ -61,3 +61,80 @@ def test_shard_range_covers():
             spans = [shard_range(total, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == total
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+class _FakeLockstep:
+    """Stand-in for LockstepSearch (host logic only): seed r of the shard
+    stays active for lengths[r] rounds; its best cost falls each round."""
+
+    def __init__(self, g0, cfg, cp, seeds, precision=None, n_threads=0):
+        import numpy as np
+
+        self.R = len(seeds)
+        self.left = [3 + 5 * (int(s) % 4) for s in seeds]
+        self.best = np.array([100.0 + int(s) for s in seeds])
+        self.rounds = 0
+
+    def round(self):
+        self.rounds += 1
+        for r in range(self.R):
+            if self.left[r] > 0:
+                self.left[r] -= 1
+                self.best[r] -= 1.0
+        return sum(1 for x in self.left if x > 0)
+
+
+def _sharded_worker(rank, world, port, q, seeds, exchange_every, max_rounds, use_round):
+    import paper_2209_12769_b200.search as S
+    from paper_2209_12769_b200.parallel import ShardedSearch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        S.LockstepSearch = _FakeLockstep
+        sh = ShardedSearch(None, None, None, seeds, rank, world)
+        if use_round:
+            n = 0
+            while sh.round("cpu") > 0:
+                n += 1
+            res = sh.best_history[-1]
+        else:
+            res = sh.run("cpu", max_rounds=max_rounds, exchange_every=exchange_every)
+        q.put((rank, res, len(sh.best_history), sh.s.rounds if sh.s is not None else 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seeds,exchange_every,max_rounds,use_round", [
+    (list(range(5)), 1, None, False),      # per-round exchange (the default)
+    (list(range(5)), 3, None, False),      # uneven shards: 3 + 2 seeds of different lengths
+    (list(range(5)), 3, 10, False),        # max_rounds cuts a block
+    ([0], 2, None, False),                 # rank 1 has no seeds at all
+    (list(range(4)), None, None, True),    # driven through round()
+])
+def test_sharded_search_exchange_gloo_world2(seeds, exchange_every, max_rounds, use_round):
+    """ShardedSearch's exchange schedule on 2 ranks: both ranks leave after the
+    same number of exchanges (no rank waits in a collective the other never
+    joins) and agree on the global best (cost, seed)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q, seeds, exchange_every, max_rounds, use_round))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[0][1] == out[1][1]
+    assert out[0][2] == out[1][2]  # same number of exchanges on both ranks
+    # the single-process answer: every seed run to its length (or max_rounds)
+    ref = _FakeLockstep(None, None, None, seeds)
+    n = 0
+    while any(x > 0 for x in ref.left) and (max_rounds is None or n < max_rounds):
+        ref.round()
+        n += 1
+    j = min(range(len(seeds)), key=lambda r: (ref.best[r], r))
+    assert out[0][1] == (float(ref.best[j]), float(j))
