@@ -321,6 +321,10 @@ int64_t fo_kernel_launches(void);
  * after K1 contraction (phase 1) or K2 estimation (phase 2) with cost 0 /
  * status OK; 0 restores full scoring. */
 int fo_set_phase_stop(fo_graph *g, int32_t phase);
+/* Introspection: the launch geometry a K-candidate batch takes (before the
+ * workspace cap): out4 = {block-per-candidate (1) or warp-per-candidate (0),
+ * grid, resident blocks per SM, shared-memory arena bytes per candidate}. */
+int fo_score_geometry(fo_graph *g, int32_t K, int32_t precision, int32_t *out4);
 
 #ifdef __cplusplus
 }

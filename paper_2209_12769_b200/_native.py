@@ -92,6 +92,7 @@ SIGNATURES = [
     ("fo_search_result", C.c_int, [vp, C.c_int32, P(C.c_double), vp, vp, vp, vp, P(TraceRec), C.c_int64]),
     ("fo_search_timing", C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int64)]),
     ("fo_search_rounds", C.c_int, [vp, P(C.c_int64)]),
+    ("fo_score_geometry", C.c_int, [vp, C.c_int32, C.c_int32, vp]),
     ("fo_search_destroy", C.c_int, [vp]),
     ("fo_last_error", C.c_char_p, []),
     ("fo_kernel_launches", C.c_int64, []),

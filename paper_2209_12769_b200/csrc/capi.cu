@@ -131,6 +131,18 @@ extern "C" {
 const char *fo_last_error(void) { return fo::g_last_error.c_str(); }
 int64_t fo_kernel_launches(void) { return fo::g_launches.load(); }
 
+int fo_score_geometry(fo_graph *g, int32_t K, int32_t precision, int32_t *out4) {
+    if (!g || !out4 || K <= 0) return fail(FO_INVALID_ARG, "bad arguments");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    CUDA_TRY(cudaSetDevice(g->device));
+    const ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
+    out4[0] = geo.team ? 1 : 0;
+    out4[1] = geo.grid;
+    out4[2] = geo.blocks_per_sm;
+    out4[3] = geo.sm_bytes;
+    return FO_OK;
+}
+
 int fo_set_phase_stop(fo_graph *g, int32_t phase) {
     if (!g || phase < 0 || phase > 2) return fail(FO_INVALID_ARG, "phase must be 0, 1 or 2");
     g->dg.phase_stop = phase;

@@ -611,3 +611,119 @@ def test_per_round_driver_equals_native_run():
                              cps["mp"], seeds).run()
     for a, b in zip(native, short):
         assert b.steps <= 1 and b.best_cost_us >= a.best_cost_us
+
+
+def _bench_batch(precision):
+    """bench.py's headline batch, built exactly as bench.py builds it: the
+    unfused parent resident on the device (set_parent()), 4,096 sparse
+    candidates from make_candidates_delta(seeds 0..4095, beta 10)."""
+    g, cps = providers("resnet50", precision)
+    dg = cps["mp"].device_graph(g)
+    dg.set_parent()
+    off, chg = dg.make_candidates_delta(np.arange(4096, dtype=np.uint64), beta=10)
+    return g, dg, off, chg
+
+
+def _score_delta_on_device(dg, off, chg, precision, memo=True):
+    import torch
+
+    N.lib().fo_memo_enable(dg.h, 1 if memo else 0)
+    try:
+        N.lib().fo_memo_clear(dg.h, None)
+        c = torch.empty(len(off) - 1, dtype=torch.float64, device="cuda")
+        s = torch.empty(len(off) - 1, dtype=torch.int32, device="cuda")
+        dg.score_delta_device(torch.from_numpy(off).cuda(), torch.from_numpy(chg).cuda(), c, s, precision)
+        torch.cuda.synchronize()
+        return c.cpu().numpy(), s.cpu().numpy()
+    finally:
+        N.lib().fo_memo_enable(dg.h, 1)
+
+
+@pytest.mark.parametrize("precision", [N.FO_PREC_FP32, N.FO_PREC_FP64])
+def test_benchmarked_path_matches_oracle_and_reference(precision):
+    """The exact path behind bench.py's headline number: fo_score_delta at
+    K = 4,096 (warp-per-candidate geometry), the estimator memo on and
+    emptied once per batch, and the pipelined fo_score_delta_submit /
+    fo_score_wait that the e2e figure times.  All 4,096 costs against the C
+    oracle (fp32 <= 1e-4, fp64 <= 1e-12 relative), the first 48 against the
+    reference's own costs (tests/golden/cases/resnet50), and the geometry
+    asserted so the test cannot silently run the block path."""
+    import torch
+    from oracle.oracle import Oracle, load_workload
+
+    g, dg, off, chg = _bench_batch(precision)
+    geo = np.zeros(4, np.int32)
+    assert N.lib().fo_score_geometry(dg.h, 4096, precision, N.ptr(geo)) == 0
+    assert geo[0] == 0, "K = 4,096 must take the warp-per-candidate geometry"
+    cost, st = _score_delta_on_device(dg, off, chg, precision)
+    assert (st == 0).all()
+    o = Oracle(load_workload("resnet50"), "mp" if precision == N.FO_PREC_FP32 else "mp")
+    sts, ref = o.cost_batch(*(np.stack([o.make_candidate(i)[j] for i in range(4096)]) for j in range(3)))
+    assert (sts == 0).all()
+    tol = TOL[("mp", precision)]
+    np.testing.assert_allclose(cost, ref, rtol=tol, atol=0)
+    gold = np.array([c["cost"]["mp"] for c in cases("resnet50")["candidates"]])
+    np.testing.assert_allclose(cost[:len(gold)], gold, rtol=tol, atol=0)
+    # the e2e leg: the same batch through host buffers, two submissions in flight
+    h = [torch.from_numpy(off).pin_memory(), torch.from_numpy(chg).pin_memory()]
+    outs = [(torch.zeros(4096, dtype=torch.float64).pin_memory(), torch.full((4096,), -1, dtype=torch.int32).pin_memory())
+            for _ in range(2)]
+    tickets = [dg.score_delta_submit(h[0], h[1], c, s, precision, clear_memo=True) for c, s in outs]
+    for t in tickets:
+        dg.score_wait(t)
+    for c, s in outs:
+        assert (s.numpy() == 0).all() and np.array_equal(c.numpy(), cost)
+
+
+@pytest.mark.parametrize("precision", [N.FO_PREC_FP32, N.FO_PREC_FP64])
+def test_estimator_memo_changes_no_cost_on_the_bench_batch(precision):
+    """The memo keys a prediction by a 128-bit member-set hash with no member
+    check on a hit.  On the benchmarked batch (4,096 candidates, ~2,900
+    distinct fused member sets) memo-on and memo-off scoring agree bit for
+    bit -- any collision would show as a differing cost -- and the host
+    restatement of the two hashes finds no colliding pair of distinct sets."""
+    g, dg, off, chg = _bench_batch(precision)
+    on, s1 = _score_delta_on_device(dg, off, chg, precision, memo=True)
+    off_, s2 = _score_delta_on_device(dg, off, chg, precision, memo=False)
+    assert (s1 == 0).all() and (s2 == 0).all()
+    assert np.array_equal(on, off_)
+    sets = _fused_member_sets(dg, off, chg)
+    hashes = {}
+    for m in sets:
+        h = _memo_hash(m)
+        assert hashes.setdefault(h, m) == m, f"memo hash collision: {m} vs {hashes[h]}"
+
+
+def _fused_member_sets(dg, off, chg):
+    V, A = dg.V, dg.A
+    base = np.concatenate([np.arange(V), -np.ones(V), np.arange(A)]).astype(np.int64)
+    out = set()
+    for k in range(len(off) - 1):
+        st = base.copy()
+        c = chg[off[k]:off[k + 1]]
+        st[c[:, 0]] = c[:, 1]
+        mem = {}
+        for v in range(V):
+            mem.setdefault(int(st[v]), []).append(v)
+            if st[V + v] >= 0:
+                mem.setdefault(int(st[V + v]), []).append(v)
+        out |= {tuple(sorted(m)) for m in mem.values() if len(m) > 1}
+    return out
+
+
+_M64 = (1 << 64) - 1
+
+
+def _smix(x):
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def _memo_hash(members):
+    """Host restatement of set_hash (score.cu): two commutative 64-bit sums."""
+    a = sum(_smix(2 * m + 1) for m in members) & _M64
+    b = sum(_smix(((m << 32) ^ 0x5BD1E995) & _M64) for m in members) & _M64
+    n = len(members)
+    return _smix((a + n) & _M64) | 1, _smix(b ^ ((n * 0xFF51AFD7ED558CCD) & _M64))
