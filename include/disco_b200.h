@@ -321,6 +321,13 @@ int64_t fo_kernel_launches(void);
  * after K1 contraction (phase 1) or K2 estimation (phase 2) with cost 0 /
  * status OK; 0 restores full scoring. */
 int fo_set_phase_stop(fo_graph *g, int32_t phase);
+/* Sparse-candidate scoring mode: 1 (default) scores each candidate as a patch
+ * of the resident parent's contracted DAG (incremental kernel, MP estimator
+ * with profile lookups; anything else falls back per candidate), 0 always
+ * runs the general kernel.  Results are identical; for A/B measurement.
+ * 2 is diagnostic: incremental kernel only, candidates it would hand to the
+ * general kernel keep status 101. */
+int fo_set_delta_mode(fo_graph *g, int32_t mode);
 /* Introspection: the launch geometry a K-candidate batch takes (before the
  * workspace cap): out4 = {block-per-candidate (1) or warp-per-candidate (0),
  * grid, resident blocks per SM, shared-memory arena bytes per candidate}. */

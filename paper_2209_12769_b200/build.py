@@ -19,7 +19,8 @@ NVCC_FLAGS = [
     "-fmad=false",  # schedule arithmetic must stay plain IEEE add/mul (bit-exact vs the reference)
     "-Xcompiler", "-fPIC,-fopenmp,-O3",
 ]
-HEADERS = [os.path.join(CSRC, "fo_internal.h"), os.path.join(os.path.dirname(HERE), "include", "disco_b200.h")]
+HEADERS = [os.path.join(CSRC, "fo_internal.h"), os.path.join(CSRC, "score_inc.cuh"),
+           os.path.join(os.path.dirname(HERE), "include", "disco_b200.h")]
 
 
 def needs_build() -> bool:

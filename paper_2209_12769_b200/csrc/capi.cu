@@ -30,6 +30,7 @@ int fail(int status, const std::string &msg) {
     } while (0)
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+static int ensure_plan(fo_graph *g, int precision);  // incremental delta scoring (below)
 
 int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int nws, int alt) {
     *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, big ? g->V : kMpCapDefault, nws);
@@ -49,7 +50,7 @@ int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int 
 static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                   int precision, double *cost, int32_t *status, const double *ext_dur, TimelineOut tl,
                   double *dur_out, int32_t *bad_out, int32_t *ngroups_out, cudaStream_t stream,
-                  const DeltaIn *delta = nullptr, int alt_ws = 0) {
+                  const DeltaIn *delta = nullptr, int alt_ws = 0, int first_retry = 0) {
     ScoreGeo geo = score_geometry(g->dg, K, g->num_sms, precision);
     const int nws = score_team_warps(geo);
     WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, kMpCapDefault, nws);
@@ -64,7 +65,7 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
     if (st) return st;
     cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, alt_ws ? g->d_ws_alt : g->d_ws, L, geo,
                                  cost, status, ext_dur, tl,
-                                 dur_out, bad_out, ngroups_out, stream, 0, delta);
+                                 dur_out, bad_out, ngroups_out, stream, first_retry, delta);
     g_launches++;
     if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("score kernel launch: ") + cudaGetErrorString(e));
     if (g->V > kMpCapDefault) {
@@ -118,6 +119,34 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
     d.base = g->d_parent;
     d.off = off;
     d.chg = chg;
+    const int pi = precision == FO_PREC_FP64 ? 1 : 0;
+    const bool inc = g->delta_mode && g->plan_ok[pi] && g->plan_pv[pi] == g->parent_ver && g->plan_mv[pi] == g->model_ver;
+    if (inc) {
+        // incremental kernel; candidates it hands back (kRetryGeneral) take the general kernel
+        const IncPlan &p = g->plan[pi];
+        IncLayout L = inc_layout(g->V, g->E, g->A, p.VB, p.P, 2 * (p.NN + 2) <= 6144);
+        int bps = score_inc_blocks_per_sm(L, precision);
+        if (bps <= 0) {
+            L = inc_layout(g->V, g->E, g->A, p.VB, p.P, false);
+            bps = score_inc_blocks_per_sm(L, precision);
+        }
+        const int warps = score_warps_per_block();
+        const int grid = std::max(1, std::min(g->num_sms * std::max(bps, 1), (K + warps - 1) / warps));
+        const size_t need = (size_t)L.total * grid * warps;
+        if (need > g->ws_inc_bytes) {
+            if (g->d_ws_inc) CUDA_TRY(cudaFree(g->d_ws_inc));
+            g->d_ws_inc = nullptr;
+            g->ws_inc_bytes = 0;
+            CUDA_TRY(cudaMalloc(&g->d_ws_inc, need));
+            g->ws_inc_bytes = need;
+        }
+        cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid, cost, status, stream);
+        g_launches++;
+        if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("incremental score launch: ") + cudaGetErrorString(e));
+        if (g->delta_mode == 2) return FO_OK;  // diagnostic: hand-backs stay visible as status 101
+        return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
+                      nullptr, nullptr, stream, &d, 0, 2);
+    }
     return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
                   nullptr, nullptr, stream, &d);
 }
@@ -140,6 +169,12 @@ int fo_score_geometry(fo_graph *g, int32_t K, int32_t precision, int32_t *out4) 
     out4[1] = geo.grid;
     out4[2] = geo.blocks_per_sm;
     out4[3] = geo.sm_bytes;
+    return FO_OK;
+}
+
+int fo_set_delta_mode(fo_graph *g, int32_t mode) {
+    if (!g || mode < 0 || mode > 2) return fail(FO_INVALID_ARG, "mode must be 0, 1 or 2");
+    g->delta_mode = mode;
     return FO_OK;
 }
 
@@ -264,6 +299,9 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_keys) cudaFree(g->d_keys);
     if (g->d_io) cudaFree(g->d_io);
     if (g->d_parent) cudaFree(g->d_parent);
+    for (void *pl : g->d_plan)
+        if (pl) cudaFree(pl);
+    if (g->d_ws_inc) cudaFree(g->d_ws_inc);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     for (auto &sl : g->aslot) {
         if (sl.done) cudaEventSynchronize(sl.done);
@@ -282,6 +320,7 @@ int fo_graph_destroy(fo_graph *g) {
 int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
     if (!g || !m) return fail(FO_INVALID_ARG, "null argument");
     std::lock_guard<std::mutex> lk(g->mu);
+    g->model_ver++;  // invalidates the incremental plans
     DGraph &dg = g->dg;
     dg.provider = m->provider;
     dg.variant = m->variant;
@@ -590,6 +629,11 @@ int fo_score_host_i16(fo_graph *g, const int16_t *ngid, const int16_t *rgid, con
 int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
                    double *cost_out, int32_t *status_out, void *stream) {
     if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    std::lock_guard<std::mutex> lk(g->mu);
+    CUDA_TRY(cudaSetDevice(g->device));
+    int st = ensure_plan(g, precision);
+    if (st) return st;
     return score_delta_device(g, offsets, changes, K, precision, cost_out, status_out, (cudaStream_t)stream);
 }
 
@@ -611,9 +655,11 @@ int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *chan
     if (K <= 0) return FO_OK;
     if (!offsets_ok(offsets, K)) return fail(FO_INVALID_ARG, "bad offsets (offsets[0] != 0 or decreasing)");
     CUDA_TRY(cudaSetDevice(g->device));
+    int st = ensure_plan(g, precision);  // before staging: building it uses the same staging buffer
+    if (st) return st;
     const size_t nc = (size_t)offsets[K];
     size_t o_c = al256(4 * ((size_t)K + 1)), o_cost = o_c + al256(8 * nc + 8), o_s = o_cost + al256((size_t)K * 8);
-    int st = ensure_io(g, o_s + al256((size_t)K * 4));
+    st = ensure_io(g, o_s + al256((size_t)K * 4));
     if (st) return st;
     char *b = (char *)g->d_io;
     cudaStream_t s = g->stream;
@@ -640,6 +686,10 @@ int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *ch
     std::lock_guard<std::mutex> lk(g->mu);
     if (K < 0 || !offsets_ok(offsets, K)) return fail(FO_INVALID_ARG, "bad offsets (offsets[0] != 0 or decreasing)");
     CUDA_TRY(cudaSetDevice(g->device));
+    {
+        const int pst = ensure_plan(g, precision);
+        if (pst) return pst;
+    }
     if (!g->hstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->hstream, cudaStreamNonBlocking));
     if (!g->dstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->dstream, cudaStreamNonBlocking));
     const int64_t t = g->next_ticket;
@@ -747,6 +797,187 @@ static int single(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
     CUDA_TRY(cudaStreamSynchronize(s));
     for (int i = 0; i < 16; i++) offs[i] = o[i];
     return FO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Parent plan of the incremental delta path (score_inc.cuh), per precision:
+// the parent's contracted schedule DAG in gid space -- the dependency slots
+// of graph.py:215-261 as a successor CSR with each slot's position, node
+// records (duration, tie-break rank, existence), group / bucket members and
+// the level-0 ready runs.  Durations come from the general kernel on the
+// parent itself, so the plan carries exactly the general path's values.
+// Only the MP estimator with profile lookups takes this path (the analytic /
+// linear / hardware-oracle providers depend on group_io of neighbours).
+static int build_plan(fo_graph *g, int precision) {
+    const int pi = precision == FO_PREC_FP64 ? 1 : 0;
+    g->plan_ok[pi] = 0;
+    g->plan_pv[pi] = g->parent_ver;
+    g->plan_mv[pi] = g->model_ver;
+    const DGraph &dg = g->dg;
+    if (!g->model_set || dg.provider != FO_PROVIDER_PROFILE || dg.variant != FO_EST_MESSAGE_PASSING) return FO_OK;
+    const int V = g->V, E = g->E, A = g->A, VB = 2 * V + 2, NN = VB + A;
+    if (NN >= 65535 || (int)g->h_parent.size() != 2 * V + A) return FO_OK;
+    const int32_t *pn = g->h_parent.data(), *pr = pn + V, *pb = pn + 2 * V;
+    std::vector<char> h;
+    size_t o[16];
+    int st = single(g, pn, pr, pb, VB, precision, nullptr, false, true, h, o);
+    if (st) return st;
+    if (*(const int32_t *)(h.data() + o[4]) != FO_OK) return FO_OK;  // the parent itself fails: general path
+    const double *dur_c = (const double *)(h.data() + o[14]);
+    std::vector<int> gcnt(VB, 0), gmin(VB, INT_MAX), bcnt(A, 0), bmin(A, INT_MAX);
+    std::vector<int64_t> bbytes(A, 0);
+    for (int v = 0; v < V; v++) {
+        gcnt[pn[v]]++;
+        gmin[pn[v]] = std::min(gmin[pn[v]], v);
+        if (pr[v] >= 0) { gcnt[pr[v]]++; gmin[pr[v]] = std::min(gmin[pr[v]], v); }
+    }
+    for (int a = 0; a < A; a++) {
+        bcnt[pb[a]]++;
+        bmin[pb[a]] = std::min(bmin[pb[a]], a);
+        bbytes[pb[a]] += g->ar_bytes[a];
+    }
+    std::vector<int32_t> mptr(VB + 1, 0), bptr(A + 1, 0);
+    for (int x = 0; x < VB; x++) mptr[x + 1] = mptr[x] + gcnt[x];
+    for (int b = 0; b < A; b++) bptr[b + 1] = bptr[b] + bcnt[b];
+    std::vector<uint16_t> mem(std::max(mptr[VB], 1)), bmem(std::max(A, 1));
+    {
+        std::vector<int32_t> cur(mptr.begin(), mptr.end() - 1);
+        for (int v = 0; v < V; v++) {  // ascending: member lists come out sorted
+            mem[cur[pn[v]]++] = (uint16_t)v;
+            if (pr[v] >= 0) mem[cur[pr[v]]++] = (uint16_t)v;
+        }
+        std::vector<int32_t> cb(bptr.begin(), bptr.end() - 1);
+        for (int a = 0; a < A; a++) bmem[cb[pb[a]]++] = (uint16_t)a;
+    }
+    std::vector<double> dur(NN, 0.0);
+    std::vector<uint16_t> prank(NN, 0);
+    std::vector<uint8_t> exists(NN, 0);
+    int r = 0;
+    for (int x = 0; x < VB; x++)
+        if (gcnt[x]) { dur[x] = dur_c[r++]; exists[x] = 1; }
+    const int G = r;
+    for (int b = 0; b < A; b++)
+        if (bcnt[b]) { dur[VB + b] = dur_c[r++]; exists[VB + b] = 1; }
+    (void)G;
+    for (int x = 0; x < VB; x++) {
+        if (!gcnt[x]) continue;
+        const int t = gmin[x], other = pn[t] == x ? pr[t] : pn[t];
+        prank[x] = (uint16_t)(2 * t + ((other >= 0 && gmin[other] == t && other < x) ? 1 : 0));  // simulator.py:63
+    }
+    for (int b = 0; b < A; b++)
+        if (bcnt[b]) prank[VB + b] = (uint16_t)bmin[b];
+    // dependency slots (graph.py:215-261), each recording its CSR position
+    auto exp_of = [&](int v) { return pr[v] >= 0 ? pr[v] : pn[v]; };
+    std::vector<int32_t> pos_e(2 * (size_t)E + 1, -1), agg_off(E + 1, 0), pos_ar(A + 1, -1);
+    for (int e = 0; e < E; e++) {
+        const int s = g->e_src[e];
+        agg_off[e + 1] = agg_off[e] + (g->agg[e] ? 2 * (g->arp_ptr[s + 1] - g->arp_ptr[s]) : 0);
+    }
+    std::vector<int32_t> pos_agg(agg_off[E] + 1, -1);
+    std::vector<int32_t> ssrc, stgt;
+    std::vector<int32_t *> spos;
+    auto slot = [&](int src, int tgt, int32_t *pos) { ssrc.push_back(src); stgt.push_back(tgt); spos.push_back(pos); };
+    for (int e = 0; e < E; e++) {
+        const int s = g->e_src[e], d = g->e_dst[e];
+        for (int k = 0; k < 2; k++) {
+            const int gid = k ? pr[d] : pn[d];
+            if (gid < 0) continue;
+            if (!g->agg[e]) {
+                if (pn[s] != gid && pr[s] != gid) slot(exp_of(s), gid, &pos_e[2 * e + k]);
+            } else {
+                for (int q = g->arp_ptr[s], j = 0; q < g->arp_ptr[s + 1]; q++, j++)
+                    slot(VB + pb[g->arp[q]], gid, &pos_agg[agg_off[e] + 2 * j + k]);
+            }
+        }
+    }
+    for (int a = 0; a < A; a++) slot(exp_of(g->ar_prod[a]), VB + pb[a], &pos_ar[a]);
+    const int P = (int)ssrc.size();
+    if (P > 32767) return FO_OK;  // successor positions are 15-bit in the ready entries
+    std::vector<int32_t> sptr(NN + 1, 0);
+    for (int i = 0; i < P; i++) sptr[ssrc[i] + 1]++;
+    for (int n = 0; n < NN; n++) sptr[n + 1] += sptr[n];
+    std::vector<uint32_t> succ(std::max(P, 1));
+    std::vector<int32_t> indeg(NN, 0);
+    {
+        std::vector<int32_t> cur(sptr.begin(), sptr.end() - 1);
+        for (int i = 0; i < P; i++) {
+            const int q = cur[ssrc[i]]++;
+            *spos[i] = q;
+            succ[q] = ((uint32_t)prank[stgt[i]] << 16) | (uint32_t)stgt[i];
+            indeg[stgt[i]]++;
+        }
+    }
+    std::vector<IncNode> rec(NN);
+    std::vector<uint16_t> indeg16(NN + 2, 0);
+    int n_exist = 0;
+    std::vector<std::pair<int, int>> rdy_g, rdy_b;
+    for (int n = 0; n < NN; n++) {
+        if (indeg[n] > 65535) return FO_OK;
+        rec[n] = IncNode{dur[n], (uint16_t)sptr[n], (uint16_t)sptr[n + 1], prank[n], exists[n], 0};
+        indeg16[n] = (uint16_t)indeg[n];
+        n_exist += exists[n];
+        if (exists[n] && indeg[n] == 0) (n < VB ? rdy_g : rdy_b).push_back({prank[n], n});
+    }
+    std::sort(rdy_g.begin(), rdy_g.end());
+    std::sort(rdy_b.begin(), rdy_b.end());
+    std::vector<uint16_t> ready;
+    for (auto &x : rdy_g) ready.push_back((uint16_t)x.second);
+    for (auto &x : rdy_b) ready.push_back((uint16_t)x.second);
+    if (ready.empty()) ready.push_back(0);
+    std::vector<uint16_t> gcnt16(VB), gmin16(VB), bcnt16(std::max(A, 1)), bmin16(std::max(A, 1));
+    for (int x = 0; x < VB; x++) { gcnt16[x] = (uint16_t)gcnt[x]; gmin16[x] = gcnt[x] ? (uint16_t)gmin[x] : 0; }
+    for (int b = 0; b < A; b++) { bcnt16[b] = (uint16_t)bcnt[b]; bmin16[b] = bcnt[b] ? (uint16_t)bmin[b] : 0; }
+    // one device allocation
+    struct Seg { const void *src; size_t bytes; size_t off; };
+    Seg segs[] = {
+        {rec.data(), sizeof(IncNode) * NN, 0}, {indeg16.data(), 2 * indeg16.size(), 0},
+        {succ.data(), 4 * succ.size(), 0}, {gcnt16.data(), 2 * gcnt16.size(), 0}, {gmin16.data(), 2 * gmin16.size(), 0},
+        {mptr.data(), 4 * mptr.size(), 0}, {mem.data(), 2 * mem.size(), 0}, {bcnt16.data(), 2 * bcnt16.size(), 0},
+        {bmin16.data(), 2 * bmin16.size(), 0}, {bbytes.data(), 8 * bbytes.size(), 0}, {bptr.data(), 4 * bptr.size(), 0},
+        {bmem.data(), 2 * bmem.size(), 0}, {pos_e.data(), 4 * pos_e.size(), 0}, {agg_off.data(), 4 * agg_off.size(), 0},
+        {pos_agg.data(), 4 * pos_agg.size(), 0}, {pos_ar.data(), 4 * pos_ar.size(), 0}, {ready.data(), 2 * ready.size(), 0},
+    };
+    size_t total = 0;
+    for (auto &sg : segs) { sg.off = total; total += al256(sg.bytes + 8); }
+    if (g->d_plan[pi]) { CUDA_TRY(cudaFree(g->d_plan[pi])); g->d_plan[pi] = nullptr; }
+    CUDA_TRY(cudaMalloc(&g->d_plan[pi], total));
+    char *b = (char *)g->d_plan[pi];
+    for (auto &sg : segs)
+        if (sg.bytes) CUDA_TRY(cudaMemcpy(b + sg.off, sg.src, sg.bytes, cudaMemcpyHostToDevice));
+    IncPlan &p = g->plan[pi];
+    p.V = V; p.E = E; p.A = A; p.VB = VB; p.NN = NN; p.P = P; p.n_exist = n_exist;
+    p.n_ready_g = (int)rdy_g.size();
+    p.n_ready_b = (int)rdy_b.size();
+    p.rec = (const IncNode *)(b + segs[0].off);
+    p.indeg = (const uint16_t *)(b + segs[1].off);
+    p.succ = (const uint32_t *)(b + segs[2].off);
+    p.gcnt = (const uint16_t *)(b + segs[3].off);
+    p.gmin = (const uint16_t *)(b + segs[4].off);
+    p.mptr = (const int32_t *)(b + segs[5].off);
+    p.mem = (const uint16_t *)(b + segs[6].off);
+    p.bcnt = (const uint16_t *)(b + segs[7].off);
+    p.bmin = (const uint16_t *)(b + segs[8].off);
+    p.bbytes = (const int64_t *)(b + segs[9].off);
+    p.bptr = (const int32_t *)(b + segs[10].off);
+    p.bmem = (const uint16_t *)(b + segs[11].off);
+    p.pos_e = (const int32_t *)(b + segs[12].off);
+    p.agg_off = (const int32_t *)(b + segs[13].off);
+    p.pos_agg = (const int32_t *)(b + segs[14].off);
+    p.pos_ar = (const int32_t *)(b + segs[15].off);
+    p.pnn = g->d_parent;
+    p.prr = g->d_parent + V;
+    p.pbk = g->d_parent + 2 * V;
+    p.ready = (const uint16_t *)(b + segs[16].off);
+    g->plan_ok[pi] = 1;
+    return FO_OK;
+}
+
+// (re)build the plan of this precision when the parent or the cost model changed
+static int ensure_plan(fo_graph *g, int precision) {
+    const int pi = precision == FO_PREC_FP64 ? 1 : 0;
+    if (!g->delta_mode || !g->d_parent) return FO_OK;
+    if (g->plan_pv[pi] == g->parent_ver && g->plan_mv[pi] == g->model_ver) return FO_OK;
+    return build_plan(g, precision);
 }
 
 int fo_simulate(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t gid_bound,

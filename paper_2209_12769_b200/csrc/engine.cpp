@@ -1423,6 +1423,7 @@ int fo_set_parent(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
     std::copy(s.ng.begin(), s.ng.end(), g->h_parent.begin());
     std::copy(s.rg.begin(), s.rg.end(), g->h_parent.begin() + V);
     std::copy(s.bk.begin(), s.bk.end(), g->h_parent.begin() + 2 * V);
+    g->parent_ver++;  // invalidates the incremental plans (capi.cu ensure_plan)
     if (g->device < 0) return FO_OK;
     if (cudaSetDevice(g->device) != cudaSuccess) return fail(FO_CUDA_ERROR, "cudaSetDevice");
     if (!g->d_parent && cudaMalloc(&g->d_parent, 4 * g->h_parent.size() + 4) != cudaSuccess)

@@ -141,6 +141,54 @@ struct FeatIn {
 };
 cudaError_t launch_predict_features(const DGraph &g, const FeatIn &in, int precision, double *pred_out,
                                     cudaStream_t stream);
+// ---------------------------------------------------------------------------
+// Incremental scoring of sparse candidates (score_inc.cuh).  A sparse
+// candidate is a handful of (index, value) changes against the resident
+// parent, so its contracted schedule DAG is the parent's with a handful of
+// nodes patched.  The parent's DAG is contracted ONCE per parent ("plan",
+// built on the host by fo_set_parent's first scoring call) in gid space:
+// group node = engine group id [0, VB), bucket node = VB + bucket id.  Per
+// candidate the kernel derives only the changed dependency slots and the
+// nodes they touch; the event loop walks the parent's successor lists (read
+// only, shared by every warp of an SM, so L1-resident) plus a few rebuilt
+// lists, with the candidate's indegrees in shared memory.
+struct IncNode {      // parent node record, 16 B: one load per released node
+    double dur;
+    uint16_t sb, se;  // successor range in IncPlan::succ (bit 15 of sb: rebuilt list, candidates only)
+    uint16_t prank;   // tie-break rank (simulator.py:63-64): 2 * min member + replica bit, or min AR
+    uint8_t exists, pad;
+};
+struct IncPlan {
+    int32_t V, E, A, VB, NN, P, n_exist, n_ready_g, n_ready_b;
+    const IncNode *rec;        // [NN]
+    const uint16_t *indeg;     // [NN + pad]
+    const uint32_t *succ;      // [P] (prank << 16) | target
+    const uint16_t *gcnt, *gmin;                 // [VB]
+    const int32_t *mptr; const uint16_t *mem;    // group members, ascending: [VB + 1], [mptr[VB]]
+    const uint16_t *bcnt, *bmin; const int64_t *bbytes;  // [A]
+    const int32_t *bptr; const uint16_t *bmem;   // bucket members (AR indices): [A + 1], [A]
+    const int32_t *pos_e;      // [2E] parent succ position of non-aggregate slot (e, copy), -1 inactive
+    const int32_t *agg_off;    // [E + 1] first aggregate slot of edge e (2 per AllReduce of its source)
+    const int32_t *pos_agg;    // [agg_off[E]]
+    const int32_t *pos_ar;     // [A] bucket <- export(producer) slot
+    const int32_t *pnn, *prr, *pbk;  // the parent state (engine ids)
+    const uint16_t *ready;     // level-0 ready nodes: lane g [0, n_ready_g), lane b after, each by prank
+};
+struct IncLayout {  // per-warp global scratch (byte offsets) and shared-memory arena
+    int64_t chg, rem, add, dn, work, dirty, mem, pcsr, ring, indeg, gs0, total;
+    int64_t g_msort, g_lidx, g_zl, g_nbptr, g_nb, g_mark, g_H, g_P;
+    int32_t mem_cap, pcsr_cap, mpcap;
+    int32_t s_indeg, s_pbm, s_abm, s_lbm, s_tbm, s_ppre, s_cbm, s_cnt, s_bytes;  // smem offsets (s_indeg < 0: global)
+    int32_t NW, CW;
+};
+constexpr int kIncMaxChg = 64, kIncMaxOps = 256, kIncMaxDirty = 192;
+constexpr int kRetryGeneral = 101;  // internal status: the incremental kernel hands the candidate to score_kernel
+IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg);
+cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
+                             const int32_t *chg, int K, int precision, char *ws, int grid, double *cost_out,
+                             int32_t *status_out, cudaStream_t stream);
+int score_inc_blocks_per_sm(const IncLayout &L, int precision);
+
 cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, int64_t id_offset, double *out,
                               cudaStream_t stream, int pairs = 0);
 
@@ -192,6 +240,16 @@ struct fo_graph {
     } aslot[2];
     cudaStream_t hstream = nullptr, dstream = nullptr;
     int64_t next_ticket = 0;
+    // incremental delta scoring (score_inc.cuh): the parent's plan per
+    // precision, rebuilt when the parent or the cost model changes
+    int parent_ver = 0, model_ver = 0;
+    void *d_plan[2] = {nullptr, nullptr};
+    fo::IncPlan plan[2]{};
+    int plan_pv[2] = {-1, -1}, plan_mv[2] = {-1, -1};
+    int plan_ok[2] = {0, 0};
+    char *d_ws_inc = nullptr;
+    size_t ws_inc_bytes = 0;
+    int delta_mode = 1;  // 1: incremental kernel when the plan allows it; 0: general kernel only
     std::mutex mu;
 };
 

@@ -602,7 +602,7 @@ struct ScoreArgs {
     const void *ngid, *rgid, *bkt;  // int32, or int16 when idx16
     const int32_t *dbase, *doff, *dchg;  // sparse candidates (DeltaIn) when dbase != nullptr
     int idx16;
-    int retry_only;  // second pass: only candidates a first pass flagged kRetryLarge
+    int retry_only;  // 1: second pass over candidates flagged kRetryLarge; 2: first pass over kRetryGeneral ones
     int stop_after;  // measurement hook (fo_set_phase_stop): 1 = after K1, 2 = after K2, 0 = full
     int K, VB;
     int sm_nodes, sm_pairs, sm_bytes;  // per-warp shared-memory simulation arena
@@ -1732,7 +1732,7 @@ __device__ void score_one(const ScoreArgs &a, int k, const Ws &w, int tid, char 
                 }
             }
             tsync<TEAM>();
-            if (TEAM > 32 && a.retry_only) {
+            if (TEAM > 32 && a.retry_only == 1) {
                 // second pass (whole-graph scratch, one copy): groups one at a
                 // time; the very large MP groups use the whole team
                 const GroupScratch gs = group_scratch(w, 0);
@@ -1807,7 +1807,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel(const __grid_cons
     Ws w = ws_at(a.ws + (int64_t)wid * a.L.total, a.L);
     char *sm = a.sm_bytes > 0 ? smem_arena + (threadIdx.x >> 5) * a.sm_bytes : nullptr;
     for (int k = wid; k < a.K; k += nw) {
-        if (a.retry_only && a.status_out[k] != kRetryLarge) continue;
+        if (a.retry_only && a.status_out[k] != (a.retry_only == 1 ? kRetryLarge : kRetryGeneral)) continue;
         score_one<T, 32>(a, k, w, lane, sm, nullptr);
     }
 }
@@ -1822,7 +1822,7 @@ __global__ void __launch_bounds__(kTeam, 4) score_kernel_team(const __grid_const
     Ws w = ws_at(a.ws + (int64_t)blockIdx.x * a.L.total, a.L);
     char *sm = a.sm_bytes > 0 ? smem_arena : nullptr;
     for (int k = blockIdx.x; k < a.K; k += gridDim.x) {
-        if (a.retry_only && a.status_out[k] != kRetryLarge) continue;
+        if (a.retry_only && a.status_out[k] != (a.retry_only == 1 ? kRetryLarge : kRetryGeneral)) continue;
         score_one<T, kTeam>(a, k, w, threadIdx.x, sm, &ts);
         __syncthreads();
     }
@@ -2097,5 +2097,7 @@ cudaError_t launch_score(const DGraph &g, const void *ngid, const void *rgid, co
 
 int score_slots(const ScoreGeo &geo) { return geo.team ? geo.grid : geo.grid * kWarps; }
 int score_team_warps(const ScoreGeo &geo) { return geo.team ? kTeam / 32 : 1; }
+
+#include "score_inc.cuh"
 
 }  // namespace fo

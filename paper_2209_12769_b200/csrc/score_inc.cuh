@@ -1,0 +1,845 @@
+// score_inc.cuh -- incremental scoring of sparse candidates (included by
+// score.cu inside namespace fo; it reuses that file's warp helpers, the MP
+// forward, the estimator memo and the ring-buffer ready runs).
+//
+// A sparse candidate is (index, value) changes over ngid | rgid | bkt against
+// the resident parent.  The reference rebuilds the whole contraction for
+// every candidate (_Index, graph.py:117-274; simulate, simulator.py:61-62);
+// here the parent's contraction exists once (IncPlan, host-built) and a
+// candidate only re-derives what its changes touch:
+//
+//   setup  the dependency SLOTS whose endpoints changed (one slot per
+//          (edge, copy of the consumer) -- graph.py:237-261 -- per
+//          (aggregate edge, AllReduce, copy), and per AllReduce -- :215-223):
+//          each is removed from / added to the parent's DAG; the nodes they
+//          leave or enter and the groups / buckets whose membership changed
+//          become PATCHED nodes (new duration, tie-break rank, existence,
+//          successor list)
+//   K2     durations of the patched groups: profile lookup for singletons,
+//          the MP forward (estimator.py:363-389, memoised) for fused groups,
+//          C * bytes + D for buckets (comm.py:45-49)
+//   K3     the event loop of simulator.py:117-140 over the parent's successor
+//          lists (read only and shared by every warp of the SM, so they stay
+//          in L1), the rebuilt lists of patched nodes, and the candidate's
+//          indegrees in shared memory
+//
+// Anything outside the fast path's bounds (more changes than kIncMaxChg, a
+// ring or scratch overflow, a missing profile entry, an invalid id) ends the
+// candidate with kRetryGeneral and the general kernel scores it instead, so
+// results and error statuses are the general path's by construction.
+
+struct IncDirty {  // a patched node of one candidate (sorted by node id)
+    double dur;
+    uint16_t prank, sb, se;
+    uint8_t exists, fused;
+};
+struct IncWork {  // setup record of a patched node, in discovery order
+    int32_t node, cnt, mn, mb, me, pad;
+    int64_t bytes;
+};
+
+IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
+    IncLayout L{};
+    const int NN = VB + A;
+    int64_t o = 0;
+    auto take = [&](int64_t bytes) { int64_t r = o; o = align8(o + bytes); return r; };
+    L.mem_cap = 2 * V + A + 64;
+    L.pcsr_cap = std::min<int64_t>(P + kIncMaxOps + 64, 32767);
+    L.chg = take(8 * kIncMaxChg);
+    L.rem = take(16 * kIncMaxOps);
+    L.add = take(8 * kIncMaxOps);
+    L.dn = take(4 * kIncMaxDirty);
+    L.work = take(sizeof(IncWork) * kIncMaxDirty);
+    L.dirty = take(sizeof(IncDirty) * (kIncMaxDirty + 1) + 2 * kIncMaxDirty);  // + rank -> slot map
+    L.mem = take(4 * (int64_t)L.mem_cap);
+    L.pcsr = take(4 * (int64_t)L.pcsr_cap);
+    L.ring = take(16 * 2 * kRing);
+    L.indeg = smem_indeg ? -1 : take(2 * (int64_t)(NN + 2));
+    const int64_t cap = std::min(V, kMpCapDefault);
+    L.mpcap = (int)cap;
+    L.gs0 = o;
+    int64_t q = 0;
+    auto sub = [&](int64_t bytes) { int64_t r = q; q = align8(q + bytes); return r; };
+    L.g_msort = sub(4 * (cap + 1));
+    L.g_lidx = sub(4 * (int64_t)V);
+    L.g_zl = sub(4 * (cap + 1));
+    L.g_nbptr = sub(4 * (cap + 1));
+    L.g_nb = sub(4 * (2 * (int64_t)E + 1));
+    L.g_mark = sub(4 * (int64_t)V);
+    L.g_H = sub(8 * cap * kHidden);
+    L.g_P = sub(8 * cap * kHidden);
+    o += q;
+    L.total = align8(o) + 128;
+    // per-warp shared-memory arena
+    L.NW = (NN + 31) / 32;
+    L.CW = (2 * V + A + 31) / 32;
+    int32_t s = 0;
+    auto stake = [&](int32_t bytes) { int32_t r = s; s = (s + bytes + 15) & ~15; return r; };
+    L.s_indeg = smem_indeg ? stake(2 * (NN + 2)) : -1;
+    L.s_pbm = stake(4 * L.NW);
+    L.s_abm = stake(4 * L.NW);
+    L.s_lbm = stake(4 * L.NW);
+    L.s_tbm = stake(4 * L.NW);
+    L.s_ppre = stake(2 * L.NW + 2);
+    L.s_cbm = stake(4 * L.CW);
+    L.s_cnt = stake(4 * 8);
+    L.s_bytes = s;
+    return L;
+}
+
+struct IncArgs {
+    DGraph g;
+    IncPlan p;
+    IncLayout L;
+    const int32_t *doff, *dchg;
+    int K;
+    char *ws;
+    double *cost_out;
+    int32_t *status_out;
+    int stop_after;
+};
+
+// counters in the per-warp shared arena
+enum { kCRem = 0, kCAdd = 1, kCDirty = 2, kCMem = 3, kCPcsr = 4, kCFail = 5, kCExist = 6 };
+
+struct IncCtx {
+    const IncArgs *a;
+    int2 *chg;
+    int4 *rem;
+    int2 *add;
+    int *dn;
+    IncWork *work;
+    IncDirty *dirty;
+    uint16_t *r2s;
+    int *mem;
+    uint32_t *pcsr;
+    Ent16 *ring;
+    uint16_t *indeg;
+    uint32_t *pbm, *abm, *lbm, *tbm, *cbm;
+    uint16_t *ppre;
+    int *cnt;
+    int nchg;
+};
+
+__device__ __forceinline__ bool ibit(const uint32_t *bm, int i) { return (bm[i >> 5] >> (i & 31)) & 1u; }
+
+// candidate value at index i of ngid | rgid | bkt: the parent's unless changed
+__device__ __forceinline__ int icval(const IncCtx &c, int i, int pv) {
+    if (!ibit(c.cbm, i)) return pv;
+    int lo = 0, hi = c.nchg - 1;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (c.chg[m].x < i) lo = m + 1;
+        else hi = m;
+    }
+    return c.chg[lo].y;
+}
+__device__ __forceinline__ int inn(const IncCtx &c, int v) { return icval(c, v, c.a->p.pnn[v]); }
+__device__ __forceinline__ int irr(const IncCtx &c, int v) { return icval(c, c.a->p.V + v, c.a->p.prr[v]); }
+__device__ __forceinline__ int ibk(const IncCtx &c, int a) { return icval(c, 2 * c.a->p.V + a, c.a->p.pbk[a]); }
+__device__ __forceinline__ bool iop_changed(const IncCtx &c, int v) {
+    return ibit(c.cbm, v) || ibit(c.cbm, c.a->p.V + v);
+}
+__device__ __forceinline__ void ifail(const IncCtx &c) { c.cnt[kCFail] = 1; }
+
+__device__ void imark(const IncCtx &c, int n, int flags) {
+    const uint32_t b = 1u << (n & 31);
+    if (flags & 1) atomicOr(&c.abm[n >> 5], b);
+    if (flags & 2) atomicOr(&c.lbm[n >> 5], b);
+    if (atomicOr(&c.pbm[n >> 5], b) & b) return;
+    const int s = atomicAdd(&c.cnt[kCDirty], 1);
+    if (s >= kIncMaxDirty) { ifail(c); return; }
+    c.dn[s] = n;
+}
+
+// one dependency slot before (parent) and after (candidate) the changes
+__device__ void islot(const IncCtx &c, int pos, bool oact, int osrc, int otgt, bool nact, int nsrc, int ntgt) {
+    if (oact && nact && osrc == nsrc && otgt == ntgt) return;
+    if (oact) {
+        const int s = atomicAdd(&c.cnt[kCRem], 1);
+        if (s >= kIncMaxOps || pos < 0) ifail(c);
+        else c.rem[s] = make_int4(pos, osrc, otgt, 0);
+    }
+    if (nact) {
+        const int s = atomicAdd(&c.cnt[kCAdd], 1);
+        if (s >= kIncMaxOps) ifail(c);
+        else c.add[s] = make_int2(nsrc, ntgt);
+    }
+}
+
+// aggregate edge e, j-th AllReduce a of its source: bucket(a) -> every copy of
+// the consumer (graph.py:237-247)
+__device__ void iagg_slots(const IncCtx &c, int e, int j, int a, int pnd, int prd, int cnd, int crd) {
+    const IncPlan &p = c.a->p;
+    const int osrc = p.VB + p.pbk[a], nsrc = p.VB + ibk(c, a);
+    const int base = p.agg_off[e] + 2 * j;
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const int ot = k ? prd : pnd, nt = k ? crd : cnd;
+        islot(c, ot >= 0 ? p.pos_agg[base + k] : -1, ot >= 0, osrc, ot, nt >= 0, nsrc, nt);
+    }
+}
+
+// every slot of edge e (graph.py:249-261 non-aggregate, :237-247 aggregate)
+__device__ void iedge_slots(const IncCtx &c, int e) {
+    const DGraph &g = c.a->g;
+    const IncPlan &p = c.a->p;
+    const int s = g.e_src[e], d = g.e_dst[e];
+    const int pnd = p.pnn[d], prd = p.prr[d], cnd = inn(c, d), crd = irr(c, d);
+    if (!g.e_agg[e]) {
+        const int pns = p.pnn[s], prs = p.prr[s], cns = inn(c, s), crs = irr(c, s);
+        const int osrc = prs >= 0 ? prs : pns, nsrc = crs >= 0 ? crs : cns;  // export group (graph.py:158-159)
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int ot = k ? prd : pnd, nt = k ? crd : cnd;
+            const bool oact = ot >= 0 && pns != ot && prs != ot, nact = nt >= 0 && cns != nt && crs != nt;
+            islot(c, oact ? p.pos_e[2 * e + k] : -1, oact, osrc, ot, nact, nsrc, nt);
+        }
+    } else {
+        for (int q = g.arp_ptr[s], j = 0; q < g.arp_ptr[s + 1]; q++, j++) iagg_slots(c, e, j, g.arp[q], pnd, prd, cnd, crd);
+    }
+}
+
+// bucket(a) <- export(producer(a)) (graph.py:215-223)
+__device__ void iar_slot(const IncCtx &c, int a) {
+    const IncPlan &p = c.a->p;
+    const int pr = c.a->g.ar_prod[a];
+    const int po = p.prr[pr] >= 0 ? p.prr[pr] : p.pnn[pr];
+    const int cr = irr(c, pr), co = cr >= 0 ? cr : inn(c, pr);
+    islot(c, p.pos_ar[a], true, po, p.VB + p.pbk[a], true, co, p.VB + ibk(c, a));
+}
+
+__device__ __forceinline__ int irank(const IncCtx &c, int n) {
+    const uint32_t w = c.pbm[n >> 5];
+    return (int)c.ppre[n >> 5] + __popc(w & ((1u << (n & 31)) - 1u));
+}
+
+// MP prediction of one patched fused group (members ascending), warp-wide:
+// memo, member-local undirected neighbour lists over the candidate's
+// membership (estimator.py:173-177, :348-355), mp_forward
+template <typename T>
+__device__ double inc_group_mp(const IncCtx &c, const GroupScratch &gs, const int *mem, int n, int gid, int lane) {
+    const DGraph &g = c.a->g;
+    MemoEnt *memo = g.memo[sizeof(T) == 8];
+    unsigned long long mh1 = 0, mh2 = 0;
+    if (memo) {
+        set_hash(mem, n, lane, mh1, mh2);
+        double mv = 0.0;
+        bool hit = false;
+        if (lane == 0) hit = memo_get(memo, g.memo_mask, mh1, mh2, &mv);
+        hit = __shfl_sync(FULL, hit, 0);
+        if (hit) return __shfl_sync(FULL, mv, 0);
+    }
+    for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = i;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+        const int v = mem[i];
+        gs.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
+    }
+    __syncwarp();
+    warp_exscan(gs.zl, gs.nbptr, n, lane);
+    for (int i = lane; i < n; i += 32) {
+        const int v = mem[i];
+        const int o = gs.nbptr[i];
+        int cc = 0;
+        for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
+            const int s = g.e_src[g.in_e[q]];
+            if (inn(c, s) != gid && irr(c, s) != gid) continue;
+            const int j = gs.lidx[s];
+            bool dup = false;
+            for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
+            if (!dup) gs.nb[o + cc++] = j;
+        }
+        for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
+            const int d = g.e_dst[g.out_e[q]];
+            if (inn(c, d) != gid && irr(c, d) != gid) continue;
+            const int j = gs.lidx[d];
+            bool dup = false;
+            for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
+            if (!dup) gs.nb[o + cc++] = j;
+        }
+        gs.msort[i] = cc;
+    }
+    __syncwarp();
+    if (lane == 0) {  // compact rows into a dense CSR
+        int o = 0;
+        for (int i = 0; i < n; i++) {
+            const int s0 = gs.nbptr[i], cc = gs.msort[i];
+            for (int t = 0; t < cc; t++) gs.nb[o + t] = gs.nb[s0 + t];
+            gs.nbptr[i] = o;
+            o += cc;
+        }
+        gs.nbptr[n] = o;
+    }
+    __syncwarp();
+    const double pred = mp_forward<T>(g, mem, n, gs.nbptr, gs.nb, (T *)gs.H, (T *)gs.P, lane);
+    if (lane == 0 && memo) memo_put(memo, g.memo_mask, mh1, mh2, pred);
+    return pred;
+}
+
+// The event loop (simulator.py:117-140) of ring_loop over the parent's
+// successor lists and the candidate's patches.  false on ring overflow.
+__device__ __forceinline__ bool inc_ring_loop(const IncCtx &c, int k, int hg, int hb, int N) {
+    const IncPlan &p = c.a->p;
+    const IncNode *__restrict__ rec = p.rec;
+    const uint32_t *__restrict__ psucc = p.succ;
+    const uint32_t *__restrict__ csucc = c.pcsr;
+    uint16_t *__restrict__ indeg = c.indeg;
+    const uint32_t *__restrict__ pbm = c.pbm;
+    const uint16_t *__restrict__ ppre = c.ppre;
+    const IncDirty *__restrict__ dirty = c.dirty;
+    Ent16 *__restrict__ rg = c.ring;
+    Ent16 *__restrict__ rb = c.ring + kRing;
+    const int VB = p.VB;
+    int headg = 0, tailg = hg, headb = 0, tailb = hb;
+    int run0 = 0, run1 = 0;
+    unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
+    double end0 = 0.0, end1 = 0.0, now = 0.0;
+    uint32_t level = 0;
+    uint32_t lastg = hg > 0 ? rg[(hg - 1) & (kRing - 1)].key : 0u;
+    uint32_t lastb = hb > 0 ? rb[(hb - 1) & (kRing - 1)].key : 0u;
+    auto release = [&](unsigned qb, unsigned qe) -> bool {
+        const uint32_t *L = (qb & 0x8000u) ? csucc : psucc;
+        for (unsigned q = qb & 0x7fffu; q < qe; q++) {
+            const uint32_t e = L[q];
+            const unsigned t = e & 0xffffu;
+            const int d = indeg[t] - 1;
+            const IncNode r = rec[t];  // issued with the indegree load
+            const uint32_t w = pbm[t >> 5];
+            indeg[t] = (uint16_t)d;
+            if (d == 0) {
+                Ent16 x;
+                if ((w >> (t & 31)) & 1u) {  // patched node: the candidate's record
+                    const IncDirty &dd = dirty[(int)ppre[t >> 5] + __popc(w & ((1u << (t & 31)) - 1u))];
+                    x.key = level | dd.prank;
+                    x.sb = dd.sb;
+                    x.se = dd.se;
+                    x.dur = dd.dur;
+                } else {
+                    x.key = level | r.prank;
+                    x.sb = r.sb;
+                    x.se = r.se;
+                    x.dur = r.dur;
+                }
+                if (!((int)t < VB ? ring_push_t(rg, headg, tailg, lastg, x) : ring_push_t(rb, headb, tailb, lastb, x)))
+                    return false;
+            }
+        }
+        return true;
+    };
+    auto start = [&]() {
+        if (!run0 && headg < tailg) {
+            const Ent16 x = rg[(headg++) & (kRing - 1)];
+            run0 = 1;
+            end0 = __dadd_rn(now, x.dur);
+            sb0 = x.sb;
+            se0 = x.se;
+        }
+        if (!run1 && headb < tailb) {
+            const Ent16 x = rb[(headb++) & (kRing - 1)];
+            run1 = 1;
+            end1 = __dadd_rn(now, x.dur);
+            sb1 = x.sb;
+            se1 = x.se;
+        }
+    };
+    start();
+    while (run0 || run1) {
+        const bool c0 = run0 && (!run1 || end0 <= end1);
+        const bool c1 = run1 && (!run0 || end1 <= end0);
+        const double t = c0 ? end0 : end1;
+        if (t > now) { now = t; level += 0x10000u; }
+        if (c0) {
+            run0 = 0;
+            if (!release(sb0, se0)) return false;
+        }
+        if (c1) {
+            run1 = 0;
+            if (!release(sb1, se1)) return false;
+        }
+        start();
+    }
+    const int done = headg + headb;
+    c.a->cost_out[k] = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
+    c.a->status_out[k] = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
+    return true;
+}
+
+// insert one ready entry into a level-0 run (kept sorted by key)
+__device__ __forceinline__ bool inc_ring_insert(Ent16 *buf, int &tail, const Ent16 &x) {
+    if (tail >= kRing) return false;
+    int dummy = tail;
+    ring_push(buf, 0, dummy, x);
+    tail = dummy;
+    return true;
+}
+
+template <typename T>
+__device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const GroupScratch &gs, int lane) {
+    IncCtx c = c0;
+    const DGraph &g = a.g;
+    const IncPlan &p = a.p;
+    const IncLayout &L = a.L;
+    const int V = p.V, A = p.A, VB = p.VB, NN = p.NN;
+    auto retry = [&]() {
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = kRetryGeneral; }
+    };
+    // ---- changes: load, validate, sort by index, changed-index bitmap
+    const int cb = a.doff[k], ce = a.doff[k + 1];
+    const int nchg = ce - cb;
+    if (cb < 0 || nchg < 0 || ce > a.doff[a.K] || nchg > kIncMaxChg) { retry(); return; }
+    for (int i = lane; i < L.CW; i += 32) c.cbm[i] = 0;
+    for (int i = lane; i < L.NW; i += 32) { c.pbm[i] = 0; c.abm[i] = 0; c.lbm[i] = 0; c.tbm[i] = 0; }
+    if (lane < 8) c.cnt[lane] = 0;
+    unsigned long long key0 = ~0ull, key1 = ~0ull;  // (index << 32) | value, two per lane
+    bool bad = false;
+    auto load = [&](int i) -> unsigned long long {
+        if (i >= nchg) return ~0ull;
+        const int idx = a.dchg[2 * (cb + i)], val = a.dchg[2 * (cb + i) + 1];
+        if (idx < 0 || idx >= 2 * V + A) { bad = true; return ~0ull; }
+        if (idx < V ? (val < 0 || val >= VB) : idx < 2 * V ? (val < -1 || val >= VB) : (val < 0 || val >= A)) bad = true;
+        return ((unsigned long long)(unsigned)idx << 32) | (unsigned)val;
+    };
+    key0 = load(lane);
+    key1 = load(lane + 32);
+    if (__any_sync(FULL, bad)) { retry(); return; }
+    // bitonic sort of 64 keys held as (key0 of lanes 0..31, key1 of lanes 0..31)
+    for (int kk = 2; kk <= 64; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // partner is the same lane's other key
+                const bool up = ((lane & kk) == 0);
+                const unsigned long long lo = min(key0, key1), hi = max(key0, key1);
+                key0 = up ? lo : hi;
+                key1 = up ? hi : lo;
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    unsigned long long &x = h ? key1 : key0;
+                    const int i = lane + 32 * h;
+                    const unsigned long long y = __shfl_xor_sync(FULL, x, j);
+                    const bool up = ((i & kk) == 0), lower = (i & j) == 0;
+                    const unsigned long long lo = min(x, y), hi = max(x, y);
+                    x = (lower == up) ? lo : hi;
+                }
+            }
+        }
+    __syncwarp();
+    c.nchg = nchg;
+    if (lane < nchg) c.chg[lane] = make_int2((int)(key0 >> 32), (int)(unsigned)key0);
+    if (lane + 32 < nchg) c.chg[lane + 32] = make_int2((int)(key1 >> 32), (int)(unsigned)key1);
+    __syncwarp();
+    for (int i = lane; i < nchg; i += 32) {
+        const int idx = c.chg[i].x;
+        atomicOr(&c.cbm[idx >> 5], 1u << (idx & 31));
+        if (i > 0 && c.chg[i - 1].x == idx) bad = true;  // one change per index
+    }
+    __syncwarp();
+    // every changed op keeps a normal group distinct from its replica group
+    for (int i = lane; i < nchg; i += 32) {
+        const int idx = c.chg[i].x;
+        if (idx < 2 * V) {
+            const int v = idx < V ? idx : idx - V;
+            if (inn(c, v) == irr(c, v)) bad = true;
+        }
+    }
+    if (__any_sync(FULL, bad)) { retry(); return; }
+
+    // ---- changed dependency slots (removed from / added to the parent DAG)
+    for (int i = lane; i < nchg; i += 32) {
+        const int idx = c.chg[i].x;
+        if (idx < 2 * V) {
+            const int v = idx < V ? idx : idx - V;
+            if (idx >= V && ibit(c.cbm, v)) continue;  // the op's ngid change covers it
+            for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) iedge_slots(c, g.in_e[q]);
+            for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
+                const int e = g.out_e[q];
+                if (!iop_changed(c, g.e_dst[e])) iedge_slots(c, e);  // else the consumer's in-edges cover it
+            }
+            for (int q = g.arp_ptr[v]; q < g.arp_ptr[v + 1]; q++) iar_slot(c, g.arp[q]);
+        } else {
+            const int aa = idx - 2 * V, s = g.ar_prod[aa];
+            if (iop_changed(c, s)) continue;  // the producer's slots cover it
+            iar_slot(c, aa);
+            int j = 0;
+            for (int q = g.arp_ptr[s]; q < g.arp_ptr[s + 1]; q++, j++)
+                if (g.arp[q] == aa) break;
+            for (int q = g.out_ptr[s]; q < g.out_ptr[s + 1]; q++) {
+                const int e = g.out_e[q], d = g.e_dst[e];
+                if (g.e_agg[e] && !iop_changed(c, d)) {
+                    const int pnd = p.pnn[d], prd = p.prr[d];
+                    iagg_slots(c, e, j, aa, pnd, prd, pnd, prd);
+                }
+            }
+        }
+    }
+    // ---- patched nodes: groups / buckets whose membership changed (attribute)
+    for (int i = lane; i < nchg; i += 32) {
+        const int idx = c.chg[i].x, val = c.chg[i].y;
+        if (idx < V) { imark(c, p.pnn[idx], 1); imark(c, val, 1); }
+        else if (idx < 2 * V) {
+            if (p.prr[idx - V] >= 0) imark(c, p.prr[idx - V], 1);
+            if (val >= 0) imark(c, val, 1);
+        } else { imark(c, VB + p.pbk[idx - 2 * V], 1); imark(c, VB + val, 1); }
+    }
+    __syncwarp();
+    if (c.cnt[kCFail]) { retry(); return; }
+    // members of attribute-patched groups / buckets
+    const int n_attr = c.cnt[kCDirty];
+    for (int s = lane; s < n_attr; s += 32) {
+        const int n = c.dn[s];
+        IncWork wk{n, -1, -1, 0, 0, 0, 0};
+        if (n < VB) {
+            int cnt = 0;
+            for (int q = p.mptr[n]; q < p.mptr[n + 1]; q++) {
+                const int u = p.mem[q];
+                cnt += (inn(c, u) == n || irr(c, u) == n);
+            }
+            for (int i = 0; i < nchg; i++) {
+                const int idx = c.chg[i].x;
+                if (idx >= 2 * V) break;
+                const int v = idx < V ? idx : idx - V;
+                if (idx >= V && ibit(c.cbm, v)) continue;
+                if ((inn(c, v) == n || irr(c, v) == n) && p.pnn[v] != n && p.prr[v] != n) cnt++;
+            }
+            const int mb = atomicAdd(&c.cnt[kCMem], cnt);
+            if (mb + cnt > L.mem_cap) { ifail(c); c.work[s] = wk; continue; }
+            int o = mb;
+            for (int q = p.mptr[n]; q < p.mptr[n + 1]; q++) {
+                const int u = p.mem[q];
+                if (inn(c, u) == n || irr(c, u) == n) c.mem[o++] = u;
+            }
+            for (int i = 0; i < nchg; i++) {
+                const int idx = c.chg[i].x;
+                if (idx >= 2 * V) break;
+                const int v = idx < V ? idx : idx - V;
+                if (idx >= V && ibit(c.cbm, v)) continue;
+                if ((inn(c, v) == n || irr(c, v) == n) && p.pnn[v] != n && p.prr[v] != n) {
+                    int j = o++;  // insertion into the ascending run
+                    while (j > mb && c.mem[j - 1] > v) { c.mem[j] = c.mem[j - 1]; j--; }
+                    c.mem[j] = v;
+                }
+            }
+            wk.cnt = cnt;
+            wk.mn = cnt ? c.mem[mb] : -1;
+            wk.mb = mb;
+            wk.me = mb + cnt;
+        } else {
+            const int b = n - VB;
+            int cnt = 0, mn = INT_MAX;
+            long long bytes = 0;
+            for (int q = p.bptr[b]; q < p.bptr[b + 1]; q++) {
+                const int ar = p.bmem[q];
+                if (ibk(c, ar) == b) { cnt++; mn = min(mn, ar); bytes += g.ar_bytes[ar]; }
+            }
+            for (int i = 0; i < nchg; i++) {
+                const int idx = c.chg[i].x;
+                if (idx < 2 * V) continue;
+                const int ar = idx - 2 * V;
+                if (c.chg[i].y == b && p.pbk[ar] != b) { cnt++; mn = min(mn, ar); bytes += g.ar_bytes[ar]; }
+            }
+            wk.cnt = cnt;
+            wk.mn = cnt ? mn : -1;
+            wk.bytes = bytes;
+        }
+        c.work[s] = wk;
+    }
+    __syncwarp();
+    // groups whose tie-break rank depends on a patched group's min member
+    // (simulator.py:63: the replica bit of 2 * min + bit), and the sources of
+    // every removed / added slot (their successor lists are rebuilt)
+    for (int s = lane; s < n_attr; s += 32) {
+        const int n = c.dn[s];
+        if (n >= VB) continue;
+        const int ts[2] = {p.gcnt[n] > 0 ? (int)p.gmin[n] : -1, c.work[s].mn};
+        for (int h = 0; h < 2; h++) {
+            if (ts[h] < 0) continue;
+            const int y0 = inn(c, ts[h]), y1 = irr(c, ts[h]);
+            if (y0 >= 0 && y0 != n) imark(c, y0, 0);
+            if (y1 >= 0 && y1 != n) imark(c, y1, 0);
+        }
+    }
+    const int nrem = min(c.cnt[kCRem], kIncMaxOps), nadd = min(c.cnt[kCAdd], kIncMaxOps);
+    for (int i = lane; i < nrem; i += 32) imark(c, c.rem[i].y, 2);
+    for (int i = lane; i < nadd; i += 32) imark(c, c.add[i].x, 2);
+    __syncwarp();
+    if (c.cnt[kCFail]) { retry(); return; }
+    const int nd = c.cnt[kCDirty];
+    // rank of a patched node = its position among patched nodes by id
+    {
+        int carry = 0;
+        for (int base = 0; base < L.NW; base += 32) {
+            const int i = base + lane;
+            const int x = i < L.NW ? __popc(c.pbm[i]) : 0;
+            int v = x;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(FULL, v, d);
+                if (lane >= d) v += y;
+            }
+            if (i < L.NW) c.ppre[i] = (uint16_t)(carry + v - x);
+            carry += __shfl_sync(FULL, v, 31);
+        }
+    }
+    __syncwarp();
+    for (int s = lane; s < nd; s += 32) c.r2s[irank(c, c.dn[s])] = (uint16_t)s;
+    __syncwarp();
+    // patched records: existence, rank, duration (singletons, buckets), list range
+    int exist_delta = 0;
+    for (int s = lane; s < nd; s += 32) {
+        const int n = c.dn[s];
+        const bool attr = s < n_attr;
+        const IncNode pr = p.rec[n];
+        IncDirty dd{pr.dur, pr.prank, pr.sb, pr.se, pr.exists, 0};
+        if (n < VB) {
+            const int cnt = attr ? c.work[s].cnt : p.gcnt[n];
+            const int mn = attr ? c.work[s].mn : (p.gcnt[n] ? (int)p.gmin[n] : -1);
+            dd.exists = cnt > 0;
+            if (cnt > 0) {
+                const int cn = inn(c, mn), cr = irr(c, mn);
+                const int other = cn == n ? cr : cn;
+                int gmo = -1;
+                if (other >= 0) {
+                    const bool oattr = ibit(c.abm, other);
+                    gmo = oattr ? c.work[c.r2s[irank(c, other)]].mn : (p.gcnt[other] ? (int)p.gmin[other] : -1);
+                }
+                dd.prank = (uint16_t)(2 * mn + ((other >= 0 && gmo == mn && other < n) ? 1 : 0));
+                if (attr) {
+                    if (cnt == 1) {  // estimator.py:810-814
+                        if (g.op_kind[mn] == 1) dd.dur = 0.0;
+                        else {
+                            dd.dur = g.op_prof[mn];
+                            if (isnan(dd.dur)) ifail(c);  // MissingCost: the general path reports it
+                        }
+                    } else {
+                        dd.fused = 1;
+                        if (cnt > L.mpcap) ifail(c);
+                    }
+                }
+            }
+        } else if (attr) {
+            const IncWork wk = c.work[s];
+            dd.exists = wk.cnt > 0;
+            if (wk.cnt > 0) {
+                dd.prank = (uint16_t)wk.mn;
+                dd.dur = __dadd_rn(__dmul_rn(g.C, (double)wk.bytes), g.D);  // comm.py:45-49
+            }
+        }
+        if (attr) exist_delta += (int)dd.exists - (int)pr.exists;
+        c.dirty[irank(c, n)] = dd;
+    }
+    exist_delta = __reduce_add_sync(FULL, exist_delta);
+    __syncwarp();
+    if (c.cnt[kCFail]) { retry(); return; }
+    if (a.stop_after == 1) {
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
+        return;
+    }
+    // ---- K2: the patched fused groups (MP forward, memoised), whole warp each
+    for (int r = 0; r < nd; r++) {
+        if (!c.dirty[r].fused) continue;
+        const int s = c.r2s[r];
+        const IncWork wk = c.work[s];
+        const double pred = inc_group_mp<T>(c, gs, c.mem + wk.mb, wk.cnt, wk.node, lane);
+        if (lane == 0) c.dirty[r].dur = pred;
+        __syncwarp();
+    }
+    if (a.stop_after == 2) {
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
+        return;
+    }
+    // ---- rebuilt successor lists of list-patched nodes
+    for (int s = lane; s < nd; s += 32) {
+        const int n = c.dn[s];
+        if (!ibit(c.lbm, n)) continue;
+        const IncNode pr = p.rec[n];
+        int cnt = 0;
+        for (int q = pr.sb; q < pr.se; q++) {
+            bool gone = false;
+            for (int i = 0; i < nrem; i++) gone |= c.rem[i].x == q;
+            cnt += !gone;
+        }
+        for (int i = 0; i < nadd; i++) cnt += c.add[i].x == n;
+        const int o0 = atomicAdd(&c.cnt[kCPcsr], cnt);
+        if (o0 + cnt > L.pcsr_cap) { ifail(c); continue; }
+        int o = o0;
+        for (int q = pr.sb; q < pr.se; q++) {
+            bool gone = false;
+            for (int i = 0; i < nrem; i++) gone |= c.rem[i].x == q;
+            if (!gone) c.pcsr[o++] = p.succ[q];
+        }
+        for (int i = 0; i < nadd; i++)
+            if (c.add[i].x == n) {
+                const int t = c.add[i].y;
+                c.pcsr[o++] = ((uint32_t)p.rec[t].prank << 16) | (uint32_t)t;  // patched targets are re-ranked at release
+            }
+        IncDirty &dd = c.dirty[irank(c, n)];
+        dd.sb = (uint16_t)(0x8000 | o0);
+        dd.se = (uint16_t)(o0 + cnt);
+    }
+    // ---- the candidate's indegrees: the parent's, minus removed, plus added slots
+    {
+        const uint32_t *src = (const uint32_t *)p.indeg;
+        uint32_t *dst = (uint32_t *)c.indeg;
+        for (int i = lane; i < (NN + 1) / 2; i += 32) dst[i] = __ldg(&src[i]);
+    }
+    __syncwarp();
+    for (int i = lane; i < nrem; i += 32) {
+        const int t = c.rem[i].z;
+        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0xffff0000u : 0xffffffffu);
+        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
+    }
+    for (int i = lane; i < nadd; i += 32) {
+        const int t = c.add[i].y;
+        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0x10000u : 1u);
+        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
+    }
+    for (int i = lane; i < L.NW; i += 32) c.tbm[i] |= c.pbm[i];
+    __syncwarp();
+    if (c.cnt[kCFail]) { retry(); return; }
+    // ---- level-0 ready runs: the parent's (sorted by rank) without touched
+    // nodes, then the touched nodes that are ready, inserted in rank order
+    Ent16 *rg = c.ring, *rbk = c.ring + kRing;
+    int hgb[2] = {0, 0};
+    for (int lanei = 0; lanei < 2; lanei++) {
+        const uint16_t *src = p.ready + (lanei ? p.n_ready_g : 0);
+        const int n0 = lanei ? p.n_ready_b : p.n_ready_g;
+        Ent16 *buf = lanei ? rbk : rg;
+        int h = 0;
+        for (int base = 0; base < n0; base += 32) {
+            const int i = base + lane;
+            const int n = i < n0 ? src[i] : 0;
+            const bool keep = i < n0 && !ibit(c.tbm, n);
+            const unsigned m = __ballot_sync(FULL, keep);
+            const int pos = h + __popc(m & lanemask_lt());
+            if (keep && pos < kRing) {
+                const IncNode r = p.rec[n];
+                Ent16 x;
+                x.key = r.prank;
+                x.sb = r.sb;
+                x.se = r.se;
+                x.dur = r.dur;
+                buf[pos] = x;
+            }
+            h += __popc(m);
+        }
+        hgb[lanei] = h;
+    }
+    __syncwarp();
+    if (hgb[0] > kRing || hgb[1] > kRing) { retry(); return; }
+    if (lane == 0) {
+        bool ok = true;
+        for (int wi = 0; wi < L.NW && ok; wi++) {
+            uint32_t m = c.tbm[wi];
+            while (m && ok) {
+                const int n = wi * 32 + __ffs(m) - 1;
+                m &= m - 1;
+                if (n >= NN || c.indeg[n] != 0) continue;
+                Ent16 x;
+                if (ibit(c.pbm, n)) {
+                    const IncDirty dd = c.dirty[irank(c, n)];
+                    if (!dd.exists) continue;
+                    x.key = dd.prank;
+                    x.sb = dd.sb;
+                    x.se = dd.se;
+                    x.dur = dd.dur;
+                } else {
+                    const IncNode r = p.rec[n];
+                    if (!r.exists) continue;
+                    x.key = r.prank;
+                    x.sb = r.sb;
+                    x.se = r.se;
+                    x.dur = r.dur;
+                }
+                ok = n < VB ? inc_ring_insert(rg, hgb[0], x) : inc_ring_insert(rbk, hgb[1], x);
+            }
+        }
+        // ---- K3: the event loop on one lane
+        if (!ok || !inc_ring_loop(c, k, hgb[0], hgb[1], p.n_exist + exist_delta)) {
+            a.cost_out[k] = 0.0;
+            a.status_out[k] = kRetryGeneral;
+        }
+    }
+    __syncwarp();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc(const __grid_constant__ IncArgs a) {
+    extern __shared__ __align__(16) char smem_arena[];
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int nw = gridDim.x * kWarps;
+    const IncLayout &L = a.L;
+    char *wsb = a.ws + (int64_t)wid * L.total;
+    char *sm = smem_arena + (threadIdx.x >> 5) * L.s_bytes;
+    IncCtx c;
+    c.a = &a;
+    c.chg = (int2 *)(wsb + L.chg);
+    c.rem = (int4 *)(wsb + L.rem);
+    c.add = (int2 *)(wsb + L.add);
+    c.dn = (int *)(wsb + L.dn);
+    c.work = (IncWork *)(wsb + L.work);
+    c.dirty = (IncDirty *)(wsb + L.dirty);
+    c.r2s = (uint16_t *)(c.dirty + kIncMaxDirty + 1);
+    c.mem = (int *)(wsb + L.mem);
+    c.pcsr = (uint32_t *)(wsb + L.pcsr);
+    c.ring = (Ent16 *)(wsb + L.ring);
+    c.indeg = L.s_indeg >= 0 ? (uint16_t *)(sm + L.s_indeg) : (uint16_t *)(wsb + L.indeg);
+    c.pbm = (uint32_t *)(sm + L.s_pbm);
+    c.abm = (uint32_t *)(sm + L.s_abm);
+    c.lbm = (uint32_t *)(sm + L.s_lbm);
+    c.tbm = (uint32_t *)(sm + L.s_tbm);
+    c.ppre = (uint16_t *)(sm + L.s_ppre);
+    c.cbm = (uint32_t *)(sm + L.s_cbm);
+    c.cnt = (int *)(sm + L.s_cnt);
+    c.nchg = 0;
+    char *gb = wsb + L.gs0;
+    const GroupScratch gs{(int *)(gb + L.g_msort), (int *)(gb + L.g_lidx), (int *)(gb + L.g_zl),
+                          (int *)(gb + L.g_nbptr), (int *)(gb + L.g_nb), (int *)(gb + L.g_mark),
+                          gb + L.g_H, gb + L.g_P};
+    for (int k = wid; k < a.K; k += nw) {
+        score_one_inc<T>(a, k, c, gs, lane);
+        __syncwarp();
+    }
+}
+
+template <typename T>
+static int inc_blocks_per_sm_q(int smem_per_block) {
+    int n = 0;
+    if (smem_per_block > 48 * 1024)
+        cudaFuncSetAttribute(score_kernel_inc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel_inc<T>, kWarps * 32, smem_per_block);
+    return n;
+}
+
+int score_inc_blocks_per_sm(const IncLayout &L, int precision) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;
+    const std::pair<int, int> key(L.s_bytes, precision);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    const int n = precision == FO_PREC_FP64 ? inc_blocks_per_sm_q<double>(L.s_bytes * kWarps)
+                                            : inc_blocks_per_sm_q<float>(L.s_bytes * kWarps);
+    cache[key] = n;
+    return n;
+}
+
+cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
+                             const int32_t *chg, int K, int precision, char *ws, int grid, double *cost_out,
+                             int32_t *status_out, cudaStream_t stream) {
+    IncArgs a;
+    a.g = g;
+    a.p = p;
+    a.L = L;
+    a.doff = off;
+    a.dchg = chg;
+    a.K = K;
+    a.ws = ws;
+    a.cost_out = cost_out;
+    a.status_out = status_out;
+    a.stop_after = g.phase_stop;
+    const size_t smem = (size_t)L.s_bytes * kWarps;
+    if (precision == FO_PREC_FP64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a);
+    else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a);
+    return cudaGetLastError();
+}
