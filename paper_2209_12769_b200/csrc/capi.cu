@@ -30,7 +30,6 @@ int fail(int status, const std::string &msg) {
     } while (0)
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
-static int ensure_plan(fo_graph *g, int precision);  // incremental delta scoring (below)
 
 int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int nws, int alt) {
     *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, big ? g->V : kMpCapDefault, nws);
@@ -154,6 +153,8 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
 }  // namespace fo
 
 using namespace fo;
+
+static int ensure_plan(fo_graph *g, int precision);  // incremental delta scoring (below)
 
 extern "C" {
 
@@ -799,6 +800,8 @@ static int single(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
     return FO_OK;
 }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------------------
 // Parent plan of the incremental delta path (score_inc.cuh), per precision:
 // the parent's contracted schedule DAG in gid space -- the dependency slots
@@ -979,6 +982,8 @@ static int ensure_plan(fo_graph *g, int precision) {
     if (g->plan_pv[pi] == g->parent_ver && g->plan_mv[pi] == g->model_ver) return FO_OK;
     return build_plan(g, precision);
 }
+
+extern "C" {
 
 int fo_simulate(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const int32_t *bkt, int32_t gid_bound,
                 int32_t precision, const double *durations, int32_t *c_id, double *c_start, double *c_end,
