@@ -42,7 +42,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     IncLayout L{};
     const int NN = VB + A;
     int64_t o = 0;
-    auto take = [&](int64_t bytes) { int64_t r = o; o = align8(o + bytes); return r; };
+    auto take = [&](int64_t bytes) { int64_t r = o; o = (o + bytes + 15) & ~int64_t(15); return r; };  // int4 / Ent16 entries
     L.mem_cap = 2 * V + A + 64;
     L.pcsr_cap = std::min<int64_t>(P + kIncMaxOps + 64, 32767);
     L.chg = take(8 * kIncMaxChg);
@@ -69,7 +69,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.g_H = sub(8 * cap * kHidden);
     L.g_P = sub(8 * cap * kHidden);
     o += q;
-    L.total = align8(o) + 128;
+    L.total = ((o + 255) & ~int64_t(255)) + 256;  // per-warp slots stay 256-byte aligned
     // per-warp shared-memory arena
     L.NW = (NN + 31) / 32;
     L.CW = (2 * V + A + 31) / 32;
