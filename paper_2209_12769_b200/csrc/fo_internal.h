@@ -152,7 +152,7 @@ cudaError_t launch_predict_features(const DGraph &g, const FeatIn &in, int preci
 // nodes they touch; the event loop walks the parent's successor lists (read
 // only, shared by every warp of an SM, so L1-resident) plus a few rebuilt
 // lists, with the candidate's indegrees in shared memory.
-struct IncNode {      // parent node record, 16 B: one load per released node
+struct __align__(16) IncNode {  // parent node record, 16 B: one 128-bit load per released node
     double dur;
     uint16_t sb, se;  // successor range in IncPlan::succ (bit 15 of sb: rebuilt list, candidates only)
     uint16_t prank;   // tie-break rank (simulator.py:63-64): 2 * min member + replica bit, or min AR
@@ -175,14 +175,16 @@ struct IncPlan {
     const uint16_t *ready;     // level-0 ready nodes: lane g [0, n_ready_g), lane b after, each by prank
 };
 struct IncLayout {  // per-warp global scratch (byte offsets) and shared-memory arena
-    int64_t chg, rem, add, dn, work, dirty, mem, pcsr, ring, indeg, gs0, total;
+    int64_t hdr, chg, rem, add, dn, work, dirty, mem, pcsr, ring, indeg, gs0, total;
     int64_t g_msort, g_lidx, g_zl, g_nbptr, g_nb, g_mark, g_H, g_P;
     int32_t mem_cap, pcsr_cap, mpcap;
+    int32_t ring_g, ring_b;  // ready-run ring sizes (powers of two >= the nodes of each lane: no overflow)
     int32_t s_indeg, s_pbm, s_abm, s_lbm, s_tbm, s_ppre, s_cbm, s_cnt, s_bytes;  // smem offsets (s_indeg < 0: global)
     int32_t NW, CW;
 };
 constexpr int kIncMaxChg = 64, kIncMaxOps = 256, kIncMaxDirty = 192;
 constexpr int kRetryGeneral = 101;  // internal status: the incremental kernel hands the candidate to score_kernel
+constexpr int kIncPending = 102;    // internal status: set up, waiting for the event-loop kernel
 IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg);
 cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
                              const int32_t *chg, int K, int precision, char *ws, int grid, double *cost_out,

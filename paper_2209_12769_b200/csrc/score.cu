@@ -756,7 +756,7 @@ __device__ __forceinline__ void event_loop(const ScoreArgs &a, int k, const doub
 // currently ready nodes and its working set stays in L1.  Returns false on
 // ring overflow (the caller reruns the linear-buffer loop).
 constexpr int kRing = 256;
-struct Ent16 {
+struct __align__(16) Ent16 {  // one 128-bit load / store per ready entry
     uint32_t key;
     uint16_t sb, se;
     double dur;

@@ -45,6 +45,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     auto take = [&](int64_t bytes) { int64_t r = o; o = (o + bytes + 15) & ~int64_t(15); return r; };  // int4 / Ent16 entries
     L.mem_cap = 2 * V + A + 64;
     L.pcsr_cap = std::min<int64_t>(P + kIncMaxOps + 64, 32767);
+    L.hdr = take(16);
     L.chg = take(8 * kIncMaxChg);
     L.rem = take(16 * kIncMaxOps);
     L.add = take(8 * kIncMaxOps);
@@ -53,7 +54,11 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.dirty = take(sizeof(IncDirty) * (kIncMaxDirty + 1) + 2 * kIncMaxDirty);  // + rank -> slot map
     L.mem = take(4 * (int64_t)L.mem_cap);
     L.pcsr = take(4 * (int64_t)L.pcsr_cap);
-    L.ring = take(16 * 2 * kRing);
+    L.ring_g = 1;
+    while (L.ring_g < VB) L.ring_g <<= 1;
+    L.ring_b = 1;
+    while (L.ring_b < A + 1) L.ring_b <<= 1;
+    L.ring = take(16 * ((int64_t)L.ring_g + L.ring_b));
     L.indeg = smem_indeg ? -1 : take(2 * (int64_t)(NN + 2));
     const int64_t cap = std::min(V, kMpCapDefault);
     L.mpcap = (int)cap;
@@ -118,6 +123,7 @@ struct IncCtx {
     uint32_t *pbm, *abm, *lbm, *tbm, *cbm;
     uint16_t *ppre;
     int *cnt;
+    int *hdr;  // hand-off from the setup kernel to the event-loop kernel: nd, nrem, nadd, N
     int nchg;
 };
 
@@ -277,66 +283,97 @@ __device__ double inc_group_mp(const IncCtx &c, const GroupScratch &gs, const in
     return pred;
 }
 
+extern __shared__ __align__(16) char fo_inc_smem[];  // the dynamic arena, addressed by 32-bit offsets
+
+// release of a patched node (rare): its record comes from the candidate's
+// table at its rank among the patched nodes
+__device__ __noinline__ Ent16 inc_patched_entry(const IncDirty *__restrict__ dirty, uint32_t s_ppre, unsigned t,
+                                                uint32_t w, uint32_t level) {
+    const uint16_t *ppre = (const uint16_t *)(fo_inc_smem + s_ppre);
+    const IncDirty dd = dirty[(int)ppre[t >> 5] + __popc(w & ((1u << (t & 31)) - 1u))];
+    Ent16 x;
+    x.key = level | dd.prank;
+    x.sb = dd.sb;
+    x.se = dd.se;
+    x.dur = dd.dur;
+    return x;
+}
+
+// push into a ready run held in a ring sized for every node of its lane
+// (no overflow); keys only grow, so an append is the common case
+__device__ __forceinline__ void inc_push(Ent16 *__restrict__ buf, unsigned m, int head, int &tail, uint32_t &last,
+                                         const Ent16 &x) {
+    if (tail == head || x.key >= last) {
+        buf[(tail++) & m] = x;
+        last = x.key;
+        return;
+    }
+    int i = tail++;
+    while (i > head) {
+        const Ent16 q = buf[(i - 1) & m];
+        if (q.key <= x.key) break;
+        buf[i & m] = q;
+        i--;
+    }
+    buf[i & m] = x;
+}
+
 // The event loop (simulator.py:117-140) of ring_loop over the parent's
-// successor lists and the candidate's patches.  false on ring overflow.
-__device__ __forceinline__ bool inc_ring_loop(const IncCtx &c, int k, int hg, int hb, int N) {
-    const IncPlan &p = c.a->p;
-    const IncNode *__restrict__ rec = p.rec;
+// successor lists and the candidate's rebuilt ones; indegrees and the
+// patched bitmap in shared memory (SI: indegrees too), 32-bit addressed.
+template <bool SI>
+__device__ __forceinline__ void inc_ring_loop(const IncPlan &p, const uint32_t *__restrict__ csucc,
+                                              const IncDirty *__restrict__ dirty, Ent16 *__restrict__ rg,
+                                              Ent16 *__restrict__ rb, unsigned mg, unsigned mb,
+                                              uint16_t *__restrict__ gindeg, uint32_t s_indeg, uint32_t s_pbm,
+                                              uint32_t s_ppre, int hg, int hb, int N, double *cost_out,
+                                              int32_t *status_out) {
     const uint32_t *__restrict__ psucc = p.succ;
-    const uint32_t *__restrict__ csucc = c.pcsr;
-    uint16_t *__restrict__ indeg = c.indeg;
-    const uint32_t *__restrict__ pbm = c.pbm;
-    const uint16_t *__restrict__ ppre = c.ppre;
-    const IncDirty *__restrict__ dirty = c.dirty;
-    Ent16 *__restrict__ rg = c.ring;
-    Ent16 *__restrict__ rb = c.ring + kRing;
-    const int VB = p.VB;
+    const IncNode *__restrict__ rec = p.rec;
+    uint16_t *__restrict__ indeg = SI ? (uint16_t *)(fo_inc_smem + s_indeg) : gindeg;
+    const uint32_t *__restrict__ pbm = (const uint32_t *)(fo_inc_smem + s_pbm);
+    const unsigned VB = (unsigned)p.VB;
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     int run0 = 0, run1 = 0;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
     double end0 = 0.0, end1 = 0.0, now = 0.0;
     uint32_t level = 0;
-    uint32_t lastg = hg > 0 ? rg[(hg - 1) & (kRing - 1)].key : 0u;
-    uint32_t lastb = hb > 0 ? rb[(hb - 1) & (kRing - 1)].key : 0u;
-    auto release = [&](unsigned qb, unsigned qe) -> bool {
-        const uint32_t *L = (qb & 0x8000u) ? csucc : psucc;
+    uint32_t lastg = hg > 0 ? rg[(hg - 1) & mg].key : 0u;
+    uint32_t lastb = hb > 0 ? rb[(hb - 1) & mb].key : 0u;
+    auto release = [&](unsigned qb, unsigned qe) {
+        const uint32_t *__restrict__ L = (qb & 0x8000u) ? csucc : psucc;
         for (unsigned q = qb & 0x7fffu; q < qe; q++) {
             const uint32_t e = L[q];
             const unsigned t = e & 0xffffu;
             const int d = indeg[t] - 1;
             const IncNode r = rec[t];  // issued with the indegree load
-            const uint32_t w = pbm[t >> 5];
             indeg[t] = (uint16_t)d;
             if (d == 0) {
+                const uint32_t w = pbm[t >> 5];
                 Ent16 x;
-                if ((w >> (t & 31)) & 1u) {  // patched node: the candidate's record
-                    const IncDirty &dd = dirty[(int)ppre[t >> 5] + __popc(w & ((1u << (t & 31)) - 1u))];
-                    x.key = level | dd.prank;
-                    x.sb = dd.sb;
-                    x.se = dd.se;
-                    x.dur = dd.dur;
+                if ((w >> (t & 31)) & 1u) {
+                    x = inc_patched_entry(dirty, s_ppre, t, w, level);
                 } else {
                     x.key = level | r.prank;
                     x.sb = r.sb;
                     x.se = r.se;
                     x.dur = r.dur;
                 }
-                if (!((int)t < VB ? ring_push_t(rg, headg, tailg, lastg, x) : ring_push_t(rb, headb, tailb, lastb, x)))
-                    return false;
+                if (t < VB) inc_push(rg, mg, headg, tailg, lastg, x);
+                else inc_push(rb, mb, headb, tailb, lastb, x);
             }
         }
-        return true;
     };
     auto start = [&]() {
         if (!run0 && headg < tailg) {
-            const Ent16 x = rg[(headg++) & (kRing - 1)];
+            const Ent16 x = rg[(headg++) & mg];
             run0 = 1;
             end0 = __dadd_rn(now, x.dur);
             sb0 = x.sb;
             se0 = x.se;
         }
         if (!run1 && headb < tailb) {
-            const Ent16 x = rb[(headb++) & (kRing - 1)];
+            const Ent16 x = rb[(headb++) & mb];
             run1 = 1;
             end1 = __dadd_rn(now, x.dur);
             sb1 = x.sb;
@@ -349,29 +386,19 @@ __device__ __forceinline__ bool inc_ring_loop(const IncCtx &c, int k, int hg, in
         const bool c1 = run1 && (!run0 || end1 <= end0);
         const double t = c0 ? end0 : end1;
         if (t > now) { now = t; level += 0x10000u; }
-        if (c0) {
-            run0 = 0;
-            if (!release(sb0, se0)) return false;
-        }
-        if (c1) {
-            run1 = 0;
-            if (!release(sb1, se1)) return false;
-        }
+        if (c0) { run0 = 0; release(sb0, se0); }
+        if (c1) { run1 = 0; release(sb1, se1); }
         start();
     }
     const int done = headg + headb;
-    c.a->cost_out[k] = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
-    c.a->status_out[k] = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
-    return true;
+    *cost_out = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
+    *status_out = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
 }
 
 // insert one ready entry into a level-0 run (kept sorted by key)
-__device__ __forceinline__ bool inc_ring_insert(Ent16 *buf, int &tail, const Ent16 &x) {
-    if (tail >= kRing) return false;
-    int dummy = tail;
-    ring_push(buf, 0, dummy, x);
-    tail = dummy;
-    return true;
+__device__ __forceinline__ void inc_ring_insert(Ent16 *buf, unsigned m, int &tail, const Ent16 &x) {
+    uint32_t last = tail > 0 ? buf[(tail - 1) & m].key : 0u;
+    inc_push(buf, m, 0, tail, last, x);
 }
 
 template <typename T>
@@ -676,103 +703,24 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         dd.sb = (uint16_t)(0x8000 | o0);
         dd.se = (uint16_t)(o0 + cnt);
     }
-    // ---- the candidate's indegrees: the parent's, minus removed, plus added slots
-    {
-        const uint32_t *src = (const uint32_t *)p.indeg;
-        uint32_t *dst = (uint32_t *)c.indeg;
-        for (int i = lane; i < (NN + 1) / 2; i += 32) dst[i] = __ldg(&src[i]);
-    }
-    __syncwarp();
-    for (int i = lane; i < nrem; i += 32) {
-        const int t = c.rem[i].z;
-        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0xffff0000u : 0xffffffffu);
-        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
-    }
-    for (int i = lane; i < nadd; i += 32) {
-        const int t = c.add[i].y;
-        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0x10000u : 1u);
-        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
-    }
-    for (int i = lane; i < L.NW; i += 32) c.tbm[i] |= c.pbm[i];
     __syncwarp();
     if (c.cnt[kCFail]) { retry(); return; }
-    // ---- level-0 ready runs: the parent's (sorted by rank) without touched
-    // nodes, then the touched nodes that are ready, inserted in rank order
-    Ent16 *rg = c.ring, *rbk = c.ring + kRing;
-    int hgb[2] = {0, 0};
-    for (int lanei = 0; lanei < 2; lanei++) {
-        const uint16_t *src = p.ready + (lanei ? p.n_ready_g : 0);
-        const int n0 = lanei ? p.n_ready_b : p.n_ready_g;
-        Ent16 *buf = lanei ? rbk : rg;
-        int h = 0;
-        for (int base = 0; base < n0; base += 32) {
-            const int i = base + lane;
-            const int n = i < n0 ? src[i] : 0;
-            const bool keep = i < n0 && !ibit(c.tbm, n);
-            const unsigned m = __ballot_sync(FULL, keep);
-            const int pos = h + __popc(m & lanemask_lt());
-            if (keep && pos < kRing) {
-                const IncNode r = p.rec[n];
-                Ent16 x;
-                x.key = r.prank;
-                x.sb = r.sb;
-                x.se = r.se;
-                x.dur = r.dur;
-                buf[pos] = x;
-            }
-            h += __popc(m);
-        }
-        hgb[lanei] = h;
-    }
-    __syncwarp();
-    if (hgb[0] > kRing || hgb[1] > kRing) { retry(); return; }
+    // hand-off to the event-loop kernel: counts in the header, lists in the scratch
     if (lane == 0) {
-        bool ok = true;
-        for (int wi = 0; wi < L.NW && ok; wi++) {
-            uint32_t m = c.tbm[wi];
-            while (m && ok) {
-                const int n = wi * 32 + __ffs(m) - 1;
-                m &= m - 1;
-                if (n >= NN || c.indeg[n] != 0) continue;
-                Ent16 x;
-                if (ibit(c.pbm, n)) {
-                    const IncDirty dd = c.dirty[irank(c, n)];
-                    if (!dd.exists) continue;
-                    x.key = dd.prank;
-                    x.sb = dd.sb;
-                    x.se = dd.se;
-                    x.dur = dd.dur;
-                } else {
-                    const IncNode r = p.rec[n];
-                    if (!r.exists) continue;
-                    x.key = r.prank;
-                    x.sb = r.sb;
-                    x.se = r.se;
-                    x.dur = r.dur;
-                }
-                ok = n < VB ? inc_ring_insert(rg, hgb[0], x) : inc_ring_insert(rbk, hgb[1], x);
-            }
-        }
-        // ---- K3: the event loop on one lane
-        if (!ok || !inc_ring_loop(c, k, hgb[0], hgb[1], p.n_exist + exist_delta)) {
-            a.cost_out[k] = 0.0;
-            a.status_out[k] = kRetryGeneral;
-        }
+        c.hdr[0] = nd;
+        c.hdr[1] = nrem;
+        c.hdr[2] = nadd;
+        c.hdr[3] = p.n_exist + exist_delta;
+        a.status_out[k] = kIncPending;
     }
-    __syncwarp();
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc(const __grid_constant__ IncArgs a) {
-    extern __shared__ __align__(16) char smem_arena[];
-    const int lane = threadIdx.x & 31;
-    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const int nw = gridDim.x * kWarps;
+__device__ __forceinline__ IncCtx inc_ctx(const IncArgs &a, int wid, char *sm) {
     const IncLayout &L = a.L;
     char *wsb = a.ws + (int64_t)wid * L.total;
-    char *sm = smem_arena + (threadIdx.x >> 5) * L.s_bytes;
     IncCtx c;
     c.a = &a;
+    c.hdr = (int *)(wsb + L.hdr);
     c.chg = (int2 *)(wsb + L.chg);
     c.rem = (int4 *)(wsb + L.rem);
     c.add = (int2 *)(wsb + L.add);
@@ -792,23 +740,154 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc(const __grid_
     c.cbm = (uint32_t *)(sm + L.s_cbm);
     c.cnt = (int *)(sm + L.s_cnt);
     c.nchg = 0;
-    char *gb = wsb + L.gs0;
+    return c;
+}
+
+// Setup + K2 of candidates [k0, k0 + warps): one warp each.
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc(const __grid_constant__ IncArgs a, int k0) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int k = k0 + wid;
+    if (k >= a.K) return;
+    const IncLayout &L = a.L;
+    const IncCtx c = inc_ctx(a, wid, fo_inc_smem + (threadIdx.x >> 5) * L.s_bytes);
+    char *gb = a.ws + (int64_t)wid * L.total + L.gs0;
     const GroupScratch gs{(int *)(gb + L.g_msort), (int *)(gb + L.g_lidx), (int *)(gb + L.g_zl),
                           (int *)(gb + L.g_nbptr), (int *)(gb + L.g_nb), (int *)(gb + L.g_mark),
                           gb + L.g_H, gb + L.g_P};
-    for (int k = wid; k < a.K; k += nw) {
-        score_one_inc<T>(a, k, c, gs, lane);
-        __syncwarp();
-    }
+    score_one_inc<T>(a, k, c, gs, lane);
 }
 
+// K3 of the same candidates: the candidate's indegrees (the parent's, minus
+// removed, plus added slots) and patched-node ranks in shared memory, the
+// level-0 ready runs, then the event loop on one lane.
+template <bool SI>
+__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __grid_constant__ IncArgs a, int k0) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int k = k0 + wid;
+    if (k >= a.K || a.status_out[k] != kIncPending) return;
+    const IncLayout &L = a.L;
+    const IncPlan &p = a.p;
+    const uint32_t warp_sm = (uint32_t)((threadIdx.x >> 5) * L.s_bytes);
+    char *sm = fo_inc_smem + warp_sm;
+    const IncCtx c = inc_ctx(a, wid, sm);
+    const int nd = c.hdr[0], nrem = c.hdr[1], nadd = c.hdr[2], N = c.hdr[3];
+    const int NN = p.NN, VB = p.VB;
+    for (int i = lane; i < L.NW; i += 32) { c.pbm[i] = 0; c.tbm[i] = 0; }
+    __syncwarp();
+    for (int s = lane; s < nd; s += 32) {
+        const int n = c.dn[s];
+        atomicOr(&c.pbm[n >> 5], 1u << (n & 31));
+    }
+    __syncwarp();
+    {
+        int carry = 0;
+        for (int base = 0; base < L.NW; base += 32) {
+            const int i = base + lane;
+            const int x = i < L.NW ? __popc(c.pbm[i]) : 0;
+            int v = x;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(FULL, v, d);
+                if (lane >= d) v += y;
+            }
+            if (i < L.NW) c.ppre[i] = (uint16_t)(carry + v - x);
+            carry += __shfl_sync(FULL, v, 31);
+        }
+    }
+    {
+        const uint32_t *src = (const uint32_t *)p.indeg;
+        uint32_t *dst = (uint32_t *)c.indeg;
+        for (int i = lane; i < (NN + 1) / 2; i += 32) dst[i] = __ldg(&src[i]);
+    }
+    __syncwarp();
+    for (int i = lane; i < nrem; i += 32) {
+        const int t = c.rem[i].z;
+        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0xffff0000u : 0xffffffffu);
+        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
+    }
+    for (int i = lane; i < nadd; i += 32) {
+        const int t = c.add[i].y;
+        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0x10000u : 1u);
+        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
+    }
+    __syncwarp();
+    for (int i = lane; i < L.NW; i += 32) c.tbm[i] |= c.pbm[i];
+    __syncwarp();
+    // level-0 ready runs: the parent's (sorted by rank) without touched nodes,
+    // then the touched nodes that are ready, inserted in rank order
+    Ent16 *rg = c.ring, *rbk = c.ring + L.ring_g;
+    const unsigned mg = (unsigned)L.ring_g - 1u, mbk = (unsigned)L.ring_b - 1u;
+    int hgb[2] = {0, 0};
+    for (int lanei = 0; lanei < 2; lanei++) {
+        const uint16_t *src = p.ready + (lanei ? p.n_ready_g : 0);
+        const int n0 = lanei ? p.n_ready_b : p.n_ready_g;
+        Ent16 *buf = lanei ? rbk : rg;
+        int h = 0;
+        for (int base = 0; base < n0; base += 32) {
+            const int i = base + lane;
+            const int n = i < n0 ? src[i] : 0;
+            const bool keep = i < n0 && !ibit(c.tbm, n);
+            const unsigned m = __ballot_sync(FULL, keep);
+            const int pos = h + __popc(m & lanemask_lt());
+            if (keep) {
+                const IncNode r = p.rec[n];
+                Ent16 x;
+                x.key = r.prank;
+                x.sb = r.sb;
+                x.se = r.se;
+                x.dur = r.dur;
+                buf[pos] = x;
+            }
+            h += __popc(m);
+        }
+        hgb[lanei] = h;
+    }
+    __syncwarp();
+    if (lane != 0) return;
+    for (int wi = 0; wi < L.NW; wi++) {
+        uint32_t m = c.tbm[wi];
+        while (m) {
+            const int n = wi * 32 + __ffs(m) - 1;
+            m &= m - 1;
+            if (n >= NN || c.indeg[n] != 0) continue;
+            Ent16 x;
+            if (ibit(c.pbm, n)) {
+                const IncDirty dd = c.dirty[irank(c, n)];
+                if (!dd.exists) continue;
+                x.key = dd.prank;
+                x.sb = dd.sb;
+                x.se = dd.se;
+                x.dur = dd.dur;
+            } else {
+                const IncNode r = p.rec[n];
+                if (!r.exists) continue;
+                x.key = r.prank;
+                x.sb = r.sb;
+                x.se = r.se;
+                x.dur = r.dur;
+            }
+            if (n < VB) inc_ring_insert(rg, mg, hgb[0], x);
+            else inc_ring_insert(rbk, mbk, hgb[1], x);
+        }
+    }
+    inc_ring_loop<SI>(p, c.pcsr, c.dirty, rg, rbk, mg, mbk, SI ? nullptr : c.indeg, warp_sm + L.s_indeg,
+                      warp_sm + L.s_pbm, warp_sm + L.s_ppre, hgb[0], hgb[1], N, a.cost_out + k, a.status_out + k);
+}
+
+template <typename KF>
+static int inc_occ(KF kf, int smem_per_block) {
+    int n = 0;
+    if (smem_per_block > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kf, kWarps * 32, smem_per_block);
+    return n;
+}
 template <typename T>
 static int inc_blocks_per_sm_q(int smem_per_block) {
-    int n = 0;
-    if (smem_per_block > 48 * 1024)
-        cudaFuncSetAttribute(score_kernel_inc<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_block);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel_inc<T>, kWarps * 32, smem_per_block);
-    return n;
+    return std::min({inc_occ(score_kernel_inc<T>, smem_per_block), inc_occ(score_kernel_inc_k3<true>, smem_per_block),
+                     inc_occ(score_kernel_inc_k3<false>, smem_per_block)});
 }
 
 int score_inc_blocks_per_sm(const IncLayout &L, int precision) {
@@ -839,7 +918,14 @@ cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout 
     a.status_out = status_out;
     a.stop_after = g.phase_stop;
     const size_t smem = (size_t)L.s_bytes * kWarps;
-    if (precision == FO_PREC_FP64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a);
-    else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a);
+    const int per_launch = grid * kWarps;  // one candidate per warp per launch pair
+    for (int k0 = 0; k0 < K; k0 += per_launch) {
+        if (precision == FO_PREC_FP64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+        else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+        if (a.stop_after == 0) {
+            if (L.s_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+            else score_kernel_inc_k3<false><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+        }
+    }
     return cudaGetLastError();
 }

@@ -44,3 +44,9 @@ ts = sum(v[0] for v in ph.values()) or 1; ti = sum(v[1] for v in ph.values()) or
 print(f"instructions/candidate {ti / ncand:.0f}")
 for k, v in sorted(ph.items(), key=lambda x: -x[1][0])[:30]:
     print(f"{k[0][:10]:10s}:{k[1]:<5d} s={100*v[0]/ts:5.1f}% i={100*v[1]/ti:5.1f}% {k[2]}")
+if regions:  # {"name": [file_suffix, first_line, last_line], ...}
+    print("per region (stall samples / instructions):")
+    for name, (fs, lo, hi) in regions.items():
+        s = sum(v[0] for k, v in ph.items() if k[0].startswith(fs) and lo <= k[1] <= hi)
+        i = sum(v[1] for k, v in ph.items() if k[0].startswith(fs) and lo <= k[1] <= hi)
+        print(f"  {name:24s} s={100*s/ts:5.1f}% i={100*i/ti:5.1f}% ({i / ncand:.0f} inst/candidate)")
