@@ -823,7 +823,10 @@ static int build_plan(fo_graph *g, int precision) {
     const int32_t *pn = g->h_parent.data(), *pr = pn + V, *pb = pn + 2 * V;
     std::vector<char> h;
     size_t o[16];
+    const int stop = g->dg.phase_stop;  // the parent's full durations, whatever the measurement hook says
+    g->dg.phase_stop = 0;
     int st = single(g, pn, pr, pb, VB, precision, nullptr, false, true, h, o);
+    g->dg.phase_stop = stop;
     if (st) return st;
     if (*(const int32_t *)(h.data() + o[4]) != FO_OK) return FO_OK;  // the parent itself fails: general path
     const double *dur_c = (const double *)(h.data() + o[14]);

@@ -122,3 +122,20 @@ def test_incremental_hands_back_invalid_and_oversized_candidates():
     assert st[8] == N.FO_INVALID_ARG and st[9] == N.FO_INVALID_ARG
     _, st_only = _score(dg, off2, chg2, N.FO_PREC_FP32, 2)
     assert (st_only[8:] == 101).all() and (st_only[:8] != 101).all()
+
+
+def test_plan_built_under_a_phase_stop_is_still_exact():
+    """The measurement hook (fo_set_phase_stop) must not leak into the plan:
+    a plan first built while a phase stop is set still carries the parent's
+    full durations."""
+    g, dg = _handle("vgg16", N.FO_PREC_FP32)
+    dg.set_parent()
+    off, chg = dg.make_candidates_delta(np.arange(512, dtype=np.uint64))
+    ref, _ = _score(dg, off, chg, N.FO_PREC_FP32, 0)
+    g2, dg2 = _handle("vgg16", N.FO_PREC_FP32)
+    dg2.set_parent()
+    N.lib().fo_set_phase_stop(dg2.h, 1)
+    _score(dg2, off, chg, N.FO_PREC_FP32, 1)  # plan built here
+    N.lib().fo_set_phase_stop(dg2.h, 0)
+    got, _ = _score(dg2, off, chg, N.FO_PREC_FP32, 1)
+    assert np.array_equal(got, ref)

@@ -22,6 +22,8 @@ else:
     ng, rg, bk, gb = dg.make_candidates(np.arange(K, dtype=np.uint64))
     d = [torch.from_numpy(x).cuda() for x in (ng, rg, bk)]
 for _ in range(reps):
+    if os.environ.get("FO_PROF_MEMO_CLEAR", "1") == "1":  # batch-local memo, as bench.py
+        N.lib().fo_memo_clear(dg.h, None)
     if delta:
         dg.score_delta_device(d_off, d_chg, cost, st, prec)
     else:
