@@ -123,7 +123,7 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
     if (inc) {
         // incremental kernel; candidates it hands back (kRetryGeneral) take the general kernel
         const IncPlan &p = g->plan[pi];
-        IncLayout L = inc_layout(g->V, g->E, g->A, p.VB, p.P, 2 * (p.NN + 2) <= 6144);
+        IncLayout L = inc_layout(g->V, g->E, g->A, p.VB, p.P, 2 * (p.NN + 2) <= 3600);  // indegrees in smem: 7 blocks of 4 warps still fit
         int bps = score_inc_blocks_per_sm(L, precision);
         if (bps <= 0) {
             L = inc_layout(g->V, g->E, g->A, p.VB, p.P, false);

@@ -179,7 +179,8 @@ struct IncLayout {  // per-warp global scratch (byte offsets) and shared-memory 
     int64_t g_msort, g_lidx, g_zl, g_nbptr, g_nb, g_mark, g_H, g_P;
     int32_t mem_cap, pcsr_cap, mpcap;
     int32_t ring_g, ring_b;  // ready-run ring sizes (powers of two >= the nodes of each lane: no overflow)
-    int32_t s_indeg, s_pbm, s_abm, s_lbm, s_tbm, s_ppre, s_cbm, s_cnt, s_bytes;  // smem offsets (s_indeg < 0: global)
+    int32_t s_indeg, s_pbm, s_abm, s_lbm, s_tbm, s_ppre, s_cbm, s_cnt, s_bytes;  // setup kernel smem (per warp)
+    int32_t k_indeg, k_pbm, k_ppre, k_tbm, k_ring, k_bytes;  // event-loop kernel smem (k_indeg < 0: global)
     int32_t NW, CW;
 };
 constexpr int kIncMaxChg = 64, kIncMaxOps = 256, kIncMaxDirty = 192;

@@ -38,6 +38,8 @@ struct IncWork {  // setup record of a patched node, in discovery order
     int64_t bytes;
 };
 
+constexpr int kIncRingG = 256, kIncRingB = 128;  // shared-memory ready-run capacities per lane
+
 IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     IncLayout L{};
     const int NN = VB + A;
@@ -54,11 +56,9 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.dirty = take(sizeof(IncDirty) * (kIncMaxDirty + 1) + 2 * kIncMaxDirty);  // + rank -> slot map
     L.mem = take(4 * (int64_t)L.mem_cap);
     L.pcsr = take(4 * (int64_t)L.pcsr_cap);
-    L.ring_g = 1;
-    while (L.ring_g < VB) L.ring_g <<= 1;
-    L.ring_b = 1;
-    while (L.ring_b < A + 1) L.ring_b <<= 1;
-    L.ring = take(16 * ((int64_t)L.ring_g + L.ring_b));
+    L.ring_g = kIncRingG;
+    L.ring_b = kIncRingB;
+    L.ring = 0;
     L.indeg = smem_indeg ? -1 : take(2 * (int64_t)(NN + 2));
     const int64_t cap = std::min(V, kMpCapDefault);
     L.mpcap = (int)cap;
@@ -89,6 +89,13 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.s_cbm = stake(4 * L.CW);
     L.s_cnt = stake(4 * 8);
     L.s_bytes = s;
+    s = 0;
+    L.k_indeg = smem_indeg ? stake(2 * (NN + 2)) : -1;
+    L.k_pbm = stake(4 * L.NW);
+    L.k_ppre = stake(2 * L.NW + 2);
+    L.k_tbm = stake(4 * L.NW);
+    L.k_ring = stake(8 * (kIncRingG + kIncRingB));
+    L.k_bytes = s;
     return L;
 }
 
@@ -285,99 +292,112 @@ __device__ double inc_group_mp(const IncCtx &c, const GroupScratch &gs, const in
 
 extern __shared__ __align__(16) char fo_inc_smem[];  // the dynamic arena, addressed by 32-bit offsets
 
-// release of a patched node (rare): its record comes from the candidate's
-// table at its rank among the patched nodes
-__device__ __noinline__ Ent16 inc_patched_entry(const IncDirty *__restrict__ dirty, uint32_t s_ppre, unsigned t,
-                                                uint32_t w, uint32_t level) {
-    const uint16_t *ppre = (const uint16_t *)(fo_inc_smem + s_ppre);
-    const IncDirty dd = dirty[(int)ppre[t >> 5] + __popc(w & ((1u << (t & 31)) - 1u))];
-    Ent16 x;
-    x.key = level | dd.prank;
-    x.sb = dd.sb;
-    x.se = dd.se;
-    x.dur = dd.dur;
-    return x;
+// A ready entry is one u64 in a shared-memory ring: (level << 16 | prank) in
+// the high word -- the reference's (rt, tiebreak, id) order -- and the node
+// (bit 16: patched) in the low word.  The node's record (duration, successor
+// range) is read when it starts: the parent's from the L1-resident plan, a
+// patched node's from the candidate's table.
+__device__ __forceinline__ unsigned long long inc_ent(uint32_t key, unsigned t, unsigned patched) {
+    return ((unsigned long long)key << 32) | (patched << 16) | t;
 }
 
-// push into a ready run held in a ring sized for every node of its lane
-// (no overflow); keys only grow, so an append is the common case
-__device__ __forceinline__ void inc_push(Ent16 *__restrict__ buf, unsigned m, int head, int &tail, uint32_t &last,
-                                         const Ent16 &x) {
-    if (tail == head || x.key >= last) {
+// the record of a patched node (rare): the candidate's table at its rank
+__device__ __noinline__ IncDirty inc_patched_rec(const IncDirty *__restrict__ dirty, uint32_t s_pbm, uint32_t s_ppre,
+                                                 unsigned t) {
+    const uint32_t w = ((const uint32_t *)(fo_inc_smem + s_pbm))[t >> 5];
+    const uint16_t *ppre = (const uint16_t *)(fo_inc_smem + s_ppre);
+    return dirty[(int)ppre[t >> 5] + __popc(w & ((1u << (t & 31)) - 1u))];
+}
+
+// push into a ready run (sorted ring); keys only grow, so an append is the
+// common case.  false when the ring is full.
+__device__ __forceinline__ bool inc_push(unsigned long long *buf, unsigned m, int head, int &tail,
+                                         unsigned long long &last, unsigned long long x) {
+    if (tail - head > (int)m) return false;
+    if (tail == head || x >= last) {
         buf[(tail++) & m] = x;
-        last = x.key;
-        return;
+        last = x;
+        return true;
     }
     int i = tail++;
     while (i > head) {
-        const Ent16 q = buf[(i - 1) & m];
-        if (q.key <= x.key) break;
+        const unsigned long long q = buf[(i - 1) & m];
+        if (q <= x) break;
         buf[i & m] = q;
         i--;
     }
     buf[i & m] = x;
+    return true;
 }
 
 // The event loop (simulator.py:117-140) of ring_loop over the parent's
-// successor lists and the candidate's rebuilt ones; indegrees and the
-// patched bitmap in shared memory (SI: indegrees too), 32-bit addressed.
+// successor lists and the candidate's rebuilt ones.  Indegrees (SI), the
+// patched bitmap and the ready rings in shared memory, 32-bit addressed.
+// false on ring overflow.
 template <bool SI>
-__device__ __forceinline__ void inc_ring_loop(const IncPlan &p, const uint32_t *__restrict__ csucc,
-                                              const IncDirty *__restrict__ dirty, Ent16 *__restrict__ rg,
-                                              Ent16 *__restrict__ rb, unsigned mg, unsigned mb,
-                                              uint16_t *__restrict__ gindeg, uint32_t s_indeg, uint32_t s_pbm,
-                                              uint32_t s_ppre, int hg, int hb, int N, double *cost_out,
-                                              int32_t *status_out) {
+__device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *__restrict__ csucc,
+                                              const IncDirty *__restrict__ dirty, uint16_t *__restrict__ gindeg,
+                                              uint32_t s_indeg, uint32_t s_pbm, uint32_t s_ppre, uint32_t s_ring,
+                                              int hg, int hb, int N, double *cost_out, int32_t *status_out) {
     const uint32_t *__restrict__ psucc = p.succ;
     const IncNode *__restrict__ rec = p.rec;
     uint16_t *__restrict__ indeg = SI ? (uint16_t *)(fo_inc_smem + s_indeg) : gindeg;
     const uint32_t *__restrict__ pbm = (const uint32_t *)(fo_inc_smem + s_pbm);
+    unsigned long long *rg = (unsigned long long *)(fo_inc_smem + s_ring);
+    unsigned long long *rb = rg + kIncRingG;
+    constexpr unsigned mg = kIncRingG - 1, mb = kIncRingB - 1;
     const unsigned VB = (unsigned)p.VB;
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     int run0 = 0, run1 = 0;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
     double end0 = 0.0, end1 = 0.0, now = 0.0;
     uint32_t level = 0;
-    uint32_t lastg = hg > 0 ? rg[(hg - 1) & mg].key : 0u;
-    uint32_t lastb = hb > 0 ? rb[(hb - 1) & mb].key : 0u;
-    auto release = [&](unsigned qb, unsigned qe) {
+    unsigned long long lastg = hg > 0 ? rg[(hg - 1) & mg] : 0ull;
+    unsigned long long lastb = hb > 0 ? rb[(hb - 1) & mb] : 0ull;
+    auto release = [&](unsigned qb, unsigned qe) -> bool {
         const uint32_t *__restrict__ L = (qb & 0x8000u) ? csucc : psucc;
         for (unsigned q = qb & 0x7fffu; q < qe; q++) {
             const uint32_t e = L[q];
             const unsigned t = e & 0xffffu;
             const int d = indeg[t] - 1;
-            const IncNode r = rec[t];  // issued with the indegree load
             indeg[t] = (uint16_t)d;
             if (d == 0) {
-                const uint32_t w = pbm[t >> 5];
-                Ent16 x;
-                if ((w >> (t & 31)) & 1u) {
-                    x = inc_patched_entry(dirty, s_ppre, t, w, level);
-                } else {
-                    x.key = level | r.prank;
-                    x.sb = r.sb;
-                    x.se = r.se;
-                    x.dur = r.dur;
-                }
-                if (t < VB) inc_push(rg, mg, headg, tailg, lastg, x);
-                else inc_push(rb, mb, headb, tailb, lastb, x);
+                const unsigned pt = (pbm[t >> 5] >> (t & 31)) & 1u;
+                // the parent's rank travels in the successor entry; a patched node's is its own
+                const uint32_t pr = pt ? inc_patched_rec(dirty, s_pbm, s_ppre, t).prank : (e >> 16);
+                const unsigned long long x = inc_ent(level | pr, t, pt);
+                if (!(t < VB ? inc_push(rg, mg, headg, tailg, lastg, x) : inc_push(rb, mb, headb, tailb, lastb, x)))
+                    return false;
             }
+        }
+        return true;
+    };
+    auto node_rec = [&](unsigned long long x, double &dur, unsigned &sb, unsigned &se) {
+        const unsigned t = (unsigned)x & 0xffffu;
+        if (x & 0x10000ull) {
+            const IncDirty r = inc_patched_rec(dirty, s_pbm, s_ppre, t);
+            dur = r.dur;
+            sb = r.sb;
+            se = r.se;
+        } else {
+            const IncNode r = rec[t];
+            dur = r.dur;
+            sb = r.sb;
+            se = r.se;
         }
     };
     auto start = [&]() {
         if (!run0 && headg < tailg) {
-            const Ent16 x = rg[(headg++) & mg];
+            double d;
+            node_rec(rg[(headg++) & mg], d, sb0, se0);
             run0 = 1;
-            end0 = __dadd_rn(now, x.dur);
-            sb0 = x.sb;
-            se0 = x.se;
+            end0 = __dadd_rn(now, d);
         }
         if (!run1 && headb < tailb) {
-            const Ent16 x = rb[(headb++) & mb];
+            double d;
+            node_rec(rb[(headb++) & mb], d, sb1, se1);
             run1 = 1;
-            end1 = __dadd_rn(now, x.dur);
-            sb1 = x.sb;
-            se1 = x.se;
+            end1 = __dadd_rn(now, d);
         }
     };
     start();
@@ -386,19 +406,26 @@ __device__ __forceinline__ void inc_ring_loop(const IncPlan &p, const uint32_t *
         const bool c1 = run1 && (!run0 || end1 <= end0);
         const double t = c0 ? end0 : end1;
         if (t > now) { now = t; level += 0x10000u; }
-        if (c0) { run0 = 0; release(sb0, se0); }
-        if (c1) { run1 = 0; release(sb1, se1); }
+        if (c0) {
+            run0 = 0;
+            if (!release(sb0, se0)) return false;
+        }
+        if (c1) {
+            run1 = 0;
+            if (!release(sb1, se1)) return false;
+        }
         start();
     }
     const int done = headg + headb;
     *cost_out = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
     *status_out = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
+    return true;
 }
 
 // insert one ready entry into a level-0 run (kept sorted by key)
-__device__ __forceinline__ void inc_ring_insert(Ent16 *buf, unsigned m, int &tail, const Ent16 &x) {
-    uint32_t last = tail > 0 ? buf[(tail - 1) & m].key : 0u;
-    inc_push(buf, m, 0, tail, last, x);
+__device__ __forceinline__ bool inc_ring_insert(unsigned long long *buf, unsigned m, int &tail, unsigned long long x) {
+    unsigned long long last = tail > 0 ? buf[(tail - 1) & m] : 0ull;
+    return inc_push(buf, m, 0, tail, last, x);
 }
 
 template <typename T>
@@ -760,8 +787,8 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc(const __grid_
 }
 
 // K3 of the same candidates: the candidate's indegrees (the parent's, minus
-// removed, plus added slots) and patched-node ranks in shared memory, the
-// level-0 ready runs, then the event loop on one lane.
+// removed, plus added slots), the patched-node ranks and the ready rings in
+// shared memory, the level-0 ready runs, then the event loop on one lane.
 template <bool SI>
 __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __grid_constant__ IncArgs a, int k0) {
     const int lane = threadIdx.x & 31;
@@ -770,111 +797,111 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
     if (k >= a.K || a.status_out[k] != kIncPending) return;
     const IncLayout &L = a.L;
     const IncPlan &p = a.p;
-    const uint32_t warp_sm = (uint32_t)((threadIdx.x >> 5) * L.s_bytes);
-    char *sm = fo_inc_smem + warp_sm;
-    const IncCtx c = inc_ctx(a, wid, sm);
-    const int nd = c.hdr[0], nrem = c.hdr[1], nadd = c.hdr[2], N = c.hdr[3];
+    const uint32_t wsm = (uint32_t)((threadIdx.x >> 5) * L.k_bytes);
+    char *wsb = a.ws + (int64_t)wid * L.total;
+    const int *hdr = (const int *)(wsb + L.hdr);
+    const int nd = hdr[0], nrem = hdr[1], nadd = hdr[2], N = hdr[3];
+    const int *dn = (const int *)(wsb + L.dn);
+    const int4 *rem = (const int4 *)(wsb + L.rem);
+    const int2 *add = (const int2 *)(wsb + L.add);
+    const IncDirty *dirty = (const IncDirty *)(wsb + L.dirty);
+    const uint32_t *pcsr = (const uint32_t *)(wsb + L.pcsr);
+    uint16_t *indeg = SI ? (uint16_t *)(fo_inc_smem + wsm + L.k_indeg) : (uint16_t *)(wsb + L.indeg);
+    uint32_t *pbm = (uint32_t *)(fo_inc_smem + wsm + L.k_pbm);
+    uint16_t *ppre = (uint16_t *)(fo_inc_smem + wsm + L.k_ppre);
+    uint32_t *tbm = (uint32_t *)(fo_inc_smem + wsm + L.k_tbm);
+    unsigned long long *rg = (unsigned long long *)(fo_inc_smem + wsm + L.k_ring), *rb = rg + kIncRingG;
     const int NN = p.NN, VB = p.VB;
-    for (int i = lane; i < L.NW; i += 32) { c.pbm[i] = 0; c.tbm[i] = 0; }
+    for (int i = lane; i < L.NW; i += 32) { pbm[i] = 0; tbm[i] = 0; }
     __syncwarp();
     for (int s = lane; s < nd; s += 32) {
-        const int n = c.dn[s];
-        atomicOr(&c.pbm[n >> 5], 1u << (n & 31));
+        const int n = dn[s];
+        atomicOr(&pbm[n >> 5], 1u << (n & 31));
     }
     __syncwarp();
     {
         int carry = 0;
         for (int base = 0; base < L.NW; base += 32) {
             const int i = base + lane;
-            const int x = i < L.NW ? __popc(c.pbm[i]) : 0;
+            const int x = i < L.NW ? __popc(pbm[i]) : 0;
             int v = x;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int y = __shfl_up_sync(FULL, v, d);
                 if (lane >= d) v += y;
             }
-            if (i < L.NW) c.ppre[i] = (uint16_t)(carry + v - x);
+            if (i < L.NW) ppre[i] = (uint16_t)(carry + v - x);
             carry += __shfl_sync(FULL, v, 31);
         }
     }
     {
         const uint32_t *src = (const uint32_t *)p.indeg;
-        uint32_t *dst = (uint32_t *)c.indeg;
+        uint32_t *dst = (uint32_t *)indeg;
         for (int i = lane; i < (NN + 1) / 2; i += 32) dst[i] = __ldg(&src[i]);
     }
     __syncwarp();
     for (int i = lane; i < nrem; i += 32) {
-        const int t = c.rem[i].z;
-        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0xffff0000u : 0xffffffffu);
-        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
+        const int t = rem[i].z;
+        atomicAdd((unsigned *)indeg + (t >> 1), (t & 1) ? 0xffff0000u : 0xffffffffu);
+        atomicOr(&tbm[t >> 5], 1u << (t & 31));
     }
     for (int i = lane; i < nadd; i += 32) {
-        const int t = c.add[i].y;
-        atomicAdd((unsigned *)c.indeg + (t >> 1), (t & 1) ? 0x10000u : 1u);
-        atomicOr(&c.tbm[t >> 5], 1u << (t & 31));
+        const int t = add[i].y;
+        atomicAdd((unsigned *)indeg + (t >> 1), (t & 1) ? 0x10000u : 1u);
+        atomicOr(&tbm[t >> 5], 1u << (t & 31));
     }
     __syncwarp();
-    for (int i = lane; i < L.NW; i += 32) c.tbm[i] |= c.pbm[i];
+    for (int i = lane; i < L.NW; i += 32) tbm[i] |= pbm[i];
     __syncwarp();
     // level-0 ready runs: the parent's (sorted by rank) without touched nodes,
     // then the touched nodes that are ready, inserted in rank order
-    Ent16 *rg = c.ring, *rbk = c.ring + L.ring_g;
-    const unsigned mg = (unsigned)L.ring_g - 1u, mbk = (unsigned)L.ring_b - 1u;
     int hgb[2] = {0, 0};
+    bool over = false;
     for (int lanei = 0; lanei < 2; lanei++) {
         const uint16_t *src = p.ready + (lanei ? p.n_ready_g : 0);
         const int n0 = lanei ? p.n_ready_b : p.n_ready_g;
-        Ent16 *buf = lanei ? rbk : rg;
+        unsigned long long *buf = lanei ? rb : rg;
+        const int cap = lanei ? kIncRingB : kIncRingG;
         int h = 0;
         for (int base = 0; base < n0; base += 32) {
             const int i = base + lane;
             const int n = i < n0 ? src[i] : 0;
-            const bool keep = i < n0 && !ibit(c.tbm, n);
+            const bool keep = i < n0 && !((tbm[n >> 5] >> (n & 31)) & 1u);
             const unsigned m = __ballot_sync(FULL, keep);
             const int pos = h + __popc(m & lanemask_lt());
-            if (keep) {
-                const IncNode r = p.rec[n];
-                Ent16 x;
-                x.key = r.prank;
-                x.sb = r.sb;
-                x.se = r.se;
-                x.dur = r.dur;
-                buf[pos] = x;
-            }
+            if (keep && pos < cap) buf[pos] = inc_ent(p.rec[n].prank, n, 0);
             h += __popc(m);
         }
         hgb[lanei] = h;
+        over |= h > cap;
     }
     __syncwarp();
     if (lane != 0) return;
-    for (int wi = 0; wi < L.NW; wi++) {
-        uint32_t m = c.tbm[wi];
-        while (m) {
+    for (int wi = 0; wi < L.NW && !over; wi++) {
+        uint32_t m = tbm[wi];
+        while (m && !over) {
             const int n = wi * 32 + __ffs(m) - 1;
             m &= m - 1;
-            if (n >= NN || c.indeg[n] != 0) continue;
-            Ent16 x;
-            if (ibit(c.pbm, n)) {
-                const IncDirty dd = c.dirty[irank(c, n)];
+            if (n >= NN || indeg[n] != 0) continue;
+            unsigned long long x;
+            if ((pbm[n >> 5] >> (n & 31)) & 1u) {
+                const IncDirty dd = dirty[(int)ppre[n >> 5] + __popc(pbm[n >> 5] & ((1u << (n & 31)) - 1u))];
                 if (!dd.exists) continue;
-                x.key = dd.prank;
-                x.sb = dd.sb;
-                x.se = dd.se;
-                x.dur = dd.dur;
+                x = inc_ent(dd.prank, n, 1);
             } else {
                 const IncNode r = p.rec[n];
                 if (!r.exists) continue;
-                x.key = r.prank;
-                x.sb = r.sb;
-                x.se = r.se;
-                x.dur = r.dur;
+                x = inc_ent(r.prank, n, 0);
             }
-            if (n < VB) inc_ring_insert(rg, mg, hgb[0], x);
-            else inc_ring_insert(rbk, mbk, hgb[1], x);
+            over = !(n < VB ? inc_ring_insert(rg, kIncRingG - 1, hgb[0], x) : inc_ring_insert(rb, kIncRingB - 1, hgb[1], x));
         }
     }
-    inc_ring_loop<SI>(p, c.pcsr, c.dirty, rg, rbk, mg, mbk, SI ? nullptr : c.indeg, warp_sm + L.s_indeg,
-                      warp_sm + L.s_pbm, warp_sm + L.s_ppre, hgb[0], hgb[1], N, a.cost_out + k, a.status_out + k);
+    if (over || !inc_ring_loop<SI>(p, pcsr, dirty, SI ? nullptr : indeg, wsm + L.k_indeg, wsm + L.k_pbm,
+                                   wsm + L.k_ppre, wsm + L.k_ring, hgb[0], hgb[1], N, a.cost_out + k,
+                                   a.status_out + k)) {
+        a.cost_out[k] = 0.0;
+        a.status_out[k] = kRetryGeneral;  // a ready run outgrew its ring: the general kernel scores it
+    }
 }
 
 template <typename KF>
@@ -885,20 +912,20 @@ static int inc_occ(KF kf, int smem_per_block) {
     return n;
 }
 template <typename T>
-static int inc_blocks_per_sm_q(int smem_per_block) {
-    return std::min({inc_occ(score_kernel_inc<T>, smem_per_block), inc_occ(score_kernel_inc_k3<true>, smem_per_block),
-                     inc_occ(score_kernel_inc_k3<false>, smem_per_block)});
+static int inc_blocks_per_sm_q(int setup_smem, int k3_smem) {
+    return std::min({inc_occ(score_kernel_inc<T>, setup_smem), inc_occ(score_kernel_inc_k3<true>, k3_smem),
+                     inc_occ(score_kernel_inc_k3<false>, k3_smem)});
 }
 
 int score_inc_blocks_per_sm(const IncLayout &L, int precision) {
     static std::mutex mu;
     static std::map<std::pair<int, int>, int> cache;
-    const std::pair<int, int> key(L.s_bytes, precision);
+    const std::pair<int, int> key(L.s_bytes * 65536 + L.k_bytes, precision);
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
-    const int n = precision == FO_PREC_FP64 ? inc_blocks_per_sm_q<double>(L.s_bytes * kWarps)
-                                            : inc_blocks_per_sm_q<float>(L.s_bytes * kWarps);
+    const int n = precision == FO_PREC_FP64 ? inc_blocks_per_sm_q<double>(L.s_bytes * kWarps, L.k_bytes * kWarps)
+                                            : inc_blocks_per_sm_q<float>(L.s_bytes * kWarps, L.k_bytes * kWarps);
     cache[key] = n;
     return n;
 }
@@ -923,8 +950,9 @@ cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout 
         if (precision == FO_PREC_FP64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a, k0);
         else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a, k0);
         if (a.stop_after == 0) {
-            if (L.s_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, smem, stream>>>(a, k0);
-            else score_kernel_inc_k3<false><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+            const size_t ksmem = (size_t)L.k_bytes * kWarps;
+            if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
+            else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
         }
     }
     return cudaGetLastError();
