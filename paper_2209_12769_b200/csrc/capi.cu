@@ -137,9 +137,21 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
             g->d_ws_inc = nullptr;
             g->ws_inc_bytes = 0;
             CUDA_TRY(cudaMalloc(&g->d_ws_inc, need));
+            // member marks of the estimator kernel start at -1 (every byte 0xff)
+            CUDA_TRY(cudaMemset(g->d_ws_inc, 0xff, need));
             g->ws_inc_bytes = need;
         }
-        cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid, cost, status, stream);
+        const int qcap = kIncQueuePerCand * std::min(K, grid * warps);
+        const size_t qneed = 64 + (size_t)qcap * 32;
+        if (qneed > g->inc_q_bytes) {
+            if (g->d_inc_q) CUDA_TRY(cudaFree(g->d_inc_q));
+            g->d_inc_q = nullptr;
+            g->inc_q_bytes = 0;
+            CUDA_TRY(cudaMalloc(&g->d_inc_q, qneed));
+            g->inc_q_bytes = qneed;
+        }
+        cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid,
+                                         (IncQ *)((char *)g->d_inc_q + 64), (int *)g->d_inc_q, qcap, cost, status, stream);
         g_launches++;
         if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("incremental score launch: ") + cudaGetErrorString(e));
         if (g->delta_mode == 2) return FO_OK;  // diagnostic: hand-backs stay visible as status 101
@@ -303,6 +315,7 @@ int fo_graph_destroy(fo_graph *g) {
     for (void *pl : g->d_plan)
         if (pl) cudaFree(pl);
     if (g->d_ws_inc) cudaFree(g->d_ws_inc);
+    if (g->d_inc_q) cudaFree(g->d_inc_q);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     for (auto &sl : g->aslot) {
         if (sl.done) cudaEventSynchronize(sl.done);

@@ -187,9 +187,11 @@ constexpr int kIncMaxChg = 64, kIncMaxOps = 256, kIncMaxDirty = 192;
 constexpr int kRetryGeneral = 101;  // internal status: the incremental kernel hands the candidate to score_kernel
 constexpr int kIncPending = 102;    // internal status: set up, waiting for the event-loop kernel
 IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg);
+struct IncQ;
 cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
-                             const int32_t *chg, int K, int precision, char *ws, int grid, double *cost_out,
-                             int32_t *status_out, cudaStream_t stream);
+                             const int32_t *chg, int K, int precision, char *ws, int grid, IncQ *queue, int *qcount,
+                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream);
+constexpr int kIncQueuePerCand = kIncMaxDirty;  // estimator queue entries per candidate: never full (a claimed memo slot always gets its value)
 int score_inc_blocks_per_sm(const IncLayout &L, int precision);
 
 cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, int64_t id_offset, double *out,
@@ -252,6 +254,8 @@ struct fo_graph {
     int plan_ok[2] = {0, 0};
     char *d_ws_inc = nullptr;
     size_t ws_inc_bytes = 0;
+    void *d_inc_q = nullptr;  // estimator queue (IncQ entries) + its counter
+    size_t inc_q_bytes = 0;
     int delta_mode = 1;  // 1: incremental kernel when the plan allows it; 0: general kernel only
     std::mutex mu;
 };

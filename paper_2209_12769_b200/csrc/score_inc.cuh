@@ -99,11 +99,23 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     return L;
 }
 
+struct IncQ {  // a member set queued for the estimator kernel
+    const int *mem;  // ascending op indices, in the queuing warp's scratch
+    int32_t slot;    // memo slot receiving the prediction, or -1: .v
+    int32_t n;
+    double v;
+    int64_t pad;
+};
+
 struct IncArgs {
     DGraph g;
     IncPlan p;
     IncLayout L;
     const int32_t *doff, *dchg;
+    IncQ *queue;
+    int *qcount;
+    int qcap;
+    MemoEnt *memo;  // this precision's memo table, or nullptr (memo off)
     int K;
     char *ws;
     double *cost_out;
@@ -225,69 +237,6 @@ __device__ void iar_slot(const IncCtx &c, int a) {
 __device__ __forceinline__ int irank(const IncCtx &c, int n) {
     const uint32_t w = c.pbm[n >> 5];
     return (int)c.ppre[n >> 5] + __popc(w & ((1u << (n & 31)) - 1u));
-}
-
-// MP prediction of one patched fused group (members ascending), warp-wide:
-// memo, member-local undirected neighbour lists over the candidate's
-// membership (estimator.py:173-177, :348-355), mp_forward
-template <typename T>
-__device__ double inc_group_mp(const IncCtx &c, const GroupScratch &gs, const int *mem, int n, int gid, int lane) {
-    const DGraph &g = c.a->g;
-    MemoEnt *memo = g.memo[sizeof(T) == 8];
-    unsigned long long mh1 = 0, mh2 = 0;
-    if (memo) {
-        set_hash(mem, n, lane, mh1, mh2);
-        double mv = 0.0;
-        bool hit = false;
-        if (lane == 0) hit = memo_get(memo, g.memo_mask, mh1, mh2, &mv);
-        hit = __shfl_sync(FULL, hit, 0);
-        if (hit) return __shfl_sync(FULL, mv, 0);
-    }
-    for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = i;
-    __syncwarp();
-    for (int i = lane; i < n; i += 32) {
-        const int v = mem[i];
-        gs.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
-    }
-    __syncwarp();
-    warp_exscan(gs.zl, gs.nbptr, n, lane);
-    for (int i = lane; i < n; i += 32) {
-        const int v = mem[i];
-        const int o = gs.nbptr[i];
-        int cc = 0;
-        for (int q = g.in_ptr[v]; q < g.in_ptr[v + 1]; q++) {
-            const int s = g.e_src[g.in_e[q]];
-            if (inn(c, s) != gid && irr(c, s) != gid) continue;
-            const int j = gs.lidx[s];
-            bool dup = false;
-            for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
-            if (!dup) gs.nb[o + cc++] = j;
-        }
-        for (int q = g.out_ptr[v]; q < g.out_ptr[v + 1]; q++) {
-            const int d = g.e_dst[g.out_e[q]];
-            if (inn(c, d) != gid && irr(c, d) != gid) continue;
-            const int j = gs.lidx[d];
-            bool dup = false;
-            for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
-            if (!dup) gs.nb[o + cc++] = j;
-        }
-        gs.msort[i] = cc;
-    }
-    __syncwarp();
-    if (lane == 0) {  // compact rows into a dense CSR
-        int o = 0;
-        for (int i = 0; i < n; i++) {
-            const int s0 = gs.nbptr[i], cc = gs.msort[i];
-            for (int t = 0; t < cc; t++) gs.nb[o + t] = gs.nb[s0 + t];
-            gs.nbptr[i] = o;
-            o += cc;
-        }
-        gs.nbptr[n] = o;
-    }
-    __syncwarp();
-    const double pred = mp_forward<T>(g, mem, n, gs.nbptr, gs.nb, (T *)gs.H, (T *)gs.P, lane);
-    if (lane == 0 && memo) memo_put(memo, g.memo_mask, mh1, mh2, pred);
-    return pred;
 }
 
 extern __shared__ __align__(16) char fo_inc_smem[];  // the dynamic arena, addressed by 32-bit offsets
@@ -426,6 +375,34 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
 __device__ __forceinline__ bool inc_ring_insert(unsigned long long *buf, unsigned m, int &tail, unsigned long long x) {
     unsigned long long last = tail > 0 ? buf[(tail - 1) & m] : 0ull;
     return inc_push(buf, m, 0, tail, last, x);
+}
+
+// Look a member set up in the memo and claim a slot when it is new (the
+// prediction is filled in later by the estimator kernel).  -1: no slot along
+// the probe sequence (the set is queued privately).
+__device__ int memo_claim(MemoEnt *t, unsigned mask, unsigned long long h1, unsigned long long h2, bool *is_new) {
+    for (int q = 0; q < kMemoProbe; q++) {
+        const unsigned i = (unsigned)(h1 + q) & mask;
+        MemoEnt *e = &t[i];
+        unsigned long long k = atomicCAS(&e->k1, 0ull, 2ull);
+        if (k == 0) {
+            e->k2 = h2;
+            e->v = __longlong_as_double(0x7ff8000000000000ll);
+            __threadfence();
+            atomicExch(&e->k1, h1);
+            *is_new = true;
+            return (int)i;
+        }
+        while (k == 2) k = *(volatile unsigned long long *)&e->k1;  // another warp is writing its key
+        if (k == h1) {
+            __threadfence();
+            if (*(volatile unsigned long long *)&e->k2 == h2) {
+                *is_new = false;
+                return (int)i;
+            }
+        }
+    }
+    return -1;
 }
 
 template <typename T>
@@ -684,20 +661,46 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
     exist_delta = __reduce_add_sync(FULL, exist_delta);
     __syncwarp();
     if (c.cnt[kCFail]) { retry(); return; }
-    if (a.stop_after == 1) {
-        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
-        return;
-    }
-    // ---- K2: the patched fused groups (MP forward, memoised), whole warp each
+    // ---- K2 registration.  The MP prediction is a function of the member set
+    // alone (estimator.py:167-177: per-op features, member-internal edges), so
+    // each patched fused group's set is looked up in the memo; new sets are
+    // queued and the estimator kernel runs one warp per queued set.  The
+    // record holds the memo slot (>= 0) or -(queue index) - 1 until K3.
     for (int r = 0; r < nd; r++) {
         if (!c.dirty[r].fused) continue;
-        const int s = c.r2s[r];
-        const IncWork wk = c.work[s];
-        const double pred = inc_group_mp<T>(c, gs, c.mem + wk.mb, wk.cnt, wk.node, lane);
-        if (lane == 0) c.dirty[r].dur = pred;
+        const IncWork wk = c.work[c.r2s[r]];
+        const int *mem = c.mem + wk.mb;
+        const int n = wk.cnt;
+        bool miss = false;
+        for (int i = lane; i < n; i += 32) miss |= isnan(g.op_prof[mem[i]]);  // MissingCost (estimator.py:170)
+        if (__any_sync(FULL, miss)) { ifail(c); break; }
+        unsigned long long h1 = 0, h2 = 0;
+        if (a.memo) set_hash(mem, n, lane, h1, h2);
+        if (lane == 0) {
+            bool fresh = true;
+            const int slot = a.memo ? memo_claim(a.memo, g.memo_mask, h1, h2, &fresh) : -1;
+            long long ref = slot;
+            if (fresh || slot < 0) {
+                const int qi = atomicAdd(a.qcount, 1);
+                if (qi >= a.qcap) ifail(c);
+                else {
+                    IncQ q;
+                    q.mem = mem;
+                    q.slot = slot;
+                    q.n = n;
+                    q.v = 0.0;
+                    q.pad = 0;
+                    a.queue[qi] = q;
+                    if (slot < 0) ref = -(long long)qi - 1;
+                }
+            }
+            c.dirty[r].dur = __longlong_as_double(ref);
+        }
         __syncwarp();
     }
-    if (a.stop_after == 2) {
+    __syncwarp();
+    if (c.cnt[kCFail]) { retry(); return; }
+    if (a.stop_after == 1) {
         if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
         return;
     }
@@ -786,6 +789,76 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc(const __grid_
     score_one_inc<T>(a, k, c, gs, lane);
 }
 
+// K2: the estimator over the queued member sets, one warp per set.  Member
+// marks (lidx: local index, -1 outside) give the member-local undirected
+// neighbour lists in the general kernel's order (in-edges, then out-edges,
+// estimator.py:173-177, :348-355), then mp_forward (estimator.py:363-389).
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __grid_constant__ IncArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int nw = gridDim.x * kWarps;
+    const DGraph &g = a.g;
+    const IncLayout &L = a.L;
+    char *gb = a.ws + (int64_t)wid * L.total + L.gs0;
+    const GroupScratch gs{(int *)(gb + L.g_msort), (int *)(gb + L.g_lidx), (int *)(gb + L.g_zl),
+                          (int *)(gb + L.g_nbptr), (int *)(gb + L.g_nb), (int *)(gb + L.g_mark),
+                          gb + L.g_H, gb + L.g_P};
+    const int nq = min(*a.qcount, a.qcap);
+    for (int qi = wid; qi < nq; qi += nw) {
+        const IncQ q = a.queue[qi];
+        const int *mem = q.mem;
+        const int n = q.n;
+        for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = i;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) {
+            const int v = mem[i];
+            gs.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
+        }
+        __syncwarp();
+        warp_exscan(gs.zl, gs.nbptr, n, lane);
+        for (int i = lane; i < n; i += 32) {
+            const int v = mem[i];
+            const int o = gs.nbptr[i];
+            int cc = 0;
+            for (int e = g.in_ptr[v]; e < g.in_ptr[v + 1]; e++) {
+                const int j = gs.lidx[g.e_src[g.in_e[e]]];
+                if (j < 0) continue;
+                bool dup = false;
+                for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
+                if (!dup) gs.nb[o + cc++] = j;
+            }
+            for (int e = g.out_ptr[v]; e < g.out_ptr[v + 1]; e++) {
+                const int j = gs.lidx[g.e_dst[g.out_e[e]]];
+                if (j < 0) continue;
+                bool dup = false;
+                for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
+                if (!dup) gs.nb[o + cc++] = j;
+            }
+            gs.msort[i] = cc;
+        }
+        __syncwarp();
+        if (lane == 0) {  // compact rows into a dense CSR
+            int o = 0;
+            for (int i = 0; i < n; i++) {
+                const int s0 = gs.nbptr[i], cc = gs.msort[i];
+                for (int t = 0; t < cc; t++) gs.nb[o + t] = gs.nb[s0 + t];
+                gs.nbptr[i] = o;
+                o += cc;
+            }
+            gs.nbptr[n] = o;
+        }
+        __syncwarp();
+        const double pred = mp_forward<T>(g, mem, n, gs.nbptr, gs.nb, (T *)gs.H, (T *)gs.P, lane);
+        if (lane == 0) {
+            if (q.slot >= 0) a.memo[q.slot].v = pred;
+            else a.queue[qi].v = pred;
+        }
+        for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = -1;
+        __syncwarp();
+    }
+}
+
 // K3 of the same candidates: the candidate's indegrees (the parent's, minus
 // removed, plus added slots), the patched-node ranks and the ready rings in
 // shared memory, the level-0 ready runs, then the event loop on one lane.
@@ -812,6 +885,17 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
     uint32_t *tbm = (uint32_t *)(fo_inc_smem + wsm + L.k_tbm);
     unsigned long long *rg = (unsigned long long *)(fo_inc_smem + wsm + L.k_ring), *rb = rg + kIncRingG;
     const int NN = p.NN, VB = p.VB;
+    if (a.stop_after == 2) {  // phase timing only (fo_set_phase_stop)
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
+        return;
+    }
+    // durations of patched fused groups, computed by the estimator kernel
+    for (int r = lane; r < nd; r += 32) {
+        IncDirty &dd = ((IncDirty *)dirty)[r];
+        if (!dd.fused) continue;
+        const long long ref = __double_as_longlong(dd.dur);
+        dd.dur = ref >= 0 ? a.memo[ref].v : a.queue[-ref - 1].v;
+    }
     for (int i = lane; i < L.NW; i += 32) { pbm[i] = 0; tbm[i] = 0; }
     __syncwarp();
     for (int s = lane; s < nd; s += 32) {
@@ -931,29 +1015,36 @@ int score_inc_blocks_per_sm(const IncLayout &L, int precision) {
 }
 
 cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
-                             const int32_t *chg, int K, int precision, char *ws, int grid, double *cost_out,
-                             int32_t *status_out, cudaStream_t stream) {
+                             const int32_t *chg, int K, int precision, char *ws, int grid, IncQ *queue, int *qcount,
+                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream) {
     IncArgs a;
     a.g = g;
     a.p = p;
     a.L = L;
     a.doff = off;
     a.dchg = chg;
+    a.queue = queue;
+    a.qcount = qcount;
+    a.qcap = qcap;
+    a.memo = g.memo[precision == FO_PREC_FP64 ? 1 : 0];
     a.K = K;
     a.ws = ws;
     a.cost_out = cost_out;
     a.status_out = status_out;
     a.stop_after = g.phase_stop;
-    const size_t smem = (size_t)L.s_bytes * kWarps;
-    const int per_launch = grid * kWarps;  // one candidate per warp per launch pair
+    const size_t smem = (size_t)L.s_bytes * kWarps, ksmem = (size_t)L.k_bytes * kWarps;
+    const int per_launch = grid * kWarps;  // one candidate per warp per launch
+    const bool fp64 = precision == FO_PREC_FP64;
     for (int k0 = 0; k0 < K; k0 += per_launch) {
-        if (precision == FO_PREC_FP64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+        cudaError_t e = cudaMemsetAsync(qcount, 0, sizeof(int), stream);
+        if (e != cudaSuccess) return e;
+        if (fp64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a, k0);
         else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a, k0);
-        if (a.stop_after == 0) {
-            const size_t ksmem = (size_t)L.k_bytes * kWarps;
-            if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
-            else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
-        }
+        if (a.stop_after == 1) continue;
+        if (fp64) score_kernel_inc_mp<double><<<grid, kWarps * 32, 0, stream>>>(a);
+        else score_kernel_inc_mp<float><<<grid, kWarps * 32, 0, stream>>>(a);
+        if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
+        else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
     }
     return cudaGetLastError();
 }
