@@ -142,7 +142,7 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
             g->ws_inc_bytes = need;
         }
         const int qcap = kIncQueuePerCand * std::min(K, grid * warps);
-        const size_t qneed = 64 + (size_t)qcap * 32;
+        const size_t qneed = 64 + (size_t)qcap * 48;
         if (qneed > g->inc_q_bytes) {
             if (g->d_inc_q) CUDA_TRY(cudaFree(g->d_inc_q));
             g->d_inc_q = nullptr;

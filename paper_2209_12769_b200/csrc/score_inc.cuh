@@ -36,6 +36,7 @@ struct IncDirty {  // a patched node of one candidate (sorted by node id)
 struct IncWork {  // setup record of a patched node, in discovery order
     int32_t node, cnt, mn, mb, me, pad;
     int64_t bytes;
+    unsigned long long h1, h2;  // member-set hash of a fused group (the memo key)
 };
 
 constexpr int kIncRingG = 256, kIncRingB = 128;  // shared-memory ready-run capacities per lane
@@ -101,9 +102,10 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
 
 struct IncQ {  // a member set queued for the estimator kernel
     const int *mem;  // ascending op indices, in the queuing warp's scratch
-    int32_t slot;    // memo slot receiving the prediction, or -1: .v
+    int32_t slot;    // memo slot that also receives the prediction, or -1
     int32_t n;
-    double v;
+    double v;        // the prediction (read by the queuing candidate)
+    unsigned long long h1, h2;  // the set's memo key
     int64_t pad;
 };
 
@@ -666,37 +668,56 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
     // each patched fused group's set is looked up in the memo; new sets are
     // queued and the estimator kernel runs one warp per queued set.  The
     // record holds the memo slot (>= 0) or -(queue index) - 1 until K3.
-    for (int r = 0; r < nd; r++) {
-        if (!c.dirty[r].fused) continue;
-        const IncWork wk = c.work[c.r2s[r]];
-        const int *mem = c.mem + wk.mb;
-        const int n = wk.cnt;
-        bool miss = false;
-        for (int i = lane; i < n; i += 32) miss |= isnan(g.op_prof[mem[i]]);  // MissingCost (estimator.py:170)
-        if (__any_sync(FULL, miss)) { ifail(c); break; }
-        unsigned long long h1 = 0, h2 = 0;
-        if (a.memo) set_hash(mem, n, lane, h1, h2);
-        if (lane == 0) {
-            bool fresh = true;
-            const int slot = a.memo ? memo_claim(a.memo, g.memo_mask, h1, h2, &fresh) : -1;
-            long long ref = slot;
-            if (fresh || slot < 0) {
-                const int qi = atomicAdd(a.qcount, 1);
-                if (qi >= a.qcap) ifail(c);
-                else {
-                    IncQ q;
-                    q.mem = mem;
-                    q.slot = slot;
-                    q.n = n;
-                    q.v = 0.0;
-                    q.pad = 0;
-                    a.queue[qi] = q;
-                    if (slot < 0) ref = -(long long)qi - 1;
-                }
+    // One lane per fused group: every lookup of the candidate is in flight at once.
+    for (int r0 = 0; r0 < nd; r0 += 32) {
+        const int r = r0 + lane;
+        bool mine = r < nd && c.dirty[r].fused;
+        int slot = -1;
+        bool fresh = true;
+        if (mine) {
+            const int ws = c.r2s[r];
+            const IncWork wk = c.work[ws];
+            const int *mem = c.mem + wk.mb;
+            unsigned long long s1 = 0, s2 = 0;
+            bool miss = false;
+            for (int i = 0; i < wk.cnt; i++) {  // set_hash's two commutative sums, one lane
+                const int m = mem[i];
+                miss |= isnan(g.op_prof[m]);  // MissingCost (estimator.py:170): the general path reports it
+                s1 += smix((unsigned long long)m * 2 + 1);
+                s2 += smix(((unsigned long long)m << 32) ^ 0x5bd1e995ull);
             }
-            c.dirty[r].dur = __longlong_as_double(ref);
+            if (miss) ifail(c);
+            const unsigned long long h1 = smix(s1 + (unsigned long long)wk.cnt) | 1ull;
+            const unsigned long long h2 = smix(s2 ^ ((unsigned long long)wk.cnt * 0xff51afd7ed558ccdull));
+            c.work[ws].h1 = h1;
+            c.work[ws].h2 = h2;
+            if (a.memo) slot = memo_claim(a.memo, g.memo_mask, h1, h2, &fresh);
         }
-        __syncwarp();
+        // new sets are queued (one atomic per warp); a memo hit keeps its slot
+        const bool q = mine && (fresh || slot < 0);
+        const unsigned qm = __ballot_sync(FULL, q);
+        int qbase = 0;
+        if (qm && lane == __ffs(qm) - 1) qbase = atomicAdd(a.qcount, __popc(qm));
+        qbase = __shfl_sync(FULL, qbase, __ffs(qm | 1u) - 1);
+        if (q) {
+            const int qi = qbase + __popc(qm & lanemask_lt());
+            if (qi >= a.qcap) ifail(c);
+            else {
+                const IncWork wk = c.work[c.r2s[r]];
+                IncQ e;
+                e.mem = c.mem + wk.mb;
+                e.slot = slot;
+                e.n = wk.cnt;
+                e.v = 0.0;
+                e.h1 = wk.h1;
+                e.h2 = wk.h2;
+                e.pad = 0;
+                a.queue[qi] = e;
+                c.dirty[r].dur = __longlong_as_double(-(long long)qi - 1);
+            }
+        } else if (mine) {
+            c.dirty[r].dur = __longlong_as_double((long long)slot);
+        }
     }
     __syncwarp();
     if (c.cnt[kCFail]) { retry(); return; }
@@ -851,8 +872,9 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __gr
         __syncwarp();
         const double pred = mp_forward<T>(g, mem, n, gs.nbptr, gs.nb, (T *)gs.H, (T *)gs.P, lane);
         if (lane == 0) {
-            if (q.slot >= 0) a.memo[q.slot].v = pred;
-            else a.queue[qi].v = pred;
+            a.queue[qi].v = pred;  // the queuing candidate reads this
+            if (q.slot >= 0 && a.memo[q.slot].k1 == q.h1 && a.memo[q.slot].k2 == q.h2)
+                a.memo[q.slot].v = pred;  // later hits read the memo
         }
         for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = -1;
         __syncwarp();
@@ -889,12 +911,30 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
         if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
         return;
     }
-    // durations of patched fused groups, computed by the estimator kernel
+    // durations of patched fused groups, computed by the estimator kernel: a
+    // queued set reads its queue entry, a memo hit its slot -- checked against
+    // the set's key (a memo clear racing on another stream hands the
+    // candidate to the general kernel instead of reading a foreign value)
+    bool stale = false;
+    const IncWork *work = (const IncWork *)(wsb + L.work);
+    const uint16_t *r2s = (const uint16_t *)(dirty + kIncMaxDirty + 1);
     for (int r = lane; r < nd; r += 32) {
         IncDirty &dd = ((IncDirty *)dirty)[r];
         if (!dd.fused) continue;
         const long long ref = __double_as_longlong(dd.dur);
-        dd.dur = ref >= 0 ? a.memo[ref].v : a.queue[-ref - 1].v;
+        if (ref < 0) {
+            dd.dur = a.queue[-ref - 1].v;
+        } else {
+            const MemoEnt *e = &a.memo[ref];
+            const IncWork &wk = work[r2s[r]];
+            const double v = e->v;
+            stale |= e->k1 != wk.h1 || e->k2 != wk.h2 || isnan(v);
+            dd.dur = v;
+        }
+    }
+    if (__any_sync(FULL, stale)) {
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = kRetryGeneral; }
+        return;
     }
     for (int i = lane; i < L.NW; i += 32) { pbm[i] = 0; tbm[i] = 0; }
     __syncwarp();

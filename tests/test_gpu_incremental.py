@@ -32,7 +32,7 @@ def _score(dg, off, chg, precision, mode, memo=True):
     N.lib().fo_set_delta_mode(dg.h, mode)
     N.lib().fo_memo_enable(dg.h, 1 if memo else 0)
     try:
-        N.lib().fo_memo_clear(dg.h, None)
+        N.lib().fo_memo_clear(dg.h, N.C.c_void_p(torch.cuda.current_stream().cuda_stream))  # stream-ordered
         K = len(off) - 1
         c = torch.empty(K, dtype=torch.float64, device="cuda")
         s = torch.empty(K, dtype=torch.int32, device="cuda")

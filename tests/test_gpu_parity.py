@@ -629,7 +629,7 @@ def _score_delta_on_device(dg, off, chg, precision, memo=True):
 
     N.lib().fo_memo_enable(dg.h, 1 if memo else 0)
     try:
-        N.lib().fo_memo_clear(dg.h, None)
+        N.lib().fo_memo_clear(dg.h, N.C.c_void_p(torch.cuda.current_stream().cuda_stream))
         c = torch.empty(len(off) - 1, dtype=torch.float64, device="cuda")
         s = torch.empty(len(off) - 1, dtype=torch.int32, device="cuda")
         dg.score_delta_device(torch.from_numpy(off).cuda(), torch.from_numpy(chg).cuda(), c, s, precision)
