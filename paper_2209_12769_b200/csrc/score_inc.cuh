@@ -379,32 +379,42 @@ __device__ __forceinline__ bool inc_ring_insert(unsigned long long *buf, unsigne
     return inc_push(buf, m, 0, tail, last, x);
 }
 
-// Look a member set up in the memo and claim a slot when it is new (the
-// prediction is filled in later by the estimator kernel).  -1: no slot along
-// the probe sequence (the set is queued privately).
-__device__ int memo_claim(MemoEnt *t, unsigned mask, unsigned long long h1, unsigned long long h2, bool *is_new) {
-    for (int q = 0; q < kMemoProbe; q++) {
-        const unsigned i = (unsigned)(h1 + q) & mask;
-        MemoEnt *e = &t[i];
-        unsigned long long k = atomicCAS(&e->k1, 0ull, 2ull);
-        if (k == 0) {
-            e->k2 = h2;
-            e->v = __longlong_as_double(0x7ff8000000000000ll);
-            __threadfence();
-            atomicExch(&e->k1, h1);
-            *is_new = true;
-            return (int)i;
-        }
-        while (k == 2) k = *(volatile unsigned long long *)&e->k1;  // another warp is writing its key
-        if (k == h1) {
-            __threadfence();
-            if (*(volatile unsigned long long *)&e->k2 == h2) {
-                *is_new = false;
-                return (int)i;
+// Look member sets up in the memo and claim a slot for every new one (its
+// prediction is filled in by the estimator kernel), all lanes of the warp at
+// once.  A slot another thread is still writing (k1 == 2) is re-read on the
+// next round -- lanes never spin on each other.  slot -1: no slot along the
+// probe sequence (the set is queued privately).
+__device__ __forceinline__ void memo_claim_warp(MemoEnt *t, unsigned mask, bool active, unsigned long long h1,
+                                                unsigned long long h2, int &slot, bool &fresh) {
+    int probe = 0;
+    bool done = !active;
+    slot = -1;
+    fresh = true;
+    while (__any_sync(FULL, !done)) {
+        if (!done) {
+            const unsigned i = (unsigned)(h1 + probe) & mask;
+            MemoEnt *e = &t[i];
+            const unsigned long long k = atomicCAS(&e->k1, 0ull, 2ull);
+            if (k == 0) {
+                e->k2 = h2;
+                e->v = __longlong_as_double(0x7ff8000000000000ll);
+                __threadfence();
+                atomicExch(&e->k1, h1);
+                slot = (int)i;
+                done = true;
+            } else if (k == h1) {
+                __threadfence();
+                if (*(volatile unsigned long long *)&e->k2 == h2) {
+                    slot = (int)i;
+                    fresh = false;
+                    done = true;
+                } else if (++probe >= kMemoProbe) done = true;
+            } else if (k != 2 && ++probe >= kMemoProbe) {
+                done = true;
             }
         }
+        __syncwarp();
     }
-    return -1;
 }
 
 template <typename T>
@@ -691,7 +701,10 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
             const unsigned long long h2 = smix(s2 ^ ((unsigned long long)wk.cnt * 0xff51afd7ed558ccdull));
             c.work[ws].h1 = h1;
             c.work[ws].h2 = h2;
-            if (a.memo) slot = memo_claim(a.memo, g.memo_mask, h1, h2, &fresh);
+        }
+        if (a.memo) {
+            const IncWork &wk = c.work[c.r2s[min(r, nd - 1)]];
+            memo_claim_warp(a.memo, g.memo_mask, mine, mine ? wk.h1 : 0ull, mine ? wk.h2 : 0ull, slot, fresh);
         }
         // new sets are queued (one atomic per warp); a memo hit keeps its slot
         const bool q = mine && (fresh || slot < 0);
