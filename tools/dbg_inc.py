@@ -19,4 +19,4 @@ c = torch.empty(K, dtype=torch.float64, device="cuda"); s = torch.empty(K, dtype
 for rep in range(2):
     dg.score_delta_device(torch.from_numpy(off).cuda(), torch.from_numpy(chg).cuda(), c, s, N.FO_PREC_FP32)
     torch.cuda.synchronize()
-    print(cfg, K, "mode", mode, "stop", stop, "memo", memo, "rep", rep, "status", np.bincount(s.cpu().numpy() + 1).tolist()[:4], float(c.sum()), flush=True)
+    print(cfg, K, "mode", mode, "stop", stop, "memo", memo, "rep", rep, "status", dict(zip(*np.unique(s.cpu().numpy(), return_counts=True))), float(c.sum()), flush=True)
