@@ -190,7 +190,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg);
 struct IncQ;
 cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
                              const int32_t *chg, int K, int precision, char *ws, int grid, IncQ *queue, int *qcount,
-                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream);
+                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag = 0);
 constexpr int kIncQueuePerCand = kIncMaxDirty;  // estimator queue entries per candidate: never full (a claimed memo slot always gets its value)
 int score_inc_blocks_per_sm(const IncLayout &L, int precision);
 

@@ -123,6 +123,7 @@ struct IncArgs {
     double *cost_out;
     int32_t *status_out;
     int stop_after;
+    int diag;  // fo_set_delta_mode 2: hand-backs keep a status that says why
 };
 
 // counters in the per-warp shared arena
@@ -167,7 +168,9 @@ __device__ __forceinline__ int ibk(const IncCtx &c, int a) { return icval(c, 2 *
 __device__ __forceinline__ bool iop_changed(const IncCtx &c, int v) {
     return ibit(c.cbm, v) || ibit(c.cbm, c.a->p.V + v);
 }
-__device__ __forceinline__ void ifail(const IncCtx &c) { c.cnt[kCFail] = 1; }
+// a setup failure hands the candidate to the general kernel; the code says why
+// (visible as status 110 + code in the diagnostic mode, fo_set_delta_mode 2)
+__device__ __forceinline__ void ifail(const IncCtx &c, int code = 1) { c.cnt[kCFail] = code; }
 
 __device__ void imark(const IncCtx &c, int n, int flags) {
     const uint32_t b = 1u << (n & 31);
@@ -175,7 +178,7 @@ __device__ void imark(const IncCtx &c, int n, int flags) {
     if (flags & 2) atomicOr(&c.lbm[n >> 5], b);
     if (atomicOr(&c.pbm[n >> 5], b) & b) return;
     const int s = atomicAdd(&c.cnt[kCDirty], 1);
-    if (s >= kIncMaxDirty) { ifail(c); return; }
+    if (s >= kIncMaxDirty) { ifail(c, 2); return; }
     c.dn[s] = n;
 }
 
@@ -184,12 +187,12 @@ __device__ void islot(const IncCtx &c, int pos, bool oact, int osrc, int otgt, b
     if (oact && nact && osrc == nsrc && otgt == ntgt) return;
     if (oact) {
         const int s = atomicAdd(&c.cnt[kCRem], 1);
-        if (s >= kIncMaxOps || pos < 0) ifail(c);
+        if (s >= kIncMaxOps || pos < 0) ifail(c, 3);
         else c.rem[s] = make_int4(pos, osrc, otgt, 0);
     }
     if (nact) {
         const int s = atomicAdd(&c.cnt[kCAdd], 1);
-        if (s >= kIncMaxOps) ifail(c);
+        if (s >= kIncMaxOps) ifail(c, 4);
         else c.add[s] = make_int2(nsrc, ntgt);
     }
 }
@@ -425,7 +428,7 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
     const IncLayout &L = a.L;
     const int V = p.V, A = p.A, VB = p.VB, NN = p.NN;
     auto retry = [&]() {
-        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = kRetryGeneral; }
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = a.diag ? 110 + c.cnt[kCFail] : kRetryGeneral; }
     };
     // ---- changes: load, validate, sort by index, changed-index bitmap
     const int cb = a.doff[k], ce = a.doff[k + 1];
@@ -545,7 +548,7 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
                 if ((inn(c, v) == n || irr(c, v) == n) && p.pnn[v] != n && p.prr[v] != n) cnt++;
             }
             const int mb = atomicAdd(&c.cnt[kCMem], cnt);
-            if (mb + cnt > L.mem_cap) { ifail(c); c.work[s] = wk; continue; }
+            if (mb + cnt > L.mem_cap) { ifail(c, 5); c.work[s] = wk; continue; }
             int o = mb;
             for (int q = p.mptr[n]; q < p.mptr[n + 1]; q++) {
                 const int u = p.mem[q];
@@ -651,11 +654,11 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
                         if (g.op_kind[mn] == 1) dd.dur = 0.0;
                         else {
                             dd.dur = g.op_prof[mn];
-                            if (isnan(dd.dur)) ifail(c);  // MissingCost: the general path reports it
+                            if (isnan(dd.dur)) ifail(c, 6);  // MissingCost: the general path reports it
                         }
                     } else {
                         dd.fused = 1;
-                        if (cnt > L.mpcap) ifail(c);
+                        if (cnt > L.mpcap) ifail(c, 7);
                     }
                 }
             }
@@ -696,7 +699,7 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
                 s1 += smix((unsigned long long)m * 2 + 1);
                 s2 += smix(((unsigned long long)m << 32) ^ 0x5bd1e995ull);
             }
-            if (miss) ifail(c);
+            if (miss) ifail(c, 8);
             const unsigned long long h1 = smix(s1 + (unsigned long long)wk.cnt) | 1ull;
             const unsigned long long h2 = smix(s2 ^ ((unsigned long long)wk.cnt * 0xff51afd7ed558ccdull));
             c.work[ws].h1 = h1;
@@ -714,7 +717,7 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         qbase = __shfl_sync(FULL, qbase, __ffs(qm | 1u) - 1);
         if (q) {
             const int qi = qbase + __popc(qm & lanemask_lt());
-            if (qi >= a.qcap) ifail(c);
+            if (qi >= a.qcap) ifail(c, 9);
             else {
                 const IncWork wk = c.work[c.r2s[r]];
                 IncQ e;
@@ -751,7 +754,7 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         }
         for (int i = 0; i < nadd; i++) cnt += c.add[i].x == n;
         const int o0 = atomicAdd(&c.cnt[kCPcsr], cnt);
-        if (o0 + cnt > L.pcsr_cap) { ifail(c); continue; }
+        if (o0 + cnt > L.pcsr_cap) { ifail(c, 10); continue; }
         int o = o0;
         for (int q = pr.sb; q < pr.se; q++) {
             bool gone = false;
@@ -843,6 +846,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __gr
         const IncQ q = a.queue[qi];
         const int *mem = q.mem;
         const int n = q.n;
+        if (n < 2 || n > L.mpcap || (const char *)mem < a.ws || (const char *)mem >= a.ws + (int64_t)nw * L.total) {
+            if (lane == 0) a.queue[qi].v = __longlong_as_double(0x7ff8000000000000ll);  // K3 hands it back
+            continue;
+        }
         for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = i;
         __syncwarp();
         for (int i = lane; i < n; i += 32) {
@@ -937,6 +944,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
         const long long ref = __double_as_longlong(dd.dur);
         if (ref < 0) {
             dd.dur = a.queue[-ref - 1].v;
+            stale |= isnan(dd.dur);
         } else {
             const MemoEnt *e = &a.memo[ref];
             const IncWork &wk = work[r2s[r]];
@@ -946,7 +954,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
         }
     }
     if (__any_sync(FULL, stale)) {
-        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = kRetryGeneral; }
+        if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = a.diag ? 103 : kRetryGeneral; }
         return;
     }
     for (int i = lane; i < L.NW; i += 32) { pbm[i] = 0; tbm[i] = 0; }
@@ -1037,7 +1045,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
                                    wsm + L.k_ppre, wsm + L.k_ring, hgb[0], hgb[1], N, a.cost_out + k,
                                    a.status_out + k)) {
         a.cost_out[k] = 0.0;
-        a.status_out[k] = kRetryGeneral;  // a ready run outgrew its ring: the general kernel scores it
+        a.status_out[k] = a.diag ? 104 : kRetryGeneral;  // a ready run outgrew its ring: the general kernel scores it
     }
 }
 
@@ -1069,8 +1077,9 @@ int score_inc_blocks_per_sm(const IncLayout &L, int precision) {
 
 cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
                              const int32_t *chg, int K, int precision, char *ws, int grid, IncQ *queue, int *qcount,
-                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream) {
+                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag) {
     IncArgs a;
+    a.diag = diag;
     a.g = g;
     a.p = p;
     a.L = L;
