@@ -152,7 +152,7 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
         }
         cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid,
                                          (IncQ *)((char *)g->d_inc_q + 64), (int *)g->d_inc_q, qcap, cost, status, stream,
-                                         g->delta_mode == 2 ? (getenv("FO_INC_SERIAL") ? 2 : 1) : 0);
+                                         g->delta_mode == 2);
         g_launches++;
         if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("incremental score launch: ") + cudaGetErrorString(e));
         if (g->delta_mode == 2) return FO_OK;  // diagnostic: hand-backs stay visible as status 101

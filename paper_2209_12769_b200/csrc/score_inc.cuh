@@ -681,45 +681,6 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
     // each patched fused group's set is looked up in the memo; new sets are
     // queued and the estimator kernel runs one warp per queued set.  The
     // record holds the memo slot (>= 0) or -(queue index) - 1 until K3.
-    if (a.diag == 2) {  // debugging: one fused group at a time
-    for (int r = 0; r < nd; r++) {
-        if (!c.dirty[r].fused) continue;
-        const IncWork wk = c.work[c.r2s[r]];
-        const int *mem = c.mem + wk.mb;
-        const int n = wk.cnt;
-        bool miss = false;
-        for (int i = lane; i < n; i += 32) miss |= isnan(g.op_prof[mem[i]]);
-        if (__any_sync(FULL, miss)) { ifail(c, 8); break; }
-        unsigned long long h1 = 0, h2 = 0;
-        set_hash(mem, n, lane, h1, h2);
-        int slot = -1;
-        bool fresh = true;
-        if (a.memo) memo_claim_warp(a.memo, g.memo_mask, lane == 0, h1, h2, slot, fresh);
-        if (lane == 0) {
-            c.work[c.r2s[r]].h1 = h1;
-            c.work[c.r2s[r]].h2 = h2;
-            long long ref = slot;
-            if (fresh || slot < 0) {
-                const int qi = atomicAdd(a.qcount, 1);
-                if (qi >= a.qcap) ifail(c, 9);
-                else {
-                    IncQ e;
-                    e.mem = mem;
-                    e.slot = slot;
-                    e.n = n;
-                    e.v = 0.0;
-                    e.h1 = h1;
-                    e.h2 = h2;
-                    e.pad = 0;
-                    a.queue[qi] = e;
-                    ref = -(long long)qi - 1;
-                }
-            }
-            c.dirty[r].dur = __longlong_as_double(ref);
-        }
-        __syncwarp();
-    }
-    } else {
     // One lane per fused group: every lookup of the candidate is in flight at once.
     for (int r0 = 0; r0 < nd; r0 += 32) {
         const int r = r0 + lane;
@@ -751,9 +712,10 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         // new sets are queued (one atomic per warp); a memo hit keeps its slot
         const bool q = mine && (fresh || slot < 0);
         const unsigned qm = __ballot_sync(FULL, q);
+        const int leader = qm ? __ffs(qm) - 1 : 0;
         int qbase = 0;
-        if (qm && lane == __ffs(qm) - 1) qbase = atomicAdd(a.qcount, __popc(qm));
-        qbase = __shfl_sync(FULL, qbase, __ffs(qm | 1u) - 1);
+        if (qm && lane == leader) qbase = atomicAdd(a.qcount, __popc(qm));
+        qbase = __shfl_sync(FULL, qbase, leader);
         if (q) {
             const int qi = qbase + __popc(qm & lanemask_lt());
             if (qi >= a.qcap) ifail(c, 9);
@@ -773,7 +735,6 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         } else if (mine) {
             c.dirty[r].dur = __longlong_as_double((long long)slot);
         }
-    }
     }
     __syncwarp();
     if (c.cnt[kCFail]) { retry(); return; }
