@@ -947,6 +947,18 @@ static int build_plan(fo_graph *g, int precision) {
     std::vector<uint16_t> gcnt16(VB), gmin16(VB), bcnt16(std::max(A, 1)), bmin16(std::max(A, 1));
     for (int x = 0; x < VB; x++) { gcnt16[x] = (uint16_t)gcnt[x]; gmin16[x] = gcnt[x] ? (uint16_t)gmin[x] : 0; }
     for (int b = 0; b < A; b++) { bcnt16[b] = (uint16_t)bcnt[b]; bmin16[b] = bcnt[b] ? (uint16_t)bmin[b] : 0; }
+    if (getenv("FO_PLAN_DUMP")) {  // debugging aid: checksums of the plan's arrays
+        auto h64 = [](const void *p, size_t n) {
+            uint64_t h = 1469598103934665603ull;
+            for (size_t i = 0; i < n; i++) h = (h ^ ((const uint8_t *)p)[i]) * 1099511628211ull;
+            return (unsigned long long)h;
+        };
+        fprintf(stderr, "plan pv=%d prec=%d NN=%d P=%d n_exist=%d ready=%d/%d rec=%llx indeg=%llx succ=%llx dur=%llx pos_e=%llx pos_agg=%llx pos_ar=%llx mem=%llx parent=%llx\n",
+                g->parent_ver, precision, NN, P, n_exist, (int)rdy_g.size(), (int)rdy_b.size(),
+                h64(rec.data(), sizeof(IncNode) * NN), h64(indeg16.data(), 2 * indeg16.size()), h64(succ.data(), 4 * succ.size()),
+                h64(dur.data(), 8 * dur.size()), h64(pos_e.data(), 4 * pos_e.size()), h64(pos_agg.data(), 4 * pos_agg.size()),
+                h64(pos_ar.data(), 4 * pos_ar.size()), h64(mem.data(), 2 * mem.size()), h64(pn, 4 * (2 * (size_t)V + A)));
+    }
     // one device allocation
     struct Seg { const void *src; size_t bytes; size_t off; };
     Seg segs[] = {
