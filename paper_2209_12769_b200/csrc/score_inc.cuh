@@ -827,10 +827,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc(const __grid_
     score_one_inc<T>(a, k, c, gs, lane);
 }
 
-// K2: the estimator over the queued member sets, one warp per set.  Member
-// marks (lidx: local index, -1 outside) give the member-local undirected
-// neighbour lists in the general kernel's order (in-edges, then out-edges,
-// estimator.py:173-177, :348-355), then mp_forward (estimator.py:363-389).
+// K2: the estimator over the queued member sets, one warp per set.  The
+// member-local undirected neighbour lists (in-edges, then out-edges, the
+// general kernel's order; estimator.py:173-177, :348-355) come from a binary
+// search in the ascending member list, then mp_forward (estimator.py:363-389).
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __grid_constant__ IncArgs a) {
     const int lane = threadIdx.x & 31;
@@ -851,27 +851,35 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __gr
             if (lane == 0) a.queue[qi].v = __longlong_as_double(0x7ff8000000000000ll);  // K3 hands it back
             continue;
         }
-        for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = i;
-        __syncwarp();
         for (int i = lane; i < n; i += 32) {
             const int v = mem[i];
             gs.zl[i] = (g.in_ptr[v + 1] - g.in_ptr[v]) + (g.out_ptr[v + 1] - g.out_ptr[v]);
         }
         __syncwarp();
         warp_exscan(gs.zl, gs.nbptr, n, lane);
+        // local index of an op among the (ascending) members, -1 outside the set
+        auto local = [&](int op) {
+            int lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const int m = (lo + hi) >> 1;
+                if (mem[m] < op) lo = m + 1;
+                else hi = m;
+            }
+            return mem[lo] == op ? lo : -1;
+        };
         for (int i = lane; i < n; i += 32) {
             const int v = mem[i];
             const int o = gs.nbptr[i];
             int cc = 0;
             for (int e = g.in_ptr[v]; e < g.in_ptr[v + 1]; e++) {
-                const int j = gs.lidx[g.e_src[g.in_e[e]]];
+                const int j = local(g.e_src[g.in_e[e]]);
                 if (j < 0) continue;
                 bool dup = false;
                 for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
                 if (!dup) gs.nb[o + cc++] = j;
             }
             for (int e = g.out_ptr[v]; e < g.out_ptr[v + 1]; e++) {
-                const int j = gs.lidx[g.e_dst[g.out_e[e]]];
+                const int j = local(g.e_dst[g.out_e[e]]);
                 if (j < 0) continue;
                 bool dup = false;
                 for (int t = 0; t < cc; t++) dup |= (gs.nb[o + t] == j);
@@ -897,7 +905,6 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __gr
             if (q.slot >= 0 && a.memo[q.slot].k1 == q.h1 && a.memo[q.slot].k2 == q.h2)
                 a.memo[q.slot].v = pred;  // later hits read the memo
         }
-        for (int i = lane; i < n; i += 32) gs.lidx[mem[i]] = -1;
         __syncwarp();
     }
 }

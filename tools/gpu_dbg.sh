@@ -1,1 +1,1 @@
-FO_PLAN_DUMP=1 timeout 90 python tools/dbg_inc3.py 2>&1 | tail -8
+timeout 90 python tools/dbg_inc3.py 2>&1 | tail -4
