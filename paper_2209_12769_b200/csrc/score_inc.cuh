@@ -81,14 +81,17 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.CW = (2 * V + A + 31) / 32;
     int32_t s = 0;
     auto stake = [&](int32_t bytes) { int32_t r = s; s = (s + bytes + 15) & ~15; return r; };
-    L.s_indeg = smem_indeg ? stake(2 * (NN + 2)) : -1;
+    L.s_indeg = -1;  // the setup kernel keeps no indegrees
     L.s_pbm = stake(4 * L.NW);
     L.s_abm = stake(4 * L.NW);
     L.s_lbm = stake(4 * L.NW);
-    L.s_tbm = stake(4 * L.NW);
+    L.s_tbm = -1;
     L.s_ppre = stake(2 * L.NW + 2);
     L.s_cbm = stake(4 * L.CW);
     L.s_cnt = stake(4 * 8);
+    L.RW = (P + 31) / 32;
+    L.s_rbm = stake(4 * L.RW);         // removed parent successor positions
+    L.s_chg = stake(8 * kIncMaxChg);   // the sorted changes
     L.s_bytes = s;
     s = 0;
     L.k_indeg = smem_indeg ? stake(2 * (NN + 2)) : -1;
@@ -142,7 +145,7 @@ struct IncCtx {
     uint32_t *pcsr;
     Ent16 *ring;
     uint16_t *indeg;
-    uint32_t *pbm, *abm, *lbm, *tbm, *cbm;
+    uint32_t *pbm, *abm, *lbm, *tbm, *cbm, *rbm;
     uint16_t *ppre;
     int *cnt;
     int *hdr;  // hand-off from the setup kernel to the event-loop kernel: nd, nrem, nadd, N
@@ -265,18 +268,19 @@ __device__ __noinline__ IncDirty inc_patched_rec(const IncDirty *__restrict__ di
 
 // push into a ready run (sorted ring); keys only grow, so an append is the
 // common case.  false when the ring is full.
-__device__ __forceinline__ bool inc_push(unsigned long long *buf, unsigned m, int head, int &tail,
-                                         unsigned long long &last, unsigned long long x) {
+__device__ __forceinline__ bool inc_push(unsigned long long *buf, unsigned m, int head, int &tail, uint32_t &last,
+                                         unsigned long long x) {
+    const uint32_t key = (uint32_t)(x >> 32);  // keys are unique: the high word orders the entries
     if (tail - head > (int)m) return false;
-    if (tail == head || x >= last) {
+    if (tail == head || key >= last) {
         buf[(tail++) & m] = x;
-        last = x;
+        last = key;
         return true;
     }
     int i = tail++;
     while (i > head) {
         const unsigned long long q = buf[(i - 1) & m];
-        if (q <= x) break;
+        if ((uint32_t)(q >> 32) <= key) break;
         buf[i & m] = q;
         i--;
     }
@@ -302,12 +306,13 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     constexpr unsigned mg = kIncRingG - 1, mb = kIncRingB - 1;
     const unsigned VB = (unsigned)p.VB;
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
-    int run0 = 0, run1 = 0;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
-    double end0 = 0.0, end1 = 0.0, now = 0.0;
+    // an idle lane's end time is +inf: the next completion is min(end0, end1)
+    const double kIdle = __longlong_as_double(0x7ff0000000000000ll);
+    double end0 = kIdle, end1 = kIdle, now = 0.0;
     uint32_t level = 0;
-    unsigned long long lastg = hg > 0 ? rg[(hg - 1) & mg] : 0ull;
-    unsigned long long lastb = hb > 0 ? rb[(hb - 1) & mb] : 0ull;
+    uint32_t lastg = hg > 0 ? (uint32_t)(rg[(hg - 1) & mg] >> 32) : 0u;
+    uint32_t lastb = hb > 0 ? (uint32_t)(rb[(hb - 1) & mb] >> 32) : 0u;
     auto release = [&](unsigned qb, unsigned qe) -> bool {
         const uint32_t *__restrict__ L = (qb & 0x8000u) ? csucc : psucc;
         for (unsigned q = qb & 0x7fffu; q < qe; q++) {
@@ -340,32 +345,32 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
             se = r.se;
         }
     };
+    // start_available (simulator.py:98-115): compute lane, then comm lane;
+    // start = max(now, rt) = now because rt is a drained completion time
     auto start = [&]() {
-        if (!run0 && headg < tailg) {
+        if (end0 == kIdle && headg < tailg) {
             double d;
             node_rec(rg[(headg++) & mg], d, sb0, se0);
-            run0 = 1;
             end0 = __dadd_rn(now, d);
         }
-        if (!run1 && headb < tailb) {
+        if (end1 == kIdle && headb < tailb) {
             double d;
             node_rec(rb[(headb++) & mb], d, sb1, se1);
-            run1 = 1;
             end1 = __dadd_rn(now, d);
         }
     };
     start();
-    while (run0 || run1) {
-        const bool c0 = run0 && (!run1 || end0 <= end1);
-        const bool c1 = run1 && (!run0 || end1 <= end0);
-        const double t = c0 ? end0 : end1;
+    while (end0 != kIdle || end1 != kIdle) {
+        // drain every lane ending at the next completion time (simulator.py:122-132)
+        const double t = fmin(end0, end1);
         if (t > now) { now = t; level += 0x10000u; }
+        const bool c0 = end0 == t, c1 = end1 == t;
         if (c0) {
-            run0 = 0;
+            end0 = kIdle;
             if (!release(sb0, se0)) return false;
         }
         if (c1) {
-            run1 = 0;
+            end1 = kIdle;
             if (!release(sb1, se1)) return false;
         }
         start();
@@ -378,7 +383,7 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
 
 // insert one ready entry into a level-0 run (kept sorted by key)
 __device__ __forceinline__ bool inc_ring_insert(unsigned long long *buf, unsigned m, int &tail, unsigned long long x) {
-    unsigned long long last = tail > 0 ? buf[(tail - 1) & m] : 0ull;
+    uint32_t last = tail > 0 ? (uint32_t)(buf[(tail - 1) & m] >> 32) : 0u;
     return inc_push(buf, m, 0, tail, last, x);
 }
 
@@ -435,7 +440,8 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
     const int nchg = ce - cb;
     if (cb < 0 || nchg < 0 || ce > a.doff[a.K] || nchg > kIncMaxChg) { retry(); return; }
     for (int i = lane; i < L.CW; i += 32) c.cbm[i] = 0;
-    for (int i = lane; i < L.NW; i += 32) { c.pbm[i] = 0; c.abm[i] = 0; c.lbm[i] = 0; c.tbm[i] = 0; }
+    for (int i = lane; i < L.NW; i += 32) { c.pbm[i] = 0; c.abm[i] = 0; c.lbm[i] = 0; }
+    for (int i = lane; i < L.RW; i += 32) c.rbm[i] = 0;
     if (lane < 8) c.cnt[lane] = 0;
     unsigned long long key0 = ~0ull, key1 = ~0ull;  // (index << 32) | value, two per lane
     bool bad = false;
@@ -605,7 +611,10 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         }
     }
     const int nrem = min(c.cnt[kCRem], kIncMaxOps), nadd = min(c.cnt[kCAdd], kIncMaxOps);
-    for (int i = lane; i < nrem; i += 32) imark(c, c.rem[i].y, 2);
+    for (int i = lane; i < nrem; i += 32) {
+        imark(c, c.rem[i].y, 2);
+        atomicOr(&c.rbm[c.rem[i].x >> 5], 1u << (c.rem[i].x & 31));
+    }
     for (int i = lane; i < nadd; i += 32) imark(c, c.add[i].x, 2);
     __syncwarp();
     if (c.cnt[kCFail]) { retry(); return; }
@@ -748,20 +757,13 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         if (!ibit(c.lbm, n)) continue;
         const IncNode pr = p.rec[n];
         int cnt = 0;
-        for (int q = pr.sb; q < pr.se; q++) {
-            bool gone = false;
-            for (int i = 0; i < nrem; i++) gone |= c.rem[i].x == q;
-            cnt += !gone;
-        }
+        for (int q = pr.sb; q < pr.se; q++) cnt += !ibit(c.rbm, q);
         for (int i = 0; i < nadd; i++) cnt += c.add[i].x == n;
         const int o0 = atomicAdd(&c.cnt[kCPcsr], cnt);
         if (o0 + cnt > L.pcsr_cap) { ifail(c, 10); continue; }
         int o = o0;
-        for (int q = pr.sb; q < pr.se; q++) {
-            bool gone = false;
-            for (int i = 0; i < nrem; i++) gone |= c.rem[i].x == q;
-            if (!gone) c.pcsr[o++] = p.succ[q];
-        }
+        for (int q = pr.sb; q < pr.se; q++)
+            if (!ibit(c.rbm, q)) c.pcsr[o++] = p.succ[q];
         for (int i = 0; i < nadd; i++)
             if (c.add[i].x == n) {
                 const int t = c.add[i].y;
@@ -789,7 +791,7 @@ __device__ __forceinline__ IncCtx inc_ctx(const IncArgs &a, int wid, char *sm) {
     IncCtx c;
     c.a = &a;
     c.hdr = (int *)(wsb + L.hdr);
-    c.chg = (int2 *)(wsb + L.chg);
+    c.chg = (int2 *)(sm + L.s_chg);
     c.rem = (int4 *)(wsb + L.rem);
     c.add = (int2 *)(wsb + L.add);
     c.dn = (int *)(wsb + L.dn);
@@ -803,7 +805,8 @@ __device__ __forceinline__ IncCtx inc_ctx(const IncArgs &a, int wid, char *sm) {
     c.pbm = (uint32_t *)(sm + L.s_pbm);
     c.abm = (uint32_t *)(sm + L.s_abm);
     c.lbm = (uint32_t *)(sm + L.s_lbm);
-    c.tbm = (uint32_t *)(sm + L.s_tbm);
+    c.tbm = nullptr;
+    c.rbm = (uint32_t *)(sm + L.s_rbm);
     c.ppre = (uint16_t *)(sm + L.s_ppre);
     c.cbm = (uint32_t *)(sm + L.s_cbm);
     c.cnt = (int *)(sm + L.s_cnt);

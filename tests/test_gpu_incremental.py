@@ -121,7 +121,7 @@ def test_incremental_hands_back_invalid_and_oversized_candidates():
     assert np.array_equal(st, st_ref) and np.array_equal(got, ref)
     assert st[8] == N.FO_INVALID_ARG and st[9] == N.FO_INVALID_ARG
     _, st_only = _score(dg, off2, chg2, N.FO_PREC_FP32, 2)
-    assert (st_only[8:] == 101).all() and (st_only[:8] != 101).all()
+    assert (st_only[8:] >= 101).all() and (st_only[:8] < 101).all()  # 101+: handed back (110 + reason in mode 2)
 
 
 def test_plan_built_under_a_phase_stop_is_still_exact():
