@@ -328,6 +328,11 @@ int fo_set_phase_stop(fo_graph *g, int32_t phase);
  * 2 is diagnostic: incremental kernel only, candidates it would hand to the
  * general kernel keep status 101. */
 int fo_set_delta_mode(fo_graph *g, int32_t mode);
+/* Arithmetic of the FP32 message-passing layer transforms (estimator.py:375):
+ * 0 FP32 FFMA (default), 1 TF32 tensor cores (mma.sync m16n8k8), 2 3xTF32
+ * tensor cores (split operands).  The FP64 estimator is unaffected.  The
+ * estimator memo is per handle: empty it when switching. */
+int fo_set_estimator_arith(fo_graph *g, int32_t mode);
 /* Introspection: the launch geometry a K-candidate batch takes (before the
  * workspace cap): out4 = {block-per-candidate (1) or warp-per-candidate (0),
  * grid, resident blocks per SM, shared-memory arena bytes per candidate}. */

@@ -186,6 +186,12 @@ int fo_score_geometry(fo_graph *g, int32_t K, int32_t precision, int32_t *out4) 
     return FO_OK;
 }
 
+int fo_set_estimator_arith(fo_graph *g, int32_t mode) {
+    if (!g || mode < 0 || mode > 2) return fail(FO_INVALID_ARG, "mode must be 0 (FFMA), 1 (TF32) or 2 (3xTF32)");
+    g->dg.mp_arith = mode;
+    return FO_OK;
+}
+
 int fo_set_delta_mode(fo_graph *g, int32_t mode) {
     if (!g || mode < 0 || mode > 2) return fail(FO_INVALID_ARG, "mode must be 0, 1 or 2");
     g->delta_mode = mode;

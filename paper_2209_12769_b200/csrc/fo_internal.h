@@ -54,6 +54,7 @@ struct DGraph {
     MemoEnt *memo[2];           // MP predictions by member set: [fp32, fp64]
     uint32_t memo_mask;
     int32_t phase_stop;         // measurement hook: launches stop after K1 (1) or K2 (2); 0 = full
+    int32_t mp_arith;           // FP32 MP transforms: 0 FFMA, 1 TF32 tensor cores, 2 3xTF32 tensor cores
     // MP embedding for feature-level prediction (fo_predict_features): W_emb
     // [h][F] row-major and the node_norm mean / std [F] (nullptr: none)
     const double *emb, *emb_mean, *emb_std;

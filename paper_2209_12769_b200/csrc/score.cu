@@ -498,6 +498,60 @@ __device__ __forceinline__ T mat32(const T *__restrict__ Wt, T x, int lane) {
     return acc;
 }
 
+// ---- tensor-core option for the FP32 layer transforms (north star: tensor
+// cores only if the result stays within tolerance).  H = relu(P @ W_l^T) as
+// m16n8k8 TF32 MMAs: rows = member nodes (16 per tile), 4 n8 tiles of output
+// channels, 4 k8 steps.  SPLIT adds the 3xTF32 correction terms (x = hi + lo,
+// hi * hi + hi * lo + lo * hi), recovering ~FP32 accuracy.
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <bool SPLIT>
+__device__ void mma_transform(const float *__restrict__ Wt, const float *P, float *H, int n, int lane) {
+    const int gq = lane >> 2, tq = lane & 3;
+    for (int m0 = 0; m0 < n; m0 += 16) {
+        float acc[4][4] = {};
+        const int r0 = m0 + gq, r1 = m0 + gq + 8;
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 8) {
+            const float af[4] = {r0 < n ? P[r0 * 32 + k0 + tq] : 0.f, r1 < n ? P[r1 * 32 + k0 + tq] : 0.f,
+                                 r0 < n ? P[r0 * 32 + k0 + tq + 4] : 0.f, r1 < n ? P[r1 * 32 + k0 + tq + 4] : 0.f};
+            uint32_t ah[4], al[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                ah[i] = to_tf32(af[i]);
+                al[i] = to_tf32(af[i] - __uint_as_float(ah[i]));
+            }
+#pragma unroll
+            for (int nt = 0; nt < 4; nt++) {
+                const float w0 = __ldg(&Wt[(k0 + tq) * 32 + nt * 8 + gq]), w1 = __ldg(&Wt[(k0 + tq + 4) * 32 + nt * 8 + gq]);
+                const uint32_t bh0 = to_tf32(w0), bh1 = to_tf32(w1);
+                if (SPLIT) {
+                    const uint32_t bl0 = to_tf32(w0 - __uint_as_float(bh0)), bl1 = to_tf32(w1 - __uint_as_float(bh1));
+                    mma_tf32(acc[nt], al, bh0, bh1);  // small terms first
+                    mma_tf32(acc[nt], ah, bl0, bl1);
+                }
+                mma_tf32(acc[nt], ah, bh0, bh1);
+            }
+        }
+        __syncwarp();  // every lane has read its P rows before H (which may alias nothing) is written
+#pragma unroll
+        for (int nt = 0; nt < 4; nt++) {
+            const int c = nt * 8 + 2 * tq;
+            if (r0 < n) { H[r0 * 32 + c] = fmaxf(acc[nt][0], 0.f); H[r0 * 32 + c + 1] = fmaxf(acc[nt][1], 0.f); }
+            if (r1 < n) { H[r1 * 32 + c] = fmaxf(acc[nt][2], 0.f); H[r1 * 32 + c + 1] = fmaxf(acc[nt][3], 0.f); }
+        }
+    }
+}
+
 template <typename T>
 __device__ double mp_forward(const DGraph &g, const int *mem, int n, const int *nbptr, const int *nb, T *H, T *P,
                              int lane) {
@@ -516,6 +570,14 @@ __device__ double mp_forward(const DGraph &g, const int *mem, int n, const int *
             P[i * 32 + lane] = acc / T(1 + e - b);
         }
         __syncwarp();
+        if constexpr (sizeof(T) == 4) {
+            if (g.mp_arith) {  // tensor-core option (measured)
+                if (g.mp_arith == 2) mma_transform<true>((const float *)Wt, (const float *)P, (float *)H, n, lane);
+                else mma_transform<false>((const float *)Wt, (const float *)P, (float *)H, n, lane);
+                __syncwarp();
+                continue;
+            }
+        }
         // H = relu(P @ W_l^T) (estimator.py:375-376); two nodes share each weight load
         for (int i = 0; i < n; i += 2) {
             const bool two = i + 1 < n;
