@@ -938,7 +938,7 @@ static int build_plan(fo_graph *g, int precision) {
     int n_exist = 0;
     std::vector<std::pair<int, int>> rdy_g, rdy_b;
     for (int n = 0; n < NN; n++) {
-        if (indeg[n] > 65535) return FO_OK;
+        if (indeg[n] > 16383) return FO_OK;  // bit 15 of a candidate's indegree marks patched nodes
         rec[n] = IncNode{dur[n], (uint16_t)sptr[n], (uint16_t)sptr[n + 1], prank[n], exists[n], 0};
         indeg16[n] = (uint16_t)indeg[n];
         n_exist += exists[n];

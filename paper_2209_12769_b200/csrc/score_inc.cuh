@@ -300,16 +300,17 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     const uint32_t *__restrict__ psucc = p.succ;
     const IncNode *__restrict__ rec = p.rec;
     uint16_t *__restrict__ indeg = SI ? (uint16_t *)(fo_inc_smem + s_indeg) : gindeg;
-    const uint32_t *__restrict__ pbm = (const uint32_t *)(fo_inc_smem + s_pbm);
     unsigned long long *rg = (unsigned long long *)(fo_inc_smem + s_ring);
     unsigned long long *rb = rg + kIncRingG;
     constexpr unsigned mg = kIncRingG - 1, mb = kIncRingB - 1;
     const unsigned VB = (unsigned)p.VB;
     int headg = 0, tailg = hg, headb = 0, tailb = hb;
     unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
-    // an idle lane's end time is +inf: the next completion is min(end0, end1)
-    const double kIdle = __longlong_as_double(0x7ff0000000000000ll);
-    double end0 = kIdle, end1 = kIdle, now = 0.0;
+    // End times are kept as the bit patterns of non-negative doubles, which
+    // order like the values: integer compares and min.  An idle lane holds +inf.
+    constexpr unsigned long long kIdle = 0x7ff0000000000000ull;
+    unsigned long long end0 = kIdle, end1 = kIdle, nowb = 0;
+    double now = 0.0;
     uint32_t level = 0;
     uint32_t lastg = hg > 0 ? (uint32_t)(rg[(hg - 1) & mg] >> 32) : 0u;
     uint32_t lastb = hb > 0 ? (uint32_t)(rb[(hb - 1) & mb] >> 32) : 0u;
@@ -318,10 +319,10 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
         for (unsigned q = qb & 0x7fffu; q < qe; q++) {
             const uint32_t e = L[q];
             const unsigned t = e & 0xffffu;
-            const int d = indeg[t] - 1;
+            const unsigned d = (unsigned)indeg[t] - 1u;  // bit 15: the node is patched
             indeg[t] = (uint16_t)d;
-            if (d == 0) {
-                const unsigned pt = (pbm[t >> 5] >> (t & 31)) & 1u;
+            if ((d & 0x7fffu) == 0) {
+                const unsigned pt = d >> 15;
                 // the parent's rank travels in the successor entry; a patched node's is its own
                 const uint32_t pr = pt ? inc_patched_rec(dirty, s_pbm, s_ppre, t).prank : (e >> 16);
                 const unsigned long long x = inc_ent(level | pr, t, pt);
@@ -351,25 +352,29 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
         if (end0 == kIdle && headg < tailg) {
             double d;
             node_rec(rg[(headg++) & mg], d, sb0, se0);
-            end0 = __dadd_rn(now, d);
+            end0 = (unsigned long long)__double_as_longlong(__dadd_rn(now, d));
         }
         if (end1 == kIdle && headb < tailb) {
             double d;
             node_rec(rb[(headb++) & mb], d, sb1, se1);
-            end1 = __dadd_rn(now, d);
+            end1 = (unsigned long long)__double_as_longlong(__dadd_rn(now, d));
         }
     };
     start();
-    while (end0 != kIdle || end1 != kIdle) {
+    for (;;) {
         // drain every lane ending at the next completion time (simulator.py:122-132)
-        const double t = fmin(end0, end1);
-        if (t > now) { now = t; level += 0x10000u; }
-        const bool c0 = end0 == t, c1 = end1 == t;
-        if (c0) {
+        const unsigned long long t = end0 < end1 ? end0 : end1;
+        if (t == kIdle) break;
+        if (t > nowb) {
+            nowb = t;
+            now = __longlong_as_double((long long)t);
+            level += 0x10000u;
+        }
+        if (end0 == t) {
             end0 = kIdle;
             if (!release(sb0, se0)) return false;
         }
-        if (c1) {
+        if (end1 == t) {
             end1 = kIdle;
             if (!release(sb1, se1)) return false;
         }
@@ -1008,6 +1013,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
     }
     __syncwarp();
     for (int i = lane; i < L.NW; i += 32) tbm[i] |= pbm[i];
+    for (int s = lane; s < nd; s += 32) {  // bit 15 of a patched node's indegree (read by the event loop)
+        const int n = dn[s];
+        atomicOr((unsigned *)indeg + (n >> 1), (n & 1) ? 0x80000000u : 0x8000u);
+    }
     __syncwarp();
     // level-0 ready runs: the parent's (sorted by rank) without touched nodes,
     // then the touched nodes that are ready, inserted in rank order
@@ -1038,7 +1047,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
         while (m && !over) {
             const int n = wi * 32 + __ffs(m) - 1;
             m &= m - 1;
-            if (n >= NN || indeg[n] != 0) continue;
+            if (n >= NN || (indeg[n] & 0x7fff) != 0) continue;
             unsigned long long x;
             if ((pbm[n >> 5] >> (n & 31)) & 1u) {
                 const IncDirty dd = dirty[(int)ppre[n >> 5] + __popc(pbm[n >> 5] & ((1u << (n & 31)) - 1u))];
