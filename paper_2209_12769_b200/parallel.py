@@ -109,6 +109,8 @@ class ShardedSearch:
 
         dist = _dist()
         multi = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        if not multi:
+            exchange_every = None  # nobody to exchange with: the native run, pipelined and speculating
         if exchange_every is None:
             if self.s is not None:
                 self.s.run(max_rounds, results=False)  # results on demand (s.result / s.best_costs)
