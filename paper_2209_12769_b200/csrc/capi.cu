@@ -54,8 +54,10 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
     const int nws = score_team_warps(geo);
     WsLayout L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, kMpCapDefault, nws);
     // bound the per-slot workspace to a fixed HBM budget (large graphs get
-    // fewer resident candidates rather than tens of GB of scratch)
-    const size_t budget = (size_t)16 << 30;
+    // fewer resident candidates rather than tens of GB of scratch);
+    // FO_WS_BUDGET_GB overrides (measurement)
+    static const char *wsb = getenv("FO_WS_BUDGET_GB");
+    const size_t budget = (size_t)(wsb && atoi(wsb) > 0 ? atoi(wsb) : 16) << 30;
     const int per_block = score_slots(geo) / geo.grid;
     int max_blocks = (int)std::max<size_t>(1, budget / ((size_t)L.total * per_block));
     geo.grid = std::min(geo.grid, max_blocks);
