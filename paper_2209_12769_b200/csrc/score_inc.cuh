@@ -314,9 +314,6 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     uint32_t level = 0;
     uint32_t lastg = hg > 0 ? (uint32_t)(rg[(hg - 1) & mg] >> 32) : 0u;
     uint32_t lastb = hb > 0 ? (uint32_t)(rb[(hb - 1) & mb] >> 32) : 0u;
-    constexpr unsigned long long kNone = ~0ull;
-    unsigned long long stash = kNone;  // invariant: holds an entry only while the lane-g ring is empty
-    int nstash = 0;                    // nodes started from the stash
     auto release = [&](unsigned qb, unsigned qe) -> bool {
         const uint32_t *__restrict__ L = (qb & 0x8000u) ? csucc : psucc;
         for (unsigned q = qb & 0x7fffu; q < qe; q++) {
@@ -329,25 +326,8 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
                 // the parent's rank travels in the successor entry; a patched node's is its own
                 const uint32_t pr = pt ? inc_patched_rec(dirty, s_pbm, s_ppre, t).prank : (e >> 16);
                 const unsigned long long x = inc_ent(level | pr, t, pt);
-                if (t < VB) {
-                    // compute lane: a lone ready node waits in a register (the common
-                    // chain case: released, then started at once, no ring round trip)
-                    if (headg == tailg) {
-                        if (stash == kNone) {
-                            stash = x;
-                        } else {  // a second ready node: both go to the ring, in key order
-                            const bool lt = (uint32_t)(x >> 32) < (uint32_t)(stash >> 32);
-                            rg[(tailg++) & mg] = lt ? x : stash;
-                            rg[(tailg++) & mg] = lt ? stash : x;
-                            lastg = (uint32_t)((lt ? stash : x) >> 32);
-                            stash = kNone;
-                        }
-                    } else if (!inc_push(rg, mg, headg, tailg, lastg, x)) {
-                        return false;
-                    }
-                } else if (!inc_push(rb, mb, headb, tailb, lastb, x)) {
+                if (!(t < VB ? inc_push(rg, mg, headg, tailg, lastg, x) : inc_push(rb, mb, headb, tailb, lastb, x)))
                     return false;
-                }
             }
         }
         return true;
@@ -369,17 +349,9 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     // start_available (simulator.py:98-115): compute lane, then comm lane;
     // start = max(now, rt) = now because rt is a drained completion time
     auto start = [&]() {
-        if (end0 == kIdle && (stash != kNone || headg < tailg)) {
+        if (end0 == kIdle && headg < tailg) {
             double d;
-            unsigned long long x;
-            if (stash != kNone) {
-                x = stash;
-                stash = kNone;
-                nstash++;
-            } else {
-                x = rg[(headg++) & mg];
-            }
-            node_rec(x, d, sb0, se0);
+            node_rec(rg[(headg++) & mg], d, sb0, se0);
             end0 = (unsigned long long)__double_as_longlong(__dadd_rn(now, d));
         }
         if (end1 == kIdle && headb < tailb) {
@@ -408,7 +380,7 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
         }
         start();
     }
-    const int done = headg + headb + nstash;
+    const int done = headg + headb;
     *cost_out = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
     *status_out = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
     return true;
