@@ -159,19 +159,10 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
             CUDA_TRY(cudaMalloc(&g->d_inc_q, qneed));
             g->inc_q_bytes = qneed;
         }
-        int nk = 0;
-        static const char *sp = getenv("FO_INC_SPLIT");  // two-half launch (default on); 0 = one sequence
-        const bool split = !sp || sp[0] != '0';
-        if (split && !g->inc_split.stream2) {
-            CUDA_TRY(cudaStreamCreateWithFlags(&g->inc_split.stream2, cudaStreamNonBlocking));
-            CUDA_TRY(cudaEventCreateWithFlags(&g->inc_split.ev_start, cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&g->inc_split.ev_a_k2, cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&g->inc_split.ev_done, cudaEventDisableTiming));
-        }
         cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid,
                                          (IncQ *)((char *)g->d_inc_q + 64), (int *)g->d_inc_q, qcap, cost, status, stream,
-                                         g->delta_mode == 2, split ? &g->inc_split : nullptr, &nk);
-        g_launches += nk;
+                                         g->delta_mode == 2);
+        g_launches++;
         if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("incremental score launch: ") + cudaGetErrorString(e));
         if (g->delta_mode == 2) return FO_OK;  // diagnostic: hand-backs stay visible as status 101
         return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
@@ -341,13 +332,6 @@ int fo_graph_destroy(fo_graph *g) {
         if (pl) cudaFree(pl);
     if (g->d_ws_inc) cudaFree(g->d_ws_inc);
     if (g->d_inc_q) cudaFree(g->d_inc_q);
-    if (g->inc_split.stream2) {
-        cudaStreamSynchronize(g->inc_split.stream2);
-        cudaStreamDestroy(g->inc_split.stream2);
-        cudaEventDestroy(g->inc_split.ev_start);
-        cudaEventDestroy(g->inc_split.ev_a_k2);
-        cudaEventDestroy(g->inc_split.ev_done);
-    }
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     for (auto &sl : g->aslot) {
         if (sl.done) cudaEventSynchronize(sl.done);

@@ -189,14 +189,9 @@ constexpr int kRetryGeneral = 101;  // internal status: the incremental kernel h
 constexpr int kIncPending = 102;    // internal status: set up, waiting for the event-loop kernel
 IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg);
 struct IncQ;
-struct IncSplit {  // two-stream launch of one batch's halves (launch_score_inc)
-    cudaStream_t stream2;
-    cudaEvent_t ev_start, ev_a_k2, ev_done;
-};
 cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
                              const int32_t *chg, int K, int precision, char *ws, int grid, IncQ *queue, int *qcount,
-                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag = 0,
-                             const IncSplit *split = nullptr, int *kernels = nullptr);
+                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag = 0);
 constexpr int kIncQueuePerCand = kIncMaxDirty;  // estimator queue entries per candidate: never full (a claimed memo slot always gets its value)
 int score_inc_blocks_per_sm(const IncLayout &L, int precision);
 
@@ -262,7 +257,6 @@ struct fo_graph {
     size_t ws_inc_bytes = 0;
     void *d_inc_q = nullptr;  // estimator queue (IncQ entries) + its counter
     size_t inc_q_bytes = 0;
-    fo::IncSplit inc_split{};  // second stream + events of the two-half launch (created on first use)
     int delta_mode = 1;  // 1: incremental kernel when the plan allows it; 0: general kernel only
     std::mutex mu;
 };

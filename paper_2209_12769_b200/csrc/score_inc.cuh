@@ -1095,31 +1095,9 @@ int score_inc_blocks_per_sm(const IncLayout &L, int precision) {
     return n;
 }
 
-// one launch sequence (setup, estimator, event loop) over candidates
-// [k0, k0 + grid * warps) of a.K, on one stream
-static int inc_sequence(const IncArgs &a, int k0, int grid, int precision, cudaStream_t st, cudaEvent_t after_k2,
-                        cudaEvent_t before_k3) {
-    const IncLayout &L = a.L;
-    const size_t smem = (size_t)L.s_bytes * kWarps, ksmem = (size_t)L.k_bytes * kWarps;
-    const bool fp64 = precision == FO_PREC_FP64;
-    cudaMemsetAsync(a.qcount, 0, sizeof(int), st);
-    if (fp64) score_kernel_inc<double><<<grid, kWarps * 32, smem, st>>>(a, k0);
-    else score_kernel_inc<float><<<grid, kWarps * 32, smem, st>>>(a, k0);
-    if (a.stop_after == 1) return 1;
-    if (fp64) score_kernel_inc_mp<double><<<grid, kWarps * 32, 0, st>>>(a);
-    else score_kernel_inc_mp<float><<<grid, kWarps * 32, 0, st>>>(a);
-    if (after_k2) cudaEventRecord(after_k2, st);
-    if (before_k3) cudaStreamWaitEvent(st, before_k3, 0);
-    if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, st>>>(a, k0);
-    else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, st>>>(a, k0);
-    return 3;
-}
-
 cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout &L, const int32_t *off,
                              const int32_t *chg, int K, int precision, char *ws, int grid, IncQ *queue, int *qcount,
-                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag,
-                             const IncSplit *split, int *kernels) {
-    int nk = 0;
+                             int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag) {
     IncArgs a;
     a.diag = diag;
     a.g = g;
@@ -1136,30 +1114,19 @@ cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout 
     a.cost_out = cost_out;
     a.status_out = status_out;
     a.stop_after = g.phase_stop;
+    const size_t smem = (size_t)L.s_bytes * kWarps, ksmem = (size_t)L.k_bytes * kWarps;
     const int per_launch = grid * kWarps;  // one candidate per warp per launch
-    if (split && K <= per_launch && K >= 8 * kWarps) {
-        // Two halves on two streams: the second half's setup overlaps the first
-        // half's estimator and event loop (the event loop is issue-bound, the
-        // setup latency-bound).  The second half's event loop waits for the
-        // first half's estimator: its memo hits may be sets the first half claimed.
-        const int ka = ((K / 2) + kWarps - 1) / kWarps * kWarps, kb = K - ka;
-        const int ga = ka / kWarps, gb = (kb + kWarps - 1) / kWarps;
-        IncArgs A = a, B = a;
-        A.K = ka;
-        A.qcap = qcap / 2;
-        B.ws = ws + (int64_t)ga * kWarps * L.total;
-        B.queue = queue + qcap / 2;
-        B.qcount = qcount + 1;
-        B.qcap = qcap / 2;
-        cudaEventRecord(split->ev_start, stream);
-        nk += inc_sequence(A, 0, ga, precision, stream, split->ev_a_k2, nullptr);
-        cudaStreamWaitEvent(split->stream2, split->ev_start, 0);
-        nk += inc_sequence(B, ka, gb, precision, split->stream2, nullptr, split->ev_a_k2);
-        cudaEventRecord(split->ev_done, split->stream2);
-        cudaStreamWaitEvent(stream, split->ev_done, 0);
-    } else {
-        for (int k0 = 0; k0 < K; k0 += per_launch) nk += inc_sequence(a, k0, grid, precision, stream, nullptr, nullptr);
+    const bool fp64 = precision == FO_PREC_FP64;
+    for (int k0 = 0; k0 < K; k0 += per_launch) {
+        cudaError_t e = cudaMemsetAsync(qcount, 0, sizeof(int), stream);
+        if (e != cudaSuccess) return e;
+        if (fp64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+        else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a, k0);
+        if (a.stop_after == 1) continue;
+        if (fp64) score_kernel_inc_mp<double><<<grid, kWarps * 32, 0, stream>>>(a);
+        else score_kernel_inc_mp<float><<<grid, kWarps * 32, 0, stream>>>(a);
+        if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
+        else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
     }
-    if (kernels) *kernels = nk;
     return cudaGetLastError();
 }

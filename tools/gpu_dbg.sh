@@ -1,4 +1,3 @@
 #!/bin/bash
-timeout 240 python -m pytest tests/test_gpu_incremental.py -x -q --timeout 60 2>&1 | tail -2
-for sp in 0 1 0 1; do FO_INC_SPLIT=$sp timeout 120 python tools/time_inc.py resnet50 4096 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('split', $sp, d['mode1'])"; done
-FO_INC_SPLIT=1 timeout 180 python bench.py --no-cpu-baseline --no-search | head -c 300; echo
+for b in 100 130; do FO_WS_BUDGET_GB=$b timeout 300 python tools/bench_configs.py synth50k 2>&1 | grep "^{" | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('budget', $b, 'GB', round(d['value']), 'cand/s', round(d['ms_per_round'],1), 'ms/round', d['oracle_check'])"; done
+nvidia-smi --query-gpu=memory.total,memory.used --format=csv
