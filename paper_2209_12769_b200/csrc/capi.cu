@@ -162,7 +162,8 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
         cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid,
                                          (IncQ *)((char *)g->d_inc_q + 64), (int *)g->d_inc_q, qcap, cost, status, stream,
                                          g->delta_mode == 2);
-        g_launches++;
+        // kernels launched: setup, estimator and event loop per chunk of one candidate per warp
+        g_launches += (int64_t)((K + grid * warps - 1) / (grid * warps)) * (g->dg.phase_stop == 1 ? 1 : 3);
         if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("incremental score launch: ") + cudaGetErrorString(e));
         if (g->delta_mode == 2) return FO_OK;  // diagnostic: hand-backs stay visible as status 101
         return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
