@@ -92,6 +92,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.RW = (P + 31) / 32;
     L.s_rbm = stake(4 * L.RW);         // removed parent successor positions
     L.s_chg = stake(8 * kIncMaxChg);   // the sorted changes
+    L.s_cpre = stake(L.CW + 4);        // their bitmap word prefix
     L.s_bytes = s;
     s = 0;
     L.k_indeg = smem_indeg ? stake(2 * (NN + 2)) : -1;
@@ -146,6 +147,7 @@ struct IncCtx {
     Ent16 *ring;
     uint16_t *indeg;
     uint32_t *pbm, *abm, *lbm, *tbm, *cbm, *rbm;
+    uint8_t *cpre;  // changed-index bitmap word prefix (<= 64 changes)
     uint16_t *ppre;
     int *cnt;
     int *hdr;  // hand-off from the setup kernel to the event-loop kernel: nd, nrem, nadd, N
@@ -155,15 +157,12 @@ struct IncCtx {
 __device__ __forceinline__ bool ibit(const uint32_t *bm, int i) { return (bm[i >> 5] >> (i & 31)) & 1u; }
 
 // candidate value at index i of ngid | rgid | bkt: the parent's unless changed
+// (the sorted change list is in index order, so a changed index's position
+// is its rank in the changed-index bitmap: a word prefix plus a popcount)
 __device__ __forceinline__ int icval(const IncCtx &c, int i, int pv) {
-    if (!ibit(c.cbm, i)) return pv;
-    int lo = 0, hi = c.nchg - 1;
-    while (lo < hi) {
-        const int m = (lo + hi) >> 1;
-        if (c.chg[m].x < i) lo = m + 1;
-        else hi = m;
-    }
-    return c.chg[lo].y;
+    const uint32_t w = c.cbm[i >> 5];
+    if (!((w >> (i & 31)) & 1u)) return pv;
+    return c.chg[(int)c.cpre[i >> 5] + __popc(w & ((1u << (i & 31)) - 1u))].y;
 }
 __device__ __forceinline__ int inn(const IncCtx &c, int v) { return icval(c, v, c.a->p.pnn[v]); }
 __device__ __forceinline__ int irr(const IncCtx &c, int v) { return icval(c, c.a->p.V + v, c.a->p.prr[v]); }
@@ -491,6 +490,22 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         if (i > 0 && c.chg[i - 1].x == idx) bad = true;  // one change per index
     }
     __syncwarp();
+    {  // word prefix of the changed-index bitmap (icval's rank)
+        int carry = 0;
+        for (int base = 0; base < L.CW; base += 32) {
+            const int i = base + lane;
+            const int x = i < L.CW ? __popc(c.cbm[i]) : 0;
+            int v = x;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(FULL, v, d);
+                if (lane >= d) v += y;
+            }
+            if (i < L.CW) c.cpre[i] = (uint8_t)(carry + v - x);
+            carry += __shfl_sync(FULL, v, 31);
+        }
+    }
+    __syncwarp();
     // every changed op keeps a normal group distinct from its replica group
     for (int i = lane; i < nchg; i += 32) {
         const int idx = c.chg[i].x;
@@ -812,6 +827,7 @@ __device__ __forceinline__ IncCtx inc_ctx(const IncArgs &a, int wid, char *sm) {
     c.lbm = (uint32_t *)(sm + L.s_lbm);
     c.tbm = nullptr;
     c.rbm = (uint32_t *)(sm + L.s_rbm);
+    c.cpre = (uint8_t *)(sm + L.s_cpre);
     c.ppre = (uint16_t *)(sm + L.s_ppre);
     c.cbm = (uint32_t *)(sm + L.s_cbm);
     c.cnt = (int *)(sm + L.s_cnt);
