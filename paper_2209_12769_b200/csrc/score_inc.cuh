@@ -51,7 +51,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.hdr = take(16);
     L.chg = take(8 * kIncMaxChg);
     L.rem = take(16 * kIncMaxOps);
-    L.add = take(8 * kIncMaxOps);
+    L.add = take(16 * kIncMaxOps);
     L.dn = take(4 * kIncMaxDirty);
     L.work = take(sizeof(IncWork) * kIncMaxDirty);
     L.dirty = take(sizeof(IncDirty) * (kIncMaxDirty + 1) + 2 * kIncMaxDirty);  // + rank -> slot map
@@ -137,7 +137,7 @@ struct IncCtx {
     const IncArgs *a;
     int2 *chg;
     int4 *rem;
-    int2 *add;
+    int4 *add;  // (source, target, the target's parent rank, 0)
     int *dn;
     IncWork *work;
     IncDirty *dirty;
@@ -195,7 +195,7 @@ __device__ void islot(const IncCtx &c, int pos, bool oact, int osrc, int otgt, b
     if (nact) {
         const int s = atomicAdd(&c.cnt[kCAdd], 1);
         if (s >= kIncMaxOps) ifail(c, 4);
-        else c.add[s] = make_int2(nsrc, ntgt);
+        else c.add[s] = make_int4(nsrc, ntgt, c.a->p.rec[ntgt].prank, 0);  // rank loaded here, lanes in parallel
     }
 }
 
@@ -786,8 +786,8 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
             if (!ibit(c.rbm, q)) c.pcsr[o++] = p.succ[q];
         for (int i = 0; i < nadd; i++)
             if (c.add[i].x == n) {
-                const int t = c.add[i].y;
-                c.pcsr[o++] = ((uint32_t)p.rec[t].prank << 16) | (uint32_t)t;  // patched targets are re-ranked at release
+                // the parent's rank (patched targets are re-ranked at release)
+                c.pcsr[o++] = ((uint32_t)c.add[i].z << 16) | (uint32_t)c.add[i].y;
             }
         IncDirty &dd = c.dirty[irank(c, n)];
         dd.sb = (uint16_t)(0x8000 | o0);
@@ -813,7 +813,7 @@ __device__ __forceinline__ IncCtx inc_ctx(const IncArgs &a, int wid, char *sm) {
     c.hdr = (int *)(wsb + L.hdr);
     c.chg = (int2 *)(sm + L.s_chg);
     c.rem = (int4 *)(wsb + L.rem);
-    c.add = (int2 *)(wsb + L.add);
+    c.add = (int4 *)(wsb + L.add);
     c.dn = (int *)(wsb + L.dn);
     c.work = (IncWork *)(wsb + L.work);
     c.dirty = (IncDirty *)(wsb + L.dirty);
@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
     const int nd = hdr[0], nrem = hdr[1], nadd = hdr[2], N = hdr[3];
     const int *dn = (const int *)(wsb + L.dn);
     const int4 *rem = (const int4 *)(wsb + L.rem);
-    const int2 *add = (const int2 *)(wsb + L.add);
+    const int4 *add = (const int4 *)(wsb + L.add);
     const IncDirty *dirty = (const IncDirty *)(wsb + L.dirty);
     const uint32_t *pcsr = (const uint32_t *)(wsb + L.pcsr);
     uint16_t *indeg = SI ? (uint16_t *)(fo_inc_smem + wsm + L.k_indeg) : (uint16_t *)(wsb + L.indeg);
