@@ -62,8 +62,11 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
     size_t budget = (size_t)16 << 30;
     if (wsb && atoi(wsb) > 0) budget = (size_t)atoi(wsb) << 30;
     else {
-        size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && tot) budget = std::max(budget, tot / 100 * 45);
+        if (!g->mem_total) {  // queried once per handle: it sits on the launch path
+            size_t fr = 0;
+            if (cudaMemGetInfo(&fr, &g->mem_total) != cudaSuccess) g->mem_total = budget;
+        }
+        budget = std::max(budget, g->mem_total / 100 * 45);
     }
     const int per_block = score_slots(geo) / geo.grid;
     int max_blocks = (int)std::max<size_t>(1, budget / ((size_t)L.total * per_block));

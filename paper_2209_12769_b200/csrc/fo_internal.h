@@ -236,6 +236,7 @@ struct fo_graph {
     size_t pinned_bytes = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 0;
+    size_t mem_total = 0;  // device memory (workspace budget)
     // fo_score_delta_submit / fo_score_wait: two in-flight submissions; H2D and
     // D2H on their own streams so one batch's transfers overlap the other's kernel
     struct AsyncSlot {
