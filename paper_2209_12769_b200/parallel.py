@@ -87,12 +87,30 @@ class ShardedSearch:
         return total
 
     def _exchange(self, device, active):
+        """(global best cost, global seed id, total active seeds): the local
+        argmin on the host, then one all-gather of 3 doubles per rank into
+        buffers allocated once (a per-round call: no per-round allocations)."""
         import torch
 
+        dist = _dist()
         best = self.s.best if self.s is not None else np.zeros(0)
-        cost = torch.as_tensor(best, dtype=torch.float64, device=device)
-        ids = torch.arange(self.seed_offset, self.seed_offset + len(best), dtype=torch.float64, device=device)
-        return global_best(cost, ids, active=active)
+        if len(best):
+            j = int(np.argmin(best))  # first minimum -> lowest local id among ties
+            mine = (float(best[j]), float(self.seed_offset + j))
+        else:
+            mine = (float("inf"), float("inf"))
+        if not (dist.is_available() and dist.is_initialized()):
+            return mine[0], mine[1], int(active)
+        world = dist.get_world_size()
+        if getattr(self, "_xbuf", None) is None or self._xbuf[0].device != torch.device(device):
+            self._xbuf = (torch.empty(3, dtype=torch.float64, device=device),
+                          torch.empty(3 * world, dtype=torch.float64, device=device))
+        send, recv = self._xbuf
+        send.copy_(torch.tensor([mine[0], mine[1], float(active)], dtype=torch.float64))
+        dist.all_gather_into_tensor(recv, send)
+        allp = recv.view(world, 3).cpu().numpy()
+        order = np.lexsort((allp[:, 1], allp[:, 0]))  # strict <: the lowest global id among equal costs
+        return float(allp[order[0], 0]), float(allp[order[0], 1]), int(round(allp[:, 2].sum()))
 
     def run(self, device, max_rounds: Optional[int] = None, exchange_every: Optional[int] = 1):
         """Advance every local seed to completion, exchanging the global best
