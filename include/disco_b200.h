@@ -328,6 +328,13 @@ int fo_set_phase_stop(fo_graph *g, int32_t phase);
  * 2 is diagnostic: incremental kernel only, candidates it would hand to the
  * general kernel keep status 101. */
 int fo_set_delta_mode(fo_graph *g, int32_t mode);
+/* Event-loop fast-forward counters of the incremental kernel, accumulated
+ * over mode-2 launches since the last call (then reset; synchronizes the
+ * device): out6 = {candidates that reached the event loop, candidates that
+ * started from a parent snapshot, parent iterations skipped in total, the
+ * parent loop's iterations, snapshots held, iterations between snapshots}
+ * for the plan of this precision. */
+int fo_inc_stats(fo_graph *g, int32_t precision, int64_t *out6);
 /* Arithmetic of the FP32 message-passing layer transforms (estimator.py:375):
  * 0 FP32 FFMA (default), 1 TF32 tensor cores (mma.sync m16n8k8), 2 3xTF32
  * tensor cores (split operands).  The FP64 estimator is unaffected.  The

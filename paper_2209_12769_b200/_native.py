@@ -79,6 +79,7 @@ SIGNATURES = [
     ("fo_set_parent", C.c_int, [vp, vp, vp, vp]),
     ("fo_set_phase_stop", C.c_int, [vp, C.c_int32]),
     ("fo_set_delta_mode", C.c_int, [vp, C.c_int32]),
+    ("fo_inc_stats", C.c_int, [vp, C.c_int32, vp]),
     ("fo_set_estimator_arith", C.c_int, [vp, C.c_int32]),
     ("fo_make_candidates_delta", C.c_int, [vp, vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp,
                                            C.c_int64]),

@@ -160,6 +160,7 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
             g->d_inc_q = nullptr;
             g->inc_q_bytes = 0;
             CUDA_TRY(cudaMalloc(&g->d_inc_q, qneed));
+            CUDA_TRY(cudaMemset(g->d_inc_q, 0, 64));  // queue count, fast-forward counters (fo_inc_stats)
             g->inc_q_bytes = qneed;
         }
         cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid,
@@ -202,6 +203,26 @@ int fo_score_geometry(fo_graph *g, int32_t K, int32_t precision, int32_t *out4) 
 int fo_set_estimator_arith(fo_graph *g, int32_t mode) {
     if (!g || mode < 0 || mode > 2) return fail(FO_INVALID_ARG, "mode must be 0 (FFMA), 1 (TF32) or 2 (3xTF32)");
     g->dg.mp_arith = mode;
+    return FO_OK;
+}
+
+int fo_inc_stats(fo_graph *g, int32_t precision, int64_t *out6) {
+    if (!g || !out6) return fail(FO_INVALID_ARG, "bad arguments");
+    const int pi = precision == FO_PREC_FP64 ? 1 : 0;
+    unsigned long long c[3] = {0, 0, 0};
+    if (g->d_inc_q) {
+        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaDeviceSynchronize());
+        CUDA_TRY(cudaMemcpy(c, (char *)g->d_inc_q + 16, sizeof(c), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemset((char *)g->d_inc_q + 16, 0, sizeof(c)));
+    }
+    const bool ok = g->plan_ok[pi] != 0;
+    out6[0] = (int64_t)c[0];
+    out6[1] = (int64_t)c[1];
+    out6[2] = (int64_t)c[2];
+    out6[3] = ok ? g->plan_iters[pi] : 0;
+    out6[4] = ok ? g->plan[pi].nsnap : 0;
+    out6[5] = ok ? g->plan[pi].snap_S : 0;
     return FO_OK;
 }
 
@@ -333,6 +354,8 @@ int fo_graph_destroy(fo_graph *g) {
     if (g->d_io) cudaFree(g->d_io);
     if (g->d_parent) cudaFree(g->d_parent);
     for (void *pl : g->d_plan)
+        if (pl) cudaFree(pl);
+    for (void *pl : g->d_snap)
         if (pl) cudaFree(pl);
     if (g->d_ws_inc) cudaFree(g->d_ws_inc);
     if (g->d_inc_q) cudaFree(g->d_inc_q);
@@ -844,6 +867,41 @@ static int single(fo_graph *g, const int32_t *ngid, const int32_t *rgid, const i
 // parent itself, so the plan carries exactly the general path's values.
 // Only the MP estimator with profile lookups takes this path (the analytic /
 // linear / hardware-oracle providers depend on group_io of neighbours).
+// Run the parent's event loop once on the device (inc_record_kernel) and keep
+// every node's push iteration plus a loop snapshot every S iterations in the
+// plan, so candidates start at the last iteration they share with the parent.
+// The recorded makespan must equal the general kernel's parent cost bit for
+// bit; otherwise (or with FO_INC_NO_SNAP set) candidates start at level 0.
+static int record_parent_loop(fo_graph *g, int pi, const char *parent_cost) {
+    IncPlan &p = g->plan[pi];
+    if (g->d_snap[pi]) { CUDA_TRY(cudaFree(g->d_snap[pi])); g->d_snap[pi] = nullptr; }
+    g->plan_iters[pi] = 0;
+    if (getenv("FO_INC_NO_SNAP") || p.n_exist < 16) return FO_OK;
+    const int S = std::max(4, (p.n_exist + 63) / 64), maxsnap = p.n_exist / S;
+    const int64_t stride = inc_snap_stride(p.NN);
+    const size_t o_push = 0, o_fin = al256(2 * (size_t)(p.NN + 2)), o_out = 2 * o_fin, o_snap = o_out + 256;
+    const size_t total = o_snap + (size_t)maxsnap * stride;
+    CUDA_TRY(cudaMalloc(&g->d_snap[pi], total));
+    char *b = (char *)g->d_snap[pi];
+    CUDA_TRY(cudaMemsetAsync(b + o_out, 0, 16, g->stream));
+    CUDA_TRY(launch_inc_record(p, (uint16_t *)(b + o_push), (uint16_t *)(b + o_fin), b + o_snap, S, maxsnap, b + o_out,
+                               g->stream));
+    int32_t out[5];
+    CUDA_TRY(cudaMemcpyAsync(out, b + o_out, 20, cudaMemcpyDeviceToHost, g->stream));
+    CUDA_TRY(cudaStreamSynchronize(g->stream));
+    double mk;
+    memcpy(&mk, out + 2, 8);
+    if (out[1] != FO_OK || memcmp(&mk, parent_cost, 8) != 0 || out[0] <= 0) return FO_OK;  // level 0 only
+    p.push = (const uint16_t *)(b + o_push);
+    p.fin = (const uint16_t *)(b + o_fin);
+    p.snap = b + o_snap;
+    p.snap_S = S;
+    p.nsnap = out[0];
+    p.snap_stride = (int32_t)stride;
+    g->plan_iters[pi] = out[4];
+    return FO_OK;
+}
+
 static int build_plan(fo_graph *g, int precision) {
     const int pi = precision == FO_PREC_FP64 ? 1 : 0;
     g->plan_ok[pi] = 0;
@@ -1019,6 +1077,14 @@ static int build_plan(fo_graph *g, int precision) {
     p.prr = g->d_parent + V;
     p.pbk = g->d_parent + 2 * V;
     p.ready = (const uint16_t *)(b + segs[16].off);
+    p.push = nullptr;
+    p.fin = nullptr;
+    p.snap = nullptr;
+    p.snap_S = 1;
+    p.nsnap = 0;
+    p.snap_stride = 0;
+    st = record_parent_loop(g, pi, h.data() + o[3]);
+    if (st) return st;
     g->plan_ok[pi] = 1;
     return FO_OK;
 }

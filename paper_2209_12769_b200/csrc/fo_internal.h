@@ -174,6 +174,11 @@ struct IncPlan {
     const int32_t *pos_ar;     // [A] bucket <- export(producer) slot
     const int32_t *pnn, *prr, *pbk;  // the parent state (engine ids)
     const uint16_t *ready;     // level-0 ready nodes: lane g [0, n_ready_g), lane b after, each by prank
+    // the parent's own event loop, recorded once per plan (inc_record_kernel):
+    const uint16_t *push;      // [NN] loop iteration + 1 in which the node became ready (0: level 0, 0xffff: never)
+    const uint16_t *fin;       // [NN] loop iteration + 1 in which it finished
+    const char *snap;          // loop state at the top of iteration j * snap_S, j = 1 .. nsnap (IncSnap layout)
+    int32_t snap_S, nsnap, snap_stride;
 };
 struct IncLayout {  // per-warp global scratch (byte offsets) and shared-memory arena
     int64_t hdr, chg, rem, add, dn, work, dirty, mem, pcsr, ring, indeg, gs0, total;
@@ -181,7 +186,7 @@ struct IncLayout {  // per-warp global scratch (byte offsets) and shared-memory 
     int32_t mem_cap, pcsr_cap, mpcap;
     int32_t ring_g, ring_b;  // ready-run ring sizes (powers of two >= the nodes of each lane: no overflow)
     int32_t s_indeg, s_pbm, s_abm, s_lbm, s_tbm, s_ppre, s_cbm, s_cnt, s_bytes;  // setup kernel smem (per warp)
-    int32_t k_indeg, k_pbm, k_ppre, k_tbm, k_ring, k_bytes;  // event-loop kernel smem (k_indeg < 0: global)
+    int32_t k_indeg, k_pbm, k_ppre, k_tbm, k_ring, k_state, k_bytes;  // event-loop kernel smem (k_indeg < 0: global)
     int32_t NW, CW, RW, s_rbm, s_chg, s_cpre;
 };
 constexpr int kIncMaxChg = 64, kIncMaxOps = 256, kIncMaxDirty = 192;
@@ -194,6 +199,11 @@ cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout 
                              int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag = 0);
 constexpr int kIncQueuePerCand = kIncMaxDirty;  // estimator queue entries per candidate: never full (a claimed memo slot always gets its value)
 int score_inc_blocks_per_sm(const IncLayout &L, int precision);
+// record the parent's event loop into the plan's push / snapshot arrays;
+// out: {nsnap, status} as int32 then the makespan as a double (16 bytes)
+int64_t inc_snap_stride(int NN);
+cudaError_t launch_inc_record(const IncPlan &p, uint16_t *push, uint16_t *fin, char *snap, int S, int maxsnap,
+                              void *out, cudaStream_t stream);
 
 cudaError_t launch_batch_best(const double *cost, const int32_t *status, int K, int64_t id_offset, double *out,
                               cudaStream_t stream, int pairs = 0);
@@ -251,6 +261,8 @@ struct fo_graph {
     // precision, rebuilt when the parent or the cost model changes
     int parent_ver = 0, model_ver = 0;
     void *d_plan[2] = {nullptr, nullptr};
+    void *d_snap[2] = {nullptr, nullptr};  // the parent loop record of each plan
+    int plan_iters[2] = {0, 0};             // the parent loop's iterations
     fo::IncPlan plan[2]{};
     int plan_pv[2] = {-1, -1}, plan_mv[2] = {-1, -1};
     int plan_ok[2] = {0, 0};

@@ -100,6 +100,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.k_ppre = stake(2 * L.NW + 2);
     L.k_tbm = stake(4 * L.NW);
     L.k_ring = stake(8 * (kIncRingG + kIncRingB));
+    L.k_state = stake(128);  // IncK3State: prep -> run hand-off
     L.k_bytes = s;
     return L;
 }
@@ -128,6 +129,7 @@ struct IncArgs {
     int32_t *status_out;
     int stop_after;
     int diag;  // fo_set_delta_mode 2: hand-backs keep a status that says why
+    unsigned long long *stats;  // diag: event-loop fast-forward counters (fo_inc_stats), or nullptr
 };
 
 // counters in the per-warp shared arena
@@ -287,15 +289,43 @@ __device__ __forceinline__ bool inc_push(unsigned long long *buf, unsigned m, in
     return true;
 }
 
+// Loop state at the top of one iteration of inc_ring_loop: the state a
+// candidate starts from -- level 0 (all zero, idle lanes) or a snapshot of the
+// parent's own loop (IncSnap).  head / tail are absolute run positions (head =
+// nodes started on the lane so far).
+struct IncLoopState {
+    int32_t headg, tailg, headb, tailb;
+    uint32_t sb0, se0, sb1, se1;  // successor ranges of the running nodes
+    unsigned long long end0, end1, nowb;
+    uint32_t level, iter;
+    uint32_t run0, run1;  // the running nodes (snapshots only)
+};
+// A snapshot: the state, then the ready runs' entries (head first), then the
+// parent's indegrees (NN + 2 u16).
+constexpr int kIncSnapRuns = 128, kIncSnapDeg = kIncSnapRuns + 8 * (kIncRingG + kIncRingB);
+int64_t inc_snap_stride(int NN) { return kIncSnapDeg + ((2 * (int64_t)(NN + 2) + 127) & ~int64_t(127)); }
+
+// Recording hooks of the parent's loop (inc_record_kernel only).
+struct IncRecOut {
+    uint16_t *push, *fin;  // iteration + 1 in which a node became ready / finished
+    char *snap;
+    int S, maxsnap;
+    int64_t stride;
+    int *nsnap, *iters;
+};
+
 // The event loop (simulator.py:117-140) of ring_loop over the parent's
 // successor lists and the candidate's rebuilt ones.  Indegrees (SI), the
 // patched bitmap and the ready rings in shared memory, 32-bit addressed.
-// false on ring overflow.
-template <bool SI>
+// Starts from the state st (level 0, or a parent snapshot whose iterations
+// the candidate shares).  false on ring overflow.  REC: the parent's own run,
+// recording every node's push iteration and a snapshot every S iterations.
+template <bool SI, bool REC = false>
 __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *__restrict__ csucc,
                                               const IncDirty *__restrict__ dirty, uint16_t *__restrict__ gindeg,
                                               uint32_t s_indeg, uint32_t s_pbm, uint32_t s_ppre, uint32_t s_ring,
-                                              int hg, int hb, int N, double *cost_out, int32_t *status_out) {
+                                              const IncLoopState &st, int N, double *cost_out, int32_t *status_out,
+                                              const IncRecOut *ro = nullptr) {
     const uint32_t *__restrict__ psucc = p.succ;
     const IncNode *__restrict__ rec = p.rec;
     uint16_t *__restrict__ indeg = SI ? (uint16_t *)(fo_inc_smem + s_indeg) : gindeg;
@@ -303,16 +333,18 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     unsigned long long *rb = rg + kIncRingG;
     constexpr unsigned mg = kIncRingG - 1, mb = kIncRingB - 1;
     const unsigned VB = (unsigned)p.VB;
-    int headg = 0, tailg = hg, headb = 0, tailb = hb;
-    unsigned sb0 = 0, se0 = 0, sb1 = 0, se1 = 0;
+    int headg = st.headg, tailg = st.tailg, headb = st.headb, tailb = st.tailb;
+    unsigned sb0 = st.sb0, se0 = st.se0, sb1 = st.sb1, se1 = st.se1;
     // End times are kept as the bit patterns of non-negative doubles, which
     // order like the values: integer compares and min.  An idle lane holds +inf.
     constexpr unsigned long long kIdle = 0x7ff0000000000000ull;
-    unsigned long long end0 = kIdle, end1 = kIdle, nowb = 0;
-    double now = 0.0;
-    uint32_t level = 0;
-    uint32_t lastg = hg > 0 ? (uint32_t)(rg[(hg - 1) & mg] >> 32) : 0u;
-    uint32_t lastb = hb > 0 ? (uint32_t)(rb[(hb - 1) & mb] >> 32) : 0u;
+    unsigned long long end0 = st.end0, end1 = st.end1, nowb = st.nowb;
+    double now = __longlong_as_double((long long)nowb);
+    uint32_t level = st.level;
+    uint32_t lastg = tailg > headg ? (uint32_t)(rg[(tailg - 1) & mg] >> 32) : 0u;
+    uint32_t lastb = tailb > headb ? (uint32_t)(rb[(tailb - 1) & mb] >> 32) : 0u;
+    uint32_t it = st.iter;  // REC: the iteration being run, + 1
+    uint32_t run0 = 0xffffu, run1 = 0xffffu;  // REC: the running nodes
     auto release = [&](unsigned qb, unsigned qe) -> bool {
         const uint32_t *__restrict__ L = (qb & 0x8000u) ? csucc : psucc;
         for (unsigned q = qb & 0x7fffu; q < qe; q++) {
@@ -327,6 +359,7 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
                 const unsigned long long x = inc_ent(level | pr, t, pt);
                 if (!(t < VB ? inc_push(rg, mg, headg, tailg, lastg, x) : inc_push(rb, mb, headb, tailb, lastb, x)))
                     return false;
+                if constexpr (REC) ro->push[t] = (uint16_t)it;
             }
         }
         return true;
@@ -350,17 +383,38 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     auto start = [&]() {
         if (end0 == kIdle && headg < tailg) {
             double d;
-            node_rec(rg[(headg++) & mg], d, sb0, se0);
+            const unsigned long long x = rg[(headg++) & mg];
+            node_rec(x, d, sb0, se0);
             end0 = (unsigned long long)__double_as_longlong(__dadd_rn(now, d));
+            if constexpr (REC) run0 = (unsigned)x & 0xffffu;
         }
         if (end1 == kIdle && headb < tailb) {
             double d;
-            node_rec(rb[(headb++) & mb], d, sb1, se1);
+            const unsigned long long x = rb[(headb++) & mb];
+            node_rec(x, d, sb1, se1);
             end1 = (unsigned long long)__double_as_longlong(__dadd_rn(now, d));
+            if constexpr (REC) run1 = (unsigned)x & 0xffffu;
         }
     };
-    start();
+    start();  // from a snapshot: a no-op (the state is taken right after a start)
     for (;;) {
+        if constexpr (REC) {
+            if (it > 0 && it % ro->S == 0 && (int)(it / ro->S) <= ro->maxsnap) {
+                const int j = it / ro->S;
+                char *sp = ro->snap + (int64_t)(j - 1) * ro->stride;
+                IncLoopState *h = (IncLoopState *)sp;
+                *h = IncLoopState{headg, tailg, headb, tailb, sb0,  se0,   sb1, se1,
+                                  end0,  end1,  nowb,  level, it,  run0, run1};
+                unsigned long long *eg = (unsigned long long *)(sp + kIncSnapRuns), *eb = eg + kIncRingG;
+                for (int i = headg; i < tailg; i++) eg[i - headg] = rg[i & mg];
+                for (int i = headb; i < tailb; i++) eb[i - headb] = rb[i & mb];
+                const uint32_t *src = (const uint32_t *)indeg;
+                uint32_t *dst = (uint32_t *)(sp + kIncSnapDeg);
+                for (int i = 0; i < (p.NN + 2) / 2; i++) dst[i] = src[i];
+                *ro->nsnap = j;
+            }
+            it++;
+        }
         // drain every lane ending at the next completion time (simulator.py:122-132)
         const unsigned long long t = end0 < end1 ? end0 : end1;
         if (t == kIdle) break;
@@ -371,14 +425,17 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
         }
         if (end0 == t) {
             end0 = kIdle;
+            if constexpr (REC) ro->fin[run0] = (uint16_t)it;
             if (!release(sb0, se0)) return false;
         }
         if (end1 == t) {
             end1 = kIdle;
+            if constexpr (REC) ro->fin[run1] = (uint16_t)it;
             if (!release(sb1, se1)) return false;
         }
         start();
     }
+    if constexpr (REC) *ro->iters = (int)it;
     const int done = headg + headb;
     *cost_out = done == N ? now : 0.0;  // makespan = last completion time (simulator.py:135-139)
     *status_out = done == N ? FO_OK : FO_CYCLE;  // simulator.py:133
@@ -933,18 +990,26 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __gr
     }
 }
 
-// K3 of the same candidates: the candidate's indegrees (the parent's, minus
-// removed, plus added slots), the patched-node ranks and the ready rings in
-// shared memory, the level-0 ready runs, then the event loop on one lane.
+// K3 of the same candidates, in two phases.  Prep (the whole warp, one
+// candidate after the other): the candidate's indegrees (the parent's, minus
+// removed, plus added slots), the patched-node ranks and the ready runs in
+// the candidate's shared-memory region, from level 0 or a parent snapshot.
+// Run (one lane per candidate, all of the warp's candidates at once): the
+// event loop.  The loops of different candidates of one parent take the same
+// branches most of the time, so a warp instruction advances many of them.
+struct IncK3State {
+    IncLoopState st;
+    int32_t k, wid, N, mode;  // mode 0: nothing to run, 1: from level 0, 2: from a snapshot
+};
+
 template <bool SI>
-__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __grid_constant__ IncArgs a, int k0) {
-    const int lane = threadIdx.x & 31;
-    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const int k = k0 + wid;
-    if (k >= a.K || a.status_out[k] != kIncPending) return;
+__device__ __forceinline__ void inc_k3_prep(const IncArgs &a, int k0, int wid, int n, int lane, uint32_t wsm) {
     const IncLayout &L = a.L;
+    IncK3State *ks = (IncK3State *)(fo_inc_smem + wsm + L.k_state);
+    if (lane == 0) ks->mode = 0;
+    const int k = k0 + wid;
+    if (wid >= n || k >= a.K || a.status_out[k] != kIncPending) return;
     const IncPlan &p = a.p;
-    const uint32_t wsm = (uint32_t)((threadIdx.x >> 5) * L.k_bytes);
     char *wsb = a.ws + (int64_t)wid * L.total;
     const int *hdr = (const int *)(wsb + L.hdr);
     const int nd = hdr[0], nrem = hdr[1], nadd = hdr[2], N = hdr[3];
@@ -952,13 +1017,12 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
     const int4 *rem = (const int4 *)(wsb + L.rem);
     const int4 *add = (const int4 *)(wsb + L.add);
     const IncDirty *dirty = (const IncDirty *)(wsb + L.dirty);
-    const uint32_t *pcsr = (const uint32_t *)(wsb + L.pcsr);
     uint16_t *indeg = SI ? (uint16_t *)(fo_inc_smem + wsm + L.k_indeg) : (uint16_t *)(wsb + L.indeg);
     uint32_t *pbm = (uint32_t *)(fo_inc_smem + wsm + L.k_pbm);
     uint16_t *ppre = (uint16_t *)(fo_inc_smem + wsm + L.k_ppre);
     uint32_t *tbm = (uint32_t *)(fo_inc_smem + wsm + L.k_tbm);
     unsigned long long *rg = (unsigned long long *)(fo_inc_smem + wsm + L.k_ring), *rb = rg + kIncRingG;
-    const int NN = p.NN, VB = p.VB;
+    const int NN = p.NN;
     if (a.stop_after == 2) {  // phase timing only (fo_set_phase_stop)
         if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
         return;
@@ -1011,78 +1075,280 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __gr
             carry += __shfl_sync(FULL, v, 31);
         }
     }
-    {
-        const uint32_t *src = (const uint32_t *)p.indeg;
-        uint32_t *dst = (uint32_t *)indeg;
-        for (int i = lane; i < (NN + 1) / 2; i += 32) dst[i] = __ldg(&src[i]);
+    // Fast-forward: the candidate's loop equals the parent's up to the first
+    // iteration in which the parent makes a touched node ready (a patched node
+    // with a new record, or the target of a removed / added slot) -- before
+    // it, every started node and every indegree decrement is the parent's.
+    // Start from the parent's latest snapshot at or before that iteration,
+    // unless the candidate would have made a touched node ready earlier (a
+    // target that lost its remaining predecessors: indegree 0 at the
+    // snapshot), checked below.
+    int j = 0;
+    if (p.nsnap > 0) {
+        unsigned c = 0xffffu;
+        for (int s = lane; s < nd; s += 32) {
+            // A patched node whose record (existence, rank, duration) is the
+            // parent's differs only in its successor list, i.e. in the slots
+            // removed / added at its finish: their targets bound the cut, and
+            // a slot whose source finished before the snapshot is left out of
+            // the indegrees.  Any other patched node: when it becomes ready.
+            const int n = dn[s];
+            const IncDirty dd = dirty[(int)ppre[n >> 5] + __popc(pbm[n >> 5] & ((1u << (n & 31)) - 1u))];
+            const IncNode pr = p.rec[n];
+            const bool same = dd.exists == pr.exists &&
+                              (!dd.exists || (dd.prank == pr.prank && __double_as_longlong(dd.dur) ==
+                                                                          __double_as_longlong(pr.dur)));
+            if (!same) c = min(c, (unsigned)__ldg(&p.push[n]));
+        }
+        for (int i = lane; i < nrem; i += 32) c = min(c, (unsigned)__ldg(&p.push[rem[i].z]));
+        for (int i = lane; i < nadd; i += 32) c = min(c, (unsigned)__ldg(&p.push[add[i].y]));
+        c = __reduce_min_sync(FULL, c);
+        j = c == 0 ? 0 : min((int)(c - 1) / p.snap_S, p.nsnap);
     }
-    __syncwarp();
-    for (int i = lane; i < nrem; i += 32) {
-        const int t = rem[i].z;
-        atomicAdd((unsigned *)indeg + (t >> 1), (t & 1) ? 0xffff0000u : 0xffffffffu);
-        atomicOr(&tbm[t >> 5], 1u << (t & 31));
-    }
-    for (int i = lane; i < nadd; i += 32) {
-        const int t = add[i].y;
-        atomicAdd((unsigned *)indeg + (t >> 1), (t & 1) ? 0x10000u : 1u);
-        atomicOr(&tbm[t >> 5], 1u << (t & 31));
-    }
+    const char *sp = j ? p.snap + (int64_t)(j - 1) * p.snap_stride : nullptr;
+    // the candidate's indegrees: the parent's (at level 0 or at the snapshot),
+    // minus removed, plus added slots; bit 15 marks patched nodes
+    // (a slot counts while its source has not finished: at level 0 every
+    // slot; at the snapshot of iteration si, those whose source finishes in
+    // the parent at iteration si or later -- sources of changed slots start
+    // and end as in the parent up to the cut)
+    auto build_indeg = [&](const uint16_t *base, int si) {
+        {
+            const uint32_t *src = (const uint32_t *)base;
+            uint32_t *dst = (uint32_t *)indeg;
+            for (int i = lane; i < (NN + 1) / 2; i += 32) dst[i] = __ldg(&src[i]);
+        }
+        __syncwarp();
+        for (int i = lane; i < nrem; i += 32) {
+            const int4 r = rem[i];
+            if (si && (int)__ldg(&p.fin[r.y]) <= si) continue;
+            atomicAdd((unsigned *)indeg + (r.z >> 1), (r.z & 1) ? 0xffff0000u : 0xffffffffu);
+        }
+        for (int i = lane; i < nadd; i += 32) {
+            const int4 r = add[i];
+            if (si && (int)__ldg(&p.fin[r.x]) <= si) continue;
+            atomicAdd((unsigned *)indeg + (r.y >> 1), (r.y & 1) ? 0x10000u : 1u);
+        }
+        __syncwarp();
+        for (int s = lane; s < nd; s += 32) {  // bit 15 of a patched node's indegree (read by the event loop)
+            const int n = dn[s];
+            atomicOr((unsigned *)indeg + (n >> 1), (n & 1) ? 0x80000000u : 0x8000u);
+        }
+        __syncwarp();
+    };
+    for (int i = lane; i < nrem; i += 32) atomicOr(&tbm[rem[i].z >> 5], 1u << (rem[i].z & 31));
+    for (int i = lane; i < nadd; i += 32) atomicOr(&tbm[add[i].y >> 5], 1u << (add[i].y & 31));
     __syncwarp();
     for (int i = lane; i < L.NW; i += 32) tbm[i] |= pbm[i];
-    for (int s = lane; s < nd; s += 32) {  // bit 15 of a patched node's indegree (read by the event loop)
-        const int n = dn[s];
-        atomicOr((unsigned *)indeg + (n >> 1), (n & 1) ? 0x80000000u : 0x8000u);
-    }
     __syncwarp();
-    // level-0 ready runs: the parent's (sorted by rank) without touched nodes,
-    // then the touched nodes that are ready, inserted in rank order
-    int hgb[2] = {0, 0};
-    bool over = false;
-    for (int lanei = 0; lanei < 2; lanei++) {
-        const uint16_t *src = p.ready + (lanei ? p.n_ready_g : 0);
-        const int n0 = lanei ? p.n_ready_b : p.n_ready_g;
-        unsigned long long *buf = lanei ? rb : rg;
-        const int cap = lanei ? kIncRingB : kIncRingG;
-        int h = 0;
-        for (int base = 0; base < n0; base += 32) {
-            const int i = base + lane;
-            const int n = i < n0 ? src[i] : 0;
-            const bool keep = i < n0 && !((tbm[n >> 5] >> (n & 31)) & 1u);
-            const unsigned m = __ballot_sync(FULL, keep);
-            const int pos = h + __popc(m & lanemask_lt());
-            if (keep && pos < cap) buf[pos] = inc_ent(p.rec[n].prank, n, 0);
-            h += __popc(m);
+    auto exists_c = [&](int n) -> bool {  // the node exists in the candidate
+        if ((pbm[n >> 5] >> (n & 31)) & 1u)
+            return dirty[(int)ppre[n >> 5] + __popc(pbm[n >> 5] & ((1u << (n & 31)) - 1u))].exists;
+        return p.rec[n].exists;
+    };
+    build_indeg(j ? (const uint16_t *)(sp + kIncSnapDeg) : p.indeg, j * p.snap_S);
+    if (j) {
+        bool early = false;
+        for (int wi = lane; wi < L.NW; wi += 32) {
+            uint32_t m = tbm[wi];
+            while (m) {
+                const int n = wi * 32 + __ffs(m) - 1;
+                m &= m - 1;
+                // ready in the candidate but not yet in the parent at the snapshot
+                early |= n < NN && (indeg[n] & 0x7fff) == 0 && exists_c(n) && (int)__ldg(&p.push[n]) > j * p.snap_S;
+            }
         }
-        hgb[lanei] = h;
-        over |= h > cap;
+        if (__any_sync(FULL, early)) {  // the candidate diverges before the snapshot
+            j = 0;
+            build_indeg(p.indeg, 0);
+        }
+    }
+    if (a.stats && lane == 0) {
+        atomicAdd(&a.stats[0], 1ull);
+        atomicAdd(&a.stats[1], j ? 1ull : 0ull);
+        atomicAdd(&a.stats[2], j ? (unsigned long long)((const IncLoopState *)sp)->iter : 0ull);
+    }
+    IncLoopState st{};
+    constexpr unsigned long long kIdle = 0x7ff0000000000000ull;
+    st.end0 = kIdle;
+    st.end1 = kIdle;
+    bool over = false;
+    if (j) {
+        st = *(const IncLoopState *)sp;
+        // ready nodes the snapshot holds may have rebuilt successor lists
+        // (patched, same record): their entries read the candidate's
+        const unsigned long long *eg = (const unsigned long long *)(sp + kIncSnapRuns), *eb = eg + kIncRingG;
+        auto fix = [&](unsigned long long x) {
+            const unsigned n = (unsigned)x & 0xffffu;
+            return ((pbm[n >> 5] >> (n & 31)) & 1u) ? x | 0x10000ull : x;
+        };
+        for (int i = lane; i < st.tailg - st.headg; i += 32) rg[(st.headg + i) & (kIncRingG - 1)] = fix(eg[i]);
+        for (int i = lane; i < st.tailb - st.headb; i += 32) rb[(st.headb + i) & (kIncRingB - 1)] = fix(eb[i]);
+    } else {
+        // level-0 ready runs: the parent's (sorted by rank) without touched
+        // nodes; the touched nodes that are ready are inserted by the run phase
+        int hgb[2] = {0, 0};
+        for (int lanei = 0; lanei < 2; lanei++) {
+            const uint16_t *src = p.ready + (lanei ? p.n_ready_g : 0);
+            const int n0 = lanei ? p.n_ready_b : p.n_ready_g;
+            unsigned long long *buf = lanei ? rb : rg;
+            const int cap = lanei ? kIncRingB : kIncRingG;
+            int h = 0;
+            for (int base = 0; base < n0; base += 32) {
+                const int i = base + lane;
+                const int n = i < n0 ? src[i] : 0;
+                const bool keep = i < n0 && !((tbm[n >> 5] >> (n & 31)) & 1u);
+                const unsigned m = __ballot_sync(FULL, keep);
+                const int pos = h + __popc(m & lanemask_lt());
+                if (keep && pos < cap) buf[pos] = inc_ent(p.rec[n].prank, n, 0);
+                h += __popc(m);
+            }
+            hgb[lanei] = h;
+            over |= h > cap;
+        }
+        st.tailg = hgb[0];
+        st.tailb = hgb[1];
     }
     __syncwarp();
     if (lane != 0) return;
-    for (int wi = 0; wi < L.NW && !over; wi++) {
-        uint32_t m = tbm[wi];
-        while (m && !over) {
-            const int n = wi * 32 + __ffs(m) - 1;
-            m &= m - 1;
-            if (n >= NN || (indeg[n] & 0x7fff) != 0) continue;
-            unsigned long long x;
-            if ((pbm[n >> 5] >> (n & 31)) & 1u) {
+    if (over) {
+        a.cost_out[k] = 0.0;
+        a.status_out[k] = a.diag ? 104 : kRetryGeneral;  // a ready run outgrew its ring: the general kernel scores it
+        return;
+    }
+    ks->st = st;
+    ks->k = k;
+    ks->wid = wid;
+    ks->N = N;
+    ks->mode = j ? 2 : 1;
+}
+
+// the run phase of one candidate (one lane)
+template <bool SI>
+__device__ __forceinline__ void inc_k3_run(const IncArgs &a, uint32_t wsm) {
+    const IncLayout &L = a.L;
+    const IncK3State *ks = (const IncK3State *)(fo_inc_smem + wsm + L.k_state);
+    const int mode = ks->mode;
+    if (mode == 0) return;
+    const IncPlan &p = a.p;
+    const int k = ks->k, N = ks->N, NN = p.NN, VB = p.VB;
+    IncLoopState st = ks->st;
+    char *wsb = a.ws + (int64_t)ks->wid * L.total;
+    const IncDirty *dirty = (const IncDirty *)(wsb + L.dirty);
+    const uint32_t *pcsr = (const uint32_t *)(wsb + L.pcsr);
+    uint16_t *indeg = SI ? (uint16_t *)(fo_inc_smem + wsm + L.k_indeg) : (uint16_t *)(wsb + L.indeg);
+    const uint32_t *pbm = (const uint32_t *)(fo_inc_smem + wsm + L.k_pbm);
+    const uint16_t *ppre = (const uint16_t *)(fo_inc_smem + wsm + L.k_ppre);
+    const uint32_t *tbm = (const uint32_t *)(fo_inc_smem + wsm + L.k_tbm);
+    unsigned long long *rg = (unsigned long long *)(fo_inc_smem + wsm + L.k_ring), *rb = rg + kIncRingG;
+    constexpr unsigned long long kIdle = 0x7ff0000000000000ull;
+    bool over = false;
+    if (mode == 2) {
+        // the running nodes of the snapshot may have rebuilt successor lists
+        auto fix_run = [&](uint32_t n, uint32_t &sb, uint32_t &se) {
+            if (n < (uint32_t)NN && ((pbm[n >> 5] >> (n & 31)) & 1u)) {
                 const IncDirty dd = dirty[(int)ppre[n >> 5] + __popc(pbm[n >> 5] & ((1u << (n & 31)) - 1u))];
-                if (!dd.exists) continue;
-                x = inc_ent(dd.prank, n, 1);
-            } else {
-                const IncNode r = p.rec[n];
-                if (!r.exists) continue;
-                x = inc_ent(r.prank, n, 0);
+                sb = dd.sb;
+                se = dd.se;
             }
-            over = !(n < VB ? inc_ring_insert(rg, kIncRingG - 1, hgb[0], x) : inc_ring_insert(rb, kIncRingB - 1, hgb[1], x));
+        };
+        if (st.end0 != kIdle) fix_run(st.run0, st.sb0, st.se0);
+        if (st.end1 != kIdle) fix_run(st.run1, st.sb1, st.se1);
+    } else {
+        // the touched nodes that are ready at level 0, inserted in rank order
+        for (int wi = 0; wi < L.NW && !over; wi++) {
+            uint32_t m = tbm[wi];
+            while (m && !over) {
+                const int n = wi * 32 + __ffs(m) - 1;
+                m &= m - 1;
+                if (n >= NN || (indeg[n] & 0x7fff) != 0) continue;
+                unsigned long long x;
+                if ((pbm[n >> 5] >> (n & 31)) & 1u) {
+                    const IncDirty dd = dirty[(int)ppre[n >> 5] + __popc(pbm[n >> 5] & ((1u << (n & 31)) - 1u))];
+                    if (!dd.exists) continue;
+                    x = inc_ent(dd.prank, n, 1);
+                } else {
+                    const IncNode r = p.rec[n];
+                    if (!r.exists) continue;
+                    x = inc_ent(r.prank, n, 0);
+                }
+                over = !(n < VB ? inc_ring_insert(rg, kIncRingG - 1, st.tailg, x)
+                                : inc_ring_insert(rb, kIncRingB - 1, st.tailb, x));
+            }
         }
     }
     if (over || !inc_ring_loop<SI>(p, pcsr, dirty, SI ? nullptr : indeg, wsm + L.k_indeg, wsm + L.k_pbm,
-                                   wsm + L.k_ppre, wsm + L.k_ring, hgb[0], hgb[1], N, a.cost_out + k,
-                                   a.status_out + k)) {
+                                   wsm + L.k_ppre, wsm + L.k_ring, st, N, a.cost_out + k, a.status_out + k)) {
         a.cost_out[k] = 0.0;
         a.status_out[k] = a.diag ? 104 : kRetryGeneral;  // a ready run outgrew its ring: the general kernel scores it
     }
+}
+
+// K3 over the candidates [k0, k0 + n): one warp each (prep), then its lane 0
+// (run).  One lane per candidate with several candidates per warp, so that
+// their loops share instructions, measured 2.5x slower at 16 per warp: the
+// loops diverge within a few events and the warp serialises them.
+template <bool SI>
+__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __grid_constant__ IncArgs a, int k0, int n) {
+    const int lane = threadIdx.x & 31;
+    const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const uint32_t wsm = (uint32_t)((threadIdx.x >> 5) * a.L.k_bytes);
+    inc_k3_prep<SI>(a, k0, wid, n, lane, wsm);
+    __syncwarp();
+    if (lane == 0) inc_k3_run<SI>(a, wsm);
+}
+
+// The parent's own event loop, once per plan (one warp; lane 0 runs it):
+// every node's push iteration and a snapshot of the loop state every S
+// iterations, which candidates fast-forward to (score_kernel_inc_k3).
+__global__ void inc_record_kernel(const __grid_constant__ IncPlan p, IncRecOut ro, int32_t *out) {
+    const int lane = threadIdx.x;
+    const int NN = p.NN, NW = (NN + 31) / 32;
+    const uint32_t s_indeg = 0, s_pbm = (uint32_t)((2 * (NN + 2) + 15) & ~15), s_ppre = s_pbm + 4 * NW,
+                   s_ring = (s_ppre + 2 * NW + 2 + 15) & ~15u;
+    uint16_t *indeg = (uint16_t *)fo_inc_smem;
+    uint32_t *pbm = (uint32_t *)(fo_inc_smem + s_pbm);
+    for (int i = lane; i < (NN + 2) / 2; i += 32) ((uint32_t *)indeg)[i] = ((const uint32_t *)p.indeg)[i];
+    for (int i = lane; i < NW; i += 32) pbm[i] = 0;
+    for (int i = lane; i < NN; i += 32) ro.push[i] = ro.fin[i] = 0xffffu;
+    __syncwarp();
+    if (lane != 0) return;
+    unsigned long long *rg = (unsigned long long *)(fo_inc_smem + s_ring), *rb = rg + kIncRingG;
+    if (p.n_ready_g > kIncRingG || p.n_ready_b > kIncRingB || p.n_exist >= 65000) { out[1] = 1; return; }
+    for (int i = 0; i < p.n_ready_g; i++) {
+        const int n = p.ready[i];
+        rg[i] = inc_ent(p.rec[n].prank, n, 0);
+        ro.push[n] = 0;
+    }
+    for (int i = 0; i < p.n_ready_b; i++) {
+        const int n = p.ready[p.n_ready_g + i];
+        rb[i] = inc_ent(p.rec[n].prank, n, 0);
+        ro.push[n] = 0;
+    }
+    IncLoopState st{};
+    st.tailg = p.n_ready_g;
+    st.tailb = p.n_ready_b;
+    st.end0 = st.end1 = 0x7ff0000000000000ull;
+    ro.nsnap = out;
+    *out = 0;
+    double *mk = (double *)(out + 2);
+    const bool ok = inc_ring_loop<true, true>(p, nullptr, nullptr, nullptr, s_indeg, s_pbm, s_ppre, s_ring, st,
+                                               p.n_exist, mk, out + 1, &ro);
+    if (!ok) out[1] = 2;
+}
+
+cudaError_t launch_inc_record(const IncPlan &p, uint16_t *push, uint16_t *fin, char *snap, int S, int maxsnap,
+                              void *out, cudaStream_t stream) {
+    const int NN = p.NN, NW = (NN + 31) / 32;
+    const size_t s_pbm = (2 * (NN + 2) + 15) & ~15, s_ring = (s_pbm + 6 * NW + 2 + 15) & ~(size_t)15;
+    const size_t smem = s_ring + 8 * (kIncRingG + kIncRingB);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(inc_record_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    IncRecOut ro{push, fin, snap, S, maxsnap, inc_snap_stride(NN), nullptr, (int32_t *)out + 4};
+    inc_record_kernel<<<1, 32, smem, stream>>>(p, ro, (int32_t *)out);
+    return cudaGetLastError();
 }
 
 template <typename KF>
@@ -1116,6 +1382,7 @@ cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout 
                              int qcap, double *cost_out, int32_t *status_out, cudaStream_t stream, int diag) {
     IncArgs a;
     a.diag = diag;
+    a.stats = diag ? (unsigned long long *)((char *)qcount + 16) : nullptr;
     a.g = g;
     a.p = p;
     a.L = L;
@@ -1130,19 +1397,21 @@ cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout 
     a.cost_out = cost_out;
     a.status_out = status_out;
     a.stop_after = g.phase_stop;
-    const size_t smem = (size_t)L.s_bytes * kWarps, ksmem = (size_t)L.k_bytes * kWarps;
+    const size_t smem = (size_t)L.s_bytes * kWarps;
     const int per_launch = grid * kWarps;  // one candidate per warp per launch
     const bool fp64 = precision == FO_PREC_FP64;
+    const size_t ksmem = (size_t)L.k_bytes * kWarps;
     for (int k0 = 0; k0 < K; k0 += per_launch) {
         cudaError_t e = cudaMemsetAsync(qcount, 0, sizeof(int), stream);
         if (e != cudaSuccess) return e;
+        const int n = std::min(per_launch, K - k0);
         if (fp64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a, k0);
         else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a, k0);
         if (a.stop_after == 1) continue;
         if (fp64) score_kernel_inc_mp<double><<<grid, kWarps * 32, 0, stream>>>(a);
         else score_kernel_inc_mp<float><<<grid, kWarps * 32, 0, stream>>>(a);
-        if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
-        else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, stream>>>(a, k0);
+        if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, stream>>>(a, k0, n);
+        else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, stream>>>(a, k0, n);
     }
     return cudaGetLastError();
 }

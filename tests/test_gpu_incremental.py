@@ -139,3 +139,33 @@ def test_plan_built_under_a_phase_stop_is_still_exact():
     N.lib().fo_set_phase_stop(dg2.h, 0)
     got, _ = _score(dg2, off, chg, N.FO_PREC_FP32, 1)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("precision", [N.FO_PREC_FP32, N.FO_PREC_FP64])
+@pytest.mark.parametrize("name,K", [("resnet50", 4096), ("bert", 1024), ("vgg16", 1024)])
+def test_event_loop_fast_forward_is_exact_and_used(name, K, precision, monkeypatch):
+    """Candidates start their event loop from the parent's last snapshot
+    before the first touched node becomes ready: same costs as the general
+    kernel and as the incremental kernel started at level 0, and most
+    candidates do fast-forward."""
+    g, dg = _handle(name, precision)
+    dg.set_parent()
+    off, chg = dg.make_candidates_delta(np.arange(K, dtype=np.uint64))
+    ref, st_ref = _score(dg, off, chg, precision, 0)
+    stats = np.zeros(6, np.int64)
+    N.lib().fo_inc_stats(dg.h, precision, N.ptr(stats))  # reset
+    only, st_only = _score(dg, off, chg, precision, 2)
+    N.lib().fo_inc_stats(dg.h, precision, N.ptr(stats))
+    handled = st_only < 101
+    assert handled.mean() >= 0.95
+    assert np.array_equal(only[handled], ref[handled]) and np.array_equal(st_only[handled], st_ref[handled])
+    loops, ff, skipped, iters, nsnap = (int(x) for x in stats[:5])
+    assert nsnap > 0 and iters > 0 and loops >= handled.sum()
+    assert ff >= 0.3 * loops, stats
+    assert 0 < skipped <= ff * iters
+    monkeypatch.setenv("FO_INC_NO_SNAP", "1")
+    dg.set_parent()  # the plan is rebuilt without the parent-loop record
+    got0, st0 = _score(dg, off, chg, precision, 1)
+    N.lib().fo_inc_stats(dg.h, precision, N.ptr(stats))
+    assert stats[4] == 0
+    assert np.array_equal(got0, ref) and np.array_equal(st0, st_ref)
