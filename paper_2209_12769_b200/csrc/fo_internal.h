@@ -187,7 +187,7 @@ struct IncLayout {  // per-warp global scratch (byte offsets) and shared-memory 
     int32_t ring_g, ring_b;  // ready-run ring sizes (powers of two >= the nodes of each lane: no overflow)
     int32_t s_indeg, s_pbm, s_abm, s_lbm, s_tbm, s_ppre, s_cbm, s_cnt, s_bytes;  // setup kernel smem (per warp)
     int32_t k_indeg, k_pbm, k_ppre, k_tbm, k_ring, k_state, k_bytes;  // event-loop kernel smem (k_indeg < 0: global)
-    int32_t NW, CW, RW, s_rbm, s_chg, s_cpre;
+    int32_t NW, CW, RW, s_rbm, s_chg, s_cpre, s_acnt;
 };
 constexpr int kIncMaxChg = 64, kIncMaxOps = 256, kIncMaxDirty = 192;
 constexpr int kRetryGeneral = 101;  // internal status: the incremental kernel hands the candidate to score_kernel

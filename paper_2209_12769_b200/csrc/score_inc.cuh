@@ -93,6 +93,7 @@ IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     L.s_rbm = stake(4 * L.RW);         // removed parent successor positions
     L.s_chg = stake(8 * kIncMaxChg);   // the sorted changes
     L.s_cpre = stake(L.CW + 4);        // their bitmap word prefix
+    L.s_acnt = stake(4 * kIncMaxDirty); // added slots per patched node
     L.s_bytes = s;
     s = 0;
     L.k_indeg = smem_indeg ? stake(2 * (NN + 2)) : -1;
@@ -150,6 +151,7 @@ struct IncCtx {
     uint16_t *indeg;
     uint32_t *pbm, *abm, *lbm, *tbm, *cbm, *rbm;
     uint8_t *cpre;  // changed-index bitmap word prefix (<= 64 changes)
+    uint32_t *acnt; // per patched rank: added slots, then their fill cursor
     uint16_t *ppre;
     int *cnt;
     int *hdr;  // hand-off from the setup kernel to the event-loop kernel: nd, nrem, nadd, N
@@ -828,27 +830,40 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
         if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = FO_OK; }
         return;
     }
-    // ---- rebuilt successor lists of list-patched nodes
+    // ---- rebuilt successor lists of list-patched nodes: the parent's entries
+    // that stay, then the node's added slots (in any order: the event loop
+    // orders ready entries by key).  Added slots are counted and placed per
+    // source rank, one lane per slot.
+    uint32_t *acnt = c.acnt;
+    for (int r = lane; r < nd; r += 32) acnt[r] = 0;
+    __syncwarp();
+    for (int i = lane; i < nadd; i += 32) atomicAdd(&acnt[irank(c, c.add[i].x)], 1u);
+    __syncwarp();
     for (int s = lane; s < nd; s += 32) {
         const int n = c.dn[s];
         if (!ibit(c.lbm, n)) continue;
+        const int r = irank(c, n);
         const IncNode pr = p.rec[n];
-        int cnt = 0;
-        for (int q = pr.sb; q < pr.se; q++) cnt += !ibit(c.rbm, q);
-        for (int i = 0; i < nadd; i++) cnt += c.add[i].x == n;
+        int keep = 0;
+        for (int q = pr.sb; q < pr.se; q++) keep += !ibit(c.rbm, q);
+        const int cnt = keep + (int)acnt[r];
         const int o0 = atomicAdd(&c.cnt[kCPcsr], cnt);
         if (o0 + cnt > L.pcsr_cap) { ifail(c, 10); continue; }
         int o = o0;
         for (int q = pr.sb; q < pr.se; q++)
             if (!ibit(c.rbm, q)) c.pcsr[o++] = p.succ[q];
-        for (int i = 0; i < nadd; i++)
-            if (c.add[i].x == n) {
-                // the parent's rank (patched targets are re-ranked at release)
-                c.pcsr[o++] = ((uint32_t)c.add[i].z << 16) | (uint32_t)c.add[i].y;
-            }
-        IncDirty &dd = c.dirty[irank(c, n)];
+        acnt[r] = (uint32_t)o;  // where the added slots go
+        IncDirty &dd = c.dirty[r];
         dd.sb = (uint16_t)(0x8000 | o0);
         dd.se = (uint16_t)(o0 + cnt);
+    }
+    __syncwarp();
+    if (c.cnt[kCFail]) { retry(); return; }
+    for (int i = lane; i < nadd; i += 32) {
+        const int4 ad = c.add[i];
+        if (!ibit(c.lbm, ad.x)) { ifail(c, 10); continue; }
+        // the parent's rank (patched targets are re-ranked at release)
+        c.pcsr[atomicAdd(&acnt[irank(c, ad.x)], 1u)] = ((uint32_t)ad.z << 16) | (uint32_t)ad.y;
     }
     __syncwarp();
     if (c.cnt[kCFail]) { retry(); return; }
@@ -887,6 +902,7 @@ __device__ __forceinline__ IncCtx inc_ctx(const IncArgs &a, int wid, char *sm) {
     c.cpre = (uint8_t *)(sm + L.s_cpre);
     c.ppre = (uint16_t *)(sm + L.s_ppre);
     c.cbm = (uint32_t *)(sm + L.s_cbm);
+    c.acnt = (uint32_t *)(sm + L.s_acnt);
     c.cnt = (int *)(sm + L.s_cnt);
     c.nchg = 0;
     return c;
