@@ -49,5 +49,19 @@ for spec in specs:
         else:
             out["same_costs"] = bool(np.array_equal(ref, c))
         out[f"ms_team{team}"] = round(float(np.median(ts)), 4)
+        for ph in (1, 2):  # phase stops: after the contraction, after the estimator
+            N.lib().fo_set_phase_stop(dg.h, ph)
+            tp = []
+            for i in range(13):
+                N.lib().fo_memo_clear(dg.h, ctypes.c_void_p(s.cuda_stream))
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                dg.score_device(d[0], d[1], d[2], gb, cost, st, prec)
+                b.record()
+                torch.cuda.synchronize()
+                if i >= 3:
+                    tp.append(a.elapsed_time(b))
+            N.lib().fo_set_phase_stop(dg.h, 0)
+            out[f"ms_team{team}_stop{ph}"] = round(float(np.median(tp)), 4)
     os.environ.pop("FO_TEAM", None)
     print(json.dumps(out), flush=True)
