@@ -303,6 +303,12 @@ int fo_search_start(fo_search *s, double *best_cost_out);
  * R >= 2 the seeds run in two halves whose device batches overlap the other
  * half's host-side expand; each seed's step sequence is unchanged. */
 int fo_search_run(fo_search *s, int64_t max_rounds, int32_t *active_out);
+/* fo_search_run with a hook after every round (every seed advanced one step):
+ * fn(ctx, round, active, best[R], R) with the seeds' best costs so far -- the
+ * multi-GPU driver posts its per-round exchange from it.  A nonzero return
+ * stops the run with FO_INVALID_ARG.  fn must not call back into this handle. */
+typedef int32_t (*fo_round_fn)(void *ctx, int64_t round, int32_t active, const double *best, int32_t R);
+int fo_search_run_cb(fo_search *s, int64_t max_rounds, fo_round_fn fn, void *ctx, int32_t *active_out);
 /* Counters: steps, candidates_evaluated, candidates_enqueued, trace length. */
 int fo_search_result(fo_search *s, int32_t r, double *best_cost, int64_t *counters4, int32_t *best_ngid,
                      int32_t *best_rgid, int32_t *best_bkt, fo_trace_rec *trace, int64_t trace_cap);

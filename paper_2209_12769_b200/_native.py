@@ -92,6 +92,7 @@ SIGNATURES = [
     ("fo_search_round", C.c_int, [vp, P(C.c_int32), vp]),
     ("fo_search_start", C.c_int, [vp, vp]),
     ("fo_search_run", C.c_int, [vp, C.c_int64, P(C.c_int32)]),
+    ("fo_search_run_cb", C.c_int, [vp, C.c_int64, vp, vp, P(C.c_int32)]),
     ("fo_search_result", C.c_int, [vp, C.c_int32, P(C.c_double), vp, vp, vp, vp, P(TraceRec), C.c_int64]),
     ("fo_search_timing", C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int64)]),
     ("fo_search_rounds", C.c_int, [vp, P(C.c_int64)]),
@@ -124,6 +125,10 @@ def lib():
 def last_error() -> str:
     msg = lib().fo_last_error()
     return msg.decode() if msg else ""
+
+
+# fo_round_fn: int32 (void *ctx, int64 round, int32 active, const double *best, int32 R)
+ROUND_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_double), C.c_int32)
 
 
 def ptr(a):

@@ -1773,6 +1773,11 @@ struct fo_search {
     int64_t scored = 0, host_steps = 0;
     int64_t rounds = 0;  // device rounds run (fo_search_rounds)
     bool started = false;
+    fo_round_fn cb = nullptr;  // per-round hook of fo_search_run_cb
+    void *cb_ctx = nullptr;
+    int64_t cb_round = 0;
+    bool cb_stop = false;
+    std::vector<double> cb_best;
     bool spec = false;  // one-step speculation (latency-bound rounds: few seeds)
     int spec_at = -1;   // switch speculation on once this few seeds are active (-1: never)
 };
@@ -2122,6 +2127,20 @@ static int count_active(fo_search *S, double *best_cost_out) {
     return active;
 }
 
+// the per-round hook (fo_search_run_cb); false once it asked to stop
+static bool round_hook(fo_search *S) {
+    if (!S->cb) return true;
+    const int R = (int)S->seeds.size();
+    S->cb_best.resize(R);
+    int active = 0;
+    for (int r = 0; r < R; r++) {
+        S->cb_best[r] = S->seeds[r].best;
+        active += S->seeds[r].active;
+    }
+    if (S->cb(S->cb_ctx, S->cb_round++, active, S->cb_best.data(), R) != 0) S->cb_stop = true;
+    return !S->cb_stop;
+}
+
 extern "C" {
 
 int fo_search_create(fo_graph *g, const fo_search_cfg *cfg, const uint64_t *seeds, int32_t R, const int32_t *ngid0,
@@ -2217,6 +2236,7 @@ static int run_single(fo_search *S, int64_t limit, int &rc) {
         S->launch_ms += ms(t0, t1);
         S->wait_ms += ms(t1, t2);
         S->replay_ms += ms(t2, clk::now());
+        if (!round_hook(S)) return (int)it + 1;
     }
     return (int)it;
 }
@@ -2248,7 +2268,7 @@ static int run_pipelined(fo_search *S, int64_t limit, int &rc) {
         }
         auto t1 = clk::now();
         S->wait_ms += ms(t0, t1);
-        bool b_live = any_active(S, mid, R);
+        bool b_live = any_active(S, mid, R) && !S->cb_stop;
         if (b_live) {
             search_expand(S, mid, R);  // overlaps A's device batch
             auto t2 = clk::now();
@@ -2260,7 +2280,8 @@ static int run_pipelined(fo_search *S, int64_t limit, int &rc) {
         if ((rc = lane_wait(S, LA))) return (int)it;
         search_replay(S, LA, 0, mid);
         S->wait_ms += ms(t3, clk::now());
-        bool a_live = any_active(S, 0, mid);
+        round_hook(S);  // a round: half A done, half B's in flight
+        bool a_live = any_active(S, 0, mid) && !S->cb_stop;
         if (!a_live && !b_inflight) { it++; break; }
         if (a_live && (limit < 0 || it + 1 < limit)) {
             search_expand(S, 0, mid);  // overlaps B's device batch
@@ -2282,8 +2303,28 @@ static int run_pipelined(fo_search *S, int64_t limit, int &rc) {
     return (int)it;
 }
 
+static int search_run(fo_search *S, int64_t max_rounds, int32_t *active_out);
+
 int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
     if (!S) return fail(FO_INVALID_ARG, "null search");
+    return search_run(S, max_rounds, active_out);
+}
+
+int fo_search_run_cb(fo_search *S, int64_t max_rounds, fo_round_fn fn, void *ctx, int32_t *active_out) {
+    if (!S) return fail(FO_INVALID_ARG, "null search");
+    S->cb = fn;
+    S->cb_ctx = ctx;
+    S->cb_round = 0;
+    S->cb_stop = false;
+    const int rc = search_run(S, max_rounds, active_out);
+    const bool stopped = S->cb_stop;
+    S->cb = nullptr;
+    S->cb_ctx = nullptr;
+    if (rc) return rc;
+    return stopped ? fail(FO_INVALID_ARG, "the round callback stopped the search") : FO_OK;
+}
+
+static int search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
     fo_graph *g = S->g;
     std::lock_guard<std::mutex> lk(g->mu);
     cudaSetDevice(g->device);
@@ -2307,7 +2348,7 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
         it += n1;
         const double w1 = std::chrono::duration<double>(clk::now() - t0).count() / std::max(n1, 1);
         t0 = clk::now();
-        int n2 = run_pipelined(S, cap(left(it), probe), rc);
+        int n2 = S->cb_stop ? 0 : run_pipelined(S, cap(left(it), probe), rc);
         if (rc) return rc;
         it += n2;
         const double w2 = std::chrono::duration<double>(clk::now() - t0).count() / std::max(n2, 1);
@@ -2316,13 +2357,13 @@ int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
     // the rest in chunks, so speculation can switch on for the tail
     for (;;) {
         const int64_t rest = left(it);
-        if (rest == 0 || !any_active(S, 0, R)) break;
+        if (rest == 0 || !any_active(S, 0, R) || S->cb_stop) break;
         if (!S->spec && S->spec_at >= 0 && count_active(S, nullptr) <= S->spec_at) S->spec = true;
         const int64_t chunk = S->spec || S->spec_at < 0 ? rest : cap(rest, 32);
         const int n = pipeline && !S->spec ? run_pipelined(S, chunk, rc) : run_single(S, chunk, rc);
         if (rc) return rc;
         it += n;
-        if (n == 0) break;
+        if (n == 0 || S->cb_stop) break;
     }
     S->rounds += it;
     if (active_out) *active_out = count_active(S, nullptr);

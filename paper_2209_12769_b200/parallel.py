@@ -76,6 +76,7 @@ class ShardedSearch:
         self.seed_offset = lo
         self.s = LockstepSearch(g0, cfg, cp, self.local_seeds, precision, n_threads) if self.local_seeds else None
         self.best_history = []
+        self.lag = 8  # exchanges in flight before a rank waits for the oldest (run())
 
     def round(self, device) -> int:
         """One lock-stepped round on this rank's seeds, then the per-round
@@ -119,10 +120,10 @@ class ShardedSearch:
         shard natively to the end (fo_search_run, with its speculation and
         host/device pipelining) and exchanges once.
 
-        The stop decision is collective: every rank counts rounds in whole
-        blocks and the blocks' active-seed counts are all-reduced, so all ranks
-        leave after the same number of exchanges (a rank whose seeds finished
-        keeps joining the exchanges with an empty shard)."""
+        The exchanges are non-blocking and waited ``self.lag`` exchanges late
+        (_LaggedExchange); the stop decision is collective, so all ranks post
+        the same number of exchanges and leave together (a rank whose seeds
+        finished keeps joining them with 0 active seeds)."""
         import torch
 
         dist = _dist()
@@ -147,17 +148,133 @@ class ShardedSearch:
             return self.best_history[-1]
         if exchange_every < 1:
             raise ValueError("exchange_every must be >= 1")
-        rounds = 0
-        local_active = self.s.R if self.s is not None else 0
-        while True:
-            block = exchange_every if max_rounds is None else min(exchange_every, max_rounds - rounds)
-            for _ in range(block):
-                if local_active == 0:
-                    break
-                local_active = self.s.round()
-            rounds += block  # identical on every rank
-            c, i, total = self._exchange(device, local_active)
-            self.best_history.append((c, i))
-            if total == 0 or (max_rounds is not None and rounds >= max_rounds):
-                break
+        ex = _LaggedExchange(self, device, self.lag)
+        s = self.s
+        native = s is not None and hasattr(s, "run_cb") and getattr(getattr(s, "cfg", None), "time_budget_s", None) is None
+        if native:
+            # the native run (speculation, host/device pipelining) hands each
+            # round's bests to the exchange thread from its per-round hook
+            def on_round(rnd, active, best):
+                if (rnd + 1) % exchange_every == 0:
+                    ex.submit(best, active)
+                return False
+
+            ex.start()
+            try:
+                s.run_cb(max_rounds, on_round)
+            finally:
+                ex.join()
+            final = s.best_costs()
+        elif s is not None:
+            rounds, active = 0, s.R
+            while active > 0 and (max_rounds is None or rounds < max_rounds):
+                active = s.round()
+                rounds += 1
+                if rounds % exchange_every == 0:
+                    ex.post(s.best, active)
+            final = s.best
+        else:
+            final = np.zeros(0)
+        ex.finish(final)
         return self.best_history[-1] if self.best_history else (float("inf"), -1.0)
+
+
+class _LaggedExchange:
+    """The per-round exchange without a per-round barrier: each post is a
+    non-blocking all-gather of (best cost, seed id, active seeds), and a rank
+    waits for an exchange only once ``lag`` newer ones are in flight, so a
+    rank's round never waits for a slower rank's same round.  Every rank waits
+    the exchanges in order and records the global best of each.
+
+    Stop protocol: a rank whose seeds are done (or whose run hit max_rounds)
+    keeps posting exchanges with 0 active seeds, one per exchange it waits,
+    until it waits one whose global active count is 0.  Every rank then holds
+    the same number of exchanges in flight (lag), so all ranks post the same
+    number of exchanges and leave together."""
+
+    def __init__(self, sh, device, lag):
+        import collections
+
+        import torch
+
+        self.sh = sh
+        self.dist = _dist()
+        self.world = self.dist.get_world_size()
+        self.lag = max(1, int(lag))
+        n = self.lag + 1
+        dev = torch.device(device)
+        self.send = [torch.empty(3, dtype=torch.float64, device=dev) for _ in range(n)]
+        self.recv = [torch.empty(3 * self.world, dtype=torch.float64, device=dev) for _ in range(n)]
+        # host staging of the sends: pinned, so the copies are asynchronous
+        self.hsend = torch.empty((n, 3), dtype=torch.float64, pin_memory=dev.type == "cuda")
+        self.hsend_np = self.hsend.numpy()
+        self.pending = collections.deque()
+        self.posted = 0
+
+    def start(self):
+        """Post the exchanges from a thread of their own (submit()), so the
+        search's native loop only copies its bests per round."""
+        import queue
+        import threading
+
+        self.q = queue.SimpleQueue()
+        self.err = None
+
+        def loop():
+            import torch
+
+            try:
+                if self.send[0].device.type == "cuda":
+                    torch.cuda.set_device(self.send[0].device)
+                while True:
+                    item = self.q.get()
+                    if item is None:
+                        return
+                    self.post(*item)
+            except BaseException as e:  # re-raised by join()
+                self.err = e
+
+        self.th = threading.Thread(target=loop, name="fo-exchange", daemon=True)
+        self.th.start()
+
+    def submit(self, best, active):
+        self.q.put((np.array(best, dtype=np.float64), int(active)))
+
+    def join(self):
+        self.q.put(None)
+        self.th.join()
+        if self.err is not None:
+            raise self.err
+
+    def post(self, best, active):
+        if len(best):
+            j = int(np.argmin(best))  # first minimum -> lowest local id among ties
+            mine = (float(best[j]), float(self.sh.seed_offset + j))
+        else:
+            mine = (float("inf"), float("inf"))
+        k = self.posted % (self.lag + 1)
+        self.hsend_np[k] = (mine[0], mine[1], float(active))  # slot k's previous copy is done: its exchange was waited
+        self.send[k].copy_(self.hsend[k], non_blocking=True)
+        work = self.dist.all_gather_into_tensor(self.recv[k], self.send[k], async_op=True)
+        self.pending.append((work, k))
+        self.posted += 1
+        while len(self.pending) > self.lag:
+            self._wait()
+
+    def _wait(self):
+        work, k = self.pending.popleft()
+        work.wait()
+        allp = self.recv[k].view(self.world, 3).cpu().numpy()
+        order = np.lexsort((allp[:, 1], allp[:, 0]))  # strict <: the lowest global id among equal costs
+        self.sh.best_history.append((float(allp[order[0], 0]), float(allp[order[0], 1])))
+        return int(round(allp[:, 2].sum()))
+
+    def finish(self, best):
+        while len(self.pending) < self.lag:
+            self.post(best, 0)
+        while True:
+            if self._wait() == 0:
+                break
+            self.post(best, 0)
+        while self.pending:
+            self._wait()

@@ -136,6 +136,30 @@ class LockstepSearch:
             self.round()
         return [self.result(r) for r in range(self.R)]
 
+    def run_cb(self, max_rounds: Optional[int], on_round):
+        """fo_search_run with on_round(round, active, best) called after every
+        round (best: the seeds' best costs so far, a view valid during the
+        call).  A truthy return, or an exception, stops the run."""
+        err = []
+
+        def _fn(ctx, rnd, active, best, R):
+            try:
+                return 1 if on_round(int(rnd), int(active), np.ctypeslib.as_array(best, (int(R),))) else 0
+            except BaseException as e:  # re-raised below, after the native run unwinds
+                err.append(e)
+                return 1
+
+        cb = N.ROUND_FN(_fn)
+        a = C.c_int32()
+        st = N.lib().fo_search_run_cb(self.h, int(max_rounds or 0), C.cast(cb, C.c_void_p), None, C.byref(a))
+        if err:
+            raise err[0]
+        _raise(st, "fo_search_run_cb", N.last_error())
+        self.active = a.value
+        n = C.c_int64()
+        N.lib().fo_search_rounds(self.h, C.byref(n))
+        self.rounds = int(n.value)
+
     def best_costs(self) -> np.ndarray:
         """Best cost found by every seed (no graph or trace reconstruction)."""
         out = np.zeros(self.R)

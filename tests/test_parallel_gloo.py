@@ -83,8 +83,25 @@ class _FakeLockstep:
                 self.best[r] -= 1.0
         return sum(1 for x in self.left if x > 0)
 
+    def run_cb(self, max_rounds, on_round):
+        """LockstepSearch.run_cb: the hook after every round (native run)."""
+        active = self.R
+        while active > 0 and (max_rounds is None or self.rounds < max_rounds):
+            active = self.round()
+            if on_round(self.rounds - 1, active, self.best):
+                raise RuntimeError("stopped")
 
-def _sharded_worker(rank, world, port, q, seeds, exchange_every, max_rounds, use_round):
+    def best_costs(self):
+        return self.best.copy()
+
+
+class _FakeLockstepRounds(_FakeLockstep):
+    """Without run_cb: ShardedSearch drives round() itself."""
+
+    run_cb = property()  # hasattr() is False
+
+
+def _sharded_worker(rank, world, port, q, seeds, exchange_every, max_rounds, use_round, lag=4, by_round=False):
     import paper_2209_12769_b200.search as S
     from paper_2209_12769_b200.parallel import ShardedSearch
 
@@ -92,8 +109,14 @@ def _sharded_worker(rank, world, port, q, seeds, exchange_every, max_rounds, use
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        S.LockstepSearch = _FakeLockstep
+        S.LockstepSearch = _FakeLockstepRounds if by_round else _FakeLockstep
         sh = ShardedSearch(None, None, None, seeds, rank, world)
+        sh.lag = lag
+        if rank == 1 and sh.s is not None:  # ranks at different speeds: the lagged exchange absorbs it
+            import time
+
+            f = sh.s.round
+            sh.s.round = lambda: (time.sleep(0.002), f())[1]
         if use_round:
             n = 0
             while sh.round("cpu") > 0:
@@ -106,21 +129,25 @@ def _sharded_worker(rank, world, port, q, seeds, exchange_every, max_rounds, use
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("seeds,exchange_every,max_rounds,use_round", [
-    (list(range(5)), 1, None, False),      # per-round exchange (the default)
-    (list(range(5)), 3, None, False),      # uneven shards: 3 + 2 seeds of different lengths
-    (list(range(5)), 3, 10, False),        # max_rounds cuts a block
-    ([0], 2, None, False),                 # rank 1 has no seeds at all
-    (list(range(4)), None, None, True),    # driven through round()
+@pytest.mark.parametrize("seeds,exchange_every,max_rounds,use_round,lag,by_round", [
+    (list(range(5)), 1, None, False, 4, False),     # per-round exchange (the default), 4 in flight
+    (list(range(5)), 1, None, False, 1, False),     # one in flight
+    (list(range(5)), 1, None, False, 64, False),    # more in flight than rounds
+    (list(range(5)), 3, None, False, 4, False),     # uneven shards: 3 + 2 seeds of different lengths
+    (list(range(5)), 3, 10, False, 2, False),       # max_rounds stops the runs early
+    (list(range(5)), 1, None, False, 3, True),      # without the native hook: round() per round
+    ([0], 2, None, False, 4, False),                # rank 1 has no seeds at all
+    (list(range(4)), None, None, True, 4, False),   # driven through round()
 ])
-def test_sharded_search_exchange_gloo_world2(seeds, exchange_every, max_rounds, use_round):
+def test_sharded_search_exchange_gloo_world2(seeds, exchange_every, max_rounds, use_round, lag, by_round):
     """ShardedSearch's exchange schedule on 2 ranks: both ranks leave after the
     same number of exchanges (no rank waits in a collective the other never
     joins) and agree on the global best (cost, seed)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q, seeds, exchange_every, max_rounds, use_round))
+    procs = [ctx.Process(target=_sharded_worker,
+                         args=(r, 2, port, q, seeds, exchange_every, max_rounds, use_round, lag, by_round))
              for r in range(2)]
     for p in procs:
         p.start()

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--precision", default="fp64")
     ap.add_argument("--oracle-seeds", type=int, default=1, help="seeds re-run on the CPU oracle (rank 0)")
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--exchange", default="round", help="round (the per-round exchange) | end (once) | N (every N rounds)")
+    ap.add_argument("--lag", type=int, default=0, help="exchanges in flight (0: ShardedSearch's default)")
     args = ap.parse_args()
 
     import numpy as np
@@ -57,7 +59,10 @@ def main():
     local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
     threads = args.threads or max(1, (os.cpu_count() or 1) // local_ws)  # no oversubscription across ranks
     sh = ShardedSearch(g, cfg, cp, seeds, rank, ws, precision=prec, n_threads=threads)
-    best_cost, best_seed = sh.run(dev)
+    if args.lag > 0:
+        sh.lag = args.lag
+    every = 1 if args.exchange == "round" else (None if args.exchange == "end" else int(args.exchange))
+    best_cost, best_seed = sh.run(dev, exchange_every=every)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     # per-seed counters straight from the native search (no graph reconstruction)
@@ -86,7 +91,8 @@ def main():
             "rounds": sh.s.rounds if sh.s else 0, "max_steps_one_seed": local_steps,
             "best_cost_us": best_cost, "best_seed": int(best_seed),
             "rank0_device_ms": tm["device_ms"], "rank0_expand_ms": tm["expand_ms"], "rank0_scored": tm["scored"],
-            "host_threads": os.cpu_count(),
+            "host_threads": os.cpu_count(), "exchange": args.exchange, "lag": sh.lag,
+            "exchanges": len(sh.best_history),
         }
         if args.oracle_seeds > 0:
             from oracle.oracle import Oracle, load_workload
