@@ -309,6 +309,23 @@ int fo_search_run(fo_search *s, int64_t max_rounds, int32_t *active_out);
  * stops the run with FO_INVALID_ARG.  fn must not call back into this handle. */
 typedef int32_t (*fo_round_fn)(void *ctx, int64_t round, int32_t active, const double *best, int32_t R);
 int fo_search_run_cb(fo_search *s, int64_t max_rounds, fo_round_fn fn, void *ctx, int32_t *active_out);
+
+/* ---- multi-GPU search exchange over NCCL (parallel.py ShardedSearch) ------
+ * One communicator per rank (NCCL bound at run time).  An attached search
+ * posts, every `every` rounds, its best (cost, global seed id) and live-seed
+ * count -- one ncclAllGather of 3 doubles per rank on the exchange's stream,
+ * waited `lag` exchanges late -- and every rank records the global best of
+ * each exchange (strict <: lowest id among equal costs, search.py:124).
+ * fo_xchg_finish (every rank, after its run) keeps posting 0-live exchanges
+ * until all ranks are done, so all ranks post the same number. */
+typedef struct fo_xchg fo_xchg;
+int fo_xchg_unique_id(uint8_t *out128); /* rank 0; broadcast to the others */
+int fo_xchg_create(const uint8_t *id128, int32_t rank, int32_t world, int32_t device, int32_t lag, fo_xchg **out);
+int fo_xchg_attach(fo_search *s, fo_xchg *x, int64_t seed_offset, int32_t every);
+int fo_xchg_finish(fo_xchg *x);
+/* out2[2 * i] = global best cost of exchange i, out2[2 * i + 1] its seed id */
+int fo_xchg_history(fo_xchg *x, double *out2, int64_t cap, int64_t *n_out);
+int fo_xchg_destroy(fo_xchg *x);
 /* Counters: steps, candidates_evaluated, candidates_enqueued, trace length. */
 int fo_search_result(fo_search *s, int32_t r, double *best_cost, int64_t *counters4, int32_t *best_ngid,
                      int32_t *best_rgid, int32_t *best_bkt, fo_trace_rec *trace, int64_t trace_cap);

@@ -93,6 +93,12 @@ SIGNATURES = [
     ("fo_search_start", C.c_int, [vp, vp]),
     ("fo_search_run", C.c_int, [vp, C.c_int64, P(C.c_int32)]),
     ("fo_search_run_cb", C.c_int, [vp, C.c_int64, vp, vp, P(C.c_int32)]),
+    ("fo_xchg_unique_id", C.c_int, [vp]),
+    ("fo_xchg_create", C.c_int, [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(vp)]),
+    ("fo_xchg_attach", C.c_int, [vp, vp, C.c_int64, C.c_int32]),
+    ("fo_xchg_finish", C.c_int, [vp]),
+    ("fo_xchg_history", C.c_int, [vp, vp, C.c_int64, P(C.c_int64)]),
+    ("fo_xchg_destroy", C.c_int, [vp]),
     ("fo_search_result", C.c_int, [vp, C.c_int32, P(C.c_double), vp, vp, vp, vp, P(TraceRec), C.c_int64]),
     ("fo_search_timing", C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int64)]),
     ("fo_search_rounds", C.c_int, [vp, P(C.c_int64)]),

@@ -1773,6 +1773,8 @@ struct fo_search {
     int64_t scored = 0, host_steps = 0;
     int64_t rounds = 0;  // device rounds run (fo_search_rounds)
     bool started = false;
+    fo_xchg *x = nullptr;      // the multi-GPU exchange (fo_xchg_attach)
+    int64_t x_round = 0;
     fo_round_fn cb = nullptr;  // per-round hook of fo_search_run_cb
     void *cb_ctx = nullptr;
     int64_t cb_round = 0;
@@ -2129,7 +2131,7 @@ static int count_active(fo_search *S, double *best_cost_out) {
 
 // the per-round hook (fo_search_run_cb); false once it asked to stop
 static bool round_hook(fo_search *S) {
-    if (!S->cb) return true;
+    if (!S->cb && !S->x) return true;
     const int R = (int)S->seeds.size();
     S->cb_best.resize(R);
     int active = 0;
@@ -2137,7 +2139,8 @@ static bool round_hook(fo_search *S) {
         S->cb_best[r] = S->seeds[r].best;
         active += S->seeds[r].active;
     }
-    if (S->cb(S->cb_ctx, S->cb_round++, active, S->cb_best.data(), R) != 0) S->cb_stop = true;
+    if (S->x && xchg_round(S->x, S->x_round++, S->cb_best.data(), R, active) != FO_OK) S->cb_stop = true;
+    if (S->cb && S->cb(S->cb_ctx, S->cb_round++, active, S->cb_best.data(), R) != 0) S->cb_stop = true;
     return !S->cb_stop;
 }
 
@@ -2307,7 +2310,19 @@ static int search_run(fo_search *S, int64_t max_rounds, int32_t *active_out);
 
 int fo_search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
     if (!S) return fail(FO_INVALID_ARG, "null search");
-    return search_run(S, max_rounds, active_out);
+    S->cb_stop = false;
+    const int rc = search_run(S, max_rounds, active_out);
+    if (rc) return rc;
+    if (S->cb_stop) return FO_CUDA_ERROR;  // the exchange failed (fo_last_error says why)
+    return FO_OK;
+}
+
+int fo_xchg_attach(fo_search *S, fo_xchg *x, int64_t seed_offset, int32_t every) {
+    if (!S || every < 1) return fail(FO_INVALID_ARG, "bad attach arguments");
+    S->x = x;
+    S->x_round = 0;
+    if (x) xchg_attach_cfg(x, seed_offset, every);
+    return FO_OK;
 }
 
 int fo_search_run_cb(fo_search *S, int64_t max_rounds, fo_round_fn fn, void *ctx, int32_t *active_out) {
@@ -2367,6 +2382,11 @@ static int search_run(fo_search *S, int64_t max_rounds, int32_t *active_out) {
     }
     S->rounds += it;
     if (active_out) *active_out = count_active(S, nullptr);
+    if (S->x) {  // the closing exchanges carry the run's final bests
+        std::vector<double> b(S->seeds.size());
+        for (size_t r = 0; r < b.size(); r++) b[r] = S->seeds[r].best;
+        xchg_final(S->x, b.data(), (int)b.size());
+    }
     if (getenv("FO_SEARCH_PROFILE"))
         fprintf(stderr, "fo_search_run: rounds %lld pipeline %d spec %d (host-only steps %lld) device %.1f ms expand %.1f ms launch %.1f ms (put %.1f, issue %.1f) wait %.1f ms replay %.1f ms\n",
                 (long long)it, (int)pipeline, (int)S->spec, (long long)S->host_steps, S->device_ms, S->expand_ms,

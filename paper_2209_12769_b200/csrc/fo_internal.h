@@ -277,6 +277,9 @@ struct fo_graph {
 namespace fo {
 void set_error(const std::string &msg);
 int fail(int status, const std::string &msg);
+int xchg_round(fo_xchg *x, int64_t round, const double *best, int R, int active);  // xchg.cpp
+void xchg_final(fo_xchg *x, const double *best, int R);
+void xchg_attach_cfg(fo_xchg *x, int64_t seed_offset, int every);
 // Ensure the handle's workspace can hold `slots` warps for gid bound VB.
 int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big = false, int nws = 1, int alt = 0);
 // Score K device-resident candidates (used by fo_score and the search engine).

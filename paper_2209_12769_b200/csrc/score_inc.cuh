@@ -495,7 +495,7 @@ __device__ void score_one_inc(const IncArgs &a, int k, const IncCtx &c0, const G
     const DGraph &g = a.g;
     const IncPlan &p = a.p;
     const IncLayout &L = a.L;
-    const int V = p.V, A = p.A, VB = p.VB, NN = p.NN;
+    const int V = p.V, A = p.A, VB = p.VB;
     auto retry = [&]() {
         if (lane == 0) { a.cost_out[k] = 0.0; a.status_out[k] = a.diag ? 110 + c.cnt[kCFail] : kRetryGeneral; }
     };

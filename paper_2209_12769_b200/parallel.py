@@ -148,9 +148,14 @@ class ShardedSearch:
             return self.best_history[-1]
         if exchange_every < 1:
             raise ValueError("exchange_every must be >= 1")
-        ex = _LaggedExchange(self, device, self.lag)
         s = self.s
         native = s is not None and hasattr(s, "run_cb") and getattr(getattr(s, "cfg", None), "time_budget_s", None) is None
+        import os
+
+        if ((native or s is None) and dist.get_backend() == "nccl" and torch.device(device).type == "cuda"
+                and os.environ.get("FO_XCHG_PY") != "1"):
+            return self._run_nccl(device, max_rounds, exchange_every)
+        ex = _LaggedExchange(self, device, self.lag)
         if native:
             # the native run (speculation, host/device pipelining) hands each
             # round's bests to the exchange thread from its per-round hook
@@ -176,6 +181,48 @@ class ShardedSearch:
         else:
             final = np.zeros(0)
         ex.finish(final)
+        return self.best_history[-1] if self.best_history else (float("inf"), -1.0)
+
+
+    def _run_nccl(self, device, max_rounds, exchange_every):
+        """The exchange natively (fo_xchg, csrc/xchg.cpp): posted from the
+        search's round hook over a communicator of its own, waited lag
+        exchanges late, closed by fo_xchg_finish on every rank."""
+        import ctypes as C
+
+        import torch
+
+        from . import _native as N
+        from .errors import _raise
+
+        dist = _dist()
+        rank, world = dist.get_rank(), dist.get_world_size()
+        idb = (C.c_uint8 * 128)()
+        if rank == 0:
+            _raise(N.lib().fo_xchg_unique_id(idb), "fo_xchg_unique_id", N.last_error())
+        box = [bytes(idb)]
+        dist.broadcast_object_list(box, src=0)
+        idb = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        dev = torch.device(device)
+        x = C.c_void_p()
+        _raise(N.lib().fo_xchg_create(idb, rank, world, dev.index if dev.index is not None else torch.cuda.current_device(),
+                                      int(self.lag), C.byref(x)), "fo_xchg_create", N.last_error())
+        try:
+            if self.s is not None:
+                _raise(N.lib().fo_xchg_attach(self.s.h, x, int(self.seed_offset), int(exchange_every)),
+                       "fo_xchg_attach", N.last_error())
+                try:
+                    self.s.run(max_rounds, results=False)
+                finally:
+                    N.lib().fo_xchg_attach(self.s.h, None, 0, 1)
+            _raise(N.lib().fo_xchg_finish(x), "fo_xchg_finish", N.last_error())
+            n = C.c_int64()
+            N.lib().fo_xchg_history(x, None, 0, C.byref(n))
+            h = np.zeros(2 * max(1, n.value))
+            N.lib().fo_xchg_history(x, N.ptr(h), n.value, C.byref(n))
+            self.best_history.extend((float(h[2 * i]), float(h[2 * i + 1])) for i in range(n.value))
+        finally:
+            N.lib().fo_xchg_destroy(x)
         return self.best_history[-1] if self.best_history else (float("inf"), -1.0)
 
 

@@ -132,3 +132,56 @@ def test_bench_exchange_chain_two_ranks():
     allc = np.concatenate([out[0][2], out[1][2]])
     j = int(np.argmin(allc))  # first minimum: the lowest global id among ties (search.py:124)
     assert out[0][1] == out[1][1] == (float(allc[j]), float(j))
+
+
+def _nccl_worker(rank, world, port, q, seeds, every):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import paper_2209_12769_b200 as P
+    from paper_2209_12769_b200 import _native as N
+    from paper_2209_12769_b200.parallel import ShardedSearch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        g, prof, comm, mpm, lin = P.load_workload("residual40")
+        cp = P.make_cost_providers(prof, comm, mpm, precision=N.FO_PREC_FP64)
+        cfg = P.SearchConfig(alpha=1.05, beta=10, max_unchanged=80)
+        sh = ShardedSearch(g, cfg, cp, seeds, rank, world)
+        sh.lag = 3
+        res = sh.run(torch.device("cuda", rank), exchange_every=every)
+        q.put((rank, res, len(sh.best_history)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("seeds,every", [(list(range(6)), 1), (list(range(5)), 3), ([2], 1)])
+def test_native_nccl_exchange_two_gpus(seeds, every):
+    """ShardedSearch over NCCL on two GPUs: the per-round exchange runs natively
+    (fo_xchg); both ranks post the same number of exchanges and return the
+    single-process answer (also when rank 1 has no seeds)."""
+    import paper_2209_12769_b200 as P
+    from paper_2209_12769_b200 import _native as N
+
+    torch.cuda.set_device(0)
+    g, prof, comm, mpm, lin = P.load_workload("residual40")
+    cp = P.make_cost_providers(prof, comm, mpm, precision=N.FO_PREC_FP64)
+    cfg = P.SearchConfig(alpha=1.05, beta=10, max_unchanged=80)
+    ref = P.lockstep_search(g, cfg, cp, seeds)
+    best = min(range(len(seeds)), key=lambda r: (ref[r].best_cost_us, r))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, q, seeds, every)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert out[0][2] == out[1][2] and out[0][2] >= 1
+    assert out[0][1] == out[1][1] == (ref[best].best_cost_us, float(best))

@@ -3,7 +3,7 @@
 TAG=${1:-xv}
 mkdir -p gpurun_out
 : > gpurun_out/${TAG}_variants.jsonl
-for v in "end 0" "round 8" "round 1" "round 8" "end 0"; do
+for v in "end 0" "round 8" "round 1" "round 32" "round 8" "end 0"; do
   set -- $v
   timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 \
     tools/bench_search.py --config bert --seeds 64 --oracle-seeds 0 --exchange $1 --lag $2 2>/dev/null | grep '"metric"' >> gpurun_out/${TAG}_variants.jsonl
