@@ -40,7 +40,10 @@ struct IncWork {  // setup record of a patched node, in discovery order
 };
 
 constexpr int kIncRingG = 256, kIncRingB = 128;  // shared-memory ready-run capacities per lane
-constexpr int kIncMpSmem = 16;  // estimator kernel: member sets up to this size keep H / P in shared memory
+// estimator kernel: member sets up to this size keep H / P in shared memory
+// (16 KB per block either way: more would cost the fp64 kernel a resident block)
+template <typename T>
+constexpr int kIncMpSmem = sizeof(T) == 8 ? 8 : 16;
 
 IncLayout inc_layout(int V, int E, int A, int VB, int P, bool smem_indeg) {
     IncLayout L{};
@@ -999,10 +1002,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_mp(const __gr
         __syncwarp();
         // node states H and aggregates P of sets up to kIncMpSmem members in the
         // warp's shared memory, larger sets in its global scratch
-        T *sh = (T *)(fo_inc_smem + (threadIdx.x >> 5) * (2 * kIncMpSmem * 32 * sizeof(T)));
-        const bool in_smem = n <= kIncMpSmem;
+        T *sh = (T *)(fo_inc_smem + (threadIdx.x >> 5) * (2 * kIncMpSmem<T> * 32 * sizeof(T)));
+        const bool in_smem = n <= kIncMpSmem<T>;
         const double pred = mp_forward<T>(g, mem, n, gs.nbptr, gs.nb, in_smem ? sh : (T *)gs.H,
-                                          in_smem ? sh + kIncMpSmem * 32 : (T *)gs.P, lane);
+                                          in_smem ? sh + kIncMpSmem<T> * 32 : (T *)gs.P, lane);
         if (lane == 0) {
             a.queue[qi].v = pred;  // the queuing candidate reads this
             if (q.slot >= 0 && a.memo[q.slot].k1 == q.h1 && a.memo[q.slot].k2 == q.h2)
@@ -1430,8 +1433,8 @@ cudaError_t launch_score_inc(const DGraph &g, const IncPlan &p, const IncLayout 
         if (fp64) score_kernel_inc<double><<<grid, kWarps * 32, smem, stream>>>(a, k0);
         else score_kernel_inc<float><<<grid, kWarps * 32, smem, stream>>>(a, k0);
         if (a.stop_after == 1) continue;
-        if (fp64) score_kernel_inc_mp<double><<<grid, kWarps * 32, kWarps * 2 * kIncMpSmem * 32 * 8, stream>>>(a);
-        else score_kernel_inc_mp<float><<<grid, kWarps * 32, kWarps * 2 * kIncMpSmem * 32 * 4, stream>>>(a);
+        if (fp64) score_kernel_inc_mp<double><<<grid, kWarps * 32, kWarps * 2 * kIncMpSmem<double> * 32 * 8, stream>>>(a);
+        else score_kernel_inc_mp<float><<<grid, kWarps * 32, kWarps * 2 * kIncMpSmem<float> * 32 * 4, stream>>>(a);
         if (L.k_indeg >= 0) score_kernel_inc_k3<true><<<grid, kWarps * 32, ksmem, stream>>>(a, k0, n);
         else score_kernel_inc_k3<false><<<grid, kWarps * 32, ksmem, stream>>>(a, k0, n);
     }
