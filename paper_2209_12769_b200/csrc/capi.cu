@@ -117,14 +117,34 @@ int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bk
                   stream, nullptr, alt_ws);
 }
 
-// sparse candidates against the resident parent (fo_set_parent)
+// sparse candidates against the resident parent (fo_set_parent).  slot 1:
+// the second set of scratch (incremental workspace, estimator queue, memo
+// tables, general-kernel workspace), so two batches can run on two streams at
+// once (fo_score_delta_submit).
 int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int K, int precision, double *cost,
-                       int32_t *status, cudaStream_t stream) {
+                       int32_t *status, cudaStream_t stream, int slot) {
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
     if (!g->model_set) return fail(FO_INVALID_ARG, "no cost model set (fo_graph_set_cost_model)");
     if (!g->d_parent) return fail(FO_INVALID_ARG, "no parent state set (fo_set_parent)");
     if (K <= 0) return FO_OK;
     CUDA_TRY(cudaSetDevice(g->device));
+    // the slot's memo tables stand in for the handle's while this batch is
+    // launched (kernel arguments are copied at launch)
+    MemoEnt *memo_save[2] = {g->dg.memo[0], g->dg.memo[1]};
+    struct Restore {
+        fo_graph *g;
+        MemoEnt *m[2];
+        ~Restore() { g->dg.memo[0] = m[0]; g->dg.memo[1] = m[1]; }
+    } restore{g, {memo_save[0], memo_save[1]}};
+    if (slot && g->dg.memo[0]) {
+        const size_t slots = (size_t)g->dg.memo_mask + 1;
+        if (!g->d_memo_alt) {
+            CUDA_TRY(cudaMalloc(&g->d_memo_alt, 2 * slots * sizeof(MemoEnt)));
+            CUDA_TRY(cudaMemset(g->d_memo_alt, 0, 2 * slots * sizeof(MemoEnt)));
+        }
+        g->dg.memo[0] = (MemoEnt *)g->d_memo_alt;
+        g->dg.memo[1] = (MemoEnt *)g->d_memo_alt + slots;
+    }
     TimelineOut tl{};
     DeltaIn d;
     d.base = g->d_parent;
@@ -143,38 +163,41 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
         }
         const int warps = score_warps_per_block();
         const int grid = std::max(1, std::min(g->num_sms * std::max(bps, 1), (K + warps - 1) / warps));
+        char *&ws = slot ? g->d_ws_inc_alt : g->d_ws_inc;
+        size_t &ws_bytes = slot ? g->ws_inc_alt_bytes : g->ws_inc_bytes;
+        void *&q = slot ? g->d_inc_q_alt : g->d_inc_q;
+        size_t &q_bytes = slot ? g->inc_q_alt_bytes : g->inc_q_bytes;
         const size_t need = (size_t)L.total * grid * warps;
-        if (need > g->ws_inc_bytes) {
-            if (g->d_ws_inc) CUDA_TRY(cudaFree(g->d_ws_inc));
-            g->d_ws_inc = nullptr;
-            g->ws_inc_bytes = 0;
-            CUDA_TRY(cudaMalloc(&g->d_ws_inc, need));
+        if (need > ws_bytes) {
+            if (ws) CUDA_TRY(cudaFree(ws));
+            ws = nullptr;
+            ws_bytes = 0;
+            CUDA_TRY(cudaMalloc(&ws, need));
             // member marks of the estimator kernel start at -1 (every byte 0xff)
-            CUDA_TRY(cudaMemset(g->d_ws_inc, 0xff, need));
-            g->ws_inc_bytes = need;
+            CUDA_TRY(cudaMemset(ws, 0xff, need));
+            ws_bytes = need;
         }
         const int qcap = kIncQueuePerCand * std::min(K, grid * warps);
         const size_t qneed = 64 + (size_t)qcap * 48;
-        if (qneed > g->inc_q_bytes) {
-            if (g->d_inc_q) CUDA_TRY(cudaFree(g->d_inc_q));
-            g->d_inc_q = nullptr;
-            g->inc_q_bytes = 0;
-            CUDA_TRY(cudaMalloc(&g->d_inc_q, qneed));
-            CUDA_TRY(cudaMemset(g->d_inc_q, 0, 64));  // queue count, fast-forward counters (fo_inc_stats)
-            g->inc_q_bytes = qneed;
+        if (qneed > q_bytes) {
+            if (q) CUDA_TRY(cudaFree(q));
+            q = nullptr;
+            q_bytes = 0;
+            CUDA_TRY(cudaMalloc(&q, qneed));
+            CUDA_TRY(cudaMemset(q, 0, 64));  // queue count, fast-forward counters (fo_inc_stats)
+            q_bytes = qneed;
         }
-        cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, g->d_ws_inc, grid,
-                                         (IncQ *)((char *)g->d_inc_q + 64), (int *)g->d_inc_q, qcap, cost, status, stream,
-                                         g->delta_mode == 2);
+        cudaError_t e = launch_score_inc(g->dg, p, L, off, chg, K, precision, ws, grid, (IncQ *)((char *)q + 64),
+                                         (int *)q, qcap, cost, status, stream, g->delta_mode == 2);
         // kernels launched: setup, estimator and event loop per chunk of one candidate per warp
         g_launches += (int64_t)((K + grid * warps - 1) / (grid * warps)) * (g->dg.phase_stop == 1 ? 1 : 3);
         if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("incremental score launch: ") + cudaGetErrorString(e));
         if (g->delta_mode == 2) return FO_OK;  // diagnostic: hand-backs stay visible as status 101
         return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
-                      nullptr, nullptr, stream, &d, 0, 2);
+                      nullptr, nullptr, stream, &d, slot, 2);
     }
     return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
-                  nullptr, nullptr, stream, &d);
+                  nullptr, nullptr, stream, &d, slot);
 }
 
 }  // namespace fo
@@ -359,6 +382,10 @@ int fo_graph_destroy(fo_graph *g) {
         if (pl) cudaFree(pl);
     if (g->d_ws_inc) cudaFree(g->d_ws_inc);
     if (g->d_inc_q) cudaFree(g->d_inc_q);
+    if (g->d_ws_inc_alt) cudaFree(g->d_ws_inc_alt);
+    if (g->d_inc_q_alt) cudaFree(g->d_inc_q_alt);
+    if (g->d_memo_alt) cudaFree(g->d_memo_alt);
+    if (g->stream_alt) cudaStreamDestroy(g->stream_alt);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     for (auto &sl : g->aslot) {
         if (sl.done) cudaEventSynchronize(sl.done);
@@ -510,6 +537,7 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         g->memo_slots = slots;
         if (!g->d_memo) CUDA_TRY(cudaMalloc(&g->d_memo, 2 * slots * sizeof(MemoEnt)));
         CUDA_TRY(cudaMemset(g->d_memo, 0, 2 * slots * sizeof(MemoEnt)));
+        if (g->d_memo_alt) { cudaFree(g->d_memo_alt); g->d_memo_alt = nullptr; }  // re-made empty on demand
         dg.memo[0] = (MemoEnt *)g->d_memo;
         dg.memo[1] = (MemoEnt *)g->d_memo + slots;
         dg.memo_mask = (uint32_t)(slots - 1);
@@ -545,6 +573,8 @@ int fo_memo_clear(fo_graph *g, void *stream) {
     if (!g->d_memo) return FO_OK;
     cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;  // NULL: the handle's own stream
     CUDA_TRY(cudaMemsetAsync(g->d_memo, 0, 2 * ((size_t)g->dg.memo_mask + 1) * sizeof(MemoEnt), s));
+    if (g->d_memo_alt)  // the second submission stream's tables
+        CUDA_TRY(cudaMemsetAsync(g->d_memo_alt, 0, 2 * ((size_t)g->dg.memo_mask + 1) * sizeof(MemoEnt), s));
     return FO_OK;
 }
 
@@ -768,18 +798,24 @@ int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *ch
         sl.bytes = need;
     }
     char *b = sl.d;
-    cudaStream_t hs = g->hstream, ds = g->dstream, s = g->stream;
+    // consecutive submissions alternate between two compute streams with
+    // their own scratch, so a batch's setup runs in the previous batch's
+    // event-loop tail (graphs whose fused groups outgrow the estimator scratch
+    // share one second-pass workspace: one stream)
+    const int ks = (g->V <= kMpCapDefault && !getenv("FO_SUBMIT_ONE_STREAM")) ? (int)(t & 1) : 0;
+    if (ks && !g->stream_alt) CUDA_TRY(cudaStreamCreateWithFlags(&g->stream_alt, cudaStreamNonBlocking));
+    cudaStream_t hs = g->hstream, ds = g->dstream, s = ks ? g->stream_alt : g->stream;
     CUDA_TRY(cudaMemcpyAsync(b, offsets, 4 * ((size_t)K + 1), cudaMemcpyHostToDevice, hs));
     if (nc) CUDA_TRY(cudaMemcpyAsync(b + o_c, changes, 8 * nc, cudaMemcpyHostToDevice, hs));
     CUDA_TRY(cudaEventRecord(sl.h2d, hs));
     CUDA_TRY(cudaStreamWaitEvent(s, sl.h2d, 0));
-    if (clear_memo && g->d_memo) {  // only the table this precision's estimator reads (score.cu K2)
+    if (clear_memo && g->d_memo && (!ks || g->d_memo_alt)) {  // only the table this precision's estimator reads
         const size_t slots = (size_t)g->dg.memo_mask + 1;
-        MemoEnt *tab = (MemoEnt *)g->d_memo + (precision == FO_PREC_FP64 ? slots : 0);
+        MemoEnt *tab = (MemoEnt *)(ks ? g->d_memo_alt : g->d_memo) + (precision == FO_PREC_FP64 ? slots : 0);
         CUDA_TRY(cudaMemsetAsync(tab, 0, slots * sizeof(MemoEnt), s));
     }
     int st = score_delta_device(g, (const int32_t *)b, (const int32_t *)(b + o_c), K, precision,
-                                (double *)(b + o_cost), (int32_t *)(b + o_s), s);
+                                (double *)(b + o_cost), (int32_t *)(b + o_s), s, ks);
     if (st) return st;
     CUDA_TRY(cudaEventRecord(sl.kdone, s));
     CUDA_TRY(cudaStreamWaitEvent(ds, sl.kdone, 0));

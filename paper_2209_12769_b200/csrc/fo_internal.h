@@ -270,6 +270,13 @@ struct fo_graph {
     size_t ws_inc_bytes = 0;
     void *d_inc_q = nullptr;  // estimator queue (IncQ entries) + its counter
     size_t inc_q_bytes = 0;
+    // the second scratch set of fo_score_delta_submit's second stream
+    char *d_ws_inc_alt = nullptr;
+    size_t ws_inc_alt_bytes = 0;
+    void *d_inc_q_alt = nullptr;
+    size_t inc_q_alt_bytes = 0;
+    void *d_memo_alt = nullptr;
+    cudaStream_t stream_alt = nullptr;
     int delta_mode = 1;  // 1: incremental kernel when the plan allows it; 0: general kernel only
     std::mutex mu;
 };
@@ -285,4 +292,6 @@ int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big = fal
 // Score K device-resident candidates (used by fo_score and the search engine).
 int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bkt, int idx16, int K, int VB,
                  int precision, double *cost, int32_t *status, cudaStream_t stream, int alt_ws = 0);
+int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int K, int precision, double *cost,
+                       int32_t *status, cudaStream_t stream, int slot = 0);
 }  // namespace fo

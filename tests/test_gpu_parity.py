@@ -407,6 +407,37 @@ def test_pipelined_delta_submissions_equal_sync():
         dg.score_wait(10**9)
 
 
+@pytest.mark.parametrize("precision", [N.FO_PREC_FP32, N.FO_PREC_FP64])
+def test_pipelined_bench_batches_on_two_streams_equal_sync(precision):
+    """Bench-sized batches (4,096 candidates) submitted back to back: the
+    submissions alternate between two compute streams with their own scratch
+    and memo tables (each cleared per batch), and every batch equals the
+    synchronous call."""
+    import torch
+
+    g, cps = providers("resnet50", precision)
+    dg = cps["mp"].device_graph(g)
+    dg.set_parent()
+    batches = []
+    for b in range(6):
+        off, chg = dg.make_candidates_delta(np.arange(b * 4096, (b + 1) * 4096, dtype=np.uint64))
+        ref, st_ref = dg.score_delta_host(off, chg, precision)
+        h = [torch.from_numpy(off).pin_memory(), torch.from_numpy(chg).pin_memory(),
+             torch.zeros(4096, dtype=torch.float64).pin_memory(), torch.full((4096,), -1, dtype=torch.int32).pin_memory()]
+        batches.append((h, ref, st_ref))
+    for rep in range(2):
+        pending = []
+        for h, ref, st_ref in batches:
+            h[2].zero_()
+            pending.append(dg.score_delta_submit(*h, precision=precision, clear_memo=True))
+            if len(pending) == 2:
+                dg.score_wait(pending.pop(0))
+        for t in pending:
+            dg.score_wait(t)
+        for h, ref, st_ref in batches:
+            assert np.array_equal(h[3].numpy(), st_ref) and np.array_equal(h[2].numpy(), ref)
+
+
 def test_delta_scoring_rejects_bad_input():
     g, cps = providers("vgg16", N.FO_PREC_FP32)
     dg = cps["mp"].device_graph(g)
