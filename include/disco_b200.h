@@ -212,8 +212,9 @@ int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *chan
 /* Pipelined fo_score_delta_host for streams of batches: enqueues H2D of the
  * candidates (host buffers, pinned for overlap), [if clear_memo, an
  * fo_memo_clear of this precision's table], the score and the D2H of cost_out / status_out, and returns a
- * ticket.  Two submissions may be in flight: a third waits for the oldest.
- * Results are valid, and the input buffers reusable, after
+ * ticket.  Three submissions may be in flight, each on its own compute
+ * stream with its own scratch and memo tables (consecutive batches overlap);
+ * a fourth waits for the oldest.  Results are valid, and the input buffers reusable, after
  * fo_score_wait(g, ticket).  Same semantics per batch as
  * fo_score_delta_host (simulator.py:143-145 per candidate). */
 int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,

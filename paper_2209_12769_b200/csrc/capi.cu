@@ -34,8 +34,9 @@ static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 int ensure_workspace(fo_graph *g, int VB, int slots, WsLayout *L, bool big, int nws, int alt) {
     *L = ws_layout(g->V, g->E, g->A, VB, g->pairs_max, big ? g->V : kMpCapDefault, nws);
     size_t need = (size_t)L->total * (size_t)slots;
-    char *&buf = big ? g->d_ws_big : (alt ? g->d_ws_alt : g->d_ws);
-    size_t &have = big ? g->ws_big_bytes : (alt ? g->ws_alt_bytes : g->ws_bytes);
+    // alt 0: the handle's workspace, 1: the search's second lane, 2..: submission slots 1..
+    char *&buf = big ? g->d_ws_big : (alt >= 2 ? g->sub[alt - 1].ws : alt ? g->d_ws_alt : g->d_ws);
+    size_t &have = big ? g->ws_big_bytes : (alt >= 2 ? g->sub[alt - 1].ws_bytes : alt ? g->ws_alt_bytes : g->ws_bytes);
     if (need > have) {
         if (buf) cudaFree(buf);
         buf = nullptr;
@@ -74,7 +75,8 @@ static int launch(fo_graph *g, const void *ngid, const void *rgid, const void *b
     int slots = score_slots(geo);
     int st = ensure_workspace(g, VB, slots, &L, false, nws, alt_ws);
     if (st) return st;
-    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, alt_ws ? g->d_ws_alt : g->d_ws, L, geo,
+    char *wsp = alt_ws >= 2 ? g->sub[alt_ws - 1].ws : alt_ws ? g->d_ws_alt : g->d_ws;
+    cudaError_t e = launch_score(g->dg, ngid, rgid, bkt, idx16, K, VB, precision, wsp, L, geo,
                                  cost, status, ext_dur, tl,
                                  dur_out, bad_out, ngroups_out, stream, first_retry, delta);
     g_launches++;
@@ -117,10 +119,10 @@ int score_device(fo_graph *g, const void *ngid, const void *rgid, const void *bk
                   stream, nullptr, alt_ws);
 }
 
-// sparse candidates against the resident parent (fo_set_parent).  slot 1:
-// the second set of scratch (incremental workspace, estimator queue, memo
-// tables, general-kernel workspace), so two batches can run on two streams at
-// once (fo_score_delta_submit).
+// sparse candidates against the resident parent (fo_set_parent).  slot k > 0:
+// submission slot k's own scratch (incremental workspace, estimator queue,
+// memo tables, general-kernel workspace), so batches can run on several
+// streams at once (fo_score_delta_submit).
 int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int K, int precision, double *cost,
                        int32_t *status, cudaStream_t stream, int slot) {
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
@@ -138,12 +140,13 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
     } restore{g, {memo_save[0], memo_save[1]}};
     if (slot && g->dg.memo[0]) {
         const size_t slots = (size_t)g->dg.memo_mask + 1;
-        if (!g->d_memo_alt) {
-            CUDA_TRY(cudaMalloc(&g->d_memo_alt, 2 * slots * sizeof(MemoEnt)));
-            CUDA_TRY(cudaMemset(g->d_memo_alt, 0, 2 * slots * sizeof(MemoEnt)));
+        void *&m = g->sub[slot].memo;
+        if (!m) {
+            CUDA_TRY(cudaMalloc(&m, 2 * slots * sizeof(MemoEnt)));
+            CUDA_TRY(cudaMemset(m, 0, 2 * slots * sizeof(MemoEnt)));
         }
-        g->dg.memo[0] = (MemoEnt *)g->d_memo_alt;
-        g->dg.memo[1] = (MemoEnt *)g->d_memo_alt + slots;
+        g->dg.memo[0] = (MemoEnt *)m;
+        g->dg.memo[1] = (MemoEnt *)m + slots;
     }
     TimelineOut tl{};
     DeltaIn d;
@@ -163,10 +166,10 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
         }
         const int warps = score_warps_per_block();
         const int grid = std::max(1, std::min(g->num_sms * std::max(bps, 1), (K + warps - 1) / warps));
-        char *&ws = slot ? g->d_ws_inc_alt : g->d_ws_inc;
-        size_t &ws_bytes = slot ? g->ws_inc_alt_bytes : g->ws_inc_bytes;
-        void *&q = slot ? g->d_inc_q_alt : g->d_inc_q;
-        size_t &q_bytes = slot ? g->inc_q_alt_bytes : g->inc_q_bytes;
+        char *&ws = slot ? g->sub[slot].ws_inc : g->d_ws_inc;
+        size_t &ws_bytes = slot ? g->sub[slot].ws_inc_bytes : g->ws_inc_bytes;
+        void *&q = slot ? g->sub[slot].inc_q : g->d_inc_q;
+        size_t &q_bytes = slot ? g->sub[slot].inc_q_bytes : g->inc_q_bytes;
         const size_t need = (size_t)L.total * grid * warps;
         if (need > ws_bytes) {
             if (ws) CUDA_TRY(cudaFree(ws));
@@ -194,10 +197,10 @@ int score_delta_device(fo_graph *g, const int32_t *off, const int32_t *chg, int 
         if (e != cudaSuccess) return fail(FO_CUDA_ERROR, std::string("incremental score launch: ") + cudaGetErrorString(e));
         if (g->delta_mode == 2) return FO_OK;  // diagnostic: hand-backs stay visible as status 101
         return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
-                      nullptr, nullptr, stream, &d, slot, 2);
+                      nullptr, nullptr, stream, &d, slot ? slot + 1 : 0, 2);
     }
     return launch(g, nullptr, nullptr, nullptr, 0, K, 2 * g->V + 2, precision, cost, status, nullptr, tl, nullptr,
-                  nullptr, nullptr, stream, &d, slot);
+                  nullptr, nullptr, stream, &d, slot ? slot + 1 : 0);
 }
 
 }  // namespace fo
@@ -382,10 +385,13 @@ int fo_graph_destroy(fo_graph *g) {
         if (pl) cudaFree(pl);
     if (g->d_ws_inc) cudaFree(g->d_ws_inc);
     if (g->d_inc_q) cudaFree(g->d_inc_q);
-    if (g->d_ws_inc_alt) cudaFree(g->d_ws_inc_alt);
-    if (g->d_inc_q_alt) cudaFree(g->d_inc_q_alt);
-    if (g->d_memo_alt) cudaFree(g->d_memo_alt);
-    if (g->stream_alt) cudaStreamDestroy(g->stream_alt);
+    for (auto &u : g->sub) {
+        if (u.ws_inc) cudaFree(u.ws_inc);
+        if (u.inc_q) cudaFree(u.inc_q);
+        if (u.memo) cudaFree(u.memo);
+        if (u.ws) cudaFree(u.ws);
+        if (u.stream) cudaStreamDestroy(u.stream);
+    }
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     for (auto &sl : g->aslot) {
         if (sl.done) cudaEventSynchronize(sl.done);
@@ -537,7 +543,8 @@ int fo_graph_set_cost_model(fo_graph *g, const fo_cost_model *m) {
         g->memo_slots = slots;
         if (!g->d_memo) CUDA_TRY(cudaMalloc(&g->d_memo, 2 * slots * sizeof(MemoEnt)));
         CUDA_TRY(cudaMemset(g->d_memo, 0, 2 * slots * sizeof(MemoEnt)));
-        if (g->d_memo_alt) { cudaFree(g->d_memo_alt); g->d_memo_alt = nullptr; }  // re-made empty on demand
+        for (auto &u : g->sub)  // re-made empty on demand
+            if (u.memo) { cudaFree(u.memo); u.memo = nullptr; }
         dg.memo[0] = (MemoEnt *)g->d_memo;
         dg.memo[1] = (MemoEnt *)g->d_memo + slots;
         dg.memo_mask = (uint32_t)(slots - 1);
@@ -573,8 +580,8 @@ int fo_memo_clear(fo_graph *g, void *stream) {
     if (!g->d_memo) return FO_OK;
     cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;  // NULL: the handle's own stream
     CUDA_TRY(cudaMemsetAsync(g->d_memo, 0, 2 * ((size_t)g->dg.memo_mask + 1) * sizeof(MemoEnt), s));
-    if (g->d_memo_alt)  // the second submission stream's tables
-        CUDA_TRY(cudaMemsetAsync(g->d_memo_alt, 0, 2 * ((size_t)g->dg.memo_mask + 1) * sizeof(MemoEnt), s));
+    for (auto &u : g->sub)  // the submission streams' tables
+        if (u.memo) CUDA_TRY(cudaMemsetAsync(u.memo, 0, 2 * ((size_t)g->dg.memo_mask + 1) * sizeof(MemoEnt), s));
     return FO_OK;
 }
 
@@ -780,7 +787,7 @@ int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *ch
     if (!g->hstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->hstream, cudaStreamNonBlocking));
     if (!g->dstream) CUDA_TRY(cudaStreamCreateWithFlags(&g->dstream, cudaStreamNonBlocking));
     const int64_t t = g->next_ticket;
-    fo_graph::AsyncSlot &sl = g->aslot[t & 1];
+    fo_graph::AsyncSlot &sl = g->aslot[t % fo_graph::kSubmitSlots];
     if (!sl.h2d) {
         CUDA_TRY(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&sl.kdone, cudaEventDisableTiming));
@@ -802,16 +809,18 @@ int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *ch
     // their own scratch, so a batch's setup runs in the previous batch's
     // event-loop tail (graphs whose fused groups outgrow the estimator scratch
     // share one second-pass workspace: one stream)
-    const int ks = (g->V <= kMpCapDefault && !getenv("FO_SUBMIT_ONE_STREAM")) ? (int)(t & 1) : 0;
-    if (ks && !g->stream_alt) CUDA_TRY(cudaStreamCreateWithFlags(&g->stream_alt, cudaStreamNonBlocking));
-    cudaStream_t hs = g->hstream, ds = g->dstream, s = ks ? g->stream_alt : g->stream;
+    static const int nstreams = getenv("FO_SUBMIT_STREAMS") ? std::max(1, std::min(fo_graph::kSubmitSlots, atoi(getenv("FO_SUBMIT_STREAMS"))))
+                                                           : fo_graph::kSubmitSlots;
+    const int ks = g->V <= kMpCapDefault ? (int)(t % nstreams) : 0;
+    if (ks && !g->sub[ks].stream) CUDA_TRY(cudaStreamCreateWithFlags(&g->sub[ks].stream, cudaStreamNonBlocking));
+    cudaStream_t hs = g->hstream, ds = g->dstream, s = ks ? g->sub[ks].stream : g->stream;
     CUDA_TRY(cudaMemcpyAsync(b, offsets, 4 * ((size_t)K + 1), cudaMemcpyHostToDevice, hs));
     if (nc) CUDA_TRY(cudaMemcpyAsync(b + o_c, changes, 8 * nc, cudaMemcpyHostToDevice, hs));
     CUDA_TRY(cudaEventRecord(sl.h2d, hs));
     CUDA_TRY(cudaStreamWaitEvent(s, sl.h2d, 0));
-    if (clear_memo && g->d_memo && (!ks || g->d_memo_alt)) {  // only the table this precision's estimator reads
+    if (clear_memo && g->d_memo && (!ks || g->sub[ks].memo)) {  // only the table this precision's estimator reads
         const size_t slots = (size_t)g->dg.memo_mask + 1;
-        MemoEnt *tab = (MemoEnt *)(ks ? g->d_memo_alt : g->d_memo) + (precision == FO_PREC_FP64 ? slots : 0);
+        MemoEnt *tab = (MemoEnt *)(ks ? g->sub[ks].memo : g->d_memo) + (precision == FO_PREC_FP64 ? slots : 0);
         CUDA_TRY(cudaMemsetAsync(tab, 0, slots * sizeof(MemoEnt), s));
     }
     int st = score_delta_device(g, (const int32_t *)b, (const int32_t *)(b + o_c), K, precision,
@@ -835,7 +844,7 @@ int fo_score_wait(fo_graph *g, int64_t ticket) {
     if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
     std::lock_guard<std::mutex> lk(g->mu);
     if (ticket < 0 || ticket >= g->next_ticket) return fail(FO_INVALID_ARG, "unknown ticket");
-    const fo_graph::AsyncSlot &sl = g->aslot[ticket & 1];
+    const fo_graph::AsyncSlot &sl = g->aslot[ticket % fo_graph::kSubmitSlots];
     // a slot that moved on to a later ticket already waited for this one
     if (sl.ticket == ticket) CUDA_TRY(cudaEventSynchronize(sl.done));
     return FO_OK;

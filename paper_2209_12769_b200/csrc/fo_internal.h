@@ -247,14 +247,27 @@ struct fo_graph {
     cudaStream_t stream = nullptr;
     int num_sms = 0;
     size_t mem_total = 0;  // device memory (workspace budget)
-    // fo_score_delta_submit / fo_score_wait: two in-flight submissions; H2D and
-    // D2H on their own streams so one batch's transfers overlap the other's kernel
+    // fo_score_delta_submit / fo_score_wait: kSubmitSlots in-flight submissions;
+    // H2D and D2H on their own streams so one batch's transfers overlap another's
+    // kernels, and the kernels of consecutive submissions on their own compute
+    // streams (slot 0: the handle's stream) with their own scratch (Sub)
+    static constexpr int kSubmitSlots = 3;
     struct AsyncSlot {
         char *d = nullptr;
         size_t bytes = 0;
         cudaEvent_t h2d = nullptr, kdone = nullptr, done = nullptr;
         int64_t ticket = -1;
-    } aslot[2];
+    } aslot[kSubmitSlots];
+    struct Sub {  // slots 1.. (slot 0 uses the handle's own scratch)
+        char *ws_inc = nullptr;
+        size_t ws_inc_bytes = 0;
+        void *inc_q = nullptr;
+        size_t inc_q_bytes = 0;
+        void *memo = nullptr;
+        char *ws = nullptr;  // general-kernel first-pass workspace
+        size_t ws_bytes = 0;
+        cudaStream_t stream = nullptr;
+    } sub[kSubmitSlots];
     cudaStream_t hstream = nullptr, dstream = nullptr;
     int64_t next_ticket = 0;
     // incremental delta scoring (score_inc.cuh): the parent's plan per
@@ -270,13 +283,6 @@ struct fo_graph {
     size_t ws_inc_bytes = 0;
     void *d_inc_q = nullptr;  // estimator queue (IncQ entries) + its counter
     size_t inc_q_bytes = 0;
-    // the second scratch set of fo_score_delta_submit's second stream
-    char *d_ws_inc_alt = nullptr;
-    size_t ws_inc_alt_bytes = 0;
-    void *d_inc_q_alt = nullptr;
-    size_t inc_q_alt_bytes = 0;
-    void *d_memo_alt = nullptr;
-    cudaStream_t stream_alt = nullptr;
     int delta_mode = 1;  // 1: incremental kernel when the plan allows it; 0: general kernel only
     std::mutex mu;
 };

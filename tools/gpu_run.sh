@@ -11,7 +11,7 @@
 #   bash tools/gpu_run.sh scale    [TAG]   # 2 / 4 GPUs: bench, synth50k, BERT 256-seed search (gpurun --gpus 4)
 #   bash tools/gpu_run.sh multirank [TAG]  # two-rank exchange tests (the NCCL ones need gpurun --gpus 2)
 #   bash tools/gpu_run.sh ab-snap  [TAG]   # K3 fast-forward on / off, bit-exactness
-#   bash tools/gpu_run.sh ab-submit [TAG]  # pipelined submissions on two compute streams vs one (e2e)
+#   bash tools/gpu_run.sh ab-submit [TAG]  # pipelined submissions on 3 / 2 / 1 compute streams (e2e)
 #   bash tools/gpu_run.sh ab-tc    [TAG]   # tensor-core MP transforms: error and K2 time
 #   bash tools/gpu_run.sh ab-exchange [TAG]  # 4 GPUs: per-round exchange (native / torch thread) vs once
 #   bash tools/gpu_run.sh search-latency [TAG]  # single-seed search breakdown (FO_SEARCH_PROFILE)
@@ -83,11 +83,11 @@ ab-snap)
   cat ${O}_ab.jsonl
   ;;
 ab-submit)
-  for rep in 1 2; do for v in 0 1; do
-    if [ $v = 1 ]; then export FO_SUBMIT_ONE_STREAM=1; else unset FO_SUBMIT_ONE_STREAM; fi
-    echo "one_stream=$v $(timeout 300 python bench.py --no-cpu-baseline --no-search --steps 20 --warmup 5 2>/dev/null | python -c 'import sys,json; d=json.loads(sys.stdin.read()); print(d["value"], d["e2e"]["value"], d["e2e"]["synchronous_value"])')"
+  for rep in 1 2; do for v in 3 2 1; do
+    export FO_SUBMIT_STREAMS=$v
+    echo "streams=$v $(timeout 300 python bench.py --no-cpu-baseline --no-search --steps 20 --warmup 5 2>/dev/null | python -c 'import sys,json; d=json.loads(sys.stdin.read()); print(d["value"], d["e2e"]["value"], d["e2e"]["synchronous_value"])')"
   done; done | tee ${O}_ab.txt
-  unset FO_SUBMIT_ONE_STREAM
+  unset FO_SUBMIT_STREAMS
   ;;
 ab-tc)
   timeout 300 python -m pytest tests/test_gpu_tensorcore.py -q -x --timeout 250 > ${O}_tc_test.log 2>&1; tail -3 ${O}_tc_test.log
