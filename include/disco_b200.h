@@ -209,6 +209,12 @@ int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, 
                    double *cost_out, int32_t *status_out, void *stream);
 int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
                         double *cost_out, int32_t *status_out);
+/* fo_score_delta on scratch set `slot` (0 .. 2; 0 is fo_score_delta's): batches
+ * on different slots may run concurrently on different streams.  clear_memo
+ * empties the slot's memo table of this precision first (on `stream`).
+ * Slots > 0 need groups that fit the estimator scratch (V <= 2048). */
+int fo_score_delta_slot(fo_graph *g, int32_t slot, const int32_t *offsets, const int32_t *changes, int32_t K,
+                        int32_t precision, int32_t clear_memo, double *cost_out, int32_t *status_out, void *stream);
 /* Pipelined fo_score_delta_host for streams of batches: enqueues H2D of the
  * candidates (host buffers, pinned for overlap), [if clear_memo, an
  * fo_memo_clear of this precision's table], the score and the D2H of cost_out / status_out, and returns a

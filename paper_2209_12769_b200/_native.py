@@ -85,6 +85,7 @@ SIGNATURES = [
                                            C.c_int64]),
     ("fo_score_delta", C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp]),
     ("fo_score_delta_host", C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp, vp]),
+    ("fo_score_delta_slot", C.c_int, [vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]),
     ("fo_score_delta_submit", C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, P(C.c_int64)]),
     ("fo_score_wait", C.c_int, [vp, C.c_int64]),
     ("fo_threshold_ar", C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, vp, vp]),

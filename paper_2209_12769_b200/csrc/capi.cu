@@ -731,6 +731,26 @@ int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, 
     return score_delta_device(g, offsets, changes, K, precision, cost_out, status_out, (cudaStream_t)stream);
 }
 
+int fo_score_delta_slot(fo_graph *g, int32_t slot, const int32_t *offsets, const int32_t *changes, int32_t K,
+                        int32_t precision, int32_t clear_memo, double *cost_out, int32_t *status_out, void *stream) {
+    if (!g) return fail(FO_INVALID_ARG, "null graph");
+    if (g->device < 0) return fail(FO_CUDA_ERROR, "graph handle was created without a device");
+    if (slot < 0 || slot >= fo_graph::kSubmitSlots) return fail(FO_INVALID_ARG, "slot out of range");
+    if (slot > 0 && g->V > kMpCapDefault)
+        return fail(FO_INVALID_ARG, "graphs whose groups outgrow the estimator scratch have one scratch slot");
+    std::lock_guard<std::mutex> lk(g->mu);
+    CUDA_TRY(cudaSetDevice(g->device));
+    int st = ensure_plan(g, precision);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (clear_memo && g->d_memo && (slot == 0 || g->sub[slot].memo)) {  // this slot's table of this precision
+        const size_t slots = (size_t)g->dg.memo_mask + 1;
+        MemoEnt *tab = (MemoEnt *)(slot ? g->sub[slot].memo : g->d_memo) + (precision == FO_PREC_FP64 ? slots : 0);
+        CUDA_TRY(cudaMemsetAsync(tab, 0, slots * sizeof(MemoEnt), s));
+    }
+    return score_delta_device(g, offsets, changes, K, precision, cost_out, status_out, s, slot);
+}
+
 // sparse-candidate offsets: offsets[0] == 0 and non-decreasing, so every
 // candidate's change range lies inside the staged changes buffer.  (Indices
 // inside one candidate must be distinct: duplicates race in K1.)

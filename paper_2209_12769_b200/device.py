@@ -277,6 +277,19 @@ class DeviceGraph:
                                     C.c_void_p(stream))
         _raise(st, "fo_score_delta", N.last_error())
 
+    def score_delta_slot(self, slot, offsets, changes, cost, status, precision=N.FO_PREC_FP32, stream=None,
+                         clear_memo=False):
+        """score_delta_device on scratch set `slot` (fo_score_delta_slot):
+        batches on different slots may run at once on different streams."""
+        import torch
+
+        K = int(cost.shape[0])
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        st = N.lib().fo_score_delta_slot(self.h, int(slot), N.ptr(offsets), N.ptr(changes), K, precision,
+                                         int(bool(clear_memo)), N.ptr(cost), N.ptr(status), C.c_void_p(stream))
+        _raise(st, "fo_score_delta_slot", N.last_error())
+
     def state_hash(self, ng, rg, bk):
         ng = np.ascontiguousarray(np.atleast_2d(ng), np.int32)
         rg = np.ascontiguousarray(np.atleast_2d(rg), np.int32)
