@@ -438,6 +438,39 @@ def test_pipelined_bench_batches_on_two_streams_equal_sync(precision):
             assert np.array_equal(h[3].numpy(), st_ref) and np.array_equal(h[2].numpy(), ref)
 
 
+def test_device_batches_on_scratch_slots_equal_serial():
+    """fo_score_delta_slot: device-resident batches on the three scratch slots,
+    each on its own stream and running concurrently (memo cleared per batch),
+    equal the serial fo_score_delta of the same batch; slot ids are checked."""
+    import torch
+
+    g, cps = providers("resnet50", N.FO_PREC_FP32)
+    dg = cps["mp"].device_graph(g)
+    dg.set_parent()
+    batches = []
+    for b in range(6):
+        off, chg = dg.make_candidates_delta(np.arange(b * 4096, (b + 1) * 4096, dtype=np.uint64))
+        batches.append((torch.from_numpy(off).cuda(), torch.from_numpy(chg).cuda()))
+    refs = []
+    for o, c in batches:
+        cost = torch.empty(4096, dtype=torch.float64, device="cuda")
+        st = torch.empty(4096, dtype=torch.int32, device="cuda")
+        dg.score_delta_device(o, c, cost, st)
+        torch.cuda.synchronize()
+        refs.append((cost.cpu(), st.cpu()))
+    streams = [torch.cuda.Stream() for _ in range(N.SUBMIT_SLOTS)]
+    outs = [(torch.empty(4096, dtype=torch.float64, device="cuda"), torch.empty(4096, dtype=torch.int32, device="cuda"))
+            for _ in batches]
+    for i, (o, c) in enumerate(batches):
+        k = i % N.SUBMIT_SLOTS
+        dg.score_delta_slot(k, o, c, outs[i][0], outs[i][1], stream=streams[k].cuda_stream, clear_memo=True)
+    torch.cuda.synchronize()
+    for (cost, st), (rc, rs) in zip(outs, refs):
+        assert torch.equal(cost.cpu(), rc) and torch.equal(st.cpu(), rs)
+    with pytest.raises(Exception):
+        dg.score_delta_slot(N.SUBMIT_SLOTS, *batches[0], *outs[0])
+
+
 def test_delta_scoring_rejects_bad_input():
     g, cps = providers("vgg16", N.FO_PREC_FP32)
     dg = cps["mp"].device_graph(g)
