@@ -12,6 +12,7 @@
 #   bash tools/gpu_run.sh multirank [TAG]  # two-rank exchange tests (the NCCL ones need gpurun --gpus 2)
 #   bash tools/gpu_run.sh ab-snap  [TAG]   # K3 fast-forward on / off, bit-exactness
 #   bash tools/gpu_run.sh ab-submit [TAG]  # pipelined submissions on 3 / 2 / 1 compute streams (e2e)
+#   bash tools/gpu_run.sh ab-snap-bench [TAG]  # bench figures (pipelined, e2e, serial) with / without the K3 fast-forward
 #   bash tools/gpu_run.sh ab-tc    [TAG]   # tensor-core MP transforms: error and K2 time
 #   bash tools/gpu_run.sh ab-exchange [TAG]  # 4 GPUs: per-round exchange (native / torch thread) vs once
 #   bash tools/gpu_run.sh search-latency [TAG]  # single-seed search breakdown (FO_SEARCH_PROFILE)
@@ -88,6 +89,13 @@ ab-submit)
     echo "streams=$v $(timeout 300 python bench.py --no-cpu-baseline --no-search --steps 20 --warmup 5 2>/dev/null | python -c 'import sys,json; d=json.loads(sys.stdin.read()); print(d["value"], d["e2e"]["value"], d["e2e"]["synchronous_value"])')"
   done; done | tee ${O}_ab.txt
   unset FO_SUBMIT_STREAMS
+  ;;
+ab-snap-bench)
+  for rep in 1 2; do for v in 0 1; do
+    if [ $v = 1 ]; then export FO_INC_NO_SNAP=1; else unset FO_INC_NO_SNAP; fi
+    echo "no_snap=$v $(timeout 300 python bench.py --no-cpu-baseline --no-search --steps 40 --warmup 5 2>/dev/null | python -c 'import sys,json; d=json.loads(sys.stdin.read()); print(d["value"], d["e2e"]["value"], d["serial"]["value"])')"
+  done; done | tee ${O}_ab.txt
+  unset FO_INC_NO_SNAP
   ;;
 ab-tc)
   timeout 300 python -m pytest tests/test_gpu_tensorcore.py -q -x --timeout 250 > ${O}_tc_test.log 2>&1; tail -3 ${O}_tc_test.log
