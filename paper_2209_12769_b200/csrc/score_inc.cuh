@@ -39,7 +39,7 @@ struct IncWork {  // setup record of a patched node, in discovery order
     unsigned long long h1, h2;  // member-set hash of a fused group (the memo key)
 };
 
-constexpr int kIncRingG = 256, kIncRingB = 128;  // shared-memory ready-run capacities per lane
+constexpr int kIncRingG = 128, kIncRingB = 64;  // shared-memory ready-run capacities per lane
 // estimator kernel: member sets up to this size keep H / P in shared memory
 // (16 KB per block either way: more would cost the fp64 kernel a resident block)
 template <typename T>
@@ -1314,7 +1314,7 @@ __device__ __forceinline__ void inc_k3_run(const IncArgs &a, uint32_t wsm) {
 // their loops share instructions, measured 2.5x slower at 16 per warp: the
 // loops diverge within a few events and the warp serialises them.
 template <bool SI>
-__global__ void __launch_bounds__(kWarps * 32, 7) score_kernel_inc_k3(const __grid_constant__ IncArgs a, int k0, int n) {
+__global__ void __launch_bounds__(kWarps * 32, 10) score_kernel_inc_k3(const __grid_constant__ IncArgs a, int k0, int n) {
     const int lane = threadIdx.x & 31;
     const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const uint32_t wsm = (uint32_t)((threadIdx.x >> 5) * a.L.k_bytes);
