@@ -209,7 +209,7 @@ int fo_score_delta(fo_graph *g, const int32_t *offsets, const int32_t *changes, 
                    double *cost_out, int32_t *status_out, void *stream);
 int fo_score_delta_host(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,
                         double *cost_out, int32_t *status_out);
-/* fo_score_delta on scratch set `slot` (0 .. 2; 0 is fo_score_delta's): batches
+/* fo_score_delta on scratch set `slot` (0 .. 3; 0 is fo_score_delta's): batches
  * on different slots may run concurrently on different streams.  clear_memo
  * empties the slot's memo table of this precision first (on `stream`).
  * Slots > 0 need groups that fit the estimator scratch (V <= 2048). */
@@ -218,9 +218,9 @@ int fo_score_delta_slot(fo_graph *g, int32_t slot, const int32_t *offsets, const
 /* Pipelined fo_score_delta_host for streams of batches: enqueues H2D of the
  * candidates (host buffers, pinned for overlap), [if clear_memo, an
  * fo_memo_clear of this precision's table], the score and the D2H of cost_out / status_out, and returns a
- * ticket.  Three submissions may be in flight, each on its own compute
+ * ticket.  Four submissions may be in flight, each on its own compute
  * stream with its own scratch and memo tables (consecutive batches overlap);
- * a fourth waits for the oldest.  Results are valid, and the input buffers reusable, after
+ * a fifth waits for the oldest.  Results are valid, and the input buffers reusable, after
  * fo_score_wait(g, ticket).  Same semantics per batch as
  * fo_score_delta_host (simulator.py:143-145 per candidate). */
 int fo_score_delta_submit(fo_graph *g, const int32_t *offsets, const int32_t *changes, int32_t K, int32_t precision,

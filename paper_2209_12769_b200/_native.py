@@ -134,7 +134,7 @@ def last_error() -> str:
     return msg.decode() if msg else ""
 
 
-SUBMIT_SLOTS = 3  # fo_score_delta_submit: batches in flight (fo_graph::kSubmitSlots)
+SUBMIT_SLOTS = 4  # fo_score_delta_submit: batches in flight (fo_graph::kSubmitSlots)
 
 # fo_round_fn: int32 (void *ctx, int64 round, int32 active, const double *best, int32 R)
 ROUND_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_double), C.c_int32)

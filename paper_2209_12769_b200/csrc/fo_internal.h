@@ -251,7 +251,7 @@ struct fo_graph {
     // H2D and D2H on their own streams so one batch's transfers overlap another's
     // kernels, and the kernels of consecutive submissions on their own compute
     // streams (slot 0: the handle's stream) with their own scratch (Sub)
-    static constexpr int kSubmitSlots = 3;
+    static constexpr int kSubmitSlots = 4;
     struct AsyncSlot {
         char *d = nullptr;
         size_t bytes = 0;

@@ -234,8 +234,8 @@ class DeviceGraph:
 
     def score_delta_submit(self, offsets, changes, cost, status, precision=N.FO_PREC_FP32, clear_memo=False):
         """Pipelined fo_score_delta_host: enqueue one batch of sparse candidates
-        held in host arrays (pinned for overlap) and return a ticket; three
-        batches may be in flight, on three compute streams.  `cost` (float64) / `status` (int32), host,
+        held in host arrays (pinned for overlap) and return a ticket; four
+        batches may be in flight, on four compute streams.  `cost` (float64) / `status` (int32), host,
         length >= K, are written once score_wait(ticket) returns.  The handle
         keeps references to all four buffers until then."""
         import ctypes
