@@ -421,20 +421,23 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
             }
             it++;
         }
-        // drain every lane ending at the next completion time (simulator.py:122-132)
-        const unsigned long long t = end0 < end1 ? end0 : end1;
-        if (t == kIdle) break;
+        // drain every lane ending at the next completion time (simulator.py:122-132):
+        // c0 / c1 say which lanes end then; an idle lane's +inf never does
+        // unless both are idle (+inf's high word: the loop ends)
+        const bool c0 = end0 <= end1, c1 = end1 <= end0;
+        const unsigned long long t = c0 ? end0 : end1;
+        if ((uint32_t)(t >> 32) == (uint32_t)(kIdle >> 32)) break;
         if (t > nowb) {
             nowb = t;
             now = __longlong_as_double((long long)t);
             level += 0x10000u;
         }
-        if (end0 == t) {
+        if (c0) {
             end0 = kIdle;
             if constexpr (REC) ro->fin[run0] = (uint16_t)it;
             if (!release(sb0, se0)) return false;
         }
-        if (end1 == t) {
+        if (c1) {
             end1 = kIdle;
             if constexpr (REC) ro->fin[run1] = (uint16_t)it;
             if (!release(sb1, se1)) return false;
