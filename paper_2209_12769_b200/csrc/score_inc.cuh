@@ -344,8 +344,8 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     // End times are kept as the bit patterns of non-negative doubles, which
     // order like the values: integer compares and min.  An idle lane holds +inf.
     constexpr unsigned long long kIdle = 0x7ff0000000000000ull;
-    unsigned long long end0 = st.end0, end1 = st.end1, nowb = st.nowb;
-    double now = __longlong_as_double((long long)nowb);
+    unsigned long long end0 = st.end0, end1 = st.end1;
+    double now = __longlong_as_double((long long)st.nowb);  // its bit pattern orders like an end time
     uint32_t level = st.level;
     uint32_t lastg = tailg > headg ? (uint32_t)(rg[(tailg - 1) & mg] >> 32) : 0u;
     uint32_t lastb = tailb > headb ? (uint32_t)(rb[(tailb - 1) & mb] >> 32) : 0u;
@@ -410,7 +410,7 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
                 char *sp = ro->snap + (int64_t)(j - 1) * ro->stride;
                 IncLoopState *h = (IncLoopState *)sp;
                 *h = IncLoopState{headg, tailg, headb, tailb, sb0,  se0,   sb1, se1,
-                                  end0,  end1,  nowb,  level, it,  run0, run1};
+                                  end0,  end1,  (unsigned long long)__double_as_longlong(now), level, it, run0, run1};
                 unsigned long long *eg = (unsigned long long *)(sp + kIncSnapRuns), *eb = eg + kIncRingG;
                 for (int i = headg; i < tailg; i++) eg[i - headg] = rg[i & mg];
                 for (int i = headb; i < tailb; i++) eb[i - headb] = rb[i & mb];
@@ -427,8 +427,7 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
         const bool c0 = end0 <= end1, c1 = end1 <= end0;
         const unsigned long long t = c0 ? end0 : end1;
         if ((uint32_t)(t >> 32) == (uint32_t)(kIdle >> 32)) break;
-        if (t > nowb) {
-            nowb = t;
+        if (t > (unsigned long long)__double_as_longlong(now)) {
             now = __longlong_as_double((long long)t);
             level += 0x10000u;
         }
