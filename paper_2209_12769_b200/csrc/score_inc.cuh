@@ -377,11 +377,11 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
             dur = r.dur;
             sb = r.sb;
             se = r.se;
-        } else {
-            const IncNode r = rec[t];
-            dur = r.dur;
-            sb = r.sb;
-            se = r.se;
+        } else {  // one 128-bit load: duration, then the successor range (sb | se << 16)
+            const uint4 r = __ldg((const uint4 *)(rec + t));
+            dur = __hiloint2double((int)r.y, (int)r.x);
+            sb = r.z & 0xffffu;
+            se = r.z >> 16;
         }
     };
     // start_available (simulator.py:98-115): compute lane, then comm lane;
