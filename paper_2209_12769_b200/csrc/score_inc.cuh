@@ -916,7 +916,7 @@ __device__ __forceinline__ IncCtx inc_ctx(const IncArgs &a, int wid, char *sm) {
 
 // Setup + K2 of candidates [k0, k0 + warps): one warp each.
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32, 8) score_kernel_inc(const __grid_constant__ IncArgs a, int k0) {
+__global__ void __launch_bounds__(kWarps * 32, 9) score_kernel_inc(const __grid_constant__ IncArgs a, int k0) {
     const int lane = threadIdx.x & 31;
     const int wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
     const int k = k0 + wid;
