@@ -352,9 +352,10 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     uint32_t it = st.iter;  // REC: the iteration being run, + 1
     uint32_t run0 = 0xffffu, run1 = 0xffffu;  // REC: the running nodes
     auto release = [&](unsigned qb, unsigned qe) -> bool {
-        const uint32_t *__restrict__ L = (qb & 0x8000u) ? csucc : psucc;
-        for (unsigned q = qb & 0x7fffu; q < qe; q++) {
-            const uint32_t e = L[q];
+        // walk the list by pointer and count: nothing to re-select per entry
+        const uint32_t *__restrict__ q = ((qb & 0x8000u) ? csucc : psucc) + (qb & 0x7fffu);
+        for (int n = (int)qe - (int)(qb & 0x7fffu); n > 0; n--, q++) {
+            const uint32_t e = *q;
             const unsigned t = e & 0xffffu;
             const unsigned d = (unsigned)indeg[t] - 1u;  // bit 15: the node is patched
             indeg[t] = (uint16_t)d;
