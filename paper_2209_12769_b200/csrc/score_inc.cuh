@@ -388,14 +388,14 @@ __device__ __forceinline__ bool inc_ring_loop(const IncPlan &p, const uint32_t *
     // start_available (simulator.py:98-115): compute lane, then comm lane;
     // start = max(now, rt) = now because rt is a drained completion time
     auto start = [&]() {
-        if (end0 == kIdle && headg < tailg) {
+        if ((uint32_t)(end0 >> 32) == (uint32_t)(kIdle >> 32) && headg < tailg) {  // idle: +inf's high word
             double d;
             const unsigned long long x = rg[(headg++) & mg];
             node_rec(x, d, sb0, se0);
             end0 = (unsigned long long)__double_as_longlong(__dadd_rn(now, d));
             if constexpr (REC) run0 = (unsigned)x & 0xffffu;
         }
-        if (end1 == kIdle && headb < tailb) {
+        if ((uint32_t)(end1 >> 32) == (uint32_t)(kIdle >> 32) && headb < tailb) {
             double d;
             const unsigned long long x = rb[(headb++) & mb];
             node_rec(x, d, sb1, se1);
