@@ -279,7 +279,9 @@ __device__ __forceinline__ bool inc_push(unsigned long long *buf, unsigned m, in
                                          unsigned long long x) {
     const uint32_t key = (uint32_t)(x >> 32);  // keys are unique: the high word orders the entries
     if (tail - head > (int)m) return false;
-    if (tail == head || key >= last) {
+    // last bounds the run's keys from above (an emptied run keeps the bound,
+    // and a smaller key then takes the insertion path, which is correct too)
+    if (key >= last) {
         buf[(tail++) & m] = x;
         last = key;
         return true;
